@@ -1,0 +1,209 @@
+"""CPU oracle of the hashed-voxel-grid primal-dual TV regulariser (arXiv 1604.03734 §III-B/C).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs may import this package.  The product path
+(``paper_1604_03734_b200``) never imports it and shares no code with it.
+
+Two independent oracles:
+  * O1 — ``hvg_oracle.c`` (plain C, fp64 and fp32 in one written formula order), loaded via ctypes:
+    its own hash table, CSR buckets and neighbour table, per-phase loops over every voxel.
+  * O2 — ``oracle.dense`` (numpy): dense brute force on the bounding box of the blocks.
+
+Parity status per function:
+  hash / tables ......... pinned (hand-evaluated hash values, brute-force neighbour search)
+  gradient / divergence . pinned (SPEC worked examples, adjointness, dense O2)
+  dual / primal / relax . pinned (worked examples, closed forms of 1-D TV-L1 and ROF steps)
+  regularise ............ pinned (closed forms, exact invariants, O1 == O2); general 3-D
+                          isotropic TV-L1 at finite iterations has no closed form ("parity unpinned
+                          beyond these", SURVEY §8(c) last pin row)
+  energy ................ pinned (worked examples, brute force, weak duality)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+_SRC = [os.path.join(_HERE, "hvg_oracle.c"), os.path.join(_HERE, "hvg_oracle_real.inc")]
+
+
+def build(force: bool = False) -> str:
+    """Compile the C oracle with -O2 -ffp-contract=off (reading c-18: no FMA contraction)."""
+    newest = max(os.path.getmtime(s) for s in _SRC)
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < newest:
+        tmp = _SO + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+                               "-Wall", "-o", tmp, _SRC[0], "-lm"])
+        os.replace(tmp, _SO)
+    return _SO
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = ctypes.CDLL(build())
+        P = ctypes.c_void_p
+        i64, u32, i32, dbl, flt, cint = ctypes.c_int64, ctypes.c_uint32, ctypes.c_int32, ctypes.c_double, ctypes.c_float, ctypes.c_int
+        L.orc_hash.restype = u32
+        L.orc_hash.argtypes = [i32, i32, i32, u32]
+        L.orc_table_size.restype = u32
+        L.orc_table_size.argtypes = [i64]
+        L.orc_build_table.restype = i64
+        L.orc_build_table.argtypes = [P, i64, u32, P, P, P]
+        L.orc_lookup.restype = i64
+        L.orc_lookup.argtypes = [P, P, P, u32, i32, i32, i32]
+        L.orc_neighbours.restype = None
+        L.orc_neighbours.argtypes = [P, i64, u32, P, P, P]
+        for sfx, real in (("f64", dbl), ("f32", flt)):
+            g = getattr(L, f"orc_gradient_{sfx}")
+            g.restype = None
+            g.argtypes = [i64, P, P, P, P]
+            d = getattr(L, f"orc_divergence_{sfx}")
+            d.restype = None
+            d.argtypes = [i64, P, P, P, P]
+            r = getattr(L, f"orc_regularise_{sfx}")
+            r.restype = cint
+            r.argtypes = [i64, P, P, P, real, real, real, real, real, cint, cint, i64, P, P, P, cint]
+        L.orc_energy.restype = None
+        L.orc_energy.argtypes = [i64, P, P, P, P, P, dbl, dbl, cint, P, P]
+        _lib = L
+    return _lib
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _np(x, dtype):
+    if hasattr(x, "detach"):
+        x = x.detach().cpu().numpy()
+    return np.ascontiguousarray(x, dtype=dtype)
+
+
+def block_hash(x: int, y: int, z: int, T: int) -> int:
+    return int(lib().orc_hash(x, y, z, T))
+
+
+def table_size(n: int) -> int:
+    return int(lib().orc_table_size(n))
+
+
+def build_table(coords):
+    """Returns (T, bucket_start[T+1] uint32, bucket_entry[n] int32, dup) with dup = None or (j, i)."""
+    c = _np(coords, np.int32).reshape(-1, 3)
+    n = c.shape[0]
+    T = table_size(n)
+    bs = np.zeros(T + 1, np.uint32)
+    be = np.zeros(max(n, 1), np.int32)
+    dj = np.zeros(1, np.int64)
+    i = lib().orc_build_table(_ptr(c), n, T, _ptr(bs), _ptr(be), _ptr(dj))
+    dup = None if i < 0 else (int(dj[0]), int(i))
+    return T, bs, be[:n], dup
+
+
+def lookup(coords, tables, x, y, z) -> int:
+    c = _np(coords, np.int32).reshape(-1, 3)
+    T, bs, be, _ = tables
+    be = np.ascontiguousarray(be) if be.size else np.zeros(1, np.int32)
+    return int(lib().orc_lookup(_ptr(c), _ptr(bs), _ptr(be), T, x, y, z))
+
+
+def neighbours(coords, tables=None) -> np.ndarray:
+    """nbr [n, 6] int32 in direction order (−x, +x, −y, +y, −z, +z), −1 = unallocated."""
+    c = _np(coords, np.int32).reshape(-1, 3)
+    n = c.shape[0]
+    if tables is None:
+        tables = build_table(c)
+    T, bs, be, dup = tables
+    if dup is not None:
+        raise ValueError(f"duplicate block coordinates at caller indices {dup}")
+    be = np.ascontiguousarray(be) if be.size else np.zeros(1, np.int32)
+    nbr = np.zeros((n, 6), np.int32)
+    lib().orc_neighbours(_ptr(c), n, T, _ptr(bs), _ptr(be), _ptr(nbr))
+    return nbr
+
+
+def _rt(precision):
+    return (np.float64, "f64") if precision == "f64" else (np.float32, "f32")
+
+
+def gradient(nbr, W, u, precision="f64") -> np.ndarray:
+    """Eq. 3 masked forward gradient; returns [3, n, 512]."""
+    dt, sfx = _rt(precision)
+    nbr = _np(nbr, np.int32)
+    n = nbr.shape[0]
+    Wf = _np(W, np.float32)
+    uu = _np(u, dt)
+    g = np.zeros((3, n, 512), dt)
+    getattr(lib(), f"orc_gradient_{sfx}")(n, _ptr(nbr), _ptr(Wf), _ptr(uu), _ptr(g))
+    return g
+
+
+def divergence(nbr, W, p, precision="f64") -> np.ndarray:
+    """Eq. 4 masked backward divergence of p [3, n, 512]; returns [n, 512]."""
+    dt, sfx = _rt(precision)
+    nbr = _np(nbr, np.int32)
+    n = nbr.shape[0]
+    Wf = _np(W, np.float32)
+    pp = _np(p, dt)
+    d = np.zeros((n, 512), dt)
+    getattr(lib(), f"orc_divergence_{sfx}")(n, _ptr(nbr), _ptr(Wf), _ptr(pp), _ptr(d))
+    return d
+
+
+def regularise(coords, f, W, lam, eps, tau, sigma, iters, theta=1.0, data_term=0, init=0, precision="f64",
+               state=None, nbr=None):
+    """Run `iters` CP iterations; returns (u, ubar, p) with u, ubar [n, 512] and p [3, n, 512].
+
+    `state` = (u, ubar, p) resumes from a previous call.  Parameters are rounded to fp32 first
+    (the values the product path receives), then widened for the fp64 oracle.
+    """
+    dt, sfx = _rt(precision)
+    if nbr is None:
+        nbr = neighbours(coords)
+    nbr = _np(nbr, np.int32)
+    n = nbr.shape[0]
+    ff = _np(f, np.float32).reshape(n, 512)
+    Wf = _np(W, np.float32).reshape(n, 512)
+    if state is None:
+        u = np.zeros((n, 512), dt)
+        ub = np.zeros((n, 512), dt)
+        p = np.zeros((3, n, 512), dt)
+        resume = 0
+    else:
+        u, ub, p = (np.array(a, dtype=dt, copy=True) for a in state)
+        resume = 1
+    r32 = lambda x: float(np.float32(x))
+    getattr(lib(), f"orc_regularise_{sfx}")(n, _ptr(nbr), _ptr(ff), _ptr(Wf), r32(lam), r32(eps), r32(tau),
+                                            r32(sigma), r32(theta), int(data_term), int(init), int(iters),
+                                            _ptr(u), _ptr(ub), _ptr(p), resume)
+    return u, ub, p
+
+
+def regularise_scene(scene, precision="f64", iters=None, state=None, nbr=None):
+    it = scene.iters if iters is None else iters
+    return regularise(scene.coords, scene.f, scene.W, scene.lam, scene.eps, scene.tau, scene.sigma, it,
+                      theta=scene.theta, data_term=scene.data_term, init=scene.init, precision=precision,
+                      state=state, nbr=nbr)
+
+
+def energy(nbr, f, W, u, lam, eps, data_term=0, p=None):
+    """(primal, dual) in fp64; dual is None when p is None."""
+    nbr = _np(nbr, np.int32)
+    n = nbr.shape[0]
+    ff = _np(f, np.float32)
+    Wf = _np(W, np.float32)
+    uu = _np(u, np.float64)
+    out = np.zeros(2, np.float64)
+    pp = _np(p, np.float64) if p is not None else None
+    r32 = lambda x: float(np.float32(x))
+    lib().orc_energy(n, _ptr(nbr), _ptr(ff), _ptr(Wf), _ptr(uu), _ptr(pp) if pp is not None else None,
+                     r32(lam), r32(eps), int(data_term), _ptr(out[0:1]), _ptr(out[1:2]))
+    return float(out[0]), (float(out[1]) if p is not None else None)
