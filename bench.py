@@ -1,0 +1,353 @@
+#!/usr/bin/env python3
+"""Benchmark of the hashed-voxel-grid primal-dual TV regulariser on B200 (BASELINE.json metric:
+voxel-updates/s and achieved HBM GB/s at 1/2/4/8 GPUs).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config street] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1: route-axis sharding over NCCL)
+
+A step is one pass of the whole hot path (SURVEY §8(a) rows a-1 … a-8) over the config's synthetic
+volume: vol_create (device hash/CSR/neighbour build from block coordinates + f + W), vol_regularise
+(init + `iters` fused Chambolle–Pock iterations), vol_energy, vol_read_u.  `value` is
+N_alloc·iters·N_gpu / step time with inputs resident in HBM; `e2e` is the same through the same C ABI
+from pinned host buffers (host→device copies of coords/f/W and the device→host read of u inside the
+timed region).  At N = 1 the workload is config 2 (street, 300 Huber-TV iterations); at N > 1 each
+GPU owns one 60 m street segment of a 60·N m street (weak scaling).
+
+--impl reference times the CPU oracle (oracle/, plain C, fp64, one thread) on a bounded sample of
+the same workload: each step runs one oracle iteration over the whole volume.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+ALG_BYTES_PER_VOXEL = 48  # 28 B read (f, W, u, ū, p×3) + 20 B written (u, ū, p×3)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="street")
+    ap.add_argument("--iters", type=int, default=None, help="override the config's iteration count")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--kernel", type=int, default=0, help="0 fused (product), 1 two-kernel baseline")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--seed", type=int, default=0)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------------ helpers
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), parts[3:7]))
+            except ValueError:
+                continue
+        os.unlink(self.path)
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for _, _, fl in rows for k, v in enumerate(fl) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic():
+    """DRAM bytes per fused-kernel launch from the committed ncu --set full capture, if any."""
+    p = os.path.join(ROOT, "profiles", "fused_traffic.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return d
+    except Exception:
+        return None
+
+
+def make_scene(cfg: str, world: int, seed: int, device):
+    from synth import scenes
+    if cfg == "street":
+        length = 60.0 * world
+        s = scenes.street(seed, length=length, device=device, chunk_blocks=4096)
+        if world > 1:
+            s.name = f"street-{int(length)}m"
+        return s
+    return scenes.by_name(cfg, seed=seed, device=device)
+
+
+def partition(coords, world):
+    """Owner rank per block: contiguous ranges of equal block count along the route (x for the
+    street; arc length for polyline routes is approximated by x + y on the staircase)."""
+    import torch
+    key = coords[:, 0].to(torch.int64) * 4096 + coords[:, 1].to(torch.int64)
+    order = torch.argsort(key * 65536 + coords[:, 2].to(torch.int64), stable=True)
+    part = torch.empty(coords.shape[0], dtype=torch.int32)
+    n = coords.shape[0]
+    for r in range(world):
+        part[order[r * n // world:(r + 1) * n // world].cpu()] = r
+    return part
+
+
+# ------------------------------------------------------------------------------ CPU oracle timing
+
+def time_oracle(scene, iters: int):
+    import numpy as np
+
+    import oracle
+    coords, f, W = scene.numpy()
+    nbr = oracle.neighbours(coords)
+    t0 = time.perf_counter()
+    oracle.regularise(coords, f, W, scene.lam, scene.eps, scene.tau, scene.sigma, iters, theta=scene.theta,
+                      data_term=scene.data_term, init=scene.init, precision="f64", nbr=nbr)
+    dt = time.perf_counter() - t0
+    del np
+    return dt
+
+
+def reference_arm(args):
+    import torch
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    scene = make_scene(args.config, 1, args.seed, dev).to("cpu")
+    n_alloc = scene.n_alloc
+    per_step_iters = 1
+    for _ in range(args.warmup):
+        time_oracle(scene, per_step_iters)
+    times = [time_oracle(scene, per_step_iters) for _ in range(args.steps)]
+    t = sum(times) / len(times)
+    val = n_alloc * per_step_iters / t
+    sample = f"{per_step_iters} oracle iteration(s) over the whole {scene.name} volume ({n_alloc} voxels) per step"
+    line = {"impl": "reference", "metric": "voxel-updates/s", "value": val, "unit": "voxel-updates/s",
+            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": scene.name, "n_alloc": n_alloc, "blocks": scene.n_blocks,
+                                            "iters_per_step": per_step_iters},
+            "cpu_baseline": {"value": val, "unit": "voxel-updates/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": val, "unit": "voxel-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------ our arm
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return reference_arm(args)
+    import torch
+    import torch.distributed as dist
+
+    from paper_1604_03734_b200 import Volume
+    from paper_1604_03734_b200 import _native as N
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            raise SystemExit("--gpus N > 1 must be launched with torchrun --nproc-per-node N")
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        group = dist.group.WORLD
+
+    scene = make_scene(args.config, world, args.seed, dev)
+    iters = scene.iters if args.iters is None else args.iters
+    coords = scene.coords.contiguous()
+    if world > 1:
+        part = partition(coords.cpu(), world)
+        mine = (part == rank).nonzero().squeeze(1).to(dev)
+        f_loc, W_loc = scene.f[mine].contiguous(), scene.W[mine].contiguous()
+    else:
+        part = None
+        f_loc, W_loc = scene.f, scene.W
+    n_local_vox = f_loc.shape[0] * 512
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local_rank])
+        torch.cuda.synchronize(dev)
+
+    kw = dict(part=part, group=group) if world > 1 else {}
+    u_out = torch.empty(f_loc.shape[0], 512, device=dev)
+    ev_a = torch.cuda.Event(enable_timing=True)
+    ev_b = torch.cuda.Event(enable_timing=True)
+    iter_ms = []
+
+    def step(c, f, W, out, record):
+        vol = Volume(c, f, W, stream=stream, **kw)
+        vol.regularise(scene.lam, scene.eps, scene.tau, scene.sigma, 0, theta=scene.theta,
+                       data_term=scene.data_term, init=scene.init, kernel=args.kernel)
+        ev_a.record(stream)
+        vol.regularise(scene.lam, scene.eps, scene.tau, scene.sigma, iters, theta=scene.theta,
+                       data_term=scene.data_term, resume=True, kernel=args.kernel)
+        ev_b.record(stream)
+        E = vol.energy(scene.lam, scene.eps, scene.data_term)
+        vol.read_u(out)
+        if record:
+            ev_b.synchronize()
+            iter_ms.append(ev_a.elapsed_time(ev_b) / iters)
+        vol.close()
+        return E
+
+    # warm-up (also validates the run end to end)
+    for _ in range(max(3, args.warmup)):
+        E = step(coords, f_loc, W_loc, u_out, False)
+    barrier()
+    launches0 = N.lib().vol_total_launches()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    t0.record(stream)
+    for _ in range(args.steps):
+        E = step(coords, f_loc, W_loc, u_out, True)
+    t1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    launches = (N.lib().vol_total_launches() - launches0) // args.steps
+    ms = t0.elapsed_time(t1) / args.steps
+    ms_t = torch.tensor([ms], device=dev)
+    it_t = torch.tensor([statistics.median(iter_ms)], device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(it_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    it_ms = float(it_t.item())
+    n_alloc_total = scene.n_alloc
+    value = n_alloc_total * iters / (ms / 1e3)
+
+    # end to end from pinned host buffers through the same API
+    e2e = None
+    if not args.no_e2e:
+        hc = coords.cpu().pin_memory()
+        hf = f_loc.cpu().pin_memory()
+        hW = W_loc.cpu().pin_memory()
+        hu = torch.empty(u_out.shape, dtype=torch.float32).pin_memory()
+        for _ in range(2):
+            step(hc, hf, hW, hu, False)
+        barrier()
+        t0.record(stream)
+        for _ in range(args.steps):
+            step(hc, hf, hW, hu, False)
+        t1.record(stream)
+        barrier()
+        ems = torch.tensor([t0.elapsed_time(t1) / args.steps], device=dev)
+        if world > 1:
+            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        ems = float(ems.item())
+        h2d = hc.numel() * 4 + hf.numel() * 4 + hW.numel() * 4
+        d2h = hu.numel() * 4 + 5 * 8
+        e2e = {"value": n_alloc_total * iters / (ems / 1e3), "unit": "voxel-updates/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": ems}
+
+    if rank != 0:
+        dist.destroy_process_group()
+        return 0
+
+    peak, peak_src = load_peaks()
+    achieved = ALG_BYTES_PER_VOXEL * n_local_vox / (it_ms / 1e3) / 1e9
+    tr = load_traffic()
+    traffic = None
+    if tr and tr.get("workload") == scene.name and tr.get("kernel") == ("k_fused" if args.kernel == 0 else "k_dual+k_primal"):
+        traffic = tr.get("dram_bytes_per_launch")
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "peak_source": peak_src,
+                "kernel": "k_fused" if args.kernel == 0 else "k_dual+k_primal",
+                "alg_bytes_per_launch": ALG_BYTES_PER_VOXEL * n_local_vox,
+                "avg_launch_ms": it_ms, "frac_of_8TBps": achieved / 8000.0}
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        sc = scene.to("cpu")
+        k = 1
+        t = time_oracle(sc, k)
+        if t < 5.0:
+            k = max(1, int(10.0 / max(t, 1e-3)))
+            t = time_oracle(sc, k)
+        cpu = {"value": sc.n_alloc * k / t, "unit": "voxel-updates/s", "cores": 1, "kind": "oracle",
+               "sample": f"{k} fp64 oracle iteration(s) over the whole {scene.name} volume ({sc.n_alloc} voxels), "
+                         f"{t:.1f} s on one host core"}
+    line = {
+        "metric": "voxel-updates/s", "value": value, "unit": "voxel-updates/s", "n_gpus": world,
+        "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": scene.name, "n_alloc": n_alloc_total, "n_omega": scene.n_omega(),
+                   "blocks": scene.n_blocks, "iters": iters, "lambda": scene.lam, "eps": scene.eps,
+                   "data_term": "L1" if scene.data_term == 0 else "L2",
+                   "step": "vol_create + vol_regularise(init + iters) + vol_energy + vol_read_u",
+                   "l2": f"inputs larger than L2 ({n_alloc_total * 32 / 1e9:.2f} GB of state)",
+                   "parallelism": f"route-axis shards x{world}" if world > 1 else "single GPU",
+                   "energy": {"primal": E[0], "dual": E[1]}},
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,178 @@
+/*
+ * vol.h — C ABI of the B200 hashed-voxel-grid primal-dual TV regulariser (arXiv 1604.03734 §III).
+ *
+ * Citations: P:n = PAPER.md line n (the paper's LaTeX), S:n = SPEC.md line n.  Readings of ambiguous
+ * passages are listed in DESIGN.md ("Readings", SURVEY.md §8(c) c-1 … c-20).
+ *
+ * Data model ("8 voxels in each dimension (512 total)", S:37 x-fastest):
+ *   - a volume is n allocated 8³ blocks with integer block coordinates (x, y, z) (int32);
+ *   - every per-voxel array is [n][512] float32 in the caller's block order, voxel index
+ *     x + 8y + 64z inside a block, global voxel coordinate 8·B + (x, y, z);
+ *   - f is the fused TSDF, W the fusion weight; Ω = {allocated voxels with W > 0}
+ *     (reading c-13); unallocated blocks are Ω̄.
+ *
+ * Pointers: every input/output pointer may be host (pageable or pinned) or device memory; the
+ * library detects which with cudaPointerGetAttributes.  Host outputs are written synchronously
+ * (the call returns after the copy); device outputs are written asynchronously on the handle's
+ * stream.  The library copies every input: the caller may free inputs when the call returns.
+ *
+ * Ownership: the caller owns the optional device workspace passed to vol_create and keeps it
+ * alive until vol_destroy; with workspace == NULL the library allocates (and frees) its own.
+ * A handle is not thread-safe: one host thread and one CUDA stream per handle.
+ *
+ * Errors: every call returns a vol_status; vol_last_error() gives a thread-local message for the
+ * last failing call of the calling thread.  No call ever falls back to a CPU implementation.
+ */
+#ifndef HVG_VOL_H
+#define HVG_VOL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct vol_s *vol_t;
+
+typedef enum {
+    VOL_OK = 0,
+    VOL_EINVAL = 1,  /* usage: bad sizes, bad parameters, NULL handle (S:542 class "usage")          */
+    VOL_EDATA = 2,   /* data: duplicate block coordinates, NaN/Inf in f or W, W < 0, empty Ω */
+    VOL_ENOMEM = 3,  /* workspace too small or device allocation failed (S:542 class "resource")     */
+    VOL_ECUDA = 4,   /* CUDA runtime error (message in vol_last_error)                                */
+    VOL_ENCCL = 5,   /* NCCL error in the sharded path                                                */
+    VOL_ENOTSUP = 6  /* feature not built into this library                                          */
+} vol_status;
+
+/* Solver options.  vol_default_opts() fills the defaults marked (d).                              */
+typedef struct {
+    float theta;     /* over-relaxation θ of Eq. 9 (reading c-3); (d) 1.0 (Table I) */
+    int data_term;   /* 0 (d): W-weighted L1 shrinkage toward f (north_star, TV-L1);
+                        1: W-weighted L2 prox, paper Eq. 8                               */
+    int init;        /* 0 (d): warm start u = ū = f, p = 0; 1: u = ū = 0 on Ω, p = 0 */
+    int resume;      /* 0 (d): initialise before iterating; 1: continue from the current state        */
+    int kernel;      /* 0 (d): fused single-pass kernel (one HBM sweep per iteration);
+                        1: two-kernel baseline (dual kernel, then primal+relax kernel)                */
+} vol_opts;
+
+/* Multi-GPU description (route-axis spatial sharding).  NULL = single GPU.          */
+typedef struct {
+    int rank;               /* this process's rank in [0, world)                                   */
+    int world;              /* number of ranks (one GPU each)                                      */
+    const int32_t *part;    /* [n_global] owner rank of each block (host pointer)                  */
+    const void *nccl_id;    /* 128-byte ncclUniqueId created by rank 0 and broadcast by the caller;
+                               NULL is only valid with world == 1                                   */
+} vol_dist;
+
+/* Defaults for vol_opts (see field comments). */
+void vol_default_opts(vol_opts *opts);
+
+/* Device bytes vol_create needs for a volume of n_global blocks (exact for dist == NULL; for a
+ * sharded volume pass the same dist as to vol_create, the value then covers local + ghost blocks).
+ * block_xyz may be NULL when dist == NULL.  Returns 0 on invalid arguments.                        */
+size_t vol_workspace_bytes(const int32_t *block_xyz, int64_t n_global, const vol_dist *dist);
+
+/* Build a volume:
+ *   block_xyz [n_global][3] int32 block coordinates (host or device), all distinct;
+ *   f, W      [n_local][512] float32 (host or device): the blocks this rank owns, in global order
+ *             (n_local = n_global when dist == NULL); f finite, W finite and >= 0;
+ *   dist      NULL (single GPU) or the sharding description;
+ *   workspace device buffer of >= vol_workspace_bytes(...) bytes, or NULL (library allocates);
+ *   stream    cudaStream_t for every later call on this handle (NULL = legacy default stream).
+ * Builds on the device: the spatial hash h(x,y,z) = ((u32)x·73856093 ⊕ (u32)y·19349669 ⊕
+ * (u32)z·83492791) mod T with T = next power of two >= 2n, a CSR bucket table ordered by caller
+ * index (reading c-14), and the 6-neighbour block table (−x,+x,−y,+y,−z,+z; −1 = unallocated).
+ * Errors: VOL_EINVAL (n_global < 1, NULL pointers), VOL_EDATA (duplicate coordinates — the first
+ * repeated pair is named in vol_last_error —, non-finite f/W, W < 0), VOL_ENOMEM, VOL_ECUDA.     */
+vol_status vol_create(const int32_t *block_xyz, int64_t n_global, const float *f, const float *W,
+                      const vol_dist *dist, void *workspace, size_t workspace_bytes, void *stream,
+                      vol_t *out);
+
+/* Run `iters` Chambolle–Pock iterations (SURVEY §8(a) rows a-2 … a-6):
+ *   dual ascent with Huber damping + projection  q = (p + σ∇_Ω ū)/(1 + σε),  p = q / max(1, ‖q‖₂)
+ *   primal step                                  ũ = u + τ·div_Ω p  (sign: reading c-2)
+ *   data prox (opts->data_term)                  L1: shrink ũ toward f by τλW;  L2: (ũ+τλWf)/(1+τλW)
+ *   over-relaxation                              ū = u' + θ(u' − u),  u = u'
+ * with the Ω-masked forward gradient (Eq. 3) and backward divergence (Eq. 4,
+ * P:252-263) across block faces.  Constraints: λ > 0, ε >= 0, τ > 0, σ > 0, 12·τσ <= 1 + 1e-6
+ * (‖∇_Ω‖² <= 12), iters >= 0 (0 = initialise only unless resuming).  Asynchronous on the handle's
+ * stream.  Errors: VOL_EINVAL (parameters), VOL_EDATA (global Ω empty), VOL_ECUDA/ENCCL.   */
+vol_status vol_regularise(vol_t v, float lambda, float eps, float tau, float sigma, int32_t iters,
+                          const vol_opts *opts);
+
+/* Copy u [n_local][512] float32 in the caller's block order into u_out (host or device);
+ * Ω̄ voxels hold f (they are never written).                                                */
+vol_status vol_read_u(vol_t v, float *u_out);
+
+/* Energy of the current state (Eq. 2, Huber TV, W-weighted data
+ * term, reading c-1), fp64 deterministic reduction over all ranks:
+ *   primal = Σ_Ω H_ε(‖∇_Ω u‖₂) + λ Σ_Ω W|u−f|   (data_term 0)  or  + (λ/2) Σ_Ω W(u−f)²  (1);
+ *   dual   = SURVEY §8(c) dual value at the current p (L1: rescaled to |div p| <= λW); may be NULL.
+ * Synchronous.                                                                                    */
+vol_status vol_energy(vol_t v, float lambda, float eps, int data_term, double *primal, double *dual);
+
+/* State checkpoint: u, ū (current relaxed primal), p = [3][n_local][512] (component-
+ * major).  Any pointer may be NULL to skip it.  vol_load_state sets p = 0 on Ω̄ and ū = u = f there. */
+vol_status vol_read_state(vol_t v, float *u, float *ubar, float *p);
+vol_status vol_load_state(vol_t v, const float *u, const float *ubar, const float *p);
+
+/* Store tables for bit-exact checks (caller indices; single-GPU volumes only):
+ *   *T; bucket_start [T+1] uint32; bucket_entry [n] int32; nbr [n][6] int32.  Pointers may be NULL. */
+vol_status vol_read_tables(vol_t v, uint32_t *T, uint32_t *bucket_start, int32_t *bucket_entry,
+                           int32_t *nbr);
+
+/* Sizes: allocated blocks on this rank, ghost blocks held, total Ω voxels on this rank.           */
+vol_status vol_info(vol_t v, int64_t *n_local, int64_t *n_ghost, int64_t *n_omega);
+
+/* Number of kernel launches the last vol_regularise issued (counted on the host; graph nodes count). */
+int64_t vol_last_launches(vol_t v);
+
+/* Kernels launched by this library in this process so far (graph replays count every node). */
+int64_t vol_total_launches(void);
+
+/* Block until all work on the handle's stream is done. */
+vol_status vol_sync(vol_t v);
+
+void vol_destroy(vol_t v);
+
+/* Thread-local message of the last error ("" if none). */
+const char *vol_last_error(void);
+
+/* Sharded volumes ----------------------------------------------------------------
+ * NCCL transport: rank 0 calls vol_nccl_unique_id, the caller broadcasts the 128 bytes (e.g. with
+ * torch.distributed), every rank passes them in dist->nccl_id to vol_create (collective: all ranks
+ * call vol_create, vol_regularise and vol_energy together).  Per iteration each rank exchanges one
+ * message per neighbouring rank (ū, p of the ghost blocks) with ncclSend/ncclRecv, overlapped with
+ * the interior blocks.
+ * Loopback transport (tests on one GPU): `world` handles created in one process with
+ * dist->nccl_id == NULL; vol_group_connect exchanges the static ghost data once, then
+ * vol_regularise_group / vol_group_energy run the same plan, pack/unpack and two-launch schedule
+ * with device-to-device copies, on handles[0]'s stream.  The result equals the single-GPU result
+ * bit for bit.                                                                                   */
+vol_status vol_nccl_unique_id(void *out128);
+vol_status vol_group_connect(vol_t *handles, int world);
+vol_status vol_regularise_group(vol_t *handles, int world, float lambda, float eps, float tau, float sigma,
+                                int32_t iters, const vol_opts *opts);
+vol_status vol_group_energy(vol_t *handles, int world, float lambda, float eps, int data_term, double *primal,
+                            double *dual);
+
+/* Host-only helpers (no GPU needed), used by the sharding planner tests -------------------------- */
+
+/* The block hash of vol_create (no device work). */
+uint32_t vol_block_hash(int32_t x, int32_t y, int32_t z, uint32_t T);
+
+/* Shard plan of `rank`: counts of local blocks, ghost blocks, and per-peer send /
+ * receive block counts.  Fills ghost_global [n_ghost] (global indices of ghost blocks, receive
+ * order), send_global [n_send] (global indices of local blocks sent, grouped by peer in rank order)
+ * and peer_send / peer_recv [world] (blocks sent to / received from each peer) when non-NULL.
+ * Call with NULL arrays first to get the sizes.  Returns VOL_OK or VOL_EINVAL/VOL_EDATA.          */
+vol_status vol_plan_shard(const int32_t *block_xyz, int64_t n_global, const int32_t *part, int world,
+                          int rank, int64_t *n_local, int64_t *n_ghost, int64_t *n_send,
+                          int64_t *ghost_global, int64_t *send_global, int64_t *peer_send,
+                          int64_t *peer_recv);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HVG_VOL_H */

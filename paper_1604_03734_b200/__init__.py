@@ -1,0 +1,8 @@
+"""B200-native hashed-voxel-grid primal-dual TV regulariser (arXiv 1604.03734 §III-B/C).
+
+The product path is libvol.so (C ABI in include/vol.h, CUDA kernels for sm_100a in csrc/);
+this package is its thin Python binding.  It never imports the CPU oracle and has no CPU fallback.
+"""
+from .volume import Volume, block_hash, connect_group, group_energy, nccl_unique_id, plan_shard, regularise_group  # noqa: F401
+
+__all__ = ["Volume", "block_hash", "plan_shard", "nccl_unique_id", "connect_group", "regularise_group", "group_energy"]

@@ -1,0 +1,94 @@
+// handle.h — the opaque vol_s handle and host helpers shared by vol_api.cu and shard.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdarg.h>
+
+#include <string>
+
+#include "../../include/vol.h"
+#include "internal.h"
+
+struct ShardRuntime;
+
+// ------------------------------------------------------------------------------ error reporting
+
+vol_status fail(vol_status st, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+
+#define CK(call)                                                                                    \
+    do {                                                                                            \
+        cudaError_t e_ = (call);                                                                    \
+        if (e_ != cudaSuccess)                                                                      \
+            return fail(e_ == cudaErrorMemoryAllocation ? VOL_ENOMEM : VOL_ECUDA, "%s: %s (%s:%d)", \
+                        #call, cudaGetErrorString(e_), __FILE__, __LINE__);                         \
+    } while (0)
+
+#define CKL(n)                                                                                 \
+    do {                                                                                       \
+        if ((n) < 0) {                                                                         \
+            cudaError_t e_ = cudaGetLastError();                                               \
+            return fail(VOL_ECUDA, "kernel launch failed: %s (%s:%d)", cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                                   \
+        }                                                                                      \
+    } while (0)
+
+// ------------------------------------------------------------------------------ workspace carving
+struct Carve {
+    size_t off = 0;
+    char *base = nullptr;
+    template <class T>
+    T *take(size_t count) {
+        off = (off + 255) & ~(size_t)255;
+        T *p = base ? reinterpret_cast<T *>(base + off) : nullptr;
+        off += count * sizeof(T);
+        return p;
+    }
+};
+
+struct Layout {
+    int64_t S, n_global, n_local;
+    uint32_t T;
+};
+
+struct vol_s {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaStream_t cap = nullptr;  // private stream used only for graph capture
+    bool owns_ws = false;
+    void *ws = nullptr;
+    size_t ws_bytes = 0;
+    Layout L{};
+    hvg::Fields F{};
+    int cur = 0;
+    bool initialised = false;
+    int64_t n_omega_local = 0, n_omega_global = 0;
+    int32_t *d_xyz = nullptr;          // [n_global][3]
+    uint32_t *d_hash = nullptr;        // [n_global]
+    uint32_t *d_count = nullptr;       // [T]
+    uint32_t *d_start = nullptr;       // [T+1]
+    int32_t *d_entry = nullptr;        // [n_global]
+    uint32_t *d_scan = nullptr;        // scan scratch
+    int32_t *d_nbr = nullptr;          // [S][6] store indices
+    int32_t *d_work = nullptr;         // [S] topological work list
+    uint8_t *d_mode = nullptr;         // [S]
+    uint32_t *d_flags = nullptr;       // [S]
+    uint32_t *d_ticket = nullptr;      // [1]
+    unsigned long long *d_misc = nullptr;  // [4]: dup, bad, n_omega, spare
+    double *d_part = nullptr;          // [S][5]
+    double *d_eout = nullptr;          // [8]
+    int64_t n_work = 0;
+    int64_t last_launches = 0;
+    // sharded state (world > 1)
+    ShardRuntime *shard = nullptr;
+    char *extra = nullptr;             // workspace tail for the sharded runtime
+    hvg::IterParams pending{};         // parameters of the current vol_regularise call
+    int pending_kernel = 0;
+};
+
+// Validates the parameters, fills v->pending, initialises the state unless opts->resume.
+vol_status vol_regularise_prepare(vol_s *v, float lambda, float eps, float tau, float sigma, int32_t iters,
+                                  const vol_opts *opts);
+// Dual value from the five reduced energy terms (see energy.cu).
+double energy_dual_value(const double *o, float eps, int data_term);
+
+bool is_device_ptr(const void *p);

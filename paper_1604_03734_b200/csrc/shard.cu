@@ -1,0 +1,597 @@
+// shard.cu — route-axis spatial sharding across GPUs (north_star (c)).
+//
+// Every rank holds the blocks it owns (caller-supplied owner map `part`, contiguous ranges along the
+// route arc length) plus ghost copies of the remote blocks its stencils touch:
+//   G−  remote −x/−y/−z face neighbours of local blocks.  A local primal step needs their p^{k+1};
+//       instead of waiting for the owner mid-iteration, the rank recomputes their dual step from
+//       ū^k, p^k, W (same device function, so bit-identical to the owner's result);
+//   G+  remote +x/+y/+z face neighbours of local blocks and of G− blocks (ū^k and W read by duals).
+// Per iteration, one message per peer carries ū^k, p_x, p_y, p_z of the ghost blocks (W once at
+// set-up).  The iteration is split into two launches of the fused kernel:
+//   A: every local block whose dual needs no ghost data (dual; primal too if its −neighbours are
+//      all in A) — runs while the halo exchange is in flight;
+//   B: G− ghost duals, the duals of local blocks with a remote +neighbour, and the remaining
+//      primal steps — after the halo has landed.
+// Both lists are in topological order and every wait of a B item is on an A item or an earlier B
+// item, so the per-block counters of iterate.cu stay deadlock free.  The result is bitwise equal
+// to the single-GPU result (no reduction crosses GPUs inside the iteration).
+// Transports: NCCL point-to-point (ncclSend/ncclRecv in one group, on a communication stream that
+// overlaps launch A) or, for tests on one GPU, a loopback of device-to-device copies between handles
+// of one process (vol_group_connect / vol_regularise_group).
+#include <nccl.h>
+
+#include <algorithm>
+#include <numeric>
+#include <unordered_map>
+#include <unordered_set>
+#include <vector>
+
+#include "handle.h"
+#include "shard.h"
+
+using namespace hvg;
+
+// ------------------------------------------------------------------------------ host planning
+
+void hvg::topo_sort_rows(const int32_t *xyz, const std::vector<int64_t> &g, std::vector<int32_t> &rows) {
+    rows.resize(g.size());
+    std::iota(rows.begin(), rows.end(), 0);
+    std::sort(rows.begin(), rows.end(), [&](int32_t a, int32_t b) {
+        const int32_t *A = xyz + 3 * g[a], *B = xyz + 3 * g[b];
+        int64_t sa = (int64_t)A[0] + A[1] + A[2], sb = (int64_t)B[0] + B[1] + B[2];
+        if (sa != sb) return sa < sb;
+        if (A[0] != B[0]) return A[0] < B[0];
+        if (A[1] != B[1]) return A[1] < B[1];
+        return A[2] < B[2];
+    });
+}
+
+namespace {
+struct Key {
+    int32_t x, y, z;
+    bool operator==(const Key &o) const { return x == o.x && y == o.y && z == o.z; }
+};
+struct KeyHash {
+    size_t operator()(const Key &k) const {
+        uint64_t h = (uint64_t)(uint32_t)k.x * 0x9E3779B97F4A7C15ull;
+        h ^= (uint64_t)(uint32_t)k.y * 0xC2B2AE3D27D4EB4Full + (h << 6) + (h >> 2);
+        h ^= (uint64_t)(uint32_t)k.z * 0x165667B19E3779F9ull + (h << 6) + (h >> 2);
+        return (size_t)h;
+    }
+};
+}  // namespace
+
+bool hvg::make_shard_plan(const int32_t *xyz, int64_t n, const int32_t *part, int world, int rank, ShardPlan &P) {
+    P = ShardPlan();
+    P.rank = rank;
+    P.world = world;
+    if (world < 1 || rank < 0 || rank >= world || n < 1 || !xyz || !part) {
+        P.error = "bad arguments";
+        return false;
+    }
+    std::unordered_map<Key, int64_t, KeyHash> idx;
+    idx.reserve((size_t)n * 2);
+    for (int64_t g = 0; g < n; g++) {
+        if (part[g] < 0 || part[g] >= world) {
+            P.error = "part[" + std::to_string(g) + "] out of range";
+            return false;
+        }
+        if (!idx.emplace(Key{xyz[3 * g], xyz[3 * g + 1], xyz[3 * g + 2]}, g).second) {
+            P.error = "duplicate block coordinates at block " + std::to_string(g);
+            return false;
+        }
+    }
+    auto nb = [&](int64_t g, int d) -> int64_t {
+        Key k{xyz[3 * g], xyz[3 * g + 1], xyz[3 * g + 2]};
+        int32_t *c = d < 2 ? &k.x : (d < 4 ? &k.y : &k.z);
+        *c += (d & 1) ? 1 : -1;
+        auto it = idx.find(k);
+        return it == idx.end() ? -1 : it->second;
+    };
+    // ghost sets of every rank (each rank's send lists are other ranks' ghost sets)
+    std::vector<std::vector<int64_t>> gm(world), gp(world);
+    for (int64_t g = 0; g < n; g++) {
+        const int q = part[g];
+        for (int d = 0; d < 6; d++) {
+            int64_t c = nb(g, d);
+            if (c >= 0 && part[c] != q) ((d & 1) ? gp : gm)[q].push_back(c);
+        }
+    }
+    for (int q = 0; q < world; q++) {
+        std::sort(gm[q].begin(), gm[q].end());
+        gm[q].erase(std::unique(gm[q].begin(), gm[q].end()), gm[q].end());
+        for (int64_t c : gm[q])
+            for (int d = 1; d < 6; d += 2) {
+                int64_t c2 = nb(c, d);
+                if (c2 >= 0 && part[c2] != q) gp[q].push_back(c2);
+            }
+        std::sort(gp[q].begin(), gp[q].end());
+        gp[q].erase(std::unique(gp[q].begin(), gp[q].end()), gp[q].end());
+    }
+    auto ghosts_of = [&](int q) {
+        std::vector<int64_t> all(gm[q]);
+        all.insert(all.end(), gp[q].begin(), gp[q].end());
+        std::sort(all.begin(), all.end(), [&](int64_t a, int64_t b) {
+            return part[a] != part[b] ? part[a] < part[b] : a < b;
+        });
+        all.erase(std::unique(all.begin(), all.end()), all.end());
+        return all;
+    };
+    for (int64_t g = 0; g < n; g++)
+        if (part[g] == rank) P.local.push_back(g);
+    P.ghost = ghosts_of(rank);
+    std::unordered_set<int64_t> gmset(gm[rank].begin(), gm[rank].end());
+    P.ghost_dual.resize(P.ghost.size());
+    for (size_t k = 0; k < P.ghost.size(); k++) P.ghost_dual[k] = gmset.count(P.ghost[k]) ? 1 : 0;
+    P.recv_off.assign(world, 0);
+    P.recv_cnt.assign(world, 0);
+    for (size_t k = 0; k < P.ghost.size(); k++) P.recv_cnt[part[P.ghost[k]]]++;
+    for (int q = 1; q < world; q++) P.recv_off[q] = P.recv_off[q - 1] + P.recv_cnt[q - 1];
+    // store row of each global block held here
+    std::unordered_map<int64_t, int64_t> row;
+    for (size_t r = 0; r < P.local.size(); r++) row[P.local[r]] = (int64_t)r;
+    for (size_t k = 0; k < P.ghost.size(); k++) row[P.ghost[k]] = (int64_t)(P.local.size() + k);
+    // send lists: what each peer's ghost set holds of ours, in that peer's receive order
+    P.send_off.assign(world, 0);
+    P.send_cnt.assign(world, 0);
+    for (int q = 0; q < world; q++) {
+        P.send_off[q] = (int64_t)P.send_rows.size();
+        if (q == rank) continue;
+        for (int64_t c : ghosts_of(q))
+            if (part[c] == rank) P.send_rows.push_back(row.at(c));
+        P.send_cnt[q] = (int64_t)P.send_rows.size() - P.send_off[q];
+    }
+    // two-launch schedule
+    const int64_t nl = (int64_t)P.local.size();
+    std::vector<uint8_t> remote_plus(nl, 0), in_pb(nl, 0);
+    for (int64_t r = 0; r < nl; r++)
+        for (int d = 1; d < 6; d += 2) {
+            int64_t c = nb(P.local[r], d);
+            if (c >= 0 && part[c] != rank) remote_plus[r] = 1;
+        }
+    for (int64_t r = 0; r < nl; r++) {
+        if (remote_plus[r]) {
+            in_pb[r] = 1;
+            continue;
+        }
+        for (int d = 0; d < 6; d += 2) {
+            int64_t c = nb(P.local[r], d);
+            if (c < 0) continue;
+            if (part[c] != rank || remote_plus[row.at(c)]) in_pb[r] = 1;
+        }
+    }
+    std::vector<int64_t> ga, gb;
+    std::vector<uint8_t> ma, mb;
+    std::vector<int64_t> ra, rb;  // store rows
+    for (int64_t r = 0; r < nl; r++) {
+        if (!remote_plus[r]) {
+            ra.push_back(r);
+            ma.push_back(in_pb[r] ? MODE_DUAL : MODE_FULL);
+            if (in_pb[r]) {
+                rb.push_back(r);
+                mb.push_back(MODE_PRIMAL);
+            }
+        } else {
+            rb.push_back(r);
+            mb.push_back(MODE_FULL);
+        }
+    }
+    for (size_t k = 0; k < P.ghost.size(); k++)
+        if (P.ghost_dual[k]) {
+            rb.push_back(nl + (int64_t)k);
+            mb.push_back(MODE_DUAL);
+        }
+    auto global_of = [&](int64_t r) { return r < nl ? P.local[r] : P.ghost[r - nl]; };
+    for (auto pr : {std::make_pair(&ra, &ma), std::make_pair(&rb, &mb)}) {
+        std::vector<int64_t> gl(pr.first->size());
+        for (size_t k = 0; k < gl.size(); k++) gl[k] = global_of((*pr.first)[k]);
+        std::vector<int32_t> ord;
+        topo_sort_rows(xyz, gl, ord);
+        std::vector<int32_t> w(ord.size());
+        std::vector<uint8_t> m(ord.size());
+        for (size_t k = 0; k < ord.size(); k++) {
+            w[k] = (int32_t)(*pr.first)[ord[k]];
+            m[k] = (*pr.second)[ord[k]];
+        }
+        if (pr.first == &ra) {
+            P.workA = w;
+            P.modeA = m;
+        } else {
+            P.workB = w;
+            P.modeB = m;
+        }
+    }
+    return true;
+}
+
+extern "C" vol_status vol_plan_shard(const int32_t *xyz, int64_t n, const int32_t *part, int world, int rank,
+                                     int64_t *n_local, int64_t *n_ghost, int64_t *n_send, int64_t *ghost_global,
+                                     int64_t *send_global, int64_t *peer_send, int64_t *peer_recv) {
+    ShardPlan P;
+    if (!make_shard_plan(xyz, n, part, world, rank, P)) return fail(VOL_EINVAL, "vol_plan_shard: %s", P.error.c_str());
+    if (n_local) *n_local = P.n_local();
+    if (n_ghost) *n_ghost = P.n_ghost();
+    if (n_send) *n_send = (int64_t)P.send_rows.size();
+    if (ghost_global) std::copy(P.ghost.begin(), P.ghost.end(), ghost_global);
+    if (send_global)
+        for (size_t k = 0; k < P.send_rows.size(); k++) send_global[k] = P.local[P.send_rows[k]];
+    if (peer_send) std::copy(P.send_cnt.begin(), P.send_cnt.end(), peer_send);
+    if (peer_recv) std::copy(P.recv_cnt.begin(), P.recv_cnt.end(), peer_recv);
+    return VOL_OK;
+}
+
+// ------------------------------------------------------------------------------ device runtime
+
+constexpr int64_t kMsgFloats = 4 * kBlockVox;  // ū (or W), p_x (or f), p_y, p_z per block
+
+struct ShardRuntime {
+    ShardPlan plan;
+    bool nccl = false;
+    ncclComm_t comm = nullptr;
+    cudaStream_t cs = nullptr;       // communication stream
+    cudaEvent_t ev_pack = nullptr, ev_halo = nullptr;
+    float *sendbuf = nullptr, *recvbuf = nullptr;
+    int32_t *send_rows = nullptr;
+    int32_t *workA = nullptr, *workB = nullptr;
+    uint8_t *modeA = nullptr, *modeB = nullptr;
+    unsigned long long *omega = nullptr;  // [2] device scratch for the Ω count all-reduce
+    bool connected = false;
+};
+
+size_t hvg::shard_extra_bytes(const ShardPlan &P) {
+    Carve c;
+    c.take<float>((size_t)P.send_rows.size() * kMsgFloats + 4);
+    c.take<float>((size_t)P.ghost.size() * kMsgFloats + 4);
+    c.take<int32_t>(P.send_rows.size() + 1);
+    c.take<int32_t>(P.workA.size() + 1);
+    c.take<int32_t>(P.workB.size() + 1);
+    c.take<uint8_t>(P.modeA.size() + 1);
+    c.take<uint8_t>(P.modeB.size() + 1);
+    c.take<unsigned long long>(4);
+    return c.off + 512;
+}
+
+__global__ void k_pack(const int32_t *__restrict__ rows, const float *a, const float *b, const float *c,
+                       const float *d, float *__restrict__ buf) {
+    const int64_t r = rows[blockIdx.x];
+    const float *src[4] = {a, b, c, d};
+    float4 *dst = reinterpret_cast<float4 *>(buf + (int64_t)blockIdx.x * kMsgFloats);
+#pragma unroll
+    for (int f = 0; f < 4; f++) {
+        const float4 *s = reinterpret_cast<const float4 *>(src[f] + r * kBlockVox);
+        dst[f * 128 + threadIdx.x] = s[threadIdx.x];
+    }
+}
+
+__global__ void k_unpack(int64_t first_row, const float *__restrict__ buf, float *a, float *b, float *c, float *d) {
+    const int64_t r = first_row + blockIdx.x;
+    float *dst[4] = {a, b, c, d};
+    const float4 *src = reinterpret_cast<const float4 *>(buf + (int64_t)blockIdx.x * kMsgFloats);
+#pragma unroll
+    for (int f = 0; f < 4; f++) reinterpret_cast<float4 *>(dst[f] + r * kBlockVox)[threadIdx.x] = src[f * 128 + threadIdx.x];
+}
+
+static vol_status pack(vol_s *v, const float *a, const float *b, const float *c, const float *d, cudaStream_t s) {
+    ShardRuntime *R = v->shard;
+    const int64_t n = (int64_t)R->plan.send_rows.size();
+    if (n > 0) {
+        k_pack<<<(unsigned)n, 128, 0, s>>>(R->send_rows, a, b, c, d, R->sendbuf);
+        counted(1);
+    }
+    CK(cudaPeekAtLastError());
+    return VOL_OK;
+}
+
+static vol_status unpack(vol_s *v, float *a, float *b, float *c, float *d, cudaStream_t s) {
+    ShardRuntime *R = v->shard;
+    const int64_t n = R->plan.n_ghost();
+    if (n > 0) {
+        k_unpack<<<(unsigned)n, 128, 0, s>>>(R->plan.n_local(), R->recvbuf, a, b, c, d);
+        counted(1);
+    }
+    CK(cudaPeekAtLastError());
+    return VOL_OK;
+}
+
+#define NCK(call)                                                                                      \
+    do {                                                                                               \
+        ncclResult_t r_ = (call);                                                                      \
+        if (r_ != ncclSuccess) return fail(VOL_ENCCL, "%s: %s (%s:%d)", #call, ncclGetErrorString(r_), \
+                                           __FILE__, __LINE__);                                        \
+    } while (0)
+
+static vol_status nccl_exchange(vol_s *v, cudaStream_t s) {
+    ShardRuntime *R = v->shard;
+    const ShardPlan &P = R->plan;
+    NCK(ncclGroupStart());
+    for (int q = 0; q < P.world; q++) {
+        if (q == P.rank) continue;
+        if (P.send_cnt[q] > 0)
+            NCK(ncclSend(R->sendbuf + P.send_off[q] * kMsgFloats, (size_t)(P.send_cnt[q] * kMsgFloats), ncclFloat, q,
+                         R->comm, s));
+        if (P.recv_cnt[q] > 0)
+            NCK(ncclRecv(R->recvbuf + P.recv_off[q] * kMsgFloats, (size_t)(P.recv_cnt[q] * kMsgFloats), ncclFloat, q,
+                         R->comm, s));
+    }
+    NCK(ncclGroupEnd());
+    return VOL_OK;
+}
+
+extern "C" vol_status vol_nccl_unique_id(void *out128) {
+    if (!out128) return fail(VOL_EINVAL, "vol_nccl_unique_id: NULL");
+    ncclUniqueId id;
+    NCK(ncclGetUniqueId(&id));
+    memcpy(out128, &id, sizeof id);
+    return VOL_OK;
+}
+
+vol_status shard_setup(vol_s *v, const ShardPlan &plan, const int32_t *hxyz, const vol_dist *dist,
+                       std::vector<int32_t> &work) {
+    (void)hxyz;
+    work.clear();
+    ShardRuntime *R = new ShardRuntime();
+    v->shard = R;
+    R->plan = plan;
+    const ShardPlan &P = R->plan;
+    cudaStream_t s = v->stream;
+    Carve c;
+    c.base = v->extra;
+    R->sendbuf = c.take<float>((size_t)P.send_rows.size() * kMsgFloats + 4);
+    R->recvbuf = c.take<float>((size_t)P.ghost.size() * kMsgFloats + 4);
+    R->send_rows = c.take<int32_t>(P.send_rows.size() + 1);
+    R->workA = c.take<int32_t>(P.workA.size() + 1);
+    R->workB = c.take<int32_t>(P.workB.size() + 1);
+    R->modeA = c.take<uint8_t>(P.modeA.size() + 1);
+    R->modeB = c.take<uint8_t>(P.modeB.size() + 1);
+    R->omega = c.take<unsigned long long>(4);
+    // neighbour table in store rows: global → store row map (reuses the hash scratch) and row → global
+    const int64_t n = v->L.n_global, S = v->L.S;
+    std::vector<int32_t> store_of_global(n, -1);
+    std::vector<int64_t> global_of_row(S);
+    for (int64_t r = 0; r < P.n_local(); r++) {
+        store_of_global[P.local[r]] = (int32_t)r;
+        global_of_row[r] = P.local[r];
+    }
+    for (int64_t k = 0; k < P.n_ghost(); k++) {
+        store_of_global[P.ghost[k]] = (int32_t)(P.n_local() + k);
+        global_of_row[P.n_local() + k] = P.ghost[k];
+    }
+    std::vector<int32_t> send32(P.send_rows.begin(), P.send_rows.end());
+    int32_t *d_sog = reinterpret_cast<int32_t *>(v->d_hash);
+    int64_t *d_rows = reinterpret_cast<int64_t *>(v->d_part);
+    CK(cudaMemcpyAsync(d_sog, store_of_global.data(), n * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d_rows, global_of_row.data(), S * 8, cudaMemcpyHostToDevice, s));
+    CKL(launch_neighbours(v->d_xyz, n, v->d_start, v->d_entry, v->L.T, d_sog, d_rows, S, v->d_nbr, s));
+    CK(cudaMemcpyAsync(R->send_rows, send32.data(), send32.size() * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(R->workA, P.workA.data(), P.workA.size() * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(R->workB, P.workB.data(), P.workB.size() * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(R->modeA, P.modeA.data(), P.modeA.size(), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(R->modeB, P.modeB.data(), P.modeB.size(), cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));  // host vectors go out of scope
+    CK(cudaStreamCreateWithFlags(&R->cs, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&R->ev_pack, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&R->ev_halo, cudaEventDisableTiming));
+    if (dist->nccl_id) {
+        ncclUniqueId id;
+        memcpy(&id, dist->nccl_id, sizeof id);
+        R->nccl = true;
+        NCK(ncclCommInitRank(&R->comm, P.world, id, P.rank));
+    }
+    return VOL_OK;
+}
+
+// Static ghost data (W, f) and the global Ω count.  NCCL: now; loopback: in vol_group_connect.
+vol_status shard_after_create(vol_s *v) {
+    ShardRuntime *R = v->shard;
+    if (!R->nccl) return VOL_OK;
+    cudaStream_t s = v->stream;
+    float *W = const_cast<float *>(v->F.W), *f = const_cast<float *>(v->F.f);
+    vol_status st = pack(v, W, f, W, f, s);
+    if (st != VOL_OK) return st;
+    if ((st = nccl_exchange(v, s)) != VOL_OK) return st;
+    if ((st = unpack(v, W, f, v->F.ub[0], v->F.ub[1], s)) != VOL_OK) return st;
+    CKL(launch_init_state(v->F, v->L.S * kBlockVox, 0, s));
+    unsigned long long cnt = (unsigned long long)v->n_omega_local, tot = 0;
+    CK(cudaMemcpyAsync(R->omega, &cnt, 8, cudaMemcpyHostToDevice, s));
+    NCK(ncclAllReduce(R->omega, R->omega + 1, 1, ncclUint64, ncclSum, R->comm, s));
+    CK(cudaMemcpyAsync(&tot, R->omega + 1, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    v->n_omega_global = (int64_t)tot;
+    R->connected = true;
+    return VOL_OK;
+}
+
+vol_status shard_reset(vol_s *v) {
+    if (!v->shard->connected) return fail(VOL_EINVAL, "sharded volume not connected (call vol_group_connect)");
+    return VOL_OK;
+}
+
+// One sharded iteration on one rank with the NCCL transport.
+static vol_status nccl_iteration(vol_s *v, const IterParams &P, int64_t &launches) {
+    ShardRuntime *R = v->shard;
+    cudaStream_t s = v->stream;
+    const int cur = v->cur;
+    vol_status st = pack(v, v->F.ub[cur], v->F.px, v->F.py, v->F.pz, s);
+    if (st != VOL_OK) return st;
+    CK(cudaEventRecord(R->ev_pack, s));
+    CK(cudaStreamWaitEvent(R->cs, R->ev_pack, 0));
+    if ((st = nccl_exchange(v, R->cs)) != VOL_OK) return st;
+    if ((st = unpack(v, v->F.ub[cur], v->F.px, v->F.py, v->F.pz, R->cs)) != VOL_OK) return st;
+    CK(cudaEventRecord(R->ev_halo, R->cs));
+    int r = launch_fused(v->F, cur, v->d_nbr, R->workA, R->modeA, (int64_t)R->plan.workA.size(), v->d_flags,
+                         v->d_ticket, P, s);
+    CKL(r);
+    CK(cudaStreamWaitEvent(s, R->ev_halo, 0));
+    int r2 = launch_fused(v->F, cur, v->d_nbr, R->workB, R->modeB, (int64_t)R->plan.workB.size(), v->d_flags,
+                          v->d_ticket, P, s);
+    CKL(r2);
+    launches += r + r2 + 2;  // + pack + unpack
+    v->cur ^= 1;
+    return VOL_OK;
+}
+
+vol_status shard_iterate(vol_s *v, const IterParams &P, int32_t iters) {
+    ShardRuntime *R = v->shard;
+    if (!R->nccl) return fail(VOL_EINVAL, "loopback-sharded volume: use vol_regularise_group");
+    int64_t launches = 0;
+    for (int32_t k = 0; k < iters; k++) {
+        vol_status st = nccl_iteration(v, P, launches);
+        if (st != VOL_OK) return st;
+    }
+    v->last_launches = launches;
+    return VOL_OK;
+}
+
+// Refresh every ghost's u and p (energy needs u of +neighbours and p of −neighbours), then the
+// per-rank partial sums are all-reduced (sum of 4 terms, min of the L1 dual scale).
+vol_status shard_refresh_for_energy(vol_s *v) {
+    ShardRuntime *R = v->shard;
+    if (!R->nccl) return VOL_OK;  // loopback: vol_group_energy refreshes
+    cudaStream_t s = v->stream;
+    vol_status st = pack(v, v->F.u, v->F.px, v->F.py, v->F.pz, s);
+    if (st != VOL_OK) return st;
+    if ((st = nccl_exchange(v, s)) != VOL_OK) return st;
+    return unpack(v, v->F.u, v->F.px, v->F.py, v->F.pz, s);
+}
+
+vol_status shard_allreduce_energy(vol_s *v, double *d_eout) {
+    ShardRuntime *R = v->shard;
+    if (!R->nccl) return VOL_OK;
+    NCK(ncclAllReduce(d_eout, d_eout, 4, ncclDouble, ncclSum, R->comm, v->stream));
+    NCK(ncclAllReduce(d_eout + 4, d_eout + 4, 1, ncclDouble, ncclMin, R->comm, v->stream));
+    return VOL_OK;
+}
+
+void shard_destroy(vol_s *v) {
+    ShardRuntime *R = v->shard;
+    if (!R) return;
+    if (v->stream) cudaStreamSynchronize(v->stream);
+    if (R->cs) {
+        cudaStreamSynchronize(R->cs);
+        cudaStreamDestroy(R->cs);
+    }
+    if (R->ev_pack) cudaEventDestroy(R->ev_pack);
+    if (R->ev_halo) cudaEventDestroy(R->ev_halo);
+    if (R->comm) ncclCommDestroy(R->comm);
+    delete R;
+    v->shard = nullptr;
+}
+
+// ------------------------------------------------------------------------- loopback transport
+
+static vol_status loopback_exchange(vol_t *h, int world, cudaStream_t s) {
+    for (int r = 0; r < world; r++) {
+        const ShardPlan &Pr = h[r]->shard->plan;
+        for (int q = 0; q < world; q++) {
+            if (q == r || Pr.send_cnt[q] == 0) continue;
+            const ShardPlan &Pq = h[q]->shard->plan;
+            if (Pq.recv_cnt[r] != Pr.send_cnt[q])
+                return fail(VOL_EINVAL, "loopback: rank %d sends %lld blocks to %d, which expects %lld", r,
+                            (long long)Pr.send_cnt[q], q, (long long)Pq.recv_cnt[r]);
+            CK(cudaMemcpyAsync(h[q]->shard->recvbuf + Pq.recv_off[r] * kMsgFloats,
+                               h[r]->shard->sendbuf + Pr.send_off[q] * kMsgFloats,
+                               (size_t)Pr.send_cnt[q] * kMsgFloats * 4, cudaMemcpyDeviceToDevice, s));
+        }
+    }
+    return VOL_OK;
+}
+
+static vol_status check_group(vol_t *h, int world) {
+    if (!h || world < 2) return fail(VOL_EINVAL, "group: need >= 2 handles");
+    for (int r = 0; r < world; r++) {
+        if (!h[r] || !h[r]->shard) return fail(VOL_EINVAL, "group: handle %d is not sharded", r);
+        if (h[r]->shard->nccl) return fail(VOL_EINVAL, "group: handle %d uses NCCL", r);
+        if (h[r]->shard->plan.rank != r || h[r]->shard->plan.world != world)
+            return fail(VOL_EINVAL, "group: handle %d has rank %d of %d", r, h[r]->shard->plan.rank,
+                        h[r]->shard->plan.world);
+    }
+    return VOL_OK;
+}
+
+extern "C" vol_status vol_group_connect(vol_t *h, int world) {
+    vol_status st = check_group(h, world);
+    if (st != VOL_OK) return st;
+    cudaStream_t s = h[0]->stream;
+    for (int r = 0; r < world; r++) CK(cudaStreamSynchronize(h[r]->stream));
+    for (int r = 0; r < world; r++) {
+        float *W = const_cast<float *>(h[r]->F.W), *f = const_cast<float *>(h[r]->F.f);
+        if ((st = pack(h[r], W, f, W, f, s)) != VOL_OK) return st;
+    }
+    if ((st = loopback_exchange(h, world, s)) != VOL_OK) return st;
+    int64_t tot = 0;
+    for (int r = 0; r < world; r++) {
+        float *W = const_cast<float *>(h[r]->F.W), *f = const_cast<float *>(h[r]->F.f);
+        if ((st = unpack(h[r], W, f, h[r]->F.ub[0], h[r]->F.ub[1], s)) != VOL_OK) return st;
+        CKL(launch_init_state(h[r]->F, h[r]->L.S * kBlockVox, 0, s));
+        tot += h[r]->n_omega_local;
+    }
+    CK(cudaStreamSynchronize(s));
+    for (int r = 0; r < world; r++) {
+        h[r]->n_omega_global = tot;
+        h[r]->shard->connected = true;
+        h[r]->cur = 0;
+    }
+    return VOL_OK;
+}
+
+extern "C" vol_status vol_regularise_group(vol_t *h, int world, float lambda, float eps, float tau, float sigma,
+                                           int32_t iters, const vol_opts *opts) {
+    vol_status st = check_group(h, world);
+    if (st != VOL_OK) return st;
+    for (int r = 0; r < world; r++)
+        if (!h[r]->shard->connected) return fail(VOL_EINVAL, "group: call vol_group_connect first");
+    // parameter validation + initialisation through the single-handle entry with iters = 0
+    for (int r = 0; r < world; r++)
+        if ((st = vol_regularise_prepare(h[r], lambda, eps, tau, sigma, iters, opts)) != VOL_OK) return st;
+    IterParams P = h[0]->pending;
+    cudaStream_t s = h[0]->stream;
+    for (int r = 1; r < world; r++) CK(cudaStreamSynchronize(h[r]->stream));
+    int64_t launches = 0;
+    for (int32_t k = 0; k < iters; k++) {
+        const int cur = h[0]->cur;
+        for (int r = 0; r < world; r++)
+            if ((st = pack(h[r], h[r]->F.ub[cur], h[r]->F.px, h[r]->F.py, h[r]->F.pz, s)) != VOL_OK) return st;
+        if ((st = loopback_exchange(h, world, s)) != VOL_OK) return st;
+        for (int r = 0; r < world; r++) {
+            ShardRuntime *R = h[r]->shard;
+            if ((st = unpack(h[r], h[r]->F.ub[cur], h[r]->F.px, h[r]->F.py, h[r]->F.pz, s)) != VOL_OK) return st;
+            int a = launch_fused(h[r]->F, cur, h[r]->d_nbr, R->workA, R->modeA, (int64_t)R->plan.workA.size(),
+                                 h[r]->d_flags, h[r]->d_ticket, P, s);
+            CKL(a);
+            int b = launch_fused(h[r]->F, cur, h[r]->d_nbr, R->workB, R->modeB, (int64_t)R->plan.workB.size(),
+                                 h[r]->d_flags, h[r]->d_ticket, P, s);
+            CKL(b);
+            launches += a + b + 2;
+        }
+        for (int r = 0; r < world; r++) h[r]->cur ^= 1;
+    }
+    CK(cudaStreamSynchronize(s));
+    for (int r = 0; r < world; r++) h[r]->last_launches = launches;
+    return VOL_OK;
+}
+
+// Energy of a loopback group: refresh ghost u/p, local partial sums, combined on the host.
+extern "C" vol_status vol_group_energy(vol_t *h, int world, float lambda, float eps, int data_term, double *primal,
+                                       double *dual) {
+    vol_status st = check_group(h, world);
+    if (st != VOL_OK) return st;
+    if (!primal) return fail(VOL_EINVAL, "vol_group_energy: primal is NULL");
+    cudaStream_t s = h[0]->stream;
+    for (int r = 0; r < world; r++)
+        if ((st = pack(h[r], h[r]->F.u, h[r]->F.px, h[r]->F.py, h[r]->F.pz, s)) != VOL_OK) return st;
+    if ((st = loopback_exchange(h, world, s)) != VOL_OK) return st;
+    double acc[5] = {0, 0, 0, 0, 1.0};
+    for (int r = 0; r < world; r++) {
+        if ((st = unpack(h[r], h[r]->F.u, h[r]->F.px, h[r]->F.py, h[r]->F.pz, s)) != VOL_OK) return st;
+        CKL(launch_energy(h[r]->F, h[r]->d_nbr, nullptr, h[r]->L.n_local, lambda, eps, data_term, h[r]->d_part,
+                          h[r]->d_eout, s));
+        double o[5];
+        CK(cudaMemcpyAsync(o, h[r]->d_eout, sizeof o, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        for (int k = 0; k < 4; k++) acc[k] += o[k];
+        acc[4] = std::min(acc[4], o[4]);
+    }
+    *primal = acc[0];
+    if (dual) *dual = energy_dual_value(acc, eps, data_term);
+    return VOL_OK;
+}

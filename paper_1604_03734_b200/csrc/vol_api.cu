@@ -1,0 +1,503 @@
+// vol_api.cu — the C ABI of include/vol.h (host runtime: validation, workspace carving, store build
+// orchestration, iteration scheduling with CUDA graphs, read-back, energy).  All arithmetic of the
+// method runs in the kernels of store.cu / iterate.cu / energy.cu; the host only plans and launches.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/vol.h"
+#include "handle.h"
+#include "internal.h"
+#include "shard.h"
+
+using namespace hvg;
+
+std::atomic<long long> hvg::g_launches{0};
+
+extern "C" int64_t vol_total_launches(void) { return (int64_t)g_launches.load(); }
+
+static thread_local std::string g_err;
+
+vol_status fail(vol_status st, const char *fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+extern "C" const char *vol_last_error(void) { return g_err.c_str(); }
+
+extern "C" void vol_default_opts(vol_opts *o) {
+    if (!o) return;
+    o->theta = 1.0f;
+    o->data_term = 0;
+    o->init = 0;
+    o->resume = 0;
+    o->kernel = 0;
+}
+
+extern "C" uint32_t vol_block_hash(int32_t x, int32_t y, int32_t z, uint32_t T) { return host_hash(x, y, z, T); }
+
+static uint32_t table_size(int64_t n) {
+    uint32_t T = 1;
+    while ((int64_t)T < 2 * n) T <<= 1;
+    return T;
+}
+
+bool is_device_ptr(const void *p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+static void carve_all(Carve &c, vol_s *v, const Layout &L) {
+    const int64_t nv = L.S * kBlockVox;
+    float *fields[8];
+    for (int k = 0; k < 8; k++) fields[k] = c.take<float>(nv);
+    if (v) {
+        v->F.f = fields[0];
+        v->F.W = fields[1];
+        v->F.u = fields[2];
+        v->F.ub[0] = fields[3];
+        v->F.ub[1] = fields[4];
+        v->F.px = fields[5];
+        v->F.py = fields[6];
+        v->F.pz = fields[7];
+    }
+    auto xyz = c.take<int32_t>(3 * (size_t)L.n_global + 3);
+    auto hash = c.take<uint32_t>((size_t)L.n_global + 1);
+    auto count = c.take<uint32_t>((size_t)L.T + 1);
+    auto start = c.take<uint32_t>((size_t)L.T + 1);
+    auto entry = c.take<int32_t>((size_t)L.n_global + 1);
+    auto scan = c.take<uint32_t>((size_t)L.T / 4096 + 4);
+    auto nbr = c.take<int32_t>(6 * (size_t)L.S);
+    auto work = c.take<int32_t>((size_t)L.S + 1);
+    auto mode = c.take<uint8_t>((size_t)L.S + 1);
+    auto flags = c.take<uint32_t>((size_t)L.S + 1);
+    auto ticket = c.take<uint32_t>(4);
+    auto misc = c.take<unsigned long long>(4);
+    auto part = c.take<double>(5 * (size_t)L.S + 5);
+    auto eout = c.take<double>(8);
+    if (v) {
+        v->d_xyz = xyz;
+        v->d_hash = hash;
+        v->d_count = count;
+        v->d_start = start;
+        v->d_entry = entry;
+        v->d_scan = scan;
+        v->d_nbr = nbr;
+        v->d_work = work;
+        v->d_mode = mode;
+        v->d_flags = flags;
+        v->d_ticket = ticket;
+        v->d_misc = misc;
+        v->d_part = part;
+        v->d_eout = eout;
+    }
+}
+
+static size_t layout_bytes(const Layout &L) {
+    Carve c;
+    carve_all(c, nullptr, L);
+    return c.off + 512;
+}
+
+extern "C" size_t vol_workspace_bytes(const int32_t *block_xyz, int64_t n_global, const vol_dist *dist) {
+    if (n_global < 1) return 0;
+    Layout L{};
+    L.n_global = n_global;
+    L.T = table_size(n_global);
+    if (!dist || dist->world <= 1) {
+        L.S = n_global;
+        L.n_local = n_global;
+        return layout_bytes(L);
+    }
+    if (!block_xyz || !dist->part) return 0;
+    ShardPlan plan;
+    if (!make_shard_plan(block_xyz, n_global, dist->part, dist->world, dist->rank, plan)) return 0;
+    L.n_local = plan.n_local();
+    L.S = plan.n_local() + plan.n_ghost();
+    return layout_bytes(L) + shard_extra_bytes(plan);
+}
+
+static vol_status copy_in(void *dst, const void *src, size_t bytes, cudaStream_t s) {
+    CK(cudaMemcpyAsync(dst, src, bytes, is_device_ptr(src) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    return VOL_OK;
+}
+
+extern "C" vol_status vol_create(const int32_t *block_xyz, int64_t n_global, const float *f, const float *W,
+                                 const vol_dist *dist, void *workspace, size_t workspace_bytes, void *stream,
+                                 vol_t *out) {
+    if (!out) return fail(VOL_EINVAL, "vol_create: out is NULL");
+    *out = nullptr;
+    if (n_global < 1) return fail(VOL_EINVAL, "vol_create: n_global must be >= 1 (got %lld)", (long long)n_global);
+    if (n_global > (int64_t)1 << 30) return fail(VOL_EINVAL, "vol_create: n_global too large");
+    if (!block_xyz || !f || !W) return fail(VOL_EINVAL, "vol_create: NULL input pointer");
+    const bool sharded = dist && dist->world > 1;
+    if (dist && (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world))
+        return fail(VOL_EINVAL, "vol_create: bad rank/world");
+    if (sharded && !dist->part) return fail(VOL_EINVAL, "vol_create: dist->part is NULL");
+
+    vol_s *v = new vol_s();
+    auto bail = [&](vol_status st) {
+        vol_destroy(v);
+        return st;
+    };
+    CK(cudaGetDevice(&v->device));
+    v->stream = (cudaStream_t)stream;
+    if (cudaStreamCreateWithFlags(&v->cap, cudaStreamNonBlocking) != cudaSuccess)
+        return bail(fail(VOL_ECUDA, "cudaStreamCreate failed"));
+
+    // host copy of the coordinates (the work order and the shard plan are host-side schedules)
+    std::vector<int32_t> hxyz(3 * (size_t)n_global);
+    if (is_device_ptr(block_xyz)) {
+        if (cudaMemcpy(hxyz.data(), block_xyz, hxyz.size() * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
+            return bail(fail(VOL_ECUDA, "copy of block_xyz failed"));
+    } else {
+        memcpy(hxyz.data(), block_xyz, hxyz.size() * 4);
+    }
+
+    ShardPlan plan;
+    Layout L{};
+    L.n_global = n_global;
+    L.T = table_size(n_global);
+    if (sharded) {
+        if (!make_shard_plan(hxyz.data(), n_global, dist->part, dist->world, dist->rank, plan))
+            return bail(fail(VOL_EDATA, "vol_create: shard plan failed: %s", plan.error.c_str()));
+        L.n_local = plan.n_local();
+        L.S = plan.n_local() + plan.n_ghost();
+    } else {
+        L.n_local = n_global;
+        L.S = n_global;
+    }
+    v->L = L;
+    size_t need = layout_bytes(L) + (sharded ? shard_extra_bytes(plan) : 0);
+    if (workspace) {
+        if (workspace_bytes < need)
+            return bail(fail(VOL_ENOMEM, "vol_create: workspace %zu bytes < %zu needed", workspace_bytes, need));
+        v->ws = workspace;
+        v->ws_bytes = workspace_bytes;
+    } else {
+        cudaError_t e = cudaMalloc(&v->ws, need);
+        if (e != cudaSuccess) return bail(fail(VOL_ENOMEM, "cudaMalloc(%zu) failed: %s", need, cudaGetErrorString(e)));
+        v->owns_ws = true;
+        v->ws_bytes = need;
+    }
+    Carve c;
+    c.base = (char *)(((uintptr_t)v->ws + 255) & ~(uintptr_t)255);
+    carve_all(c, v, L);
+    v->extra = c.base + ((c.off + 255) & ~(size_t)255);
+    cudaStream_t s = v->stream;
+
+    // inputs
+    vol_status st;
+    if ((st = copy_in(v->d_xyz, block_xyz, 3 * (size_t)n_global * 4, s)) != VOL_OK) return bail(st);
+    const size_t fbytes = (size_t)L.n_local * kBlockVox * 4;
+    if ((st = copy_in((void *)v->F.f, f, fbytes, s)) != VOL_OK) return bail(st);
+    if ((st = copy_in((void *)v->F.W, W, fbytes, s)) != VOL_OK) return bail(st);
+
+    // K1: hash + CSR bucket table over all n_global blocks
+    if (cudaMemsetAsync(v->d_count, 0, ((size_t)L.T + 1) * 4, s) != cudaSuccess ||
+        cudaMemsetAsync(v->d_misc, 0, 4 * 8, s) != cudaSuccess ||
+        cudaMemsetAsync(v->d_misc, 0xFF, 2 * 8, s) != cudaSuccess)
+        return bail(fail(VOL_ECUDA, "memset failed"));
+    int nl = 0;
+    if ((nl = launch_hash_count(v->d_xyz, n_global, L.T, v->d_hash, v->d_count, s)) < 0 ||
+        (nl = launch_exclusive_scan_u32(v->d_count, v->d_start, L.T, v->d_scan, s)) < 0)
+        return bail(fail(VOL_ECUDA, "store build launch failed: %s", cudaGetErrorString(cudaGetLastError())));
+    if (cudaMemcpyAsync(v->d_count, v->d_start, (size_t)L.T * 4, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+        return bail(fail(VOL_ECUDA, "cursor copy failed"));
+    if ((nl = launch_bucket_fill(v->d_hash, n_global, v->d_count, v->d_entry, s)) < 0 ||
+        (nl = launch_bucket_sort_and_dups(v->d_xyz, v->d_start, v->d_entry, L.T, n_global, &v->d_misc[0], s)) < 0 ||
+        (nl = launch_validate(v->F.f, v->F.W, (int64_t)L.n_local * kBlockVox, &v->d_misc[1], &v->d_misc[2], s)) < 0)
+        return bail(fail(VOL_ECUDA, "store build launch failed: %s", cudaGetErrorString(cudaGetLastError())));
+    unsigned long long misc[3];
+    if (cudaMemcpyAsync(misc, v->d_misc, 3 * 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+        return bail(fail(VOL_ECUDA, "store build failed: %s", cudaGetErrorString(cudaGetLastError())));
+    if (misc[0] != ~0ULL) {
+        long long i = (long long)(misc[0] >> 32), j = (long long)(misc[0] & 0xFFFFFFFFu);
+        return bail(fail(VOL_EDATA, "duplicate block coordinates: blocks %lld and %lld are both (%d, %d, %d)", j, i,
+                         hxyz[3 * i], hxyz[3 * i + 1], hxyz[3 * i + 2]));
+    }
+    if (misc[1] != ~0ULL) {
+        long long i = (long long)misc[1];
+        return bail(fail(VOL_EDATA, "invalid input at local voxel %lld (block %lld, voxel %lld): f must be finite, "
+                                    "W finite and >= 0",
+                         i, i / kBlockVox, i % kBlockVox));
+    }
+    v->n_omega_local = (int64_t)misc[2];
+    v->n_omega_global = v->n_omega_local;
+
+    // K2: neighbour table (store indices) + work list
+    std::vector<int32_t> work;
+    if (!sharded) {
+        if (launch_neighbours(v->d_xyz, n_global, v->d_start, v->d_entry, L.T, nullptr, nullptr, n_global, v->d_nbr,
+                              s) < 0)
+            return bail(fail(VOL_ECUDA, "neighbour launch failed"));
+        std::vector<int64_t> rows(n_global);
+        std::iota(rows.begin(), rows.end(), 0);
+        topo_sort_rows(hxyz.data(), rows, work);
+    } else {
+        st = shard_setup(v, plan, hxyz.data(), dist, work);
+        if (st != VOL_OK) return bail(st);
+    }
+    v->n_work = (int64_t)work.size();
+    if (cudaMemcpyAsync(v->d_work, work.data(), work.size() * 4, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemsetAsync(v->d_flags, 0, ((size_t)L.S + 1) * 4, s) != cudaSuccess ||
+        cudaMemsetAsync(v->d_ticket, 0, 16, s) != cudaSuccess)
+        return bail(fail(VOL_ECUDA, "work list upload failed"));
+    // K3: initial state (warm start) so read_u / energy are defined before the first iteration
+    if (launch_init_state(v->F, L.S * kBlockVox, 0, s) < 0) return bail(fail(VOL_ECUDA, "init launch failed"));
+    if (cudaStreamSynchronize(s) != cudaSuccess)
+        return bail(fail(VOL_ECUDA, "vol_create: %s", cudaGetErrorString(cudaGetLastError())));
+    if (sharded) {
+        st = shard_after_create(v);
+        if (st != VOL_OK) return bail(st);
+    }
+    v->cur = 0;
+    v->initialised = true;
+    *out = v;
+    return VOL_OK;
+}
+
+extern "C" void vol_destroy(vol_t v) {
+    if (!v) return;
+    if (v->shard) shard_destroy(v);
+    if (v->stream) cudaStreamSynchronize(v->stream);
+    if (v->cap) cudaStreamDestroy(v->cap);
+    if (v->owns_ws && v->ws) cudaFree(v->ws);
+    delete v;
+}
+
+// ------------------------------------------------------------------------------- iterations
+
+static vol_status run_iterations_single(vol_s *v, const IterParams &P, int32_t iters, int kernel) {
+    cudaStream_t s = v->stream;
+    int64_t launches = 0;
+    auto one = [&](cudaStream_t st, int cur) -> int {
+        if (kernel == 1) return launch_two_kernel(v->F, cur, v->d_nbr, v->d_work, v->n_work, P, st);
+        return launch_fused(v->F, cur, v->d_nbr, v->d_work, nullptr, v->n_work, v->d_flags, v->d_ticket, P, st);
+    };
+    // CUDA graph of 2·m iterations (ū parity returns to the start), replayed; remainder launched directly.
+    const int m = std::min<int>(16, iters / 2);
+    if (m >= 1) {
+        cudaGraph_t g = nullptr;
+        cudaGraphExec_t ge = nullptr;
+        CK(cudaStreamBeginCapture(v->cap, cudaStreamCaptureModeThreadLocal));
+        int per = 0, cur = v->cur, bad = 0;
+        for (int k = 0; k < 2 * m; k++) {
+            int r = one(v->cap, cur);
+            if (r < 0) bad = 1;
+            per += r;
+            cur ^= 1;
+        }
+        cudaError_t e = cudaStreamEndCapture(v->cap, &g);
+        if (bad || e != cudaSuccess) {
+            if (g) cudaGraphDestroy(g);
+            return fail(VOL_ECUDA, "graph capture failed: %s", cudaGetErrorString(e != cudaSuccess ? e : cudaGetLastError()));
+        }
+        g_launches.fetch_sub(per);  // capture does not execute; replays are counted below
+        e = cudaGraphInstantiate(&ge, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) return fail(VOL_ECUDA, "graph instantiate failed: %s", cudaGetErrorString(e));
+        const int reps = iters / (2 * m);
+        for (int r = 0; r < reps; r++) {
+            e = cudaGraphLaunch(ge, s);
+            if (e != cudaSuccess) {
+                cudaGraphExecDestroy(ge);
+                return fail(VOL_ECUDA, "graph launch failed: %s", cudaGetErrorString(e));
+            }
+            launches += per;
+            g_launches.fetch_add(per);
+        }
+        cudaGraphExecDestroy(ge);  // safe: destruction is deferred until the launches complete
+        iters -= reps * 2 * m;
+    }
+    for (int k = 0; k < iters; k++) {
+        int r = one(s, v->cur);
+        CKL(r);
+        launches += r;
+        v->cur ^= 1;
+    }
+    v->last_launches = launches;
+    return VOL_OK;
+}
+
+vol_status vol_regularise_prepare(vol_s *v, float lambda, float eps, float tau, float sigma, int32_t iters,
+                                  const vol_opts *opts) {
+    if (!v) return fail(VOL_EINVAL, "vol_regularise: NULL handle");
+    vol_opts o;
+    vol_default_opts(&o);
+    if (opts) o = *opts;
+    if (!(lambda > 0.0f) || !std::isfinite(lambda)) return fail(VOL_EINVAL, "lambda must be > 0 (got %g)", lambda);
+    if (!(eps >= 0.0f) || !std::isfinite(eps)) return fail(VOL_EINVAL, "eps must be >= 0 (got %g)", eps);
+    if (!(tau > 0.0f) || !(sigma > 0.0f) || !std::isfinite(tau) || !std::isfinite(sigma))
+        return fail(VOL_EINVAL, "tau and sigma must be > 0");
+    if ((double)tau * (double)sigma * 12.0 > 1.0 + 1e-6)
+        return fail(VOL_EINVAL, "step sizes violate 12*tau*sigma <= 1 (||grad||^2 <= 12): %g", (double)tau * sigma * 12.0);
+    if (iters < 0) return fail(VOL_EINVAL, "iters must be >= 0");
+    if (!(o.theta >= 0.0f) || !std::isfinite(o.theta)) return fail(VOL_EINVAL, "theta must be >= 0");
+    if (o.data_term != 0 && o.data_term != 1) return fail(VOL_EINVAL, "data_term must be 0 (L1) or 1 (L2)");
+    if (o.init != 0 && o.init != 1) return fail(VOL_EINVAL, "init must be 0 (warm) or 1 (zero)");
+    if (o.kernel != 0 && o.kernel != 1) return fail(VOL_EINVAL, "kernel must be 0 (fused) or 1 (two-kernel)");
+    if (v->shard && o.kernel == 1) return fail(VOL_ENOTSUP, "two-kernel baseline is single-GPU only");
+    if (v->shard) {
+        vol_status st = shard_reset(v);
+        if (st != VOL_OK) return st;
+    }
+    if (v->n_omega_global == 0) return fail(VOL_EDATA, "empty Omega: no voxel with W > 0 (S:261)");
+
+    IterParams &P = v->pending;
+    P.sigma = sigma;
+    P.tau = tau;
+    volatile float tl = tau * lambda;  // fl(τ·λ)
+    volatile float se = sigma * eps;   // fl(σ·ε)
+    volatile float dn = 1.0f + se;     // fl(1 + σε)
+    P.tl = tl;
+    P.denom = dn;
+    P.theta = o.theta;
+    P.data_term = o.data_term;
+    v->pending_kernel = o.kernel;
+    v->last_launches = 0;
+    if (!o.resume) {
+        CKL(launch_init_state(v->F, v->L.S * kBlockVox, o.init, v->stream));
+        v->cur = 0;
+        v->last_launches = 1;
+    }
+    return VOL_OK;
+}
+
+extern "C" vol_status vol_regularise(vol_t v, float lambda, float eps, float tau, float sigma, int32_t iters,
+                                     const vol_opts *opts) {
+    vol_status st = vol_regularise_prepare(v, lambda, eps, tau, sigma, iters, opts);
+    if (st != VOL_OK) return st;
+    if (iters == 0) return VOL_OK;
+    if (v->shard) return shard_iterate(v, v->pending, iters);
+    return run_iterations_single(v, v->pending, iters, v->pending_kernel);
+}
+
+extern "C" int64_t vol_last_launches(vol_t v) { return v ? v->last_launches : -1; }
+
+extern "C" vol_status vol_sync(vol_t v) {
+    if (!v) return fail(VOL_EINVAL, "NULL handle");
+    CK(cudaStreamSynchronize(v->stream));
+    return VOL_OK;
+}
+
+static vol_status copy_out(void *dst, const void *src, size_t bytes, cudaStream_t s) {
+    if (is_device_ptr(dst)) {
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s));
+    } else {
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    return VOL_OK;
+}
+
+extern "C" vol_status vol_read_u(vol_t v, float *u_out) {
+    if (!v || !u_out) return fail(VOL_EINVAL, "vol_read_u: NULL argument");
+    return copy_out(u_out, v->F.u, (size_t)v->L.n_local * kBlockVox * 4, v->stream);
+}
+
+extern "C" vol_status vol_read_state(vol_t v, float *u, float *ubar, float *p) {
+    if (!v) return fail(VOL_EINVAL, "vol_read_state: NULL handle");
+    const size_t nb = (size_t)v->L.n_local * kBlockVox * 4;
+    vol_status st;
+    if (u && (st = copy_out(u, v->F.u, nb, v->stream)) != VOL_OK) return st;
+    if (ubar && (st = copy_out(ubar, v->F.ub[v->cur], nb, v->stream)) != VOL_OK) return st;
+    if (p) {
+        const size_t nv = (size_t)v->L.n_local * kBlockVox;
+        if ((st = copy_out(p, v->F.px, nb, v->stream)) != VOL_OK) return st;
+        if ((st = copy_out(p + nv, v->F.py, nb, v->stream)) != VOL_OK) return st;
+        if ((st = copy_out(p + 2 * nv, v->F.pz, nb, v->stream)) != VOL_OK) return st;
+    }
+    return VOL_OK;
+}
+
+extern "C" vol_status vol_load_state(vol_t v, const float *u, const float *ubar, const float *p) {
+    if (!v) return fail(VOL_EINVAL, "vol_load_state: NULL handle");
+    if (v->shard) return fail(VOL_ENOTSUP, "vol_load_state: single-GPU volumes only");
+    const size_t nb = (size_t)v->L.n_local * kBlockVox * 4;
+    cudaStream_t s = v->stream;
+    vol_status st;
+    if (u && (st = copy_in(v->F.u, u, nb, s)) != VOL_OK) return st;
+    if (ubar && (st = copy_in(v->F.ub[v->cur], ubar, nb, s)) != VOL_OK) return st;
+    if (p) {
+        const size_t nv = (size_t)v->L.n_local * kBlockVox;
+        if ((st = copy_in(v->F.px, p, nb, s)) != VOL_OK) return st;
+        if ((st = copy_in(v->F.py, p + nv, nb, s)) != VOL_OK) return st;
+        if ((st = copy_in(v->F.pz, p + 2 * nv, nb, s)) != VOL_OK) return st;
+    }
+    CKL(launch_sanitize_state(v->F, v->cur, v->d_nbr, v->L.n_local, s));
+    CK(cudaStreamSynchronize(s));
+    return VOL_OK;
+}
+
+extern "C" vol_status vol_energy(vol_t v, float lambda, float eps, int data_term, double *primal, double *dual) {
+    if (!v || !primal) return fail(VOL_EINVAL, "vol_energy: NULL argument");
+    if (!(lambda > 0.0f) || !(eps >= 0.0f) || (data_term != 0 && data_term != 1))
+        return fail(VOL_EINVAL, "vol_energy: bad parameters");
+    if (v->shard) {
+        vol_status st = shard_refresh_for_energy(v);
+        if (st != VOL_OK) return st;
+    }
+    CKL(launch_energy(v->F, v->d_nbr, nullptr, v->L.n_local, lambda, eps, data_term, v->d_part, v->d_eout, v->stream));
+    double o[5];
+    if (v->shard) {
+        vol_status st = shard_allreduce_energy(v, v->d_eout);
+        if (st != VOL_OK) return st;
+    }
+    CK(cudaMemcpyAsync(o, v->d_eout, sizeof o, cudaMemcpyDeviceToHost, v->stream));
+    CK(cudaStreamSynchronize(v->stream));
+    *primal = o[0];
+    if (dual) *dual = energy_dual_value(o, eps, data_term);
+    return VOL_OK;
+}
+
+double energy_dual_value(const double *o, float eps, int data_term) {
+    const double e = (double)eps;
+    if (data_term == 0) {
+        const double sc = std::min(1.0, o[4]);
+        return -0.5 * e * sc * sc * o[1] - sc * o[2];
+    }
+    return -0.5 * e * o[1] - o[2] - o[3];
+}
+
+extern "C" vol_status vol_read_tables(vol_t v, uint32_t *T, uint32_t *bucket_start, int32_t *bucket_entry,
+                                      int32_t *nbr) {
+    if (!v) return fail(VOL_EINVAL, "vol_read_tables: NULL handle");
+    if (T) *T = v->L.T;
+    vol_status st;
+    if (bucket_start && (st = copy_out(bucket_start, v->d_start, ((size_t)v->L.T + 1) * 4, v->stream)) != VOL_OK)
+        return st;
+    if (bucket_entry && (st = copy_out(bucket_entry, v->d_entry, (size_t)v->L.n_global * 4, v->stream)) != VOL_OK)
+        return st;
+    if (nbr) {
+        if (v->shard) return fail(VOL_ENOTSUP, "vol_read_tables: nbr of a sharded volume is in store indices");
+        if ((st = copy_out(nbr, v->d_nbr, (size_t)v->L.S * 6 * 4, v->stream)) != VOL_OK) return st;
+    }
+    return VOL_OK;
+}
+
+extern "C" vol_status vol_info(vol_t v, int64_t *n_local, int64_t *n_ghost, int64_t *n_omega) {
+    if (!v) return fail(VOL_EINVAL, "vol_info: NULL handle");
+    if (n_local) *n_local = v->L.n_local;
+    if (n_ghost) *n_ghost = v->L.S - v->L.n_local;
+    if (n_omega) *n_omega = v->n_omega_local;
+    return VOL_OK;
+}

@@ -1,0 +1,243 @@
+"""Python surface of the C ABI (SURVEY §8(b) "Python surface"): `Volume(coords, f, W, group=None)`,
+`.regularise(...)`, `.u()`, `.energy(...)`.  PyTorch provides device memory (the workspace), the
+CUDA stream and the process group; the method itself runs in libvol.so's kernels.
+
+Inputs may be torch tensors (CUDA or CPU, pinned or not) or numpy arrays; the library detects
+host/device pointers.  Names follow the paper: λ (lam), ε (eps, Huber), τ (tau), σ (sigma),
+θ (theta), f (fused TSDF), W (fusion weight), u / ū (primal / relaxed primal), p (dual).
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native as N
+
+
+def _ptr(x):
+    """(pointer, keep-alive object) of a contiguous torch tensor or numpy array."""
+    if isinstance(x, torch.Tensor):
+        if not x.is_contiguous():
+            x = x.contiguous()
+        return ctypes.c_void_p(x.data_ptr()), x
+    a = np.ascontiguousarray(x)
+    return ctypes.c_void_p(a.ctypes.data), a
+
+
+def _as(x, dtype_t, dtype_np):
+    if isinstance(x, torch.Tensor):
+        return x.to(dtype_t).contiguous() if x.dtype != dtype_t else x.contiguous()
+    return np.ascontiguousarray(x, dtype=dtype_np)
+
+
+def _require_cuda():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1604_03734_b200 needs a CUDA device (B200); there is no CPU fallback")
+
+
+def block_hash(x: int, y: int, z: int, T: int) -> int:
+    return int(N.lib().vol_block_hash(x, y, z, T))
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    N.check(N.lib().vol_nccl_unique_id(buf))
+    return buf.raw
+
+
+def plan_shard(coords, part, world: int, rank: int) -> dict:
+    """Host-only shard plan of `rank`; no GPU needed."""
+    c = np.ascontiguousarray(coords, dtype=np.int32).reshape(-1, 3)
+    pt = np.ascontiguousarray(part, dtype=np.int32)
+    n = c.shape[0]
+    L = N.lib()
+    nl, ng, ns = (ctypes.c_int64() for _ in range(3))
+    N.check(L.vol_plan_shard(c.ctypes.data, n, pt.ctypes.data, world, rank, ctypes.byref(nl), ctypes.byref(ng),
+                             ctypes.byref(ns), None, None, None, None))
+    ghost = np.zeros(max(ng.value, 1), np.int64)
+    send = np.zeros(max(ns.value, 1), np.int64)
+    psend = np.zeros(world, np.int64)
+    precv = np.zeros(world, np.int64)
+    N.check(L.vol_plan_shard(c.ctypes.data, n, pt.ctypes.data, world, rank, None, None, None, ghost.ctypes.data,
+                             send.ctypes.data, psend.ctypes.data, precv.ctypes.data))
+    return dict(n_local=nl.value, n_ghost=ng.value, ghost=ghost[:ng.value], send=send[:ns.value],
+                peer_send=psend, peer_recv=precv)
+
+
+class Volume:
+    """A hashed voxel-block volume resident on one GPU (or one shard of a sharded volume).
+
+    coords: int32 [n_global, 3] block coordinates; f, W: float32 [n_local, 512] (blocks this rank
+    owns, in global order).  For sharding pass `part` (owner rank per block) and either a
+    torch.distributed `group` (NCCL transport; the unique id is broadcast through the group) or
+    `loopback=(rank, world)` for the one-process test transport.
+    """
+
+    def __init__(self, coords, f, W, *, part=None, group=None, loopback=None, device=None, stream=None):
+        _require_cuda()
+        self._lib = N.lib()
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        coords = _as(coords, torch.int32, np.int32)
+        f = _as(f, torch.float32, np.float32)
+        W = _as(W, torch.float32, np.float32)
+        n = int(coords.shape[0])
+        self.n_global = n
+        dist = None
+        self._keep = []
+        if part is not None:
+            part_np = np.ascontiguousarray(part.cpu().numpy() if isinstance(part, torch.Tensor) else part, dtype=np.int32)
+            if group is not None:
+                import torch.distributed as dist_mod
+                rank, world = dist_mod.get_rank(group), dist_mod.get_world_size(group)
+                idbuf = torch.zeros(128, dtype=torch.uint8)
+                if rank == 0:
+                    idbuf = torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8).clone()
+                if dist_mod.get_backend(group) == "nccl":
+                    idd = idbuf.to(self.device)
+                    dist_mod.broadcast(idd, src=dist_mod.get_global_rank(group, 0), group=group)
+                    idbuf = idd.cpu()
+                else:
+                    dist_mod.broadcast(idbuf, src=dist_mod.get_global_rank(group, 0), group=group)
+                nid = ctypes.create_string_buffer(bytes(idbuf.numpy().tobytes()), 128)
+                self._keep.append(nid)
+                dist = N.vol_dist(rank, world, part_np.ctypes.data, ctypes.cast(nid, ctypes.c_void_p))
+            elif loopback is not None:
+                rank, world = loopback
+                dist = N.vol_dist(rank, world, part_np.ctypes.data, None)
+            else:
+                raise ValueError("part given without group or loopback")
+            self._keep.append(part_np)
+            self.rank, self.world = rank, world
+        else:
+            self.rank, self.world = 0, 1
+        with torch.cuda.device(self.device):
+            self.stream = torch.cuda.current_stream(self.device) if stream is None else stream
+            cp, ck = _ptr(coords)
+            fp, fk = _ptr(f)
+            wp, wk = _ptr(W)
+            dptr = ctypes.byref(dist) if dist is not None else None
+            nbytes = self._lib.vol_workspace_bytes(cp, n, dptr)
+            if nbytes == 0:
+                raise N.VolError(N.VOL_EINVAL, "vol_workspace_bytes failed (bad coordinates or partition)")
+            self.workspace = torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
+            h = ctypes.c_void_p()
+            N.check(self._lib.vol_create(cp, n, fp, wp, dptr, ctypes.c_void_p(self.workspace.data_ptr()), nbytes,
+                                         ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(h)))
+            del ck, fk, wk
+        self._h = h
+        nl, ng, no = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        N.check(self._lib.vol_info(self._h, ctypes.byref(nl), ctypes.byref(ng), ctypes.byref(no)))
+        self.n_local, self.n_ghost, self.n_omega = nl.value, ng.value, no.value
+
+    # -- solver ---------------------------------------------------------------------------------
+    @staticmethod
+    def _opts(theta=1.0, data_term=0, init=0, resume=False, kernel=0):
+        o = N.vol_opts()
+        N.lib().vol_default_opts(ctypes.byref(o))
+        o.theta, o.data_term, o.init, o.resume, o.kernel = float(theta), int(data_term), int(init), int(bool(resume)), int(kernel)
+        return o
+
+    def regularise(self, lam: float, eps: float, tau: float, sigma: float, iters: int, *, theta: float = 1.0,
+                   data_term: int = 0, init: int = 0, resume: bool = False, kernel: int = 0):
+        """`iters` Chambolle–Pock iterations (asynchronous on the volume's stream)."""
+        o = self._opts(theta, data_term, init, resume, kernel)
+        N.check(self._lib.vol_regularise(self._h, lam, eps, tau, sigma, int(iters), ctypes.byref(o)))
+        return self
+
+    def regularise_scene(self, scene, iters=None, **kw):
+        it = scene.iters if iters is None else iters
+        kw.setdefault("theta", scene.theta)
+        kw.setdefault("data_term", scene.data_term)
+        kw.setdefault("init", scene.init)
+        return self.regularise(scene.lam, scene.eps, scene.tau, scene.sigma, it, **kw)
+
+    @property
+    def last_launches(self) -> int:
+        return int(self._lib.vol_last_launches(self._h))
+
+    def sync(self):
+        N.check(self._lib.vol_sync(self._h))
+
+    # -- read-back ------------------------------------------------------------------------------
+    def read_u(self, out):
+        """Copy u [n_local, 512] into `out` (host or device tensor / numpy array)."""
+        p, k = _ptr(out)
+        N.check(self._lib.vol_read_u(self._h, p))
+        return out
+
+    def u(self, device=None) -> torch.Tensor:
+        out = torch.empty(self.n_local, 512, dtype=torch.float32, device=self.device if device is None else device)
+        self.read_u(out)
+        if out.device.type == "cuda":
+            self.sync()
+        return out
+
+    def energy(self, lam: float, eps: float, data_term: int = 0):
+        """(primal, dual) energies of the current state (fp64, deterministic)."""
+        P, D = ctypes.c_double(), ctypes.c_double()
+        N.check(self._lib.vol_energy(self._h, lam, eps, data_term, ctypes.byref(P), ctypes.byref(D)))
+        return P.value, D.value
+
+    def state(self):
+        """(u, ū, p[3]) as CPU tensors."""
+        u = torch.empty(self.n_local, 512)
+        ub = torch.empty(self.n_local, 512)
+        p = torch.empty(3, self.n_local, 512)
+        N.check(self._lib.vol_read_state(self._h, ctypes.c_void_p(u.data_ptr()), ctypes.c_void_p(ub.data_ptr()),
+                                         ctypes.c_void_p(p.data_ptr())))
+        return u, ub, p
+
+    def load_state(self, u, ub, p):
+        keep = [_ptr(_as(x, torch.float32, np.float32)) for x in (u, ub, p)]
+        N.check(self._lib.vol_load_state(self._h, *(k[0] for k in keep)))
+
+    def tables(self):
+        """(T, bucket_start[T+1] uint32, bucket_entry[n] int32, nbr[n, 6] int32) as numpy arrays."""
+        T = ctypes.c_uint32()
+        N.check(self._lib.vol_read_tables(self._h, ctypes.byref(T), None, None, None))
+        bs = np.zeros(T.value + 1, np.uint32)
+        be = np.zeros(self.n_global, np.int32)
+        nbr = np.zeros((self.n_global, 6), np.int32)
+        N.check(self._lib.vol_read_tables(self._h, None, bs.ctypes.data, be.ctypes.data, nbr.ctypes.data))
+        return T.value, bs, be, nbr
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.vol_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+# -- loopback groups (one process, one GPU; tests of the sharded path) --------------------------------
+
+def _handles(vols):
+    arr = (ctypes.c_void_p * len(vols))(*[v._h.value for v in vols])
+    return arr
+
+
+def connect_group(vols):
+    N.check(N.lib().vol_group_connect(_handles(vols), len(vols)))
+
+
+def regularise_group(vols, lam, eps, tau, sigma, iters, **kw):
+    o = Volume._opts(**kw)
+    N.check(N.lib().vol_regularise_group(_handles(vols), len(vols), lam, eps, tau, sigma, int(iters), ctypes.byref(o)))
+
+
+def group_energy(vols, lam, eps, data_term=0):
+    P, D = ctypes.c_double(), ctypes.c_double()
+    N.check(N.lib().vol_group_energy(_handles(vols), len(vols), lam, eps, data_term, ctypes.byref(P), ctypes.byref(D)))
+    return P.value, D.value

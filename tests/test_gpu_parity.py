@@ -1,0 +1,216 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on seeded inputs.
+
+Tolerances: hash, CSR and neighbour tables bit-exact; u within 1e-5 of the
+fp64 oracle (north_star); and, because both sides evaluate the same written fp32 formula order
+without FMA contraction, u bit-identical to the oracle's fp32 build.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from synth import dense_box, random_instance, tiny
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def V():
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    from paper_1604_03734_b200 import Volume
+    return Volume
+
+
+def run_gpu(V, s, iters=None, **kw):
+    vol = V(s.coords.cuda(), s.f.cuda(), s.W.cuda())
+    vol.regularise_scene(s, iters=iters, **kw)
+    u = vol.u().cpu().numpy()
+    return vol, u
+
+
+def check_against_oracle(s, u, iters=None):
+    u64, _, _ = oracle.regularise_scene(s, precision="f64", iters=iters)
+    u32, _, _ = oracle.regularise_scene(s, precision="f32", iters=iters)
+    err64 = float(np.abs(u - u64).max())
+    assert err64 <= TOL, f"max|u_gpu − u_oracle64| = {err64}"
+    mism = int((u != u32).sum())
+    assert mism == 0, f"{mism} voxels differ from the fp32 oracle (max {np.abs(u - u32).max()})"
+
+
+# ------------------------------------------------------------------------------------ tables
+
+@pytest.mark.parametrize("maker", [lambda: tiny(), lambda: random_instance(700, seed=3, extent=6),
+                                   lambda: dense_box(3, 2, 2)])
+def test_tables_bit_exact(V, maker):
+    s = maker()
+    vol = V(s.coords, s.f, s.W)
+    T, bs, be, nbr = vol.tables()
+    To, bso, beo, dup = oracle.build_table(s.coords)
+    assert dup is None and T == To
+    assert np.array_equal(bs, bso) and np.array_equal(be, beo)
+    assert np.array_equal(nbr, oracle.neighbours(s.coords))
+
+
+def test_tables_10k_random_coords(V):
+    g = np.random.default_rng(1)
+    c = np.unique(g.integers(-2**20, 2**20, size=(10000, 3)).astype(np.int32), axis=0)
+    g.shuffle(c)
+    n = c.shape[0]
+    vol = V(torch.from_numpy(c).cuda(), torch.zeros(n, 512).cuda(), torch.ones(n, 512).cuda())
+    T, bs, be, nbr = vol.tables()
+    To, bso, beo, _ = oracle.build_table(c)
+    assert np.array_equal(bs, bso) and np.array_equal(be, beo)
+    assert np.array_equal(nbr, oracle.neighbours(c))
+
+
+# ------------------------------------------------------------------------------- errors
+
+def test_input_errors(V):
+    from paper_1604_03734_b200._native import VolError, VOL_EDATA, VOL_EINVAL
+    s = random_instance(20, seed=1, extent=2)
+    c = s.coords.clone()
+    c[7] = c[3]
+    with pytest.raises(VolError) as e:
+        V(c, s.f, s.W)
+    assert e.value.status == VOL_EDATA and "3 and 7" in str(e.value)
+    f = s.f.clone()
+    f[2, 5] = float("nan")
+    with pytest.raises(VolError) as e:
+        V(s.coords, f, s.W)
+    assert e.value.status == VOL_EDATA
+    W = s.W.clone()
+    W[0, 0] = -1
+    with pytest.raises(VolError) as e:
+        V(s.coords, s.f, W)
+    assert e.value.status == VOL_EDATA
+    vol = V(s.coords, s.f, torch.zeros_like(s.W))
+    with pytest.raises(VolError) as e:
+        vol.regularise(1.0, 0.0, 0.2, 0.2, 5)
+    assert e.value.status == VOL_EDATA          # empty Ω
+    vol = V(s.coords, s.f, s.W)
+    for bad in [dict(lam=0.0), dict(eps=-1.0), dict(tau=0.5, sigma=0.5), dict(iters=-1)]:
+        args = dict(lam=1.0, eps=0.0, tau=0.2, sigma=0.2, iters=3)
+        args.update(bad)
+        with pytest.raises(VolError) as e:
+            vol.regularise(args["lam"], args["eps"], args["tau"], args["sigma"], args["iters"])
+        assert e.value.status == VOL_EINVAL
+
+
+# ------------------------------------------------------------------------------- parity
+
+def test_tiny_config_parity(V, tiny_scene):
+    # config 1 at its full 200 iterations
+    _, u = run_gpu(V, tiny_scene)
+    check_against_oracle(tiny_scene, u)
+
+
+def test_tiny_stress_parity(V, tiny_stress_scene):
+    s = tiny_stress_scene
+    _, u = run_gpu(V, s)
+    check_against_oracle(s, u)
+    W = s.W.numpy()
+    assert np.abs(u - s.f.numpy())[W > 0].max() > 0.05   # the shrinkage path is exercised
+
+
+CASES = [
+    dict(n=300, seed=0, eps=0.0, data_term=0, init=0, theta=1.0),
+    dict(n=300, seed=1, eps=0.01, data_term=0, init=0, theta=1.0),
+    dict(n=250, seed=2, eps=0.0, data_term=1, init=0, theta=1.0),
+    dict(n=250, seed=3, eps=0.05, data_term=1, init=1, theta=1.0),
+    dict(n=200, seed=4, eps=0.0, data_term=0, init=1, theta=0.5),
+]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_random_instances_parity(V, case):
+    s = random_instance(case["n"], seed=case["seed"], extent=5, w_density=0.6, lam=0.4, eps=case["eps"],
+                        data_term=case["data_term"], iters=60)
+    s.init = case["init"]
+    s.theta = case["theta"]
+    _, u = run_gpu(V, s)
+    check_against_oracle(s, u)
+
+
+@pytest.mark.parametrize("kernel", [0, 1])
+def test_dense_box_and_two_kernel_parity(V, kernel):
+    s = dense_box(3, 3, 2, seed=5, w_density=0.85, lam=0.6, eps=0.02, iters=40)
+    _, u = run_gpu(V, s, kernel=kernel)
+    check_against_oracle(s, u)
+
+
+def test_fused_equals_two_kernel_bitwise(V):
+    s = random_instance(400, seed=9, extent=5, lam=0.3, eps=0.01, iters=50)
+    _, a = run_gpu(V, s, kernel=0)
+    _, b = run_gpu(V, s, kernel=1)
+    assert np.array_equal(a, b)
+
+
+def test_single_block_and_odd_iteration_counts(V):
+    s = random_instance(1, seed=2, extent=1, iters=7)
+    _, u = run_gpu(V, s)
+    check_against_oracle(s, u)
+    for it in (0, 1, 2, 3, 33, 65):
+        s2 = random_instance(30, seed=2, extent=2, iters=it)
+        _, u = run_gpu(V, s2)
+        check_against_oracle(s2, u)
+
+
+def test_resume_and_determinism(V):
+    s = random_instance(200, seed=6, extent=4, eps=0.02, iters=0)
+    vol = V(s.coords.cuda(), s.f.cuda(), s.W.cuda())
+    vol.regularise(s.lam, s.eps, s.tau, s.sigma, 17)
+    vol.regularise(s.lam, s.eps, s.tau, s.sigma, 13, resume=True)
+    a = vol.u().cpu().numpy()
+    vol.regularise(s.lam, s.eps, s.tau, s.sigma, 30)
+    b = vol.u().cpu().numpy()
+    assert np.array_equal(a, b)
+    u, ub, p = vol.state()
+    vol.regularise(s.lam, s.eps, s.tau, s.sigma, 30)
+    assert np.array_equal(vol.u().cpu().numpy(), b)
+    # checkpoint / resume through load_state
+    vol2 = V(s.coords, s.f, s.W)
+    vol2.load_state(u, ub, p)
+    vol2.regularise(s.lam, s.eps, s.tau, s.sigma, 10, resume=True)
+    vol.regularise(s.lam, s.eps, s.tau, s.sigma, 40)
+    assert np.array_equal(vol2.u().cpu().numpy(), vol.u().cpu().numpy())
+
+
+def test_permutation_invariance_and_host_device_io(V):
+    s = random_instance(150, seed=8, extent=4, iters=25)
+    _, u = run_gpu(V, s)
+    perm = torch.randperm(150, generator=torch.Generator().manual_seed(0))
+    vol = V(s.coords[perm].numpy(), s.f[perm].numpy(), s.W[perm].pin_memory())
+    vol.regularise_scene(s)
+    out = np.zeros((150, 512), np.float32)
+    vol.read_u(out)                                   # pageable host output
+    assert np.array_equal(out, u[perm.numpy()])
+
+
+def test_energy_matches_oracle(V, tiny_scene):
+    s = tiny_scene
+    vol = V(s.coords.cuda(), s.f.cuda(), s.W.cuda())
+    nbr = oracle.neighbours(s.coords)
+    for dt, eps in ((0, 0.0), (0, 0.05), (1, 0.0), (1, 0.05)):
+        vol.regularise(s.lam, eps, s.tau, s.sigma, 30, data_term=dt)
+        u, _, p = vol.state()
+        P, D = vol.energy(s.lam, eps, dt)
+        Po, Do = oracle.energy(nbr, s.f, s.W, u.double().numpy(), s.lam, eps, dt, p=p.double().numpy())
+        assert abs(P - Po) <= 1e-9 * abs(Po)
+        assert abs(D - Do) <= 1e-9 * abs(Po)
+        assert D <= P
+
+
+def test_gpu_invariants_tiny(V, tiny_scene):
+    s = tiny_scene
+    vol, u = run_gpu(V, s)
+    f, W = s.f.numpy(), s.W.numpy()
+    assert np.array_equal(u[W == 0], f[W == 0])                     # Ω̄ untouched
+    pin = (W > 0) & (s.lam * W >= 3 + math.sqrt(3))
+    assert np.array_equal(u[pin], f[pin])                           # λ→∞ pinning
+    _, _, p = vol.state()
+    assert float(torch.sqrt((p ** 2).sum(0)).max()) <= 1 + 1e-6     # feasibility
