@@ -102,15 +102,15 @@ def regularise(coords, f, W, lam, eps, tau, sigma, iters, theta=1.0, data_term=0
     u = np.where(omega & (init == 1), T(0), f_).astype(dtype)
     ub = u.copy()
     p = [np.zeros_like(u) for _ in range(3)]
-    denom = one + sigma * eps
+    kappa = one / (one + sigma * eps)          # Huber damping 1/(1+σε), applied as a product (c-18)
     tl = tau * lam
     t = tl * W_
     for _ in range(iters):
         g = gradient(ub, omega)
-        q = [(p[a] + sigma * g[a]) / denom for a in range(3)]
+        q = [(p[a] + sigma * g[a]) * kappa for a in range(3)]
         nrm = np.sqrt((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2])
-        m = np.where(nrm > one, nrm, one)
-        p = [np.where(omega, q[a] / m, T(0)) for a in range(3)]
+        r = one / np.where(nrm > one, nrm, one)  # p = q · (1 / max(1, ‖q‖₂))
+        p = [np.where(omega, q[a] * r, T(0)) for a in range(3)]
         d = divergence(p, omega)
         ut = u + tau * d
         if data_term == 0:

@@ -12,52 +12,66 @@ namespace hvg {
 
 constexpr int kNPart = 5;  // [0] primal, [1] Σ‖p‖², [2] Σ f·div p, [3] Σ (div p)²/(2λW), [4] min λW/|div p|
 
-__device__ __forceinline__ int64_t step_voxel(const int32_t *nbr, int64_t b, int i, int axis, int dir) {
-    int c[3] = {i & 7, (i >> 3) & 7, i >> 6};
-    c[axis] += dir;
-    if (c[axis] < 0 || c[axis] > 7) {
-        int32_t nb = nbr[6 * b + 2 * axis + (dir > 0 ? 1 : 0)];
-        if (nb < 0) return -1;
-        c[axis] &= 7;
-        b = nb;
-    }
-    return b * kBlockVox + c[0] + 8 * c[1] + 64 * c[2];
+__device__ __forceinline__ int face_idx(int a, int k, int c) {
+    return a == 0 ? c + 8 * k : (a == 1 ? (k & 7) + 8 * c + 64 * (k >> 3) : k + 64 * c);
 }
 
+// One CTA per block; the block and its face halos are staged in shared memory (u, W of the +faces;
+// p_a of the −faces, which is 0 on invalid edges by the iteration's invariant, see iterate.cu).
 __global__ void __launch_bounds__(kThreads)
-k_energy_blocks(Fields F, const int32_t *__restrict__ nbr, const int32_t *__restrict__ blocks, double lam, double eps,
+k_energy_blocks(View F, const int32_t *__restrict__ nbr, const int32_t *__restrict__ blocks, double lam, double eps,
                 int data_term, double *__restrict__ partials) {
+    __shared__ float su[kBlockVox + 192], sW[kBlockVox + 192];
+    __shared__ float sp[3][64 + kBlockVox];
     __shared__ double red[kNPart][kThreads];
     const int tid = threadIdx.x;
     const int64_t b = blocks ? blocks[blockIdx.x] : blockIdx.x;
+    const int64_t base = b * kBlockVox;
+    for (int j = 0; j < 4; j++) {
+        const int i = tid + kThreads * j;
+        su[i] = F.u[base + i];
+        sW[i] = F.W[base + i];
+        sp[0][64 + i] = F.px_in[base + i];
+        sp[1][64 + i] = F.py_in[base + i];
+        sp[2][64 + i] = F.pz_in[base + i];
+    }
+    for (int it = tid; it < 384; it += kThreads) {
+        const int a = (it >> 6) % 3, k = it & 63;
+        if (it < 192) {                                   // + faces: u, W
+            const int32_t nb = nbr[kNbr * b + 2 * a + 1];
+            const int64_t idx = nb < 0 ? 0 : (int64_t)nb * kBlockVox + face_idx(a, k, 0);
+            su[kBlockVox + it] = nb < 0 ? 0.0f : F.u[idx];
+            sW[kBlockVox + it] = nb < 0 ? 0.0f : F.W[idx];
+        } else {                                          // − faces: p_a
+            const int32_t nb = nbr[kNbr * b + 2 * a];
+            const float *pa = a == 0 ? F.px_in : (a == 1 ? F.py_in : F.pz_in);
+            sp[a][k] = nb < 0 ? 0.0f : pa[(int64_t)nb * kBlockVox + face_idx(a, k, 7)];
+        }
+    }
+    __syncthreads();
     double acc[kNPart] = {0.0, 0.0, 0.0, 0.0, 1.0};
     for (int j = 0; j < 4; j++) {
         const int i = tid + kThreads * j;
-        const int64_t v = b * kBlockVox + i;
-        const float Wv = F.W[v];
+        const float Wv = sW[i];
         if (!(Wv > 0.0f)) continue;
-        const double uv = F.u[v], fv = F.f[v], Wd = Wv;
-        double g2 = 0.0, dv = 0.0, p2 = 0.0;
-        const float *pc[3] = {F.px, F.py, F.pz};
-        for (int a = 0; a < 3; a++) {
-            const int64_t w = step_voxel(nbr, b, i, a, +1);
-            const bool fwd = w >= 0 && F.W[w] > 0.0f;
-            const double ga = fwd ? (double)F.u[w] - uv : 0.0;
-            g2 += ga * ga;
-            const int64_t m = step_voxel(nbr, b, i, a, -1);
-            const bool bwd = m >= 0 && F.W[m] > 0.0f;
-            const double own = fwd ? (double)pc[a][v] : 0.0;
-            const double prv = bwd ? (double)pc[a][m] : 0.0;
-            dv += own - prv;
-            const double pa = pc[a][v];
-            p2 += pa * pa;
-        }
-        const double s = sqrt(g2);
+        const int x = i & 7, y = (i >> 3) & 7, z = i >> 6;
+        const int nx = x < 7 ? i + 1 : kBlockVox + (y + 8 * z);
+        const int ny = y < 7 ? i + 8 : kBlockVox + 64 + (x + 8 * z);
+        const int nz = z < 7 ? i + 64 : kBlockVox + 128 + (x + 8 * y);
+        const double uv = su[i], fv = F.f[base + i], Wd = Wv;
+        const double gx = sW[nx] > 0.0f ? (double)su[nx] - uv : 0.0;
+        const double gy = sW[ny] > 0.0f ? (double)su[ny] - uv : 0.0;
+        const double gz = sW[nz] > 0.0f ? (double)su[nz] - uv : 0.0;
+        const double pxv = sp[0][64 + i], pyv = sp[1][64 + i], pzv = sp[2][64 + i];
+        const double dv = (pxv - (double)sp[0][x > 0 ? 64 + i - 1 : y + 8 * z]) +
+                          (pyv - (double)sp[1][y > 0 ? 64 + i - 8 : x + 8 * z]) +
+                          (pzv - (double)sp[2][z > 0 ? i : x + 8 * y]);
+        const double s = sqrt(gx * gx + gy * gy + gz * gz);
         const double h = (eps > 0.0 && s <= eps) ? s * s / (2.0 * eps) : s - eps / 2.0;
         const double r = uv - fv;
         const double dt = data_term == 0 ? lam * Wd * fabs(r) : 0.5 * lam * Wd * r * r;
         acc[0] += h + dt;
-        acc[1] += p2;
+        acc[1] += pxv * pxv + pyv * pyv + pzv * pzv;
         acc[2] += fv * dv;
         acc[3] += dv * dv / (2.0 * lam * Wd);
         const double lim = lam * Wd;
@@ -97,7 +111,7 @@ __global__ void __launch_bounds__(1024) k_energy_final(const double *__restrict_
         for (int q = 0; q < kNPart; q++) out[q] = red[q][0];
 }
 
-int launch_energy(const Fields &F, const int32_t *nbr, const int32_t *blocks, int64_t n_blocks, float lam, float eps,
+int launch_energy(const View &F, const int32_t *nbr, const int32_t *blocks, int64_t n_blocks, float lam, float eps,
                   int data_term, double *partials, double *out, cudaStream_t s) {
     if (n_blocks > 0)
         k_energy_blocks<<<(unsigned)n_blocks, kThreads, 0, s>>>(F, nbr, blocks, (double)lam, (double)eps, data_term,

@@ -68,11 +68,8 @@ struct vol_s {
     uint32_t *d_start = nullptr;       // [T+1]
     int32_t *d_entry = nullptr;        // [n_global]
     uint32_t *d_scan = nullptr;        // scan scratch
-    int32_t *d_nbr = nullptr;          // [S][6] store indices
-    int32_t *d_work = nullptr;         // [S] topological work list
-    uint8_t *d_mode = nullptr;         // [S]
-    uint32_t *d_flags = nullptr;       // [S]
-    uint32_t *d_ticket = nullptr;      // [1]
+    int32_t *d_nbr = nullptr;          // [S][12] store indices (6 faces + 6 edge neighbours)
+    int32_t *d_work = nullptr;         // [S] work list (Morton order)
     unsigned long long *d_misc = nullptr;  // [4]: dup, bad, n_omega, spare
     double *d_part = nullptr;          // [S][5]
     double *d_eout = nullptr;          // [8]

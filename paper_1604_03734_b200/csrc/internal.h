@@ -3,7 +3,9 @@
 // Layout in HBM: structure of arrays, one float32 field per quantity,
 // [S][512] with S = local + ghost blocks ("store order" = the caller's block order, ghosts last),
 // voxel index x + 8y + 64z inside a block.  Each 8^3 block of one field is a contiguous,
-// 2 KiB-aligned run, so one warp reads 128 contiguous bytes per instruction.
+// 256 B-aligned 2 KiB run: one TMA bulk copy per field per block, 128 contiguous bytes per warp load.
+// ū and p are double-buffered (in = [cur], out = [cur ^ 1]) so a launch only reads values that no
+// CTA of the same launch writes.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -22,33 +24,48 @@ inline int counted(int r) {
 
 constexpr int kBlockVox = 512;     // 8^3 voxels per block
 constexpr int kThreads = 128;      // CTA size of the per-block kernels: 4 voxels per thread
-constexpr int kVoxPerThread = 4;
-
-// Work-item modes of the fused kernel (SURVEY §8(e) two-launch schedule).
-enum : uint8_t { MODE_FULL = 0, MODE_DUAL = 1, MODE_PRIMAL = 2 };
+constexpr int kNbr = 12;           // 6 face neighbours (−x,+x,−y,+y,−z,+z) + 6 edge (diagonal) neighbours
+// Edge neighbours read by the −face halo recompute, as block-coordinate offsets (iterate.cu):
+//   6: (−1,+1,0)  7: (−1,0,+1)  8: (+1,−1,0)  9: (0,−1,+1)  10: (+1,0,−1)  11: (0,+1,−1)
 
 struct Fields {
-    const float *f;       // fused TSDF (read only)
-    const float *W;       // fusion weight (read only), Ω ⇔ W > 0
-    float *u;             // primal u
-    float *ub[2];         // relaxed primal ū, ping-pong (in = ub[cur], out = ub[cur ^ 1])
-    float *px, *py, *pz;  // dual p, in place
+    const float *f;        // fused TSDF (read only)
+    const float *W;        // fusion weight (read only), Ω ⇔ W > 0
+    float *u;              // primal u (in place: only its own CTA touches a voxel's u)
+    float *ub[2];          // relaxed primal ū, double-buffered
+    float *px[2], *py[2], *pz[2];  // dual p, double-buffered
 };
+
+// The buffers of one iteration, selected on the host (no dynamic indexing in kernels).
+struct View {
+    const float *f, *W;
+    float *u;
+    const float *ub_in;
+    float *ub_out;
+    const float *px_in, *py_in, *pz_in;
+    float *px_out, *py_out, *pz_out;
+};
+
+inline View view_of(const Fields &F, int cur) {
+    const int o = cur ^ 1;
+    return View{F.f, F.W, F.u, F.ub[cur], F.ub[o], F.px[cur], F.py[cur], F.pz[cur], F.px[o], F.py[o], F.pz[o]};
+}
 
 struct IterParams {
     float sigma;     // σ
     float tau;       // τ
     float tl;        // fl(τ·λ) (data-term threshold per unit weight)
     float theta;     // θ
-    float denom;     // fl(1 + σ·ε) (Huber damping divisor)
+    float kappa;     // fl(1 / fl(1 + σ·ε)) (Huber damping factor, reading c-18)
     int data_term;   // 0 L1, 1 L2
 };
 
-// Launchers (return the number of kernel launches issued, or -1 on a launch error).
-int launch_fused(const Fields &F, int cur, const int32_t *nbr, const int32_t *work, const uint8_t *mode,
-                 int64_t n_work, uint32_t *flags, uint32_t *ticket, const IterParams &P, cudaStream_t s);
-int launch_two_kernel(const Fields &F, int cur, const int32_t *nbr, const int32_t *work, int64_t n_work,
-                      const IterParams &P, cudaStream_t s);
+// Iteration launchers (return the number of kernel launches, or -1 on a launch error).
+// work == nullptr means blocks 0 .. n_work-1.
+int launch_fused(const View &V, const int32_t *nbr, const int32_t *work, int64_t n_work, const IterParams &P,
+                 cudaStream_t s);
+int launch_two_kernel(const View &V, const int32_t *nbr, const int32_t *work, int64_t n_work, const IterParams &P,
+                      cudaStream_t s);
 
 // store build
 int launch_hash_count(const int32_t *xyz, int64_t n, uint32_t T, uint32_t *hash, uint32_t *count,
@@ -67,7 +84,7 @@ int launch_init_state(const Fields &F, int64_t nvox, int init, cudaStream_t s);
 int launch_sanitize_state(const Fields &F, int cur, const int32_t *nbr, int64_t n_blocks, cudaStream_t s);
 
 // energy: per-block partial sums, then one deterministic final reduction into out[5]
-int launch_energy(const Fields &F, const int32_t *nbr, const int32_t *blocks, int64_t n_blocks, float lam,
+int launch_energy(const View &V, const int32_t *nbr, const int32_t *blocks, int64_t n_blocks, float lam,
                   float eps, int data_term, double *partials, double *out, cudaStream_t s);
 
 uint32_t host_hash(int32_t x, int32_t y, int32_t z, uint32_t T);

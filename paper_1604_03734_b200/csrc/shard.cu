@@ -1,23 +1,20 @@
 // shard.cu — route-axis spatial sharding across GPUs (north_star (c)).
 //
-// Every rank holds the blocks it owns (caller-supplied owner map `part`, contiguous ranges along the
-// route arc length) plus ghost copies of the remote blocks its stencils touch:
-//   G−  remote −x/−y/−z face neighbours of local blocks.  A local primal step needs their p^{k+1};
-//       instead of waiting for the owner mid-iteration, the rank recomputes their dual step from
-//       ū^k, p^k, W (same device function, so bit-identical to the owner's result);
-//   G+  remote +x/+y/+z face neighbours of local blocks and of G− blocks (ū^k and W read by duals).
-// Per iteration, one message per peer carries ū^k, p_x, p_y, p_z of the ghost blocks (W once at
-// set-up).  The iteration is split into two launches of the fused kernel:
-//   A: every local block whose dual needs no ghost data (dual; primal too if its −neighbours are
-//      all in A) — runs while the halo exchange is in flight;
-//   B: G− ghost duals, the duals of local blocks with a remote +neighbour, and the remaining
-//      primal steps — after the halo has landed.
-// Both lists are in topological order and every wait of a B item is on an A item or an earlier B
-// item, so the per-block counters of iterate.cu stay deadlock free.  The result is bitwise equal
-// to the single-GPU result (no reduction crosses GPUs inside the iteration).
-// Transports: NCCL point-to-point (ncclSend/ncclRecv in one group, on a communication stream that
-// overlaps launch A) or, for tests on one GPU, a loopback of device-to-device copies between handles
-// of one process (vol_group_connect / vol_regularise_group).
+// Every rank holds the blocks it owns (caller-supplied owner map `part`: contiguous ranges along the
+// route arc length) plus ghost copies of the remote blocks its stencil reads: every remote block among
+// the 12 neighbours (6 faces + 6 edges) of a local block.  The fused kernel (iterate.cu) recomputes the
+// −face duals itself, so one halo message per peer and iteration — ū^k, p^k (x, y, z) of the ghost
+// blocks; W and f once at set-up — makes every local block computable without any other
+// inter-GPU dependency.  Per iteration:
+//   pack (send blocks' ū^k, p^k → send buffer) on the compute stream;
+//   [comm stream]    ncclSend/ncclRecv with each peer in one group → unpack into the ghost rows;
+//   [compute stream] launch A = local blocks with no remote neighbour (overlaps the exchange),
+//                    wait for the halo, launch B = the remaining local blocks.
+// Reads and writes never alias: the kernels read buffers [cur] and write [cur^1]; ghost rows are
+// only written by unpack and only read by launch B.  The result is bitwise equal to the single-GPU
+// result (no reduction crosses GPUs inside the iteration).
+// Transports: NCCL point-to-point, or for tests on one GPU a loopback of device-to-device copies
+// between handles of one process (vol_group_connect / vol_regularise_group / vol_group_energy).
 #include <nccl.h>
 
 #include <algorithm>
@@ -33,17 +30,29 @@ using namespace hvg;
 
 // ------------------------------------------------------------------------------ host planning
 
-void hvg::topo_sort_rows(const int32_t *xyz, const std::vector<int64_t> &g, std::vector<int32_t> &rows) {
+static uint64_t spread3(uint32_t v) {  // 21 bits → every third bit
+    uint64_t x = v & 0x1FFFFFu;
+    x = (x | (x << 32)) & 0x1F00000000FFFFull;
+    x = (x | (x << 16)) & 0x1F0000FF0000FFull;
+    x = (x | (x << 8)) & 0x100F00F00F00F00Full;
+    x = (x | (x << 4)) & 0x10C30C30C30C30C3ull;
+    x = (x | (x << 2)) & 0x1249249249249249ull;
+    return x;
+}
+
+// Morton (Z-order) of the block coordinates (offset by 2^20): consecutive CTAs work on spatially
+// close blocks, so the halo a CTA reads was recently brought into L2 by its neighbours' CTAs.
+void hvg::morton_sort_rows(const int32_t *xyz, const std::vector<int64_t> &g, std::vector<int32_t> &rows) {
+    std::vector<std::pair<uint64_t, int32_t>> key(g.size());
+    for (size_t k = 0; k < g.size(); k++) {
+        const int32_t *c = xyz + 3 * g[k];
+        uint64_t m = spread3((uint32_t)(c[0] + (1 << 20))) | (spread3((uint32_t)(c[1] + (1 << 20))) << 1) |
+                     (spread3((uint32_t)(c[2] + (1 << 20))) << 2);
+        key[k] = {m, (int32_t)k};
+    }
+    std::sort(key.begin(), key.end());
     rows.resize(g.size());
-    std::iota(rows.begin(), rows.end(), 0);
-    std::sort(rows.begin(), rows.end(), [&](int32_t a, int32_t b) {
-        const int32_t *A = xyz + 3 * g[a], *B = xyz + 3 * g[b];
-        int64_t sa = (int64_t)A[0] + A[1] + A[2], sb = (int64_t)B[0] + B[1] + B[2];
-        if (sa != sb) return sa < sb;
-        if (A[0] != B[0]) return A[0] < B[0];
-        if (A[1] != B[1]) return A[1] < B[1];
-        return A[2] < B[2];
-    });
+    for (size_t k = 0; k < g.size(); k++) rows[k] = key[k].second;
 }
 
 namespace {
@@ -81,126 +90,64 @@ bool hvg::make_shard_plan(const int32_t *xyz, int64_t n, const int32_t *part, in
             return false;
         }
     }
+    static const int OFF[kNbr][3] = {{-1, 0, 0}, {1, 0, 0},  {0, -1, 0}, {0, 1, 0},  {0, 0, -1}, {0, 0, 1},
+                                     {-1, 1, 0}, {-1, 0, 1}, {1, -1, 0}, {0, -1, 1}, {1, 0, -1}, {0, 1, -1}};
     auto nb = [&](int64_t g, int d) -> int64_t {
-        Key k{xyz[3 * g], xyz[3 * g + 1], xyz[3 * g + 2]};
-        int32_t *c = d < 2 ? &k.x : (d < 4 ? &k.y : &k.z);
-        *c += (d & 1) ? 1 : -1;
+        Key k{xyz[3 * g] + OFF[d][0], xyz[3 * g + 1] + OFF[d][1], xyz[3 * g + 2] + OFF[d][2]};
         auto it = idx.find(k);
         return it == idx.end() ? -1 : it->second;
     };
-    // ghost sets of every rank (each rank's send lists are other ranks' ghost sets)
-    std::vector<std::vector<int64_t>> gm(world), gp(world);
+    // ghost sets of every rank (a rank's send lists are the other ranks' ghost sets)
+    std::vector<std::vector<int64_t>> gh(world);
     for (int64_t g = 0; g < n; g++) {
         const int q = part[g];
-        for (int d = 0; d < 6; d++) {
+        for (int d = 0; d < kNbr; d++) {
             int64_t c = nb(g, d);
-            if (c >= 0 && part[c] != q) ((d & 1) ? gp : gm)[q].push_back(c);
+            if (c >= 0 && part[c] != q) gh[q].push_back(c);
         }
     }
     for (int q = 0; q < world; q++) {
-        std::sort(gm[q].begin(), gm[q].end());
-        gm[q].erase(std::unique(gm[q].begin(), gm[q].end()), gm[q].end());
-        for (int64_t c : gm[q])
-            for (int d = 1; d < 6; d += 2) {
-                int64_t c2 = nb(c, d);
-                if (c2 >= 0 && part[c2] != q) gp[q].push_back(c2);
-            }
-        std::sort(gp[q].begin(), gp[q].end());
-        gp[q].erase(std::unique(gp[q].begin(), gp[q].end()), gp[q].end());
-    }
-    auto ghosts_of = [&](int q) {
-        std::vector<int64_t> all(gm[q]);
-        all.insert(all.end(), gp[q].begin(), gp[q].end());
-        std::sort(all.begin(), all.end(), [&](int64_t a, int64_t b) {
+        std::sort(gh[q].begin(), gh[q].end(), [&](int64_t a, int64_t b) {
             return part[a] != part[b] ? part[a] < part[b] : a < b;
         });
-        all.erase(std::unique(all.begin(), all.end()), all.end());
-        return all;
-    };
+        gh[q].erase(std::unique(gh[q].begin(), gh[q].end()), gh[q].end());
+    }
     for (int64_t g = 0; g < n; g++)
         if (part[g] == rank) P.local.push_back(g);
-    P.ghost = ghosts_of(rank);
-    std::unordered_set<int64_t> gmset(gm[rank].begin(), gm[rank].end());
-    P.ghost_dual.resize(P.ghost.size());
-    for (size_t k = 0; k < P.ghost.size(); k++) P.ghost_dual[k] = gmset.count(P.ghost[k]) ? 1 : 0;
+    P.ghost = gh[rank];
     P.recv_off.assign(world, 0);
     P.recv_cnt.assign(world, 0);
     for (size_t k = 0; k < P.ghost.size(); k++) P.recv_cnt[part[P.ghost[k]]]++;
     for (int q = 1; q < world; q++) P.recv_off[q] = P.recv_off[q - 1] + P.recv_cnt[q - 1];
-    // store row of each global block held here
     std::unordered_map<int64_t, int64_t> row;
     for (size_t r = 0; r < P.local.size(); r++) row[P.local[r]] = (int64_t)r;
-    for (size_t k = 0; k < P.ghost.size(); k++) row[P.ghost[k]] = (int64_t)(P.local.size() + k);
-    // send lists: what each peer's ghost set holds of ours, in that peer's receive order
     P.send_off.assign(world, 0);
     P.send_cnt.assign(world, 0);
     for (int q = 0; q < world; q++) {
         P.send_off[q] = (int64_t)P.send_rows.size();
         if (q == rank) continue;
-        for (int64_t c : ghosts_of(q))
+        for (int64_t c : gh[q])
             if (part[c] == rank) P.send_rows.push_back(row.at(c));
         P.send_cnt[q] = (int64_t)P.send_rows.size() - P.send_off[q];
     }
-    // two-launch schedule
-    const int64_t nl = (int64_t)P.local.size();
-    std::vector<uint8_t> remote_plus(nl, 0), in_pb(nl, 0);
-    for (int64_t r = 0; r < nl; r++)
-        for (int d = 1; d < 6; d += 2) {
+    // launch A: local blocks whose 12 neighbours are all local (or unallocated); launch B: the rest
+    std::vector<int64_t> ga, gb, ra, rb;
+    for (int64_t r = 0; r < (int64_t)P.local.size(); r++) {
+        bool remote = false;
+        for (int d = 0; d < kNbr && !remote; d++) {
             int64_t c = nb(P.local[r], d);
-            if (c >= 0 && part[c] != rank) remote_plus[r] = 1;
+            remote = c >= 0 && part[c] != rank;
         }
-    for (int64_t r = 0; r < nl; r++) {
-        if (remote_plus[r]) {
-            in_pb[r] = 1;
-            continue;
-        }
-        for (int d = 0; d < 6; d += 2) {
-            int64_t c = nb(P.local[r], d);
-            if (c < 0) continue;
-            if (part[c] != rank || remote_plus[row.at(c)]) in_pb[r] = 1;
-        }
+        (remote ? gb : ga).push_back(P.local[r]);
+        (remote ? rb : ra).push_back(r);
     }
-    std::vector<int64_t> ga, gb;
-    std::vector<uint8_t> ma, mb;
-    std::vector<int64_t> ra, rb;  // store rows
-    for (int64_t r = 0; r < nl; r++) {
-        if (!remote_plus[r]) {
-            ra.push_back(r);
-            ma.push_back(in_pb[r] ? MODE_DUAL : MODE_FULL);
-            if (in_pb[r]) {
-                rb.push_back(r);
-                mb.push_back(MODE_PRIMAL);
-            }
-        } else {
-            rb.push_back(r);
-            mb.push_back(MODE_FULL);
-        }
-    }
-    for (size_t k = 0; k < P.ghost.size(); k++)
-        if (P.ghost_dual[k]) {
-            rb.push_back(nl + (int64_t)k);
-            mb.push_back(MODE_DUAL);
-        }
-    auto global_of = [&](int64_t r) { return r < nl ? P.local[r] : P.ghost[r - nl]; };
-    for (auto pr : {std::make_pair(&ra, &ma), std::make_pair(&rb, &mb)}) {
-        std::vector<int64_t> gl(pr.first->size());
-        for (size_t k = 0; k < gl.size(); k++) gl[k] = global_of((*pr.first)[k]);
-        std::vector<int32_t> ord;
-        topo_sort_rows(xyz, gl, ord);
-        std::vector<int32_t> w(ord.size());
-        std::vector<uint8_t> m(ord.size());
-        for (size_t k = 0; k < ord.size(); k++) {
-            w[k] = (int32_t)(*pr.first)[ord[k]];
-            m[k] = (*pr.second)[ord[k]];
-        }
-        if (pr.first == &ra) {
-            P.workA = w;
-            P.modeA = m;
-        } else {
-            P.workB = w;
-            P.modeB = m;
-        }
-    }
+    std::vector<int32_t> ord;
+    morton_sort_rows(xyz, ga, ord);
+    P.workA.resize(ord.size());
+    for (size_t k = 0; k < ord.size(); k++) P.workA[k] = (int32_t)ra[ord[k]];
+    morton_sort_rows(xyz, gb, ord);
+    P.workB.resize(ord.size());
+    for (size_t k = 0; k < ord.size(); k++) P.workB[k] = (int32_t)rb[ord[k]];
     return true;
 }
 
@@ -233,7 +180,6 @@ struct ShardRuntime {
     float *sendbuf = nullptr, *recvbuf = nullptr;
     int32_t *send_rows = nullptr;
     int32_t *workA = nullptr, *workB = nullptr;
-    uint8_t *modeA = nullptr, *modeB = nullptr;
     unsigned long long *omega = nullptr;  // [2] device scratch for the Ω count all-reduce
     bool connected = false;
 };
@@ -245,8 +191,6 @@ size_t hvg::shard_extra_bytes(const ShardPlan &P) {
     c.take<int32_t>(P.send_rows.size() + 1);
     c.take<int32_t>(P.workA.size() + 1);
     c.take<int32_t>(P.workB.size() + 1);
-    c.take<uint8_t>(P.modeA.size() + 1);
-    c.take<uint8_t>(P.modeB.size() + 1);
     c.take<unsigned long long>(4);
     return c.off + 512;
 }
@@ -341,8 +285,6 @@ vol_status shard_setup(vol_s *v, const ShardPlan &plan, const int32_t *hxyz, con
     R->send_rows = c.take<int32_t>(P.send_rows.size() + 1);
     R->workA = c.take<int32_t>(P.workA.size() + 1);
     R->workB = c.take<int32_t>(P.workB.size() + 1);
-    R->modeA = c.take<uint8_t>(P.modeA.size() + 1);
-    R->modeB = c.take<uint8_t>(P.modeB.size() + 1);
     R->omega = c.take<unsigned long long>(4);
     // neighbour table in store rows: global → store row map (reuses the hash scratch) and row → global
     const int64_t n = v->L.n_global, S = v->L.S;
@@ -365,8 +307,6 @@ vol_status shard_setup(vol_s *v, const ShardPlan &plan, const int32_t *hxyz, con
     CK(cudaMemcpyAsync(R->send_rows, send32.data(), send32.size() * 4, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(R->workA, P.workA.data(), P.workA.size() * 4, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(R->workB, P.workB.data(), P.workB.size() * 4, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(R->modeA, P.modeA.data(), P.modeA.size(), cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(R->modeB, P.modeB.data(), P.modeB.size(), cudaMemcpyHostToDevice, s));
     CK(cudaStreamSynchronize(s));  // host vectors go out of scope
     CK(cudaStreamCreateWithFlags(&R->cs, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&R->ev_pack, cudaEventDisableTiming));
@@ -411,19 +351,18 @@ static vol_status nccl_iteration(vol_s *v, const IterParams &P, int64_t &launche
     ShardRuntime *R = v->shard;
     cudaStream_t s = v->stream;
     const int cur = v->cur;
-    vol_status st = pack(v, v->F.ub[cur], v->F.px, v->F.py, v->F.pz, s);
+    vol_status st = pack(v, v->F.ub[cur], v->F.px[cur], v->F.py[cur], v->F.pz[cur], s);
     if (st != VOL_OK) return st;
     CK(cudaEventRecord(R->ev_pack, s));
     CK(cudaStreamWaitEvent(R->cs, R->ev_pack, 0));
     if ((st = nccl_exchange(v, R->cs)) != VOL_OK) return st;
-    if ((st = unpack(v, v->F.ub[cur], v->F.px, v->F.py, v->F.pz, R->cs)) != VOL_OK) return st;
+    if ((st = unpack(v, v->F.ub[cur], v->F.px[cur], v->F.py[cur], v->F.pz[cur], R->cs)) != VOL_OK) return st;
     CK(cudaEventRecord(R->ev_halo, R->cs));
-    int r = launch_fused(v->F, cur, v->d_nbr, R->workA, R->modeA, (int64_t)R->plan.workA.size(), v->d_flags,
-                         v->d_ticket, P, s);
+    const View V = view_of(v->F, cur);
+    int r = launch_fused(V, v->d_nbr, R->workA, (int64_t)R->plan.workA.size(), P, s);
     CKL(r);
     CK(cudaStreamWaitEvent(s, R->ev_halo, 0));
-    int r2 = launch_fused(v->F, cur, v->d_nbr, R->workB, R->modeB, (int64_t)R->plan.workB.size(), v->d_flags,
-                          v->d_ticket, P, s);
+    int r2 = launch_fused(V, v->d_nbr, R->workB, (int64_t)R->plan.workB.size(), P, s);
     CKL(r2);
     launches += r + r2 + 2;  // + pack + unpack
     v->cur ^= 1;
@@ -448,10 +387,11 @@ vol_status shard_refresh_for_energy(vol_s *v) {
     ShardRuntime *R = v->shard;
     if (!R->nccl) return VOL_OK;  // loopback: vol_group_energy refreshes
     cudaStream_t s = v->stream;
-    vol_status st = pack(v, v->F.u, v->F.px, v->F.py, v->F.pz, s);
+    const int c = v->cur;
+    vol_status st = pack(v, v->F.u, v->F.px[c], v->F.py[c], v->F.pz[c], s);
     if (st != VOL_OK) return st;
     if ((st = nccl_exchange(v, s)) != VOL_OK) return st;
-    return unpack(v, v->F.u, v->F.px, v->F.py, v->F.pz, s);
+    return unpack(v, v->F.u, v->F.px[c], v->F.py[c], v->F.pz[c], s);
 }
 
 vol_status shard_allreduce_energy(vol_s *v, double *d_eout) {
@@ -550,16 +490,17 @@ extern "C" vol_status vol_regularise_group(vol_t *h, int world, float lambda, fl
     for (int32_t k = 0; k < iters; k++) {
         const int cur = h[0]->cur;
         for (int r = 0; r < world; r++)
-            if ((st = pack(h[r], h[r]->F.ub[cur], h[r]->F.px, h[r]->F.py, h[r]->F.pz, s)) != VOL_OK) return st;
+            if ((st = pack(h[r], h[r]->F.ub[cur], h[r]->F.px[cur], h[r]->F.py[cur], h[r]->F.pz[cur], s)) != VOL_OK)
+                return st;
         if ((st = loopback_exchange(h, world, s)) != VOL_OK) return st;
         for (int r = 0; r < world; r++) {
             ShardRuntime *R = h[r]->shard;
-            if ((st = unpack(h[r], h[r]->F.ub[cur], h[r]->F.px, h[r]->F.py, h[r]->F.pz, s)) != VOL_OK) return st;
-            int a = launch_fused(h[r]->F, cur, h[r]->d_nbr, R->workA, R->modeA, (int64_t)R->plan.workA.size(),
-                                 h[r]->d_flags, h[r]->d_ticket, P, s);
+            if ((st = unpack(h[r], h[r]->F.ub[cur], h[r]->F.px[cur], h[r]->F.py[cur], h[r]->F.pz[cur], s)) != VOL_OK)
+                return st;
+            const View V = view_of(h[r]->F, cur);
+            int a = launch_fused(V, h[r]->d_nbr, R->workA, (int64_t)R->plan.workA.size(), P, s);
             CKL(a);
-            int b = launch_fused(h[r]->F, cur, h[r]->d_nbr, R->workB, R->modeB, (int64_t)R->plan.workB.size(),
-                                 h[r]->d_flags, h[r]->d_ticket, P, s);
+            int b = launch_fused(V, h[r]->d_nbr, R->workB, (int64_t)R->plan.workB.size(), P, s);
             CKL(b);
             launches += a + b + 2;
         }
@@ -577,13 +518,16 @@ extern "C" vol_status vol_group_energy(vol_t *h, int world, float lambda, float 
     if (st != VOL_OK) return st;
     if (!primal) return fail(VOL_EINVAL, "vol_group_energy: primal is NULL");
     cudaStream_t s = h[0]->stream;
-    for (int r = 0; r < world; r++)
-        if ((st = pack(h[r], h[r]->F.u, h[r]->F.px, h[r]->F.py, h[r]->F.pz, s)) != VOL_OK) return st;
+    for (int r = 0; r < world; r++) {
+        const int c = h[r]->cur;
+        if ((st = pack(h[r], h[r]->F.u, h[r]->F.px[c], h[r]->F.py[c], h[r]->F.pz[c], s)) != VOL_OK) return st;
+    }
     if ((st = loopback_exchange(h, world, s)) != VOL_OK) return st;
     double acc[5] = {0, 0, 0, 0, 1.0};
     for (int r = 0; r < world; r++) {
-        if ((st = unpack(h[r], h[r]->F.u, h[r]->F.px, h[r]->F.py, h[r]->F.pz, s)) != VOL_OK) return st;
-        CKL(launch_energy(h[r]->F, h[r]->d_nbr, nullptr, h[r]->L.n_local, lambda, eps, data_term, h[r]->d_part,
+        const int c = h[r]->cur;
+        if ((st = unpack(h[r], h[r]->F.u, h[r]->F.px[c], h[r]->F.py[c], h[r]->F.pz[c], s)) != VOL_OK) return st;
+        CKL(launch_energy(view_of(h[r]->F, c), h[r]->d_nbr, nullptr, h[r]->L.n_local, lambda, eps, data_term, h[r]->d_part,
                           h[r]->d_eout, s));
         double o[5];
         CK(cudaMemcpyAsync(o, h[r]->d_eout, sizeof o, cudaMemcpyDeviceToHost, s));

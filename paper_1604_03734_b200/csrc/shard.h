@@ -21,13 +21,11 @@ struct ShardPlan {
     int rank = 0, world = 1;
     std::vector<int64_t> local;        // global index of store row r < n_local
     std::vector<int64_t> ghost;        // global index of store row n_local + k
-    std::vector<uint8_t> ghost_dual;   // 1: −neighbour ghost (its dual is recomputed here), 0: +side only
     std::vector<int64_t> recv_off, recv_cnt;  // [world] slice of `ghost` received from each peer
     std::vector<int64_t> send_rows;    // local store rows sent, grouped by peer (rank order), peer's recv order
     std::vector<int64_t> send_off, send_cnt;  // [world] slice of send_rows per peer
-    // work lists (store rows) of the two launches per iteration, topological order, with modes
+    // work lists (store rows, Morton order): A = no remote neighbour, B = the rest
     std::vector<int32_t> workA, workB;
-    std::vector<uint8_t> modeA, modeB;
     std::string error;
     int64_t n_local() const { return (int64_t)local.size(); }
     int64_t n_ghost() const { return (int64_t)ghost.size(); }
@@ -36,8 +34,8 @@ struct ShardPlan {
 // Computes rank `rank`'s plan from the global block coordinates and owner map (host only).
 bool make_shard_plan(const int32_t *xyz, int64_t n_global, const int32_t *part, int world, int rank, ShardPlan &plan);
 
-// Topological order of store rows given their global indices (key x+y+z, then x, y, z).
-void topo_sort_rows(const int32_t *xyz, const std::vector<int64_t> &global_of_row, std::vector<int32_t> &rows);
+// Morton order of the given global blocks: rows[k] = position (in `global_of_row`) of the k-th block.
+void morton_sort_rows(const int32_t *xyz, const std::vector<int64_t> &global_of_row, std::vector<int32_t> &rows);
 
 size_t shard_extra_bytes(const ShardPlan &plan);
 

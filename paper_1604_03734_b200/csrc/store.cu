@@ -186,19 +186,21 @@ int launch_bucket_sort_and_dups(const int32_t *xyz, const uint32_t *start, int32
     return cudaPeekAtLastError() == cudaSuccess ? counted(1) : -1;
 }
 
-// nbr[6r + d] for store row r (global block index rows[r], or r itself when rows == NULL): the store
-// index of the face neighbour in direction d = (−x,+x,−y,+y,−z,+z), −1 if unallocated (Ω̄) or
-// not held by this rank.
+// nbr[12r + d] for store row r (global block index rows[r], or r itself when rows == NULL): the store
+// index of the neighbour at offset d — faces (−x,+x,−y,+y,−z,+z), then the six edge neighbours of
+// internal.h — or −1 if unallocated (Ω̄) or not held by this rank.
+__constant__ int8_t c_nbr_off[kNbr][3] = {{-1, 0, 0}, {1, 0, 0},  {0, -1, 0}, {0, 1, 0},  {0, 0, -1}, {0, 0, 1},
+                                          {-1, 1, 0}, {-1, 0, 1}, {1, -1, 0}, {0, -1, 1}, {1, 0, -1}, {0, 1, -1}};
+
 __global__ void k_neighbours(const int32_t *__restrict__ xyz, const uint32_t *__restrict__ start,
                              const int32_t *__restrict__ entry, uint32_t T, const int32_t *__restrict__ store_of_global,
                              const int64_t *__restrict__ rows, int64_t n_rows, int32_t *__restrict__ nbr) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= 6 * n_rows) return;
-    int64_t r = k / 6;
-    int d = (int)(k % 6);
+    if (k >= kNbr * n_rows) return;
+    int64_t r = k / kNbr;
+    int d = (int)(k % kNbr);
     int64_t g = rows ? rows[r] : r;
-    int32_t q[3] = {xyz[3 * g], xyz[3 * g + 1], xyz[3 * g + 2]};
-    q[d >> 1] += (d & 1) ? 1 : -1;
+    int32_t q[3] = {xyz[3 * g] + c_nbr_off[d][0], xyz[3 * g + 1] + c_nbr_off[d][1], xyz[3 * g + 2] + c_nbr_off[d][2]};
     uint32_t h = hash3(q[0], q[1], q[2], T);
     int32_t found = -1;
     for (uint32_t m = start[h]; m < start[h + 1]; m++) {
@@ -217,29 +219,34 @@ int launch_neighbours(const int32_t *xyz, int64_t n, const uint32_t *start, cons
                       cudaStream_t s) {
     (void)n;
     if (n_rows == 0) return 0;
-    k_neighbours<<<grid_for(6 * n_rows, 256), 256, 0, s>>>(xyz, start, entry, T, store_of_global, rows, n_rows, nbr);
+    k_neighbours<<<grid_for(kNbr * n_rows, 256), 256, 0, s>>>(xyz, start, entry, T, store_of_global, rows, n_rows,
+                                                              nbr);
     return cudaPeekAtLastError() == cudaSuccess ? counted(1) : -1;
 }
 
-// f finite, W finite and >= 0 (VOL_EDATA otherwise); counts Ω = {W > 0}.
+// f finite, W finite and >= 0 (VOL_EDATA otherwise); counts Ω = {W > 0}: one atomic per CTA.
 __global__ void k_validate(const float *__restrict__ f, const float *__restrict__ W, int64_t nvox,
                            unsigned long long *bad, unsigned long long *n_omega) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    __shared__ unsigned s_cnt;
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
     unsigned om = 0;
-    if (i < nvox) {
-        float fv = f[i], wv = W[i];
-        bool ok = isfinite(fv) && isfinite(wv) && wv >= 0.0f;
-        if (!ok) atomicMin(bad, (unsigned long long)i);
-        om = wv > 0.0f ? 1u : 0u;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvox; i += (int64_t)gridDim.x * blockDim.x) {
+        const float fv = f[i], wv = W[i];
+        if (!(isfinite(fv) && isfinite(wv) && wv >= 0.0f)) atomicMin(bad, (unsigned long long)i);
+        om += wv > 0.0f ? 1u : 0u;
     }
-    unsigned c = __popc(__ballot_sync(0xffffffffu, om));
-    if ((threadIdx.x & 31) == 0 && c) atomicAdd(n_omega, (unsigned long long)c);
+    for (int o = 16; o > 0; o >>= 1) om += __shfl_xor_sync(0xffffffffu, om, o);
+    if ((threadIdx.x & 31) == 0 && om) atomicAdd(&s_cnt, om);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_cnt) atomicAdd(n_omega, (unsigned long long)s_cnt);
 }
 
 int launch_validate(const float *f, const float *W, int64_t nvox, unsigned long long *bad, unsigned long long *n_omega,
                     cudaStream_t s) {
     if (nvox == 0) return 0;
-    k_validate<<<grid_for(nvox, 256), 256, 0, s>>>(f, W, nvox, bad, n_omega);
+    int64_t g = grid_for(nvox, 256);
+    k_validate<<<(unsigned)(g < 148 * 16 ? g : 148 * 16), 256, 0, s>>>(f, W, nvox, bad, n_omega);
     return cudaPeekAtLastError() == cudaSuccess ? counted(1) : -1;
 }
 
@@ -253,9 +260,12 @@ __global__ void k_init_state(Fields F, int64_t nvox, int init) {
     F.u[i] = u0;
     F.ub[0][i] = u0;
     F.ub[1][i] = u0;
-    F.px[i] = 0.0f;
-    F.py[i] = 0.0f;
-    F.pz[i] = 0.0f;
+    F.px[0][i] = 0.0f;
+    F.py[0][i] = 0.0f;
+    F.pz[0][i] = 0.0f;
+    F.px[1][i] = 0.0f;
+    F.py[1][i] = 0.0f;
+    F.pz[1][i] = 0.0f;
 }
 
 int launch_init_state(const Fields &F, int64_t nvox, int init, cudaStream_t s) {
@@ -264,44 +274,46 @@ int launch_init_state(const Fields &F, int64_t nvox, int init, cudaStream_t s) {
     return cudaPeekAtLastError() == cudaSuccess ? counted(1) : -1;
 }
 
-// After vol_load_state: Ω̄ voxels get u = ū = f (both ū buffers) and p = 0; on Ω voxels the
-// components of p that live on invalid edges are set to 0 (the invariant the iteration keeps, see
-// iterate.cu), so a loaded state behaves exactly like one produced by the iteration.
+// After vol_load_state: Ω̄ voxels get u = ū = f (both ū buffers) and p = 0 (both buffers); on Ω
+// voxels the components of p that live on invalid edges are set to 0 (the invariant the iteration
+// keeps, see iterate.cu), so a loaded state behaves exactly like one produced by the iteration.
 __global__ void k_sanitize_state(Fields F, int cur, const int32_t *__restrict__ nbr, int64_t nvox) {
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= nvox) return;
-    const int64_t b = v / 512;
-    const int i = (int)(v % 512);
-    float *pc[3] = {F.px, F.py, F.pz};
+    const int64_t b = v / kBlockVox;
+    const int i = (int)(v % kBlockVox);
+    float *ubc = cur ? F.ub[1] : F.ub[0];
+    float *ubo = cur ? F.ub[0] : F.ub[1];
+    float *pc[3] = {cur ? F.px[1] : F.px[0], cur ? F.py[1] : F.py[0], cur ? F.pz[1] : F.pz[0]};
+    float *po[3] = {cur ? F.px[0] : F.px[1], cur ? F.py[0] : F.py[1], cur ? F.pz[0] : F.pz[1]};
     if (!(F.W[v] > 0.0f)) {
         float fv = F.f[v];
         F.u[v] = fv;
-        F.ub[cur][v] = fv;
-        F.ub[cur ^ 1][v] = fv;
-        F.px[v] = 0.0f;
-        F.py[v] = 0.0f;
-        F.pz[v] = 0.0f;
+        ubc[v] = fv;
+        ubo[v] = fv;
+        for (int a = 0; a < 3; a++) pc[a][v] = po[a][v] = 0.0f;
         return;
     }
-    F.ub[cur ^ 1][v] = F.ub[cur][v];
+    ubo[v] = ubc[v];
     int c[3] = {i & 7, (i >> 3) & 7, i >> 6};
     for (int a = 0; a < 3; a++) {
         int q[3] = {c[0], c[1], c[2]};
         q[a] += 1;
         int64_t w;
         if (q[a] > 7) {
-            int32_t nb = nbr[6 * b + 2 * a + 1];
+            int32_t nb = nbr[kNbr * b + 2 * a + 1];
             q[a] = 0;
-            w = nb < 0 ? -1 : (int64_t)nb * 512 + q[0] + 8 * q[1] + 64 * q[2];
+            w = nb < 0 ? -1 : (int64_t)nb * kBlockVox + q[0] + 8 * q[1] + 64 * q[2];
         } else {
-            w = b * 512 + q[0] + 8 * q[1] + 64 * q[2];
+            w = b * kBlockVox + q[0] + 8 * q[1] + 64 * q[2];
         }
         if (w < 0 || !(F.W[w] > 0.0f)) pc[a][v] = 0.0f;
+        po[a][v] = pc[a][v];
     }
 }
 
 int launch_sanitize_state(const Fields &F, int cur, const int32_t *nbr, int64_t n_blocks, cudaStream_t s) {
-    int64_t nvox = n_blocks * 512;
+    int64_t nvox = n_blocks * kBlockVox;
     if (nvox == 0) return 0;
     k_sanitize_state<<<grid_for(nvox, 256), 256, 0, s>>>(F, cur, nbr, nvox);
     return cudaPeekAtLastError() == cudaSuccess ? counted(1) : -1;

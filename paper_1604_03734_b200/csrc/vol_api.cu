@@ -66,17 +66,18 @@ bool is_device_ptr(const void *p) {
 
 static void carve_all(Carve &c, vol_s *v, const Layout &L) {
     const int64_t nv = L.S * kBlockVox;
-    float *fields[8];
-    for (int k = 0; k < 8; k++) fields[k] = c.take<float>(nv);
+    float *fields[11];
+    for (int k = 0; k < 11; k++) fields[k] = c.take<float>(nv);
     if (v) {
         v->F.f = fields[0];
         v->F.W = fields[1];
         v->F.u = fields[2];
-        v->F.ub[0] = fields[3];
-        v->F.ub[1] = fields[4];
-        v->F.px = fields[5];
-        v->F.py = fields[6];
-        v->F.pz = fields[7];
+        for (int k = 0; k < 2; k++) {
+            v->F.ub[k] = fields[3 + k];
+            v->F.px[k] = fields[5 + k];
+            v->F.py[k] = fields[7 + k];
+            v->F.pz[k] = fields[9 + k];
+        }
     }
     auto xyz = c.take<int32_t>(3 * (size_t)L.n_global + 3);
     auto hash = c.take<uint32_t>((size_t)L.n_global + 1);
@@ -84,11 +85,8 @@ static void carve_all(Carve &c, vol_s *v, const Layout &L) {
     auto start = c.take<uint32_t>((size_t)L.T + 1);
     auto entry = c.take<int32_t>((size_t)L.n_global + 1);
     auto scan = c.take<uint32_t>((size_t)L.T / 4096 + 4);
-    auto nbr = c.take<int32_t>(6 * (size_t)L.S);
+    auto nbr = c.take<int32_t>(kNbr * (size_t)L.S);
     auto work = c.take<int32_t>((size_t)L.S + 1);
-    auto mode = c.take<uint8_t>((size_t)L.S + 1);
-    auto flags = c.take<uint32_t>((size_t)L.S + 1);
-    auto ticket = c.take<uint32_t>(4);
     auto misc = c.take<unsigned long long>(4);
     auto part = c.take<double>(5 * (size_t)L.S + 5);
     auto eout = c.take<double>(8);
@@ -101,9 +99,6 @@ static void carve_all(Carve &c, vol_s *v, const Layout &L) {
         v->d_scan = scan;
         v->d_nbr = nbr;
         v->d_work = work;
-        v->d_mode = mode;
-        v->d_flags = flags;
-        v->d_ticket = ticket;
         v->d_misc = misc;
         v->d_part = part;
         v->d_eout = eout;
@@ -135,7 +130,7 @@ extern "C" size_t vol_workspace_bytes(const int32_t *block_xyz, int64_t n_global
 }
 
 static vol_status copy_in(void *dst, const void *src, size_t bytes, cudaStream_t s) {
-    CK(cudaMemcpyAsync(dst, src, bytes, is_device_ptr(src) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s));
     return VOL_OK;
 }
 
@@ -251,15 +246,13 @@ extern "C" vol_status vol_create(const int32_t *block_xyz, int64_t n_global, con
             return bail(fail(VOL_ECUDA, "neighbour launch failed"));
         std::vector<int64_t> rows(n_global);
         std::iota(rows.begin(), rows.end(), 0);
-        topo_sort_rows(hxyz.data(), rows, work);
+        morton_sort_rows(hxyz.data(), rows, work);
     } else {
         st = shard_setup(v, plan, hxyz.data(), dist, work);
         if (st != VOL_OK) return bail(st);
     }
     v->n_work = (int64_t)work.size();
-    if (cudaMemcpyAsync(v->d_work, work.data(), work.size() * 4, cudaMemcpyHostToDevice, s) != cudaSuccess ||
-        cudaMemsetAsync(v->d_flags, 0, ((size_t)L.S + 1) * 4, s) != cudaSuccess ||
-        cudaMemsetAsync(v->d_ticket, 0, 16, s) != cudaSuccess)
+    if (cudaMemcpyAsync(v->d_work, work.data(), work.size() * 4, cudaMemcpyHostToDevice, s) != cudaSuccess)
         return bail(fail(VOL_ECUDA, "work list upload failed"));
     // K3: initial state (warm start) so read_u / energy are defined before the first iteration
     if (launch_init_state(v->F, L.S * kBlockVox, 0, s) < 0) return bail(fail(VOL_ECUDA, "init launch failed"));
@@ -290,8 +283,9 @@ static vol_status run_iterations_single(vol_s *v, const IterParams &P, int32_t i
     cudaStream_t s = v->stream;
     int64_t launches = 0;
     auto one = [&](cudaStream_t st, int cur) -> int {
-        if (kernel == 1) return launch_two_kernel(v->F, cur, v->d_nbr, v->d_work, v->n_work, P, st);
-        return launch_fused(v->F, cur, v->d_nbr, v->d_work, nullptr, v->n_work, v->d_flags, v->d_ticket, P, st);
+        const View V = view_of(v->F, cur);
+        if (kernel == 1) return launch_two_kernel(V, v->d_nbr, v->d_work, v->n_work, P, st);
+        return launch_fused(V, v->d_nbr, v->d_work, v->n_work, P, st);
     };
     // CUDA graph of 2·m iterations (ū parity returns to the start), replayed; remainder launched directly.
     const int m = std::min<int>(16, iters / 2);
@@ -368,8 +362,9 @@ vol_status vol_regularise_prepare(vol_s *v, float lambda, float eps, float tau, 
     volatile float tl = tau * lambda;  // fl(τ·λ)
     volatile float se = sigma * eps;   // fl(σ·ε)
     volatile float dn = 1.0f + se;     // fl(1 + σε)
+    volatile float kp = 1.0f / dn;     // κ = fl(1 / fl(1 + σε))
     P.tl = tl;
-    P.denom = dn;
+    P.kappa = kp;
     P.theta = o.theta;
     P.data_term = o.data_term;
     v->pending_kernel = o.kernel;
@@ -400,12 +395,8 @@ extern "C" vol_status vol_sync(vol_t v) {
 }
 
 static vol_status copy_out(void *dst, const void *src, size_t bytes, cudaStream_t s) {
-    if (is_device_ptr(dst)) {
-        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s));
-    } else {
-        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-    }
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s));
+    if (!is_device_ptr(dst)) CK(cudaStreamSynchronize(s));
     return VOL_OK;
 }
 
@@ -422,9 +413,9 @@ extern "C" vol_status vol_read_state(vol_t v, float *u, float *ubar, float *p) {
     if (ubar && (st = copy_out(ubar, v->F.ub[v->cur], nb, v->stream)) != VOL_OK) return st;
     if (p) {
         const size_t nv = (size_t)v->L.n_local * kBlockVox;
-        if ((st = copy_out(p, v->F.px, nb, v->stream)) != VOL_OK) return st;
-        if ((st = copy_out(p + nv, v->F.py, nb, v->stream)) != VOL_OK) return st;
-        if ((st = copy_out(p + 2 * nv, v->F.pz, nb, v->stream)) != VOL_OK) return st;
+        if ((st = copy_out(p, v->F.px[v->cur], nb, v->stream)) != VOL_OK) return st;
+        if ((st = copy_out(p + nv, v->F.py[v->cur], nb, v->stream)) != VOL_OK) return st;
+        if ((st = copy_out(p + 2 * nv, v->F.pz[v->cur], nb, v->stream)) != VOL_OK) return st;
     }
     return VOL_OK;
 }
@@ -439,9 +430,9 @@ extern "C" vol_status vol_load_state(vol_t v, const float *u, const float *ubar,
     if (ubar && (st = copy_in(v->F.ub[v->cur], ubar, nb, s)) != VOL_OK) return st;
     if (p) {
         const size_t nv = (size_t)v->L.n_local * kBlockVox;
-        if ((st = copy_in(v->F.px, p, nb, s)) != VOL_OK) return st;
-        if ((st = copy_in(v->F.py, p + nv, nb, s)) != VOL_OK) return st;
-        if ((st = copy_in(v->F.pz, p + 2 * nv, nb, s)) != VOL_OK) return st;
+        if ((st = copy_in(v->F.px[v->cur], p, nb, s)) != VOL_OK) return st;
+        if ((st = copy_in(v->F.py[v->cur], p + nv, nb, s)) != VOL_OK) return st;
+        if ((st = copy_in(v->F.pz[v->cur], p + 2 * nv, nb, s)) != VOL_OK) return st;
     }
     CKL(launch_sanitize_state(v->F, v->cur, v->d_nbr, v->L.n_local, s));
     CK(cudaStreamSynchronize(s));
@@ -456,7 +447,8 @@ extern "C" vol_status vol_energy(vol_t v, float lambda, float eps, int data_term
         vol_status st = shard_refresh_for_energy(v);
         if (st != VOL_OK) return st;
     }
-    CKL(launch_energy(v->F, v->d_nbr, nullptr, v->L.n_local, lambda, eps, data_term, v->d_part, v->d_eout, v->stream));
+    CKL(launch_energy(view_of(v->F, v->cur), v->d_nbr, nullptr, v->L.n_local, lambda, eps, data_term, v->d_part,
+                      v->d_eout, v->stream));
     double o[5];
     if (v->shard) {
         vol_status st = shard_allreduce_energy(v, v->d_eout);
@@ -489,7 +481,13 @@ extern "C" vol_status vol_read_tables(vol_t v, uint32_t *T, uint32_t *bucket_sta
         return st;
     if (nbr) {
         if (v->shard) return fail(VOL_ENOTSUP, "vol_read_tables: nbr of a sharded volume is in store indices");
-        if ((st = copy_out(nbr, v->d_nbr, (size_t)v->L.S * 6 * 4, v->stream)) != VOL_OK) return st;
+        std::vector<int32_t> all((size_t)v->L.S * kNbr);
+        CK(cudaMemcpyAsync(all.data(), v->d_nbr, all.size() * 4, cudaMemcpyDeviceToHost, v->stream));
+        CK(cudaStreamSynchronize(v->stream));
+        std::vector<int32_t> faces((size_t)v->L.S * 6);
+        for (int64_t r = 0; r < v->L.S; r++)
+            for (int d = 0; d < 6; d++) faces[6 * r + d] = all[kNbr * r + d];
+        if ((st = copy_out(nbr, faces.data(), faces.size() * 4, v->stream)) != VOL_OK) return st;
     }
     return VOL_OK;
 }

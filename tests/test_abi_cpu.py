@@ -55,25 +55,20 @@ def test_block_hash_matches_oracle(native):
         assert block_hash(x, y, z, T) == oracle.block_hash(x, y, z, T)
 
 
-def _brute_ghosts(c, part, rank):
-    idx = {tuple(v): i for i, v in enumerate(c.tolist())}
-    D = [(-1, 0, 0), (1, 0, 0), (0, -1, 0), (0, 1, 0), (0, 0, -1), (0, 0, 1)]
+OFF12 = [(-1, 0, 0), (1, 0, 0), (0, -1, 0), (0, 1, 0), (0, 0, -1), (0, 0, 1),
+         (-1, 1, 0), (-1, 0, 1), (1, -1, 0), (0, -1, 1), (1, 0, -1), (0, 1, -1)]
 
-    def nb(g, d):
-        q = tuple(np.add(c[g], D[d]))
-        return idx.get(q, -1)
-    gm, gp = set(), set()
+
+def _brute_ghosts(c, part, rank):
+    """Remote blocks among the 12 stencil neighbours (6 faces + 6 edges) of the rank's blocks."""
+    idx = {tuple(v): i for i, v in enumerate(c.tolist())}
+    out = set()
     for g in np.nonzero(part == rank)[0]:
-        for d in range(6):
-            k = nb(g, d)
+        for o in OFF12:
+            k = idx.get(tuple(np.add(c[g], o)), -1)
             if k >= 0 and part[k] != rank:
-                (gp if d % 2 else gm).add(k)
-    for k in list(gm):
-        for d in (1, 3, 5):
-            k2 = nb(k, d)
-            if k2 >= 0 and part[k2] != rank:
-                gp.add(k2)
-    return gm | gp
+                out.add(k)
+    return out
 
 
 @pytest.mark.parametrize("world", [2, 3, 4])

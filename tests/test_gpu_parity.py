@@ -214,3 +214,34 @@ def test_gpu_invariants_tiny(V, tiny_scene):
     assert np.array_equal(u[pin], f[pin])                           # λ→∞ pinning
     _, _, p = vol.state()
     assert float(torch.sqrt((p ** 2).sum(0)).max()) <= 1 + 1e-6     # feasibility
+
+
+# ------------------------------------------------------------------ sharded path (loopback, 1 GPU)
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_loopback_shards_bitwise_equal_single(V, world):
+    from paper_1604_03734_b200 import connect_group, group_energy, regularise_group
+    s = random_instance(500, seed=10 + world, extent=6, w_density=0.7, lam=0.4, eps=0.01, iters=40)
+    c = s.coords
+    # contiguous ranges along x (the route axis), ties by y
+    key = c[:, 0].to(torch.int64) * 64 + c[:, 1].to(torch.int64)
+    order = torch.argsort(key, stable=True)
+    part = torch.empty(len(c), dtype=torch.int32)
+    for r in range(world):
+        part[order[r * len(c) // world:(r + 1) * len(c) // world]] = r
+    vols = []
+    for r in range(world):
+        mine = (part == r).nonzero().squeeze(1)
+        vols.append(V(c, s.f[mine], s.W[mine], part=part, loopback=(r, world)))
+    assert all(v.n_ghost > 0 for v in vols)
+    connect_group(vols)
+    regularise_group(vols, s.lam, s.eps, s.tau, s.sigma, s.iters)
+    u = torch.empty(len(c), 512)
+    for r, v in enumerate(vols):
+        mine = (part == r).nonzero().squeeze(1)
+        u[mine] = v.u().cpu()
+    single, u1 = run_gpu(V, s)
+    assert np.array_equal(u.numpy(), u1)
+    P1, D1 = single.energy(s.lam, s.eps, s.data_term)
+    Pg, Dg = group_energy(vols, s.lam, s.eps, s.data_term)
+    assert abs(P1 - Pg) <= 1e-9 * abs(P1) and abs(D1 - Dg) <= 1e-9 * abs(P1)
