@@ -69,11 +69,11 @@ struct vol_s {
     int32_t *d_entry = nullptr;        // [n_global]
     uint32_t *d_scan = nullptr;        // scan scratch
     int32_t *d_nbr = nullptr;          // [S][12] store indices (6 faces + 6 edge neighbours)
-    int32_t *d_work = nullptr;         // [S] work list (Morton order)
+    int32_t *d_perm = nullptr;         // [n_local] caller index of store row r
+    float *d_tmp = nullptr;            // [n_local][512] scratch for caller-order I/O
     unsigned long long *d_misc = nullptr;  // [4]: dup, bad, n_omega, spare
     double *d_part = nullptr;          // [S][5]
     double *d_eout = nullptr;          // [8]
-    int64_t n_work = 0;
     int64_t last_launches = 0;
     // sharded state (world > 1)
     ShardRuntime *shard = nullptr;

@@ -62,8 +62,9 @@ struct IterParams {
 
 // Iteration launchers (return the number of kernel launches, or -1 on a launch error).
 // work == nullptr means blocks 0 .. n_work-1.
-int launch_fused(const View &V, const int32_t *nbr, const int32_t *work, int64_t n_work, const IterParams &P,
-                 cudaStream_t s);
+// Fused iteration over work items [first, first + n_work) (work == nullptr: store rows).
+int launch_fused(const View &V, const int32_t *nbr, const int32_t *work, int64_t first, int64_t n_work,
+                 const IterParams &P, cudaStream_t s);
 int launch_two_kernel(const View &V, const int32_t *nbr, const int32_t *work, int64_t n_work, const IterParams &P,
                       cudaStream_t s);
 
@@ -81,6 +82,8 @@ int launch_neighbours(const int32_t *xyz, int64_t n, const uint32_t *start, cons
 int launch_validate(const float *f, const float *W, int64_t nvox, unsigned long long *bad,
                     unsigned long long *n_omega, cudaStream_t s);
 int launch_init_state(const Fields &F, int64_t nvox, int init, cudaStream_t s);
+// gather: dst[r] = src[perm[r]] (caller → store order); scatter: dst[perm[r]] = src[r] (store → caller)
+int launch_permute_blocks(const float *src, float *dst, const int32_t *perm, int64_t n, bool gather, cudaStream_t s);
 int launch_sanitize_state(const Fields &F, int cur, const int32_t *nbr, int64_t n_blocks, cudaStream_t s);
 
 // energy: per-block partial sums, then one deterministic final reduction into out[5]

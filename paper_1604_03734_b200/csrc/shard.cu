@@ -112,8 +112,30 @@ bool hvg::make_shard_plan(const int32_t *xyz, int64_t n, const int32_t *part, in
         });
         gh[q].erase(std::unique(gh[q].begin(), gh[q].end()), gh[q].end());
     }
-    for (int64_t g = 0; g < n; g++)
-        if (part[g] == rank) P.local.push_back(g);
+    // store order of the local blocks: launch A (no remote neighbour among the 12) then launch B, each in
+    // Morton order, so both launches are contiguous row ranges; local_caller maps a row to the block's
+    // position among the rank's blocks in global order (the caller's f / W / u layout).
+    std::vector<int64_t> ga, gb, ca, cb;
+    int64_t nl = 0;
+    for (int64_t g = 0; g < n; g++) {
+        if (part[g] != rank) continue;
+        bool remote = false;
+        for (int d = 0; d < kNbr && !remote; d++) {
+            int64_t c = nb(g, d);
+            remote = c >= 0 && part[c] != rank;
+        }
+        (remote ? gb : ga).push_back(g);
+        (remote ? cb : ca).push_back(nl++);
+    }
+    std::vector<int32_t> ord;
+    for (auto pr : {std::make_pair(&ga, &ca), std::make_pair(&gb, &cb)}) {
+        morton_sort_rows(xyz, *pr.first, ord);
+        for (int32_t k : ord) {
+            P.local.push_back((*pr.first)[k]);
+            P.local_caller.push_back((int32_t)(*pr.second)[k]);
+        }
+    }
+    P.nA = (int64_t)ga.size();
     P.ghost = gh[rank];
     P.recv_off.assign(world, 0);
     P.recv_cnt.assign(world, 0);
@@ -130,24 +152,6 @@ bool hvg::make_shard_plan(const int32_t *xyz, int64_t n, const int32_t *part, in
             if (part[c] == rank) P.send_rows.push_back(row.at(c));
         P.send_cnt[q] = (int64_t)P.send_rows.size() - P.send_off[q];
     }
-    // launch A: local blocks whose 12 neighbours are all local (or unallocated); launch B: the rest
-    std::vector<int64_t> ga, gb, ra, rb;
-    for (int64_t r = 0; r < (int64_t)P.local.size(); r++) {
-        bool remote = false;
-        for (int d = 0; d < kNbr && !remote; d++) {
-            int64_t c = nb(P.local[r], d);
-            remote = c >= 0 && part[c] != rank;
-        }
-        (remote ? gb : ga).push_back(P.local[r]);
-        (remote ? rb : ra).push_back(r);
-    }
-    std::vector<int32_t> ord;
-    morton_sort_rows(xyz, ga, ord);
-    P.workA.resize(ord.size());
-    for (size_t k = 0; k < ord.size(); k++) P.workA[k] = (int32_t)ra[ord[k]];
-    morton_sort_rows(xyz, gb, ord);
-    P.workB.resize(ord.size());
-    for (size_t k = 0; k < ord.size(); k++) P.workB[k] = (int32_t)rb[ord[k]];
     return true;
 }
 
@@ -179,7 +183,6 @@ struct ShardRuntime {
     cudaEvent_t ev_pack = nullptr, ev_halo = nullptr;
     float *sendbuf = nullptr, *recvbuf = nullptr;
     int32_t *send_rows = nullptr;
-    int32_t *workA = nullptr, *workB = nullptr;
     unsigned long long *omega = nullptr;  // [2] device scratch for the Ω count all-reduce
     bool connected = false;
 };
@@ -189,8 +192,6 @@ size_t hvg::shard_extra_bytes(const ShardPlan &P) {
     c.take<float>((size_t)P.send_rows.size() * kMsgFloats + 4);
     c.take<float>((size_t)P.ghost.size() * kMsgFloats + 4);
     c.take<int32_t>(P.send_rows.size() + 1);
-    c.take<int32_t>(P.workA.size() + 1);
-    c.take<int32_t>(P.workB.size() + 1);
     c.take<unsigned long long>(4);
     return c.off + 512;
 }
@@ -269,10 +270,7 @@ extern "C" vol_status vol_nccl_unique_id(void *out128) {
     return VOL_OK;
 }
 
-vol_status shard_setup(vol_s *v, const ShardPlan &plan, const int32_t *hxyz, const vol_dist *dist,
-                       std::vector<int32_t> &work) {
-    (void)hxyz;
-    work.clear();
+vol_status shard_setup(vol_s *v, const ShardPlan &plan, const vol_dist *dist) {
     ShardRuntime *R = new ShardRuntime();
     v->shard = R;
     R->plan = plan;
@@ -283,31 +281,10 @@ vol_status shard_setup(vol_s *v, const ShardPlan &plan, const int32_t *hxyz, con
     R->sendbuf = c.take<float>((size_t)P.send_rows.size() * kMsgFloats + 4);
     R->recvbuf = c.take<float>((size_t)P.ghost.size() * kMsgFloats + 4);
     R->send_rows = c.take<int32_t>(P.send_rows.size() + 1);
-    R->workA = c.take<int32_t>(P.workA.size() + 1);
-    R->workB = c.take<int32_t>(P.workB.size() + 1);
     R->omega = c.take<unsigned long long>(4);
-    // neighbour table in store rows: global → store row map (reuses the hash scratch) and row → global
-    const int64_t n = v->L.n_global, S = v->L.S;
-    std::vector<int32_t> store_of_global(n, -1);
-    std::vector<int64_t> global_of_row(S);
-    for (int64_t r = 0; r < P.n_local(); r++) {
-        store_of_global[P.local[r]] = (int32_t)r;
-        global_of_row[r] = P.local[r];
-    }
-    for (int64_t k = 0; k < P.n_ghost(); k++) {
-        store_of_global[P.ghost[k]] = (int32_t)(P.n_local() + k);
-        global_of_row[P.n_local() + k] = P.ghost[k];
-    }
     std::vector<int32_t> send32(P.send_rows.begin(), P.send_rows.end());
-    int32_t *d_sog = reinterpret_cast<int32_t *>(v->d_hash);
-    int64_t *d_rows = reinterpret_cast<int64_t *>(v->d_part);
-    CK(cudaMemcpyAsync(d_sog, store_of_global.data(), n * 4, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(d_rows, global_of_row.data(), S * 8, cudaMemcpyHostToDevice, s));
-    CKL(launch_neighbours(v->d_xyz, n, v->d_start, v->d_entry, v->L.T, d_sog, d_rows, S, v->d_nbr, s));
     CK(cudaMemcpyAsync(R->send_rows, send32.data(), send32.size() * 4, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(R->workA, P.workA.data(), P.workA.size() * 4, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(R->workB, P.workB.data(), P.workB.size() * 4, cudaMemcpyHostToDevice, s));
-    CK(cudaStreamSynchronize(s));  // host vectors go out of scope
+    CK(cudaStreamSynchronize(s));  // the host vector goes out of scope
     CK(cudaStreamCreateWithFlags(&R->cs, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&R->ev_pack, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&R->ev_halo, cudaEventDisableTiming));
@@ -359,10 +336,11 @@ static vol_status nccl_iteration(vol_s *v, const IterParams &P, int64_t &launche
     if ((st = unpack(v, v->F.ub[cur], v->F.px[cur], v->F.py[cur], v->F.pz[cur], R->cs)) != VOL_OK) return st;
     CK(cudaEventRecord(R->ev_halo, R->cs));
     const View V = view_of(v->F, cur);
-    int r = launch_fused(V, v->d_nbr, R->workA, (int64_t)R->plan.workA.size(), P, s);
+    const ShardPlan &SP = R->plan;
+    int r = launch_fused(V, v->d_nbr, nullptr, 0, SP.nA, P, s);
     CKL(r);
     CK(cudaStreamWaitEvent(s, R->ev_halo, 0));
-    int r2 = launch_fused(V, v->d_nbr, R->workB, (int64_t)R->plan.workB.size(), P, s);
+    int r2 = launch_fused(V, v->d_nbr, nullptr, SP.nA, SP.n_local() - SP.nA, P, s);
     CKL(r2);
     launches += r + r2 + 2;  // + pack + unpack
     v->cur ^= 1;
@@ -498,9 +476,9 @@ extern "C" vol_status vol_regularise_group(vol_t *h, int world, float lambda, fl
             if ((st = unpack(h[r], h[r]->F.ub[cur], h[r]->F.px[cur], h[r]->F.py[cur], h[r]->F.pz[cur], s)) != VOL_OK)
                 return st;
             const View V = view_of(h[r]->F, cur);
-            int a = launch_fused(V, h[r]->d_nbr, R->workA, (int64_t)R->plan.workA.size(), P, s);
+            int a = launch_fused(V, h[r]->d_nbr, nullptr, 0, R->plan.nA, P, s);
             CKL(a);
-            int b = launch_fused(V, h[r]->d_nbr, R->workB, (int64_t)R->plan.workB.size(), P, s);
+            int b = launch_fused(V, h[r]->d_nbr, nullptr, R->plan.nA, R->plan.n_local() - R->plan.nA, P, s);
             CKL(b);
             launches += a + b + 2;
         }

@@ -19,13 +19,13 @@ namespace hvg {
 // index inside a group (= the order in which that owner sends them).
 struct ShardPlan {
     int rank = 0, world = 1;
-    std::vector<int64_t> local;        // global index of store row r < n_local
+    std::vector<int64_t> local;        // global index of store row r < n_local (launch A rows, then B rows)
+    std::vector<int32_t> local_caller; // position of store row r among the rank's blocks in global order
+    int64_t nA = 0;                    // rows [0, nA): no remote neighbour (launch A); [nA, n_local): launch B
     std::vector<int64_t> ghost;        // global index of store row n_local + k
     std::vector<int64_t> recv_off, recv_cnt;  // [world] slice of `ghost` received from each peer
     std::vector<int64_t> send_rows;    // local store rows sent, grouped by peer (rank order), peer's recv order
     std::vector<int64_t> send_off, send_cnt;  // [world] slice of send_rows per peer
-    // work lists (store rows, Morton order): A = no remote neighbour, B = the rest
-    std::vector<int32_t> workA, workB;
     std::string error;
     int64_t n_local() const { return (int64_t)local.size(); }
     int64_t n_ghost() const { return (int64_t)ghost.size(); }
@@ -43,8 +43,7 @@ size_t shard_extra_bytes(const ShardPlan &plan);
 
 // runtime hooks (shard.cu)
 struct ShardRuntime;
-vol_status shard_setup(vol_s *v, const hvg::ShardPlan &plan, const int32_t *hxyz, const vol_dist *dist,
-                       std::vector<int32_t> &work_unused);
+vol_status shard_setup(vol_s *v, const hvg::ShardPlan &plan, const vol_dist *dist);
 vol_status shard_after_create(vol_s *v);
 vol_status shard_reset(vol_s *v);
 vol_status shard_iterate(vol_s *v, const hvg::IterParams &P, int32_t iters);

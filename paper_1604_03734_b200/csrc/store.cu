@@ -319,4 +319,21 @@ int launch_sanitize_state(const Fields &F, int cur, const int32_t *nbr, int64_t 
     return cudaPeekAtLastError() == cudaSuccess ? counted(1) : -1;
 }
 
+// Block permutation between the caller's order and the store order (one 2 KiB row per block):
+// gather: dst[r] = src[perm[r]];  scatter: dst[perm[r]] = src[r].
+__global__ void k_permute_blocks(const float4 *__restrict__ src, float4 *__restrict__ dst,
+                                 const int32_t *__restrict__ perm, int gather) {
+    const int64_t r = blockIdx.x;
+    const int64_t p = perm[r];
+    const int64_t from = gather ? p : r, to = gather ? r : p;
+    dst[to * 128 + threadIdx.x] = src[from * 128 + threadIdx.x];
+}
+
+int launch_permute_blocks(const float *src, float *dst, const int32_t *perm, int64_t n, bool gather, cudaStream_t s) {
+    if (n == 0) return 0;
+    k_permute_blocks<<<(unsigned)n, 128, 0, s>>>(reinterpret_cast<const float4 *>(src), reinterpret_cast<float4 *>(dst),
+                                                 perm, gather ? 1 : 0);
+    return cudaPeekAtLastError() == cudaSuccess ? counted(1) : -1;
+}
+
 }  // namespace hvg

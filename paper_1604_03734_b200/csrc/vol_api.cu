@@ -17,6 +17,8 @@
 #include "internal.h"
 #include "shard.h"
 
+#include <cstdarg>
+
 using namespace hvg;
 
 std::atomic<long long> hvg::g_launches{0};
@@ -86,7 +88,8 @@ static void carve_all(Carve &c, vol_s *v, const Layout &L) {
     auto entry = c.take<int32_t>((size_t)L.n_global + 1);
     auto scan = c.take<uint32_t>((size_t)L.T / 4096 + 4);
     auto nbr = c.take<int32_t>(kNbr * (size_t)L.S);
-    auto work = c.take<int32_t>((size_t)L.S + 1);
+    auto perm = c.take<int32_t>((size_t)L.n_local + 1);
+    auto tmp = c.take<float>((size_t)L.n_local * kBlockVox + 4);
     auto misc = c.take<unsigned long long>(4);
     auto part = c.take<double>(5 * (size_t)L.S + 5);
     auto eout = c.take<double>(8);
@@ -98,7 +101,8 @@ static void carve_all(Carve &c, vol_s *v, const Layout &L) {
         v->d_entry = entry;
         v->d_scan = scan;
         v->d_nbr = nbr;
-        v->d_work = work;
+        v->d_perm = perm;
+        v->d_tmp = tmp;
         v->d_misc = misc;
         v->d_part = part;
         v->d_eout = eout;
@@ -198,27 +202,48 @@ extern "C" vol_status vol_create(const int32_t *block_xyz, int64_t n_global, con
     v->extra = c.base + ((c.off + 255) & ~(size_t)255);
     cudaStream_t s = v->stream;
 
-    // inputs
+    // store order: Morton order of the blocks (single GPU) or the shard plan's [launch A | launch B]
+    // rows + ghosts; row_caller[r] is the block's index in the caller's f / W / u arrays
+    std::vector<int64_t> row_global;
+    std::vector<int32_t> row_caller;
+    if (!sharded) {
+        std::vector<int64_t> all(n_global);
+        std::iota(all.begin(), all.end(), 0);
+        morton_sort_rows(hxyz.data(), all, row_caller);
+        row_global.assign(row_caller.begin(), row_caller.end());
+    } else {
+        row_global = plan.local;
+        row_global.insert(row_global.end(), plan.ghost.begin(), plan.ghost.end());
+        row_caller = plan.local_caller;
+    }
+    std::vector<int32_t> store_of_global(n_global, -1);
+    for (int64_t r = 0; r < L.S; r++) store_of_global[row_global[r]] = (int32_t)r;
+
+    // inputs: coordinates as given; f and W through a staging copy, then permuted into store order
     vol_status st;
     if ((st = copy_in(v->d_xyz, block_xyz, 3 * (size_t)n_global * 4, s)) != VOL_OK) return bail(st);
     const size_t fbytes = (size_t)L.n_local * kBlockVox * 4;
-    if ((st = copy_in((void *)v->F.f, f, fbytes, s)) != VOL_OK) return bail(st);
-    if ((st = copy_in((void *)v->F.W, W, fbytes, s)) != VOL_OK) return bail(st);
+    if (cudaMemcpyAsync(v->d_perm, row_caller.data(), (size_t)L.n_local * 4, cudaMemcpyHostToDevice, s) != cudaSuccess)
+        return bail(fail(VOL_ECUDA, "permutation upload failed"));
+    if ((st = copy_in(v->d_tmp, f, fbytes, s)) != VOL_OK) return bail(st);
+    if ((st = copy_in(v->F.u, W, fbytes, s)) != VOL_OK) return bail(st);
+    if (launch_permute_blocks(v->d_tmp, const_cast<float *>(v->F.f), v->d_perm, L.n_local, true, s) < 0 ||
+        launch_permute_blocks(v->F.u, const_cast<float *>(v->F.W), v->d_perm, L.n_local, true, s) < 0)
+        return bail(fail(VOL_ECUDA, "input permutation failed"));
 
     // K1: hash + CSR bucket table over all n_global blocks
     if (cudaMemsetAsync(v->d_count, 0, ((size_t)L.T + 1) * 4, s) != cudaSuccess ||
         cudaMemsetAsync(v->d_misc, 0, 4 * 8, s) != cudaSuccess ||
         cudaMemsetAsync(v->d_misc, 0xFF, 2 * 8, s) != cudaSuccess)
         return bail(fail(VOL_ECUDA, "memset failed"));
-    int nl = 0;
-    if ((nl = launch_hash_count(v->d_xyz, n_global, L.T, v->d_hash, v->d_count, s)) < 0 ||
-        (nl = launch_exclusive_scan_u32(v->d_count, v->d_start, L.T, v->d_scan, s)) < 0)
+    if (launch_hash_count(v->d_xyz, n_global, L.T, v->d_hash, v->d_count, s) < 0 ||
+        launch_exclusive_scan_u32(v->d_count, v->d_start, L.T, v->d_scan, s) < 0)
         return bail(fail(VOL_ECUDA, "store build launch failed: %s", cudaGetErrorString(cudaGetLastError())));
     if (cudaMemcpyAsync(v->d_count, v->d_start, (size_t)L.T * 4, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
         return bail(fail(VOL_ECUDA, "cursor copy failed"));
-    if ((nl = launch_bucket_fill(v->d_hash, n_global, v->d_count, v->d_entry, s)) < 0 ||
-        (nl = launch_bucket_sort_and_dups(v->d_xyz, v->d_start, v->d_entry, L.T, n_global, &v->d_misc[0], s)) < 0 ||
-        (nl = launch_validate(v->F.f, v->F.W, (int64_t)L.n_local * kBlockVox, &v->d_misc[1], &v->d_misc[2], s)) < 0)
+    if (launch_bucket_fill(v->d_hash, n_global, v->d_count, v->d_entry, s) < 0 ||
+        launch_bucket_sort_and_dups(v->d_xyz, v->d_start, v->d_entry, L.T, n_global, &v->d_misc[0], s) < 0 ||
+        launch_validate(v->F.f, v->F.W, (int64_t)L.n_local * kBlockVox, &v->d_misc[1], &v->d_misc[2], s) < 0)
         return bail(fail(VOL_ECUDA, "store build launch failed: %s", cudaGetErrorString(cudaGetLastError())));
     unsigned long long misc[3];
     if (cudaMemcpyAsync(misc, v->d_misc, 3 * 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
@@ -231,29 +256,26 @@ extern "C" vol_status vol_create(const int32_t *block_xyz, int64_t n_global, con
     }
     if (misc[1] != ~0ULL) {
         long long i = (long long)misc[1];
-        return bail(fail(VOL_EDATA, "invalid input at local voxel %lld (block %lld, voxel %lld): f must be finite, "
-                                    "W finite and >= 0",
-                         i, i / kBlockVox, i % kBlockVox));
+        return bail(fail(VOL_EDATA, "invalid input in block %lld, voxel %lld: f must be finite, W finite and >= 0",
+                         (long long)row_caller[i / kBlockVox], i % kBlockVox));
     }
     v->n_omega_local = (int64_t)misc[2];
     v->n_omega_global = v->n_omega_local;
 
-    // K2: neighbour table (store indices) + work list
-    std::vector<int32_t> work;
-    if (!sharded) {
-        if (launch_neighbours(v->d_xyz, n_global, v->d_start, v->d_entry, L.T, nullptr, nullptr, n_global, v->d_nbr,
-                              s) < 0)
-            return bail(fail(VOL_ECUDA, "neighbour launch failed"));
-        std::vector<int64_t> rows(n_global);
-        std::iota(rows.begin(), rows.end(), 0);
-        morton_sort_rows(hxyz.data(), rows, work);
-    } else {
-        st = shard_setup(v, plan, hxyz.data(), dist, work);
+    // K2: neighbour table in store rows (faces + edges); the row maps reuse build scratch
+    int32_t *d_sog = reinterpret_cast<int32_t *>(v->d_hash);
+    int64_t *d_rows = reinterpret_cast<int64_t *>(v->d_part);
+    if (cudaMemcpyAsync(d_sog, store_of_global.data(), (size_t)n_global * 4, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemcpyAsync(d_rows, row_global.data(), (size_t)L.S * 8, cudaMemcpyHostToDevice, s) != cudaSuccess)
+        return bail(fail(VOL_ECUDA, "row map upload failed"));
+    if (launch_neighbours(v->d_xyz, n_global, v->d_start, v->d_entry, L.T, d_sog, d_rows, L.S, v->d_nbr, s) < 0)
+        return bail(fail(VOL_ECUDA, "neighbour launch failed"));
+    if (cudaStreamSynchronize(s) != cudaSuccess)  // the host row maps go out of scope
+        return bail(fail(VOL_ECUDA, "vol_create: %s", cudaGetErrorString(cudaGetLastError())));
+    if (sharded) {
+        st = shard_setup(v, plan, dist);
         if (st != VOL_OK) return bail(st);
     }
-    v->n_work = (int64_t)work.size();
-    if (cudaMemcpyAsync(v->d_work, work.data(), work.size() * 4, cudaMemcpyHostToDevice, s) != cudaSuccess)
-        return bail(fail(VOL_ECUDA, "work list upload failed"));
     // K3: initial state (warm start) so read_u / energy are defined before the first iteration
     if (launch_init_state(v->F, L.S * kBlockVox, 0, s) < 0) return bail(fail(VOL_ECUDA, "init launch failed"));
     if (cudaStreamSynchronize(s) != cudaSuccess)
@@ -284,8 +306,8 @@ static vol_status run_iterations_single(vol_s *v, const IterParams &P, int32_t i
     int64_t launches = 0;
     auto one = [&](cudaStream_t st, int cur) -> int {
         const View V = view_of(v->F, cur);
-        if (kernel == 1) return launch_two_kernel(V, v->d_nbr, v->d_work, v->n_work, P, st);
-        return launch_fused(V, v->d_nbr, v->d_work, v->n_work, P, st);
+        if (kernel == 1) return launch_two_kernel(V, v->d_nbr, nullptr, v->L.n_local, P, st);
+        return launch_fused(V, v->d_nbr, nullptr, 0, v->L.n_local, P, st);
     };
     // CUDA graph of 2·m iterations (ū parity returns to the start), replayed; remainder launched directly.
     const int m = std::min<int>(16, iters / 2);
@@ -400,22 +422,45 @@ static vol_status copy_out(void *dst, const void *src, size_t bytes, cudaStream_
     return VOL_OK;
 }
 
+// store order → caller order: scatter straight into a device destination, or through the scratch
+// buffer for a host destination
+static vol_status read_field(vol_s *v, float *dst, const float *src) {
+    cudaStream_t s = v->stream;
+    const int64_t n = v->L.n_local;
+    if (is_device_ptr(dst)) {
+        CKL(launch_permute_blocks(src, dst, v->d_perm, n, false, s));
+        return VOL_OK;
+    }
+    CKL(launch_permute_blocks(src, v->d_tmp, v->d_perm, n, false, s));
+    return copy_out(dst, v->d_tmp, (size_t)n * kBlockVox * 4, s);
+}
+
+// caller order → store order, through the scratch buffer
+static vol_status write_field(vol_s *v, float *dst, const float *src) {
+    cudaStream_t s = v->stream;
+    const int64_t n = v->L.n_local;
+    vol_status st = copy_in(v->d_tmp, src, (size_t)n * kBlockVox * 4, s);
+    if (st != VOL_OK) return st;
+    CKL(launch_permute_blocks(v->d_tmp, dst, v->d_perm, n, true, s));
+    return VOL_OK;
+}
+
 extern "C" vol_status vol_read_u(vol_t v, float *u_out) {
     if (!v || !u_out) return fail(VOL_EINVAL, "vol_read_u: NULL argument");
-    return copy_out(u_out, v->F.u, (size_t)v->L.n_local * kBlockVox * 4, v->stream);
+    return read_field(v, u_out, v->F.u);
 }
 
 extern "C" vol_status vol_read_state(vol_t v, float *u, float *ubar, float *p) {
     if (!v) return fail(VOL_EINVAL, "vol_read_state: NULL handle");
-    const size_t nb = (size_t)v->L.n_local * kBlockVox * 4;
+    const size_t nv = (size_t)v->L.n_local * kBlockVox;
+    const int c = v->cur;
     vol_status st;
-    if (u && (st = copy_out(u, v->F.u, nb, v->stream)) != VOL_OK) return st;
-    if (ubar && (st = copy_out(ubar, v->F.ub[v->cur], nb, v->stream)) != VOL_OK) return st;
+    if (u && (st = read_field(v, u, v->F.u)) != VOL_OK) return st;
+    if (ubar && (st = read_field(v, ubar, v->F.ub[c])) != VOL_OK) return st;
     if (p) {
-        const size_t nv = (size_t)v->L.n_local * kBlockVox;
-        if ((st = copy_out(p, v->F.px[v->cur], nb, v->stream)) != VOL_OK) return st;
-        if ((st = copy_out(p + nv, v->F.py[v->cur], nb, v->stream)) != VOL_OK) return st;
-        if ((st = copy_out(p + 2 * nv, v->F.pz[v->cur], nb, v->stream)) != VOL_OK) return st;
+        if ((st = read_field(v, p, v->F.px[c])) != VOL_OK) return st;
+        if ((st = read_field(v, p + nv, v->F.py[c])) != VOL_OK) return st;
+        if ((st = read_field(v, p + 2 * nv, v->F.pz[c])) != VOL_OK) return st;
     }
     return VOL_OK;
 }
@@ -423,19 +468,18 @@ extern "C" vol_status vol_read_state(vol_t v, float *u, float *ubar, float *p) {
 extern "C" vol_status vol_load_state(vol_t v, const float *u, const float *ubar, const float *p) {
     if (!v) return fail(VOL_EINVAL, "vol_load_state: NULL handle");
     if (v->shard) return fail(VOL_ENOTSUP, "vol_load_state: single-GPU volumes only");
-    const size_t nb = (size_t)v->L.n_local * kBlockVox * 4;
-    cudaStream_t s = v->stream;
+    const size_t nv = (size_t)v->L.n_local * kBlockVox;
+    const int c = v->cur;
     vol_status st;
-    if (u && (st = copy_in(v->F.u, u, nb, s)) != VOL_OK) return st;
-    if (ubar && (st = copy_in(v->F.ub[v->cur], ubar, nb, s)) != VOL_OK) return st;
+    if (u && (st = write_field(v, v->F.u, u)) != VOL_OK) return st;
+    if (ubar && (st = write_field(v, v->F.ub[c], ubar)) != VOL_OK) return st;
     if (p) {
-        const size_t nv = (size_t)v->L.n_local * kBlockVox;
-        if ((st = copy_in(v->F.px[v->cur], p, nb, s)) != VOL_OK) return st;
-        if ((st = copy_in(v->F.py[v->cur], p + nv, nb, s)) != VOL_OK) return st;
-        if ((st = copy_in(v->F.pz[v->cur], p + 2 * nv, nb, s)) != VOL_OK) return st;
+        if ((st = write_field(v, v->F.px[c], p)) != VOL_OK) return st;
+        if ((st = write_field(v, v->F.py[c], p + nv)) != VOL_OK) return st;
+        if ((st = write_field(v, v->F.pz[c], p + 2 * nv)) != VOL_OK) return st;
     }
-    CKL(launch_sanitize_state(v->F, v->cur, v->d_nbr, v->L.n_local, s));
-    CK(cudaStreamSynchronize(s));
+    CKL(launch_sanitize_state(v->F, c, v->d_nbr, v->L.n_local, v->stream));
+    CK(cudaStreamSynchronize(v->stream));
     return VOL_OK;
 }
 
@@ -481,12 +525,16 @@ extern "C" vol_status vol_read_tables(vol_t v, uint32_t *T, uint32_t *bucket_sta
         return st;
     if (nbr) {
         if (v->shard) return fail(VOL_ENOTSUP, "vol_read_tables: nbr of a sharded volume is in store indices");
-        std::vector<int32_t> all((size_t)v->L.S * kNbr);
+        std::vector<int32_t> all((size_t)v->L.S * kNbr), perm((size_t)v->L.n_local);
         CK(cudaMemcpyAsync(all.data(), v->d_nbr, all.size() * 4, cudaMemcpyDeviceToHost, v->stream));
+        CK(cudaMemcpyAsync(perm.data(), v->d_perm, perm.size() * 4, cudaMemcpyDeviceToHost, v->stream));
         CK(cudaStreamSynchronize(v->stream));
         std::vector<int32_t> faces((size_t)v->L.S * 6);
         for (int64_t r = 0; r < v->L.S; r++)
-            for (int d = 0; d < 6; d++) faces[6 * r + d] = all[kNbr * r + d];
+            for (int d = 0; d < 6; d++) {
+                const int32_t q = all[kNbr * r + d];
+                faces[6 * (size_t)perm[r] + d] = q < 0 ? -1 : perm[q];
+            }
         if ((st = copy_out(nbr, faces.data(), faces.size() * 4, v->stream)) != VOL_OK) return st;
     }
     return VOL_OK;

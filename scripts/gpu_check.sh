@@ -10,6 +10,8 @@ for what in "$@"; do
     tests) timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest=$?" >> gpurun_out/status.txt ;;
     smoke) timeout 300 python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1; echo "smoke=$?" >> gpurun_out/status.txt ;;
     bench) timeout 900 python bench.py --steps 3 --warmup 3 > gpurun_out/bench.log 2>&1; echo "bench=$?" >> gpurun_out/status.txt ;;
+    variants)
+      for vv in 0 1; do HVG_FUSED_VARIANT=$vv timeout 600 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/bench_v$vv.log 2>&1; echo "v$vv=$?" >> gpurun_out/status.txt; done ;;
     k1) timeout 600 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --kernel 1 > gpurun_out/bench_k1.log 2>&1; echo "k1=$?" >> gpurun_out/status.txt ;;
     ncu)
       P="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
