@@ -38,7 +38,7 @@ ALG_BYTES_PER_VOXEL = 48  # 28 B read (f, W, u, ū, p×3) + 20 B 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="street")
     ap.add_argument("--iters", type=int, default=None, help="override the config's iteration count")
@@ -69,7 +69,7 @@ class ClockSampler:
         os.close(fd)
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -337,7 +337,7 @@ def main():
                    "blocks": scene.n_blocks, "iters": iters, "lambda": scene.lam, "eps": scene.eps,
                    "data_term": "L1" if scene.data_term == 0 else "L2",
                    "step": "vol_create + vol_regularise(init + iters) + vol_energy + vol_read_u",
-                   "l2": f"inputs larger than L2 ({n_alloc_total * 32 / 1e9:.2f} GB of state)",
+                   "l2": f"inputs larger than L2 ({n_alloc_total * 48 / 1e9:.2f} GB of state vs 126 MB L2)",
                    "parallelism": f"route-axis shards x{world}" if world > 1 else "single GPU",
                    "energy": {"primal": E[0], "dual": E[1]}},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
