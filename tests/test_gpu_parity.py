@@ -245,3 +245,13 @@ def test_loopback_shards_bitwise_equal_single(V, world):
     P1, D1 = single.energy(s.lam, s.eps, s.data_term)
     Pg, Dg = group_energy(vols, s.lam, s.eps, s.data_term)
     assert abs(P1 - Pg) <= 1e-9 * abs(P1) and abs(D1 - Dg) <= 1e-9 * abs(P1)
+
+
+def test_paper_literal_variant(V):
+    # the paper's own iteration — W-weighted L2 prox (Eq. 8), zero init
+    # (P:291), Table I steps σ = 0.5, τ = 1/6, θ = 1 (12·τσ = 1) — with the sign fix of
+    # reading c-2 and the relaxation of c-3, on the tiny sphere at λ = 0.8 (Table I, 10 cm)
+    s = tiny()
+    s.lam, s.eps, s.sigma, s.tau, s.data_term, s.init, s.iters = 0.8, 0.0, 0.5, 1.0 / 6.0, 1, 1, 150
+    _, u = run_gpu(V, s)
+    check_against_oracle(s, u)
