@@ -7,7 +7,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libvol.so")
+LIB_PATH = os.environ.get("HVG_LIBVOL") or os.path.join(_HERE, "libvol.so")  # override: experiments only
 
 VOL_OK, VOL_EINVAL, VOL_EDATA, VOL_ENOMEM, VOL_ECUDA, VOL_ENCCL, VOL_ENOTSUP = range(7)
 _NAMES = {1: "EINVAL", 2: "EDATA", 3: "ENOMEM", 4: "ECUDA", 5: "ENCCL", 6: "ENOTSUP"}

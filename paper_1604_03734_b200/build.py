@@ -44,16 +44,16 @@ def deps():
     return sources() + sorted(glob.glob(os.path.join(CSRC, "*.h"))) + [os.path.join(ROOT, "include", "vol.h"), __file__]
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str = SO, defines=()) -> str:
     newest = max(os.path.getmtime(p) for p in deps())
-    if not force and os.path.exists(SO) and os.path.getmtime(SO) >= newest:
-        return SO
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= newest:
+        return out
     nd = nccl_dir()
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build", os.path.basename(out).replace(".so", ""))
     os.makedirs(objdir, exist_ok=True)
     common = ARCH + ["-O3", "-lineinfo", "-std=c++17", "--fmad=false", "-prec-div=true", "-prec-sqrt=true",
                      "-Xcompiler", "-fPIC,-ffp-contract=off,-O2", "-I", os.path.join(ROOT, "include"),
-                     "-I", os.path.join(nd, "include"), "-Xptxas", "-v" if verbose else "-O3"]
+                     "-I", os.path.join(nd, "include"), "-Xptxas", "-v" if verbose else "-O3"] + [f"-D{d}" for d in defines]
     objs = []
     procs = []
     for src in sources():
@@ -62,18 +62,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
         cmd = [NVCC, "-c", src, "-o", obj] + common
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
     for cmd, p in procs:
-        out, _ = p.communicate()
+        log, _ = p.communicate()
         if verbose or p.returncode:
-            sys.stdout.write(out.decode())
+            sys.stdout.write(log.decode())
         if p.returncode:
             raise RuntimeError("nvcc failed: " + " ".join(cmd))
-    tmp = SO + f".tmp{os.getpid()}"
+    tmp = out + f".tmp{os.getpid()}"
     link = [NVCC, "-shared", "-o", tmp] + objs + ARCH + [
         "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath," + os.path.join(nd, "lib"),
         "-cudart", "shared"]
     subprocess.check_call(link)
-    os.replace(tmp, SO)
-    return SO
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":

@@ -22,3 +22,7 @@ for what in "$@"; do
       echo "full=$?" >> gpurun_out/status.txt ;;
   esac
 done
+# experiment: alternative builds selected with HVG_LIBVOL (names after 'libs')
+if [ "${LIBS:-}" != "" ]; then
+  for L in $LIBS; do HVG_LIBVOL=$PWD/paper_1604_03734_b200/$L timeout 600 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/bench_$L.log 2>&1; echo "$L=$?" >> gpurun_out/status.txt; done
+fi
