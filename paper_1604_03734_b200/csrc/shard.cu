@@ -97,36 +97,33 @@ bool hvg::make_shard_plan(const int32_t *xyz, int64_t n, const int32_t *part, in
         auto it = idx.find(k);
         return it == idx.end() ? -1 : it->second;
     };
-    // ghost sets of every rank (a rank's send lists are the other ranks' ghost sets)
-    std::vector<std::vector<int64_t>> gh(world);
-    for (int64_t g = 0; g < n; g++) {
-        const int q = part[g];
-        for (int d = 0; d < kNbr; d++) {
-            int64_t c = nb(g, d);
-            if (c >= 0 && part[c] != q) gh[q].push_back(c);
-        }
-    }
-    for (int q = 0; q < world; q++) {
-        std::sort(gh[q].begin(), gh[q].end(), [&](int64_t a, int64_t b) {
-            return part[a] != part[b] ? part[a] < part[b] : a < b;
-        });
-        gh[q].erase(std::unique(gh[q].begin(), gh[q].end()), gh[q].end());
-    }
-    // store order of the local blocks: launch A (no remote neighbour among the 12) then launch B, each in
-    // Morton order, so both launches are contiguous row ranges; local_caller maps a row to the block's
-    // position among the rank's blocks in global order (the caller's f / W / u layout).
+    // One pass over the rank's own blocks.  The 12-neighbour relation is symmetric (each edge offset's
+    // inverse is in the set: 6 ↔ 8, 7 ↔ 10, 9 ↔ 11), so the blocks rank q needs from this rank are
+    // exactly this rank's blocks that have a neighbour owned by q: no other rank's plan is needed.
+    std::vector<int64_t> ghosts;
+    std::vector<std::vector<int64_t>> send_g(world);
     std::vector<int64_t> ga, gb, ca, cb;
     int64_t nl = 0;
     for (int64_t g = 0; g < n; g++) {
         if (part[g] != rank) continue;
         bool remote = false;
-        for (int d = 0; d < kNbr && !remote; d++) {
-            int64_t c = nb(g, d);
-            remote = c >= 0 && part[c] != rank;
+        for (int d = 0; d < kNbr; d++) {
+            const int64_t c = nb(g, d);
+            if (c < 0 || part[c] == rank) continue;
+            remote = true;
+            ghosts.push_back(c);
+            send_g[part[c]].push_back(g);
         }
+        // store order of the local blocks: launch A (no remote neighbour) then launch B, each in Morton
+        // order, so both launches are contiguous row ranges; local_caller maps a row to the block's
+        // position among the rank's blocks in global order (the caller's f / W / u layout)
         (remote ? gb : ga).push_back(g);
         (remote ? cb : ca).push_back(nl++);
     }
+    std::sort(ghosts.begin(), ghosts.end(), [&](int64_t a, int64_t b) {
+        return part[a] != part[b] ? part[a] < part[b] : a < b;
+    });
+    ghosts.erase(std::unique(ghosts.begin(), ghosts.end()), ghosts.end());
     std::vector<int32_t> ord;
     for (auto pr : {std::make_pair(&ga, &ca), std::make_pair(&gb, &cb)}) {
         morton_sort_rows(xyz, *pr.first, ord);
@@ -136,20 +133,23 @@ bool hvg::make_shard_plan(const int32_t *xyz, int64_t n, const int32_t *part, in
         }
     }
     P.nA = (int64_t)ga.size();
-    P.ghost = gh[rank];
+    P.ghost = ghosts;
     P.recv_off.assign(world, 0);
     P.recv_cnt.assign(world, 0);
     for (size_t k = 0; k < P.ghost.size(); k++) P.recv_cnt[part[P.ghost[k]]]++;
     for (int q = 1; q < world; q++) P.recv_off[q] = P.recv_off[q - 1] + P.recv_cnt[q - 1];
     std::unordered_map<int64_t, int64_t> row;
+    row.reserve(P.local.size() * 2);
     for (size_t r = 0; r < P.local.size(); r++) row[P.local[r]] = (int64_t)r;
+    // send lists in each peer's receive order (ascending global index within an owner)
     P.send_off.assign(world, 0);
     P.send_cnt.assign(world, 0);
     for (int q = 0; q < world; q++) {
         P.send_off[q] = (int64_t)P.send_rows.size();
-        if (q == rank) continue;
-        for (int64_t c : gh[q])
-            if (part[c] == rank) P.send_rows.push_back(row.at(c));
+        std::vector<int64_t> &sg = send_g[q];
+        std::sort(sg.begin(), sg.end());
+        sg.erase(std::unique(sg.begin(), sg.end()), sg.end());
+        for (int64_t g : sg) P.send_rows.push_back(row.at(g));
         P.send_cnt[q] = (int64_t)P.send_rows.size() - P.send_off[q];
     }
     return true;
@@ -262,6 +262,39 @@ static vol_status nccl_exchange(vol_s *v, cudaStream_t s) {
     return VOL_OK;
 }
 
+// NCCL communicators are cached by (unique id, world, rank, device): creating a communicator costs
+// hundreds of milliseconds, and a process typically builds many volumes over one process group (the
+// Python binding reuses one unique id per torch.distributed group).
+namespace {
+struct CommEntry {
+    unsigned char id[NCCL_UNIQUE_ID_BYTES];
+    int world, rank, device;
+    ncclComm_t comm;
+};
+std::vector<CommEntry> g_comms;
+}  // namespace
+
+static vol_status comm_acquire(const void *id_bytes, int world, int rank, int device, ncclComm_t *out) {
+    for (const CommEntry &e : g_comms)
+        if (e.world == world && e.rank == rank && e.device == device && !memcmp(e.id, id_bytes, NCCL_UNIQUE_ID_BYTES)) {
+            *out = e.comm;
+            return VOL_OK;
+        }
+    ncclUniqueId id;
+    memcpy(&id, id_bytes, sizeof id);
+    ncclComm_t comm;
+    NCK(ncclCommInitRank(&comm, world, id, rank));
+    CommEntry e;
+    memcpy(e.id, id_bytes, NCCL_UNIQUE_ID_BYTES);
+    e.world = world;
+    e.rank = rank;
+    e.device = device;
+    e.comm = comm;
+    g_comms.push_back(e);
+    *out = comm;
+    return VOL_OK;
+}
+
 extern "C" vol_status vol_nccl_unique_id(void *out128) {
     if (!out128) return fail(VOL_EINVAL, "vol_nccl_unique_id: NULL");
     ncclUniqueId id;
@@ -289,10 +322,9 @@ vol_status shard_setup(vol_s *v, const ShardPlan &plan, const vol_dist *dist) {
     CK(cudaEventCreateWithFlags(&R->ev_pack, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&R->ev_halo, cudaEventDisableTiming));
     if (dist->nccl_id) {
-        ncclUniqueId id;
-        memcpy(&id, dist->nccl_id, sizeof id);
         R->nccl = true;
-        NCK(ncclCommInitRank(&R->comm, P.world, id, P.rank));
+        vol_status st = comm_acquire(dist->nccl_id, P.world, P.rank, v->device, &R->comm);
+        if (st != VOL_OK) return st;
     }
     return VOL_OK;
 }
@@ -390,7 +422,7 @@ void shard_destroy(vol_s *v) {
     }
     if (R->ev_pack) cudaEventDestroy(R->ev_pack);
     if (R->ev_halo) cudaEventDestroy(R->ev_halo);
-    if (R->comm) ncclCommDestroy(R->comm);
+    // the communicator stays cached for later volumes of the same process group (comm_acquire)
     delete R;
     v->shard = nullptr;
 }

@@ -126,8 +126,15 @@ extern "C" size_t vol_workspace_bytes(const int32_t *block_xyz, int64_t n_global
         return layout_bytes(L);
     }
     if (!block_xyz || !dist->part) return 0;
+    std::vector<int32_t> hxyz;
+    const int32_t *xyz = block_xyz;
+    if (is_device_ptr(block_xyz)) {   // the plan is a host-side schedule
+        hxyz.resize(3 * (size_t)n_global);
+        if (cudaMemcpy(hxyz.data(), block_xyz, hxyz.size() * 4, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+        xyz = hxyz.data();
+    }
     ShardPlan plan;
-    if (!make_shard_plan(block_xyz, n_global, dist->part, dist->world, dist->rank, plan)) return 0;
+    if (!make_shard_plan(xyz, n_global, dist->part, dist->world, dist->rank, plan)) return 0;
     L.n_local = plan.n_local();
     L.S = plan.n_local() + plan.n_ghost();
     return layout_bytes(L) + shard_extra_bytes(plan);

@@ -66,6 +66,29 @@ def plan_shard(coords, part, world: int, rank: int) -> dict:
                 peer_send=psend, peer_recv=precv)
 
 
+_GROUP_IDS = {}
+
+
+def _group_nccl_id(group, device) -> bytes:
+    """One NCCL unique id per torch.distributed group (created by the group's rank 0, broadcast once);
+    libvol caches the communicator built from it, so later volumes of the group reuse it."""
+    import torch.distributed as dist_mod
+    key = id(group)
+    if key not in _GROUP_IDS:
+        idbuf = torch.zeros(128, dtype=torch.uint8)
+        if dist_mod.get_rank(group) == 0:
+            idbuf = torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8).clone()
+        src = dist_mod.get_global_rank(group, 0)
+        if dist_mod.get_backend(group) == "nccl":
+            idd = idbuf.to(device)
+            dist_mod.broadcast(idd, src=src, group=group)
+            idbuf = idd.cpu()
+        else:
+            dist_mod.broadcast(idbuf, src=src, group=group)
+        _GROUP_IDS[key] = bytes(idbuf.numpy().tobytes())
+    return _GROUP_IDS[key]
+
+
 class Volume:
     """A hashed voxel-block volume resident on one GPU (or one shard of a sharded volume).
 
@@ -91,16 +114,7 @@ class Volume:
             if group is not None:
                 import torch.distributed as dist_mod
                 rank, world = dist_mod.get_rank(group), dist_mod.get_world_size(group)
-                idbuf = torch.zeros(128, dtype=torch.uint8)
-                if rank == 0:
-                    idbuf = torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8).clone()
-                if dist_mod.get_backend(group) == "nccl":
-                    idd = idbuf.to(self.device)
-                    dist_mod.broadcast(idd, src=dist_mod.get_global_rank(group, 0), group=group)
-                    idbuf = idd.cpu()
-                else:
-                    dist_mod.broadcast(idbuf, src=dist_mod.get_global_rank(group, 0), group=group)
-                nid = ctypes.create_string_buffer(bytes(idbuf.numpy().tobytes()), 128)
+                nid = ctypes.create_string_buffer(_group_nccl_id(group, self.device), 128)
                 self._keep.append(nid)
                 dist = N.vol_dist(rank, world, part_np.ctypes.data, ctypes.cast(nid, ctypes.c_void_p))
             elif loopback is not None:
