@@ -69,6 +69,7 @@ struct vol_s {
     int32_t *d_entry = nullptr;        // [n_global]
     uint32_t *d_scan = nullptr;        // scan scratch
     int32_t *d_nbr = nullptr;          // [S][12] store indices (6 faces + 6 edge neighbours)
+    uint8_t *d_w8 = nullptr;           // [S][512] exact 8-bit weights (used when F.W8 != null)
     int32_t *d_perm = nullptr;         // [n_local] caller index of store row r
     float *d_tmp = nullptr;            // [n_local][512] scratch for caller-order I/O
     unsigned long long *d_misc = nullptr;  // [4]: dup, bad, n_omega, spare
@@ -78,6 +79,7 @@ struct vol_s {
     // sharded state (world > 1)
     ShardRuntime *shard = nullptr;
     char *extra = nullptr;             // workspace tail for the sharded runtime
+    bool shard_nccl() const;
     hvg::IterParams pending{};         // parameters of the current vol_regularise call
     int pending_kernel = 0;
 };
@@ -85,6 +87,8 @@ struct vol_s {
 // Validates the parameters, fills v->pending, initialises the state unless opts->resume.
 vol_status vol_regularise_prepare(vol_s *v, float lambda, float eps, float tau, float sigma, int32_t iters,
                                   const vol_opts *opts);
+// Fills the 8-bit weight copy (or disables it) once all held W, ghosts included, are final.
+vol_status finalize_w8(vol_s *v);
 // Dual value from the five reduced energy terms (see energy.cu).
 double energy_dual_value(const double *o, float eps, int data_term);
 

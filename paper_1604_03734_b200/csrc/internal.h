@@ -31,6 +31,7 @@ constexpr int kNbr = 12;           // 6 face neighbours (−x,+x,−y,+y,−z,+z
 struct Fields {
     const float *f;        // fused TSDF (read only)
     const float *W;        // fusion weight (read only), Ω ⇔ W > 0
+    const uint8_t *W8;     // W as exact 8-bit counts when every W is an integer in [0, 255], else null
     float *u;              // primal u (in place: only its own CTA touches a voxel's u)
     float *ub[2];          // relaxed primal ū, double-buffered
     float *px[2], *py[2], *pz[2];  // dual p, double-buffered
@@ -39,6 +40,7 @@ struct Fields {
 // The buffers of one iteration, selected on the host (no dynamic indexing in kernels).
 struct View {
     const float *f, *W;
+    const uint8_t *W8;
     float *u;
     const float *ub_in;
     float *ub_out;
@@ -48,7 +50,7 @@ struct View {
 
 inline View view_of(const Fields &F, int cur) {
     const int o = cur ^ 1;
-    return View{F.f, F.W, F.u, F.ub[cur], F.ub[o], F.px[cur], F.py[cur], F.pz[cur], F.px[o], F.py[o], F.pz[o]};
+    return View{F.f, F.W, F.W8, F.u, F.ub[cur], F.ub[o], F.px[cur], F.py[cur], F.pz[cur], F.px[o], F.py[o], F.pz[o]};
 }
 
 struct IterParams {
@@ -82,6 +84,8 @@ int launch_neighbours(const int32_t *xyz, int64_t n, const uint32_t *start, cons
 int launch_validate(const float *f, const float *W, int64_t nvox, unsigned long long *bad,
                     unsigned long long *n_omega, cudaStream_t s);
 int launch_init_state(const Fields &F, int64_t nvox, int init, cudaStream_t s);
+// W8[i] = W[i] for W integer in [0, 255]; *bad = 1 if some W is not (W8 then unusable)
+int launch_pack_w8(const float *W, uint8_t *W8, int64_t nvox, unsigned *bad, cudaStream_t s);
 // gather: dst[r] = src[perm[r]] (caller → store order); scatter: dst[perm[r]] = src[r] (store → caller)
 int launch_permute_blocks(const float *src, float *dst, const int32_t *perm, int64_t n, bool gather, cudaStream_t s);
 int launch_sanitize_state(const Fields &F, int cur, const int32_t *nbr, int64_t n_blocks, cudaStream_t s);

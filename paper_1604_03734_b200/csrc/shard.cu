@@ -350,6 +350,8 @@ vol_status shard_after_create(vol_s *v) {
     return VOL_OK;
 }
 
+bool vol_s::shard_nccl() const { return shard && shard->nccl; }
+
 vol_status shard_reset(vol_s *v) {
     if (!v->shard->connected) return fail(VOL_EINVAL, "sharded volume not connected (call vol_group_connect)");
     return VOL_OK;
@@ -480,6 +482,7 @@ extern "C" vol_status vol_group_connect(vol_t *h, int world) {
         h[r]->n_omega_global = tot;
         h[r]->shard->connected = true;
         h[r]->cur = 0;
+        if ((st = finalize_w8(h[r])) != VOL_OK) return st;
     }
     return VOL_OK;
 }

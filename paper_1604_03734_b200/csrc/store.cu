@@ -336,4 +336,25 @@ int launch_permute_blocks(const float *src, float *dst, const int32_t *perm, int
     return cudaPeekAtLastError() == cudaSuccess ? counted(1) : -1;
 }
 
+// The fusion weight is an observation count (Eq. 1: w_k = w_{k-1} + 1), so it is usually an
+// exact small integer; then the fused kernel reads it as one byte instead of four (exact: the kernel
+// converts back to the same float).
+__global__ void k_pack_w8(const float *__restrict__ W, uint8_t *__restrict__ W8, int64_t nvox, unsigned *bad) {
+    bool ok = true;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvox; i += (int64_t)gridDim.x * blockDim.x) {
+        const float w = W[i];
+        const bool e = w >= 0.0f && w <= 255.0f && w == truncf(w);
+        W8[i] = e ? (uint8_t)w : 0;
+        ok &= e;
+    }
+    if (__any_sync(0xffffffffu, !ok) && (threadIdx.x & 31) == 0) atomicOr(bad, 1u);
+}
+
+int launch_pack_w8(const float *W, uint8_t *W8, int64_t nvox, unsigned *bad, cudaStream_t s) {
+    if (nvox == 0) return 0;
+    int64_t g = grid_for(nvox, 256);
+    k_pack_w8<<<(unsigned)(g < 148 * 16 ? g : 148 * 16), 256, 0, s>>>(W, W8, nvox, bad);
+    return cudaPeekAtLastError() == cudaSuccess ? counted(1) : -1;
+}
+
 }  // namespace hvg

@@ -88,6 +88,7 @@ static void carve_all(Carve &c, vol_s *v, const Layout &L) {
     auto entry = c.take<int32_t>((size_t)L.n_global + 1);
     auto scan = c.take<uint32_t>((size_t)L.T / 4096 + 4);
     auto nbr = c.take<int32_t>(kNbr * (size_t)L.S);
+    auto w8 = c.take<uint8_t>((size_t)L.S * kBlockVox + 16);
     auto perm = c.take<int32_t>((size_t)L.n_local + 1);
     auto tmp = c.take<float>((size_t)L.n_local * kBlockVox + 4);
     auto misc = c.take<unsigned long long>(4);
@@ -101,6 +102,7 @@ static void carve_all(Carve &c, vol_s *v, const Layout &L) {
         v->d_entry = entry;
         v->d_scan = scan;
         v->d_nbr = nbr;
+        v->d_w8 = w8;
         v->d_perm = perm;
         v->d_tmp = tmp;
         v->d_misc = misc;
@@ -291,9 +293,26 @@ extern "C" vol_status vol_create(const int32_t *block_xyz, int64_t n_global, con
         st = shard_after_create(v);
         if (st != VOL_OK) return bail(st);
     }
+    if (!sharded || v->shard_nccl()) {   // loopback shards finish in vol_group_connect
+        st = finalize_w8(v);
+        if (st != VOL_OK) return bail(st);
+    }
     v->cur = 0;
     v->initialised = true;
     *out = v;
+    return VOL_OK;
+}
+
+// Store W additionally as exact 8-bit counts when every held W (ghosts included) is an integer in
+// [0, 255]; the fused kernel then reads 1 B instead of 4 B per voxel for W.
+vol_status finalize_w8(vol_s *v) {
+    unsigned *d_bad = reinterpret_cast<unsigned *>(&v->d_misc[3]);
+    unsigned bad = 0;
+    CK(cudaMemsetAsync(d_bad, 0, sizeof(unsigned), v->stream));
+    CKL(launch_pack_w8(v->F.W, v->d_w8, v->L.S * kBlockVox, d_bad, v->stream));
+    CK(cudaMemcpyAsync(&bad, d_bad, sizeof bad, cudaMemcpyDeviceToHost, v->stream));
+    CK(cudaStreamSynchronize(v->stream));
+    v->F.W8 = bad ? nullptr : v->d_w8;
     return VOL_OK;
 }
 

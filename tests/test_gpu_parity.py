@@ -255,3 +255,13 @@ def test_paper_literal_variant(V):
     s.lam, s.eps, s.sigma, s.tau, s.data_term, s.init, s.iters = 0.8, 0.0, 0.5, 1.0 / 6.0, 1, 1, 150
     _, u = run_gpu(V, s)
     check_against_oracle(s, u)
+
+
+@pytest.mark.parametrize("scale", [0.37, 97.0])
+def test_non_count_weights_use_float_path(V, scale):
+    # W that are not 8-bit integer counts (fractional, or > 255) take the fp32-weight kernel variant;
+    # integer counts take the 8-bit variant — both must reproduce the oracle bit for bit
+    s = random_instance(250, seed=12, extent=5, w_density=0.7, lam=0.4, eps=0.01, iters=40)
+    s.W = (s.W * scale).contiguous()
+    _, u = run_gpu(V, s)
+    check_against_oracle(s, u)
