@@ -18,6 +18,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <climits>
 #include <numeric>
 #include <unordered_map>
 #include <unordered_set>
@@ -43,16 +44,38 @@ static uint64_t spread3(uint32_t v) {  // 21 bits → every third bit
 // Morton (Z-order) of the block coordinates (offset by 2^20): consecutive CTAs work on spatially
 // close blocks, so the halo a CTA reads was recently brought into L2 by its neighbours' CTAs.
 void hvg::morton_sort_rows(const int32_t *xyz, const std::vector<int64_t> &g, std::vector<int32_t> &rows) {
-    std::vector<std::pair<uint64_t, int32_t>> key(g.size());
-    for (size_t k = 0; k < g.size(); k++) {
+    // Morton key relative to the bounding box (fewer significant bits), then a stable LSD radix sort
+    // (11-bit digits) of (key, index): linear time, and ties keep the input order (deterministic).
+    const size_t n = g.size();
+    rows.resize(n);
+    if (n == 0) return;
+    int32_t lo[3] = {INT32_MAX, INT32_MAX, INT32_MAX};
+    for (size_t k = 0; k < n; k++)
+        for (int a = 0; a < 3; a++) lo[a] = std::min(lo[a], xyz[3 * g[k] + a]);
+    std::vector<uint64_t> key(n), key2(n);
+    std::vector<int32_t> idx2(n);
+    uint64_t kmax = 0;
+    for (size_t k = 0; k < n; k++) {
         const int32_t *c = xyz + 3 * g[k];
-        uint64_t m = spread3((uint32_t)(c[0] + (1 << 20))) | (spread3((uint32_t)(c[1] + (1 << 20))) << 1) |
-                     (spread3((uint32_t)(c[2] + (1 << 20))) << 2);
-        key[k] = {m, (int32_t)k};
+        key[k] = spread3((uint32_t)(c[0] - lo[0])) | (spread3((uint32_t)(c[1] - lo[1])) << 1) |
+                 (spread3((uint32_t)(c[2] - lo[2])) << 2);
+        kmax = std::max(kmax, key[k]);
+        rows[k] = (int32_t)k;
     }
-    std::sort(key.begin(), key.end());
-    rows.resize(g.size());
-    for (size_t k = 0; k < g.size(); k++) rows[k] = key[k].second;
+    constexpr int kBits = 11, kRadix = 1 << kBits;
+    std::vector<uint32_t> cnt(kRadix + 1);
+    for (int shift = 0; shift < 64 && (kmax >> shift) != 0; shift += kBits) {
+        std::fill(cnt.begin(), cnt.end(), 0u);
+        for (size_t k = 0; k < n; k++) cnt[((key[k] >> shift) & (kRadix - 1)) + 1]++;
+        for (int d = 0; d < kRadix; d++) cnt[d + 1] += cnt[d];
+        for (size_t k = 0; k < n; k++) {
+            const uint32_t pos = cnt[(key[k] >> shift) & (kRadix - 1)]++;
+            key2[pos] = key[k];
+            idx2[pos] = rows[k];
+        }
+        key.swap(key2);
+        rows.swap(idx2);
+    }
 }
 
 namespace {
