@@ -54,6 +54,10 @@ typedef struct {
     int resume;      /* 0 (d): initialise before iterating; 1: continue from the current state        */
     int kernel;      /* 0 (d): fused single-pass kernel (one HBM sweep per iteration);
                         1: two-kernel baseline (dual kernel, then primal+relax kernel)                */
+    int freeze;      /* 1 (d): with the L1 data term, voxels whose primal step is provably the identity
+                        for the whole call (τλW >= τ(3+√3) plus rounding margin, and u = ū = f in both
+                        buffers at the start of the call) are not recomputed nor rewritten — the result
+                        is bit-identical; 0: every Ω voxel is updated every iteration               */
 } vol_opts;
 
 /* Multi-GPU description (route-axis spatial sharding).  NULL = single GPU.          */

@@ -21,7 +21,7 @@ class VolError(RuntimeError):
 
 class vol_opts(ctypes.Structure):
     _fields_ = [("theta", ctypes.c_float), ("data_term", ctypes.c_int), ("init", ctypes.c_int),
-                ("resume", ctypes.c_int), ("kernel", ctypes.c_int)]
+                ("resume", ctypes.c_int), ("kernel", ctypes.c_int), ("freeze", ctypes.c_int)]
 
 
 class vol_dist(ctypes.Structure):

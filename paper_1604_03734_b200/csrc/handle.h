@@ -69,6 +69,8 @@ struct vol_s {
     int32_t *d_entry = nullptr;        // [n_global]
     uint32_t *d_scan = nullptr;        // scan scratch
     int32_t *d_nbr = nullptr;          // [S][12] store indices (6 faces + 6 edge neighbours)
+    uint32_t *d_frozen = nullptr;      // [n_local][16] frozen-voxel bits of the current call
+    const uint32_t *pending_frozen = nullptr;
     uint8_t *d_w8 = nullptr;           // [S][512] exact 8-bit weights (used when F.W8 != null)
     int32_t *d_perm = nullptr;         // [n_local] caller index of store row r
     float *d_tmp = nullptr;            // [n_local][512] scratch for caller-order I/O

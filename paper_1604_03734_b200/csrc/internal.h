@@ -41,6 +41,7 @@ struct Fields {
 struct View {
     const float *f, *W;
     const uint8_t *W8;
+    const uint32_t *frozen;   // [rows][16] bit per voxel: primal step is the identity this call (or null)
     float *u;
     const float *ub_in;
     float *ub_out;
@@ -50,7 +51,8 @@ struct View {
 
 inline View view_of(const Fields &F, int cur) {
     const int o = cur ^ 1;
-    return View{F.f, F.W, F.W8, F.u, F.ub[cur], F.ub[o], F.px[cur], F.py[cur], F.pz[cur], F.px[o], F.py[o], F.pz[o]};
+    return View{F.f, F.W, F.W8, nullptr, F.u, F.ub[cur], F.ub[o], F.px[cur], F.py[cur], F.pz[cur], F.px[o], F.py[o],
+                F.pz[o]};
 }
 
 struct IterParams {
@@ -84,6 +86,9 @@ int launch_neighbours(const int32_t *xyz, int64_t n, const uint32_t *start, cons
 int launch_validate(const float *f, const float *W, int64_t nvox, unsigned long long *bad,
                     unsigned long long *n_omega, cudaStream_t s);
 int launch_init_state(const Fields &F, int64_t nvox, int init, cudaStream_t s);
+// frozen[row][w] bit b: voxel 32w + b of the row has an identity primal step for this call (L1 only)
+int launch_freeze_mask(const Fields &F, int cur, const IterParams &P, int64_t n_blocks, uint32_t *frozen,
+                       cudaStream_t s);
 // W8[i] = W[i] for W integer in [0, 255]; *bad = 1 if some W is not (W8 then unusable)
 int launch_pack_w8(const float *W, uint8_t *W8, int64_t nvox, unsigned *bad, cudaStream_t s);
 // gather: dst[r] = src[perm[r]] (caller → store order); scatter: dst[perm[r]] = src[r] (store → caller)

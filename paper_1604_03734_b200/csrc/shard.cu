@@ -392,7 +392,8 @@ static vol_status nccl_iteration(vol_s *v, const IterParams &P, int64_t &launche
     if ((st = nccl_exchange(v, R->cs)) != VOL_OK) return st;
     if ((st = unpack(v, v->F.ub[cur], v->F.px[cur], v->F.py[cur], v->F.pz[cur], R->cs)) != VOL_OK) return st;
     CK(cudaEventRecord(R->ev_halo, R->cs));
-    const View V = view_of(v->F, cur);
+    View V = view_of(v->F, cur);
+    V.frozen = v->pending_frozen;
     const ShardPlan &SP = R->plan;
     int r = launch_fused(V, v->d_nbr, nullptr, 0, SP.nA, P, s);
     CKL(r);
@@ -533,7 +534,8 @@ extern "C" vol_status vol_regularise_group(vol_t *h, int world, float lambda, fl
             ShardRuntime *R = h[r]->shard;
             if ((st = unpack(h[r], h[r]->F.ub[cur], h[r]->F.px[cur], h[r]->F.py[cur], h[r]->F.pz[cur], s)) != VOL_OK)
                 return st;
-            const View V = view_of(h[r]->F, cur);
+            View V = view_of(h[r]->F, cur);
+            V.frozen = h[r]->pending_frozen;
             int a = launch_fused(V, h[r]->d_nbr, nullptr, 0, R->plan.nA, P, s);
             CKL(a);
             int b = launch_fused(V, h[r]->d_nbr, nullptr, R->plan.nA, R->plan.n_local() - R->plan.nA, P, s);

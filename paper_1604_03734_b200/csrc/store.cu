@@ -357,4 +357,38 @@ int launch_pack_w8(const float *W, uint8_t *W8, int64_t nvox, unsigned *bad, cud
     return cudaPeekAtLastError() == cudaSuccess ? counted(1) : -1;
 }
 
+// Frozen voxels (opts.freeze): with the L1 data term the primal step of a voxel with u = f is
+//   ũ = fl(f + fl(τ·d)),  r = fl(ũ − f),  u' = f  whenever |r| <= t = fl(fl(τλ)·W),
+// and |d| = |Σ_a p_a(v) − p_a(v−ê_a)| <= √3 + 3 because every p the primal step reads was just projected
+// onto the unit ball (‖p‖₂ <= 1 up to a few ulps).  |r| <= τ|d|(1 + 2^-21) + |f|·2^-23, so
+// t >= τ(3+√3)(1 + 2^-19) + |f|·2^-22 guarantees u' = f and then ū' = f + θ·(f − f) = f, at every
+// iteration of the call.  A voxel that satisfies it with u = ū = f in both ū buffers at the start of the
+// call therefore never changes during the call; the fused kernel skips its primal step and stores.
+__global__ void k_freeze_mask(Fields F, int cur, IterParams P, uint32_t *__restrict__ frozen) {
+    const int64_t b = blockIdx.x;
+    const float *ubc = cur ? F.ub[1] : F.ub[0];
+    const float *ubo = cur ? F.ub[0] : F.ub[1];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        const int i = threadIdx.x + 128 * j;
+        const int64_t v = b * 512 + i;
+        const float fv = F.f[v], w = F.W[v];
+        const float t = P.tl * w;
+        const float bound = P.tau * (4.7320508f * 1.0000019f) + fabsf(fv) * 2.3841858e-7f;
+        // bitwise equality, and f ≠ −0 (ū' = f + (+0) would turn −0 into +0)
+        const uint32_t fb = __float_as_uint(fv);
+        const bool fz = P.data_term == 0 && w > 0.0f && t >= bound && fb != 0x80000000u &&
+                        __float_as_uint(F.u[v]) == fb && __float_as_uint(ubc[v]) == fb && __float_as_uint(ubo[v]) == fb;
+        const unsigned m = __ballot_sync(0xffffffffu, fz);
+        if ((threadIdx.x & 31) == 0) frozen[b * 16 + (i >> 5)] = m;
+    }
+}
+
+int launch_freeze_mask(const Fields &F, int cur, const IterParams &P, int64_t n_blocks, uint32_t *frozen,
+                       cudaStream_t s) {
+    if (n_blocks == 0) return 0;
+    k_freeze_mask<<<(unsigned)n_blocks, 128, 0, s>>>(F, cur, P, frozen);
+    return cudaPeekAtLastError() == cudaSuccess ? counted(1) : -1;
+}
+
 }  // namespace hvg

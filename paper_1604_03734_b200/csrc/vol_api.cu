@@ -46,6 +46,7 @@ extern "C" void vol_default_opts(vol_opts *o) {
     o->init = 0;
     o->resume = 0;
     o->kernel = 0;
+    o->freeze = 1;
 }
 
 extern "C" uint32_t vol_block_hash(int32_t x, int32_t y, int32_t z, uint32_t T) { return host_hash(x, y, z, T); }
@@ -89,6 +90,7 @@ static void carve_all(Carve &c, vol_s *v, const Layout &L) {
     auto scan = c.take<uint32_t>((size_t)L.T / 4096 + 4);
     auto nbr = c.take<int32_t>(kNbr * (size_t)L.S);
     auto w8 = c.take<uint8_t>((size_t)L.S * kBlockVox + 16);
+    auto frozen = c.take<uint32_t>((size_t)L.n_local * 16 + 16);
     auto perm = c.take<int32_t>((size_t)L.n_local + 1);
     auto tmp = c.take<float>((size_t)L.n_local * kBlockVox + 4);
     auto misc = c.take<unsigned long long>(4);
@@ -103,6 +105,7 @@ static void carve_all(Carve &c, vol_s *v, const Layout &L) {
         v->d_scan = scan;
         v->d_nbr = nbr;
         v->d_w8 = w8;
+        v->d_frozen = frozen;
         v->d_perm = perm;
         v->d_tmp = tmp;
         v->d_misc = misc;
@@ -331,7 +334,8 @@ static vol_status run_iterations_single(vol_s *v, const IterParams &P, int32_t i
     cudaStream_t s = v->stream;
     int64_t launches = 0;
     auto one = [&](cudaStream_t st, int cur) -> int {
-        const View V = view_of(v->F, cur);
+        View V = view_of(v->F, cur);
+        V.frozen = v->pending_frozen;
         if (kernel == 1) return launch_two_kernel(V, v->d_nbr, nullptr, v->L.n_local, P, st);
         return launch_fused(V, v->d_nbr, nullptr, 0, v->L.n_local, P, st);
     };
@@ -376,7 +380,7 @@ static vol_status run_iterations_single(vol_s *v, const IterParams &P, int32_t i
         launches += r;
         v->cur ^= 1;
     }
-    v->last_launches = launches;
+    v->last_launches += launches;
     return VOL_OK;
 }
 
@@ -421,6 +425,12 @@ vol_status vol_regularise_prepare(vol_s *v, float lambda, float eps, float tau, 
         CKL(launch_init_state(v->F, v->L.S * kBlockVox, o.init, v->stream));
         v->cur = 0;
         v->last_launches = 1;
+    }
+    v->pending_frozen = nullptr;
+    if (o.freeze && o.data_term == 0 && o.kernel == 0 && iters > 0) {
+        CKL(launch_freeze_mask(v->F, v->cur, P, v->L.n_local, v->d_frozen, v->stream));
+        v->pending_frozen = v->d_frozen;
+        v->last_launches += 1;
     }
     return VOL_OK;
 }

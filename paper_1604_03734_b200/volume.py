@@ -147,16 +147,17 @@ class Volume:
 
     # -- solver ---------------------------------------------------------------------------------
     @staticmethod
-    def _opts(theta=1.0, data_term=0, init=0, resume=False, kernel=0):
+    def _opts(theta=1.0, data_term=0, init=0, resume=False, kernel=0, freeze=True):
         o = N.vol_opts()
         N.lib().vol_default_opts(ctypes.byref(o))
         o.theta, o.data_term, o.init, o.resume, o.kernel = float(theta), int(data_term), int(init), int(bool(resume)), int(kernel)
+        o.freeze = int(bool(freeze))
         return o
 
     def regularise(self, lam: float, eps: float, tau: float, sigma: float, iters: int, *, theta: float = 1.0,
-                   data_term: int = 0, init: int = 0, resume: bool = False, kernel: int = 0):
+                   data_term: int = 0, init: int = 0, resume: bool = False, kernel: int = 0, freeze: bool = True):
         """`iters` Chambolle–Pock iterations (asynchronous on the volume's stream)."""
-        o = self._opts(theta, data_term, init, resume, kernel)
+        o = self._opts(theta, data_term, init, resume, kernel, freeze)
         N.check(self._lib.vol_regularise(self._h, lam, eps, tau, sigma, int(iters), ctypes.byref(o)))
         return self
 

@@ -265,3 +265,18 @@ def test_non_count_weights_use_float_path(V, scale):
     s.W = (s.W * scale).contiguous()
     _, u = run_gpu(V, s)
     check_against_oracle(s, u)
+
+
+def test_freeze_is_bit_identical(V, tiny_scene):
+    # opts.freeze skips voxels whose primal step is provably the identity; results must not change,
+    # including across calls that resume with other parameters (the frozen set is rebuilt per call)
+    s = tiny_scene
+    outs = []
+    for fz in (True, False):
+        vol = V(s.coords.cuda(), s.f.cuda(), s.W.cuda())
+        vol.regularise(s.lam, 0.01, s.tau, s.sigma, 37, freeze=fz)
+        vol.regularise(0.3, 0.0, s.tau, s.sigma, 21, resume=True, freeze=fz)     # most voxels unpinned now
+        vol.regularise(2.0, 0.0, s.tau, s.sigma, 15, resume=True, freeze=fz)     # pinned again, u ≠ f
+        outs.append(vol.state())
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
