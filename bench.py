@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--iters", type=int, default=None, help="override the config's iteration count")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kernel", type=int, default=0, help="0 fused (product), 1 two-kernel baseline")
+    ap.add_argument("--freeze", type=int, default=1, help="opts.freeze (bit-identical skip of identity updates)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
@@ -239,19 +240,19 @@ def main():
     ev_b = torch.cuda.Event(enable_timing=True)
     iter_ms = []
 
-    def step(c, f, W, out, record):
+    def step(c, f, W, out, record, freeze=bool(args.freeze), rec=None):
         vol = Volume(c, f, W, stream=stream, **kw)
         vol.regularise(scene.lam, scene.eps, scene.tau, scene.sigma, 0, theta=scene.theta,
                        data_term=scene.data_term, init=scene.init, kernel=args.kernel)
         ev_a.record(stream)
         vol.regularise(scene.lam, scene.eps, scene.tau, scene.sigma, iters, theta=scene.theta,
-                       data_term=scene.data_term, resume=True, kernel=args.kernel)
+                       data_term=scene.data_term, resume=True, kernel=args.kernel, freeze=freeze)
         ev_b.record(stream)
         E = vol.energy(scene.lam, scene.eps, scene.data_term)
         vol.read_u(out)
         if record:
             ev_b.synchronize()
-            iter_ms.append(ev_a.elapsed_time(ev_b) / iters)
+            (iter_ms if rec is None else rec).append(ev_a.elapsed_time(ev_b) / iters)
         vol.close()
         return E
 
@@ -282,6 +283,24 @@ def main():
     it_ms = float(it_t.item())
     n_alloc_total = scene.n_alloc
     value = n_alloc_total * iters / (ms / 1e3)
+
+    # transparency: the same step with opts.freeze = 0 (every Ω voxel recomputed and rewritten)
+    nf = None
+    if args.freeze and args.kernel == 0:
+        nf_ms = []
+        step(coords, f_loc, W_loc, u_out, False, freeze=False)
+        barrier()
+        t0.record(stream)
+        nsteps = max(2, args.steps // 2)
+        for _ in range(nsteps):
+            step(coords, f_loc, W_loc, u_out, True, freeze=False, rec=nf_ms)
+        t1.record(stream)
+        barrier()
+        nfm = torch.tensor([t0.elapsed_time(t1) / nsteps, statistics.median(nf_ms)], device=dev)
+        if world > 1:
+            dist.all_reduce(nfm, op=dist.ReduceOp.MAX)
+        nf = {"value": scene.n_alloc * iters / (float(nfm[0]) / 1e3), "ms_per_step": float(nfm[0]),
+              "avg_launch_ms": float(nfm[1]), "steps": nsteps}
 
     # end to end from pinned host buffers through the same API
     e2e = None
@@ -315,13 +334,20 @@ def main():
     achieved = ALG_BYTES_PER_VOXEL * n_local_vox / (it_ms / 1e3) / 1e9
     tr = load_traffic()
     traffic = None
-    if tr and tr.get("workload") == scene.name and tr.get("kernel") == ("k_fused" if args.kernel == 0 else "k_dual+k_primal"):
+    if tr and tr.get("workload") == scene.name and tr.get("kernel") == ("k_fused" if args.kernel == 0 else "k_dual+k_primal") \
+            and bool(tr.get("freeze", True)) == bool(args.freeze):
         traffic = tr.get("dram_bytes_per_launch")
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "peak_source": peak_src,
                 "kernel": "k_fused" if args.kernel == 0 else "k_dual+k_primal",
                 "alg_bytes_per_launch": ALG_BYTES_PER_VOXEL * n_local_vox,
                 "avg_launch_ms": it_ms, "frac_of_8TBps": achieved / 8000.0}
+    if traffic:
+        roofline["dram_gbs_actual"] = traffic / (it_ms / 1e3) / 1e9
+        roofline["dram_frac_actual"] = roofline["dram_gbs_actual"] / peak
+    if nf:
+        nf_ach = ALG_BYTES_PER_VOXEL * n_local_vox / (nf["avg_launch_ms"] / 1e3) / 1e9
+        nf.update({"achieved": nf_ach, "frac": nf_ach / peak})
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         sc = scene.to("cpu")
@@ -345,6 +371,7 @@ def main():
                    "parallelism": f"route-axis shards x{world}" if world > 1 else "single GPU",
                    "energy": {"primal": E[0], "dual": E[1]}},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+        "freeze": bool(args.freeze), "no_freeze": nf,
         "clocks": clk,
     }
     print(json.dumps(line), flush=True)
