@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kernel", type=int, default=0, help="0 fused (product), 1 two-kernel baseline")
     ap.add_argument("--freeze", type=int, default=1, help="opts.freeze (bit-identical skip of identity updates)")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the NCCL sharded runtime even at one rank (tests the N > 1 code path on one GPU)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
@@ -212,14 +214,18 @@ def main():
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     group = None
-    if world > 1:
+    sharded = world > 1 or args.sharded
+    if sharded:
+        if "MASTER_ADDR" not in os.environ:   # plain `python bench.py --sharded`: a one-rank group
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=os.environ.get("MASTER_PORT", "29531"),
+                              RANK="0", WORLD_SIZE="1")
         dist.init_process_group("nccl", device_id=dev)
         group = dist.group.WORLD
 
     scene = make_scene(args.config, world, args.seed, dev)
     iters = scene.iters if args.iters is None else args.iters
     coords = scene.coords.contiguous()
-    if world > 1:
+    if sharded:
         part = partition(coords.cpu(), world)
         mine = (part == rank).nonzero().squeeze(1).to(dev)
         f_loc, W_loc = scene.f[mine].contiguous(), scene.W[mine].contiguous()
@@ -230,11 +236,11 @@ def main():
     stream = torch.cuda.current_stream(dev)
 
     def barrier():
-        if world > 1:
+        if sharded:
             dist.barrier(device_ids=[local_rank])
         torch.cuda.synchronize(dev)
 
-    kw = dict(part=part, group=group) if world > 1 else {}
+    kw = dict(part=part, group=group) if sharded else {}
     u_out = torch.empty(f_loc.shape[0], 512, device=dev)
     ev_a = torch.cuda.Event(enable_timing=True)
     ev_b = torch.cuda.Event(enable_timing=True)
@@ -276,7 +282,7 @@ def main():
     ms = t0.elapsed_time(t1) / args.steps
     ms_t = torch.tensor([ms], device=dev)
     it_t = torch.tensor([statistics.median(iter_ms)], device=dev)
-    if world > 1:
+    if sharded:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
         dist.all_reduce(it_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
@@ -297,7 +303,7 @@ def main():
         t1.record(stream)
         barrier()
         nfm = torch.tensor([t0.elapsed_time(t1) / nsteps, statistics.median(nf_ms)], device=dev)
-        if world > 1:
+        if sharded:
             dist.all_reduce(nfm, op=dist.ReduceOp.MAX)
         nf = {"value": scene.n_alloc * iters / (float(nfm[0]) / 1e3), "ms_per_step": float(nfm[0]),
               "avg_launch_ms": float(nfm[1]), "steps": nsteps}
@@ -318,7 +324,7 @@ def main():
         t1.record(stream)
         barrier()
         ems = torch.tensor([t0.elapsed_time(t1) / args.steps], device=dev)
-        if world > 1:
+        if sharded:
             dist.all_reduce(ems, op=dist.ReduceOp.MAX)
         ems = float(ems.item())
         h2d = hc.numel() * 4 + hf.numel() * 4 + hW.numel() * 4
@@ -368,14 +374,14 @@ def main():
                    "data_term": "L1" if scene.data_term == 0 else "L2",
                    "step": "vol_create + vol_regularise(init + iters) + vol_energy + vol_read_u",
                    "l2": f"inputs larger than L2 ({n_alloc_total * 48 / 1e9:.2f} GB of state vs 126 MB L2)",
-                   "parallelism": f"route-axis shards x{world}" if world > 1 else "single GPU",
+                   "parallelism": f"route-axis shards x{world}" if sharded else "single GPU",
                    "energy": {"primal": E[0], "dual": E[1]}},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
         "freeze": bool(args.freeze), "no_freeze": nf,
         "clocks": clk,
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if sharded:
         dist.destroy_process_group()
     return 0
 

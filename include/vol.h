@@ -65,8 +65,9 @@ typedef struct {
     int rank;               /* this process's rank in [0, world)                                   */
     int world;              /* number of ranks (one GPU each)                                      */
     const int32_t *part;    /* [n_global] owner rank of each block (host pointer)                  */
-    const void *nccl_id;    /* 128-byte ncclUniqueId created by rank 0 and broadcast by the caller;
-                               NULL is only valid with world == 1                                   */
+    const void *nccl_id;    /* 128-byte ncclUniqueId created by rank 0 and broadcast by the caller
+                               (NCCL transport; with world == 1 the sharded runtime runs with no
+                               peers); NULL: loopback transport (world > 1) or plain single GPU      */
 } vol_dist;
 
 /* Defaults for vol_opts (see field comments). */

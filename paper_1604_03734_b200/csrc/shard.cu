@@ -101,24 +101,39 @@ bool hvg::make_shard_plan(const int32_t *xyz, int64_t n, const int32_t *part, in
         P.error = "bad arguments";
         return false;
     }
-    std::unordered_map<Key, int64_t, KeyHash> idx;
-    idx.reserve((size_t)n * 2);
+    // open-addressing table (linear probing, power-of-two capacity >= 2n) of the global block set
+    size_t cap = 1;
+    while (cap < 2 * (size_t)n) cap <<= 1;
+    std::vector<int32_t> slot(cap, -1);
+    KeyHash hasher;
+    auto find = [&](int32_t x, int32_t y, int32_t z) -> int64_t {
+        for (size_t h = hasher(Key{x, y, z}) & (cap - 1);; h = (h + 1) & (cap - 1)) {
+            const int32_t g = slot[h];
+            if (g < 0) return -1;
+            if (xyz[3 * g] == x && xyz[3 * g + 1] == y && xyz[3 * g + 2] == z) return g;
+        }
+    };
     for (int64_t g = 0; g < n; g++) {
         if (part[g] < 0 || part[g] >= world) {
             P.error = "part[" + std::to_string(g) + "] out of range";
             return false;
         }
-        if (!idx.emplace(Key{xyz[3 * g], xyz[3 * g + 1], xyz[3 * g + 2]}, g).second) {
-            P.error = "duplicate block coordinates at block " + std::to_string(g);
-            return false;
+        const int32_t x = xyz[3 * g], y = xyz[3 * g + 1], z = xyz[3 * g + 2];
+        size_t h = hasher(Key{x, y, z}) & (cap - 1);
+        for (;; h = (h + 1) & (cap - 1)) {
+            const int32_t o = slot[h];
+            if (o < 0) break;
+            if (xyz[3 * o] == x && xyz[3 * o + 1] == y && xyz[3 * o + 2] == z) {
+                P.error = "duplicate block coordinates at block " + std::to_string(g);
+                return false;
+            }
         }
+        slot[h] = (int32_t)g;
     }
     static const int OFF[kNbr][3] = {{-1, 0, 0}, {1, 0, 0},  {0, -1, 0}, {0, 1, 0},  {0, 0, -1}, {0, 0, 1},
                                      {-1, 1, 0}, {-1, 0, 1}, {1, -1, 0}, {0, -1, 1}, {1, 0, -1}, {0, 1, -1}};
     auto nb = [&](int64_t g, int d) -> int64_t {
-        Key k{xyz[3 * g] + OFF[d][0], xyz[3 * g + 1] + OFF[d][1], xyz[3 * g + 2] + OFF[d][2]};
-        auto it = idx.find(k);
-        return it == idx.end() ? -1 : it->second;
+        return find(xyz[3 * g] + OFF[d][0], xyz[3 * g + 1] + OFF[d][1], xyz[3 * g + 2] + OFF[d][2]);
     };
     // One pass over the rank's own blocks.  The 12-neighbour relation is symmetric (each edge offset's
     // inverse is in the set: 6 ↔ 8, 7 ↔ 10, 9 ↔ 11), so the blocks rank q needs from this rank are
@@ -161,9 +176,8 @@ bool hvg::make_shard_plan(const int32_t *xyz, int64_t n, const int32_t *part, in
     P.recv_cnt.assign(world, 0);
     for (size_t k = 0; k < P.ghost.size(); k++) P.recv_cnt[part[P.ghost[k]]]++;
     for (int q = 1; q < world; q++) P.recv_off[q] = P.recv_off[q - 1] + P.recv_cnt[q - 1];
-    std::unordered_map<int64_t, int64_t> row;
-    row.reserve(P.local.size() * 2);
-    for (size_t r = 0; r < P.local.size(); r++) row[P.local[r]] = (int64_t)r;
+    std::vector<int32_t> row(n, -1);
+    for (size_t r = 0; r < P.local.size(); r++) row[P.local[r]] = (int32_t)r;
     // send lists in each peer's receive order (ascending global index within an owner)
     P.send_off.assign(world, 0);
     P.send_cnt.assign(world, 0);
@@ -172,7 +186,7 @@ bool hvg::make_shard_plan(const int32_t *xyz, int64_t n, const int32_t *part, in
         std::vector<int64_t> &sg = send_g[q];
         std::sort(sg.begin(), sg.end());
         sg.erase(std::unique(sg.begin(), sg.end()), sg.end());
-        for (int64_t g : sg) P.send_rows.push_back(row.at(g));
+        for (int64_t g : sg) P.send_rows.push_back(row[g]);
         P.send_cnt[q] = (int64_t)P.send_rows.size() - P.send_off[q];
     }
     return true;

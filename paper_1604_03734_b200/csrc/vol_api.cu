@@ -120,12 +120,53 @@ static size_t layout_bytes(const Layout &L) {
     return c.off + 512;
 }
 
+// The shard plan is needed twice per volume (workspace size, then creation); the last plan is cached
+// per thread, keyed by a digest of the coordinates and the owner map.
+namespace {
+struct PlanCache {
+    bool valid = false;
+    int64_t n = 0;
+    int world = 0, rank = 0;
+    uint64_t digest = 0;
+    ShardPlan plan;
+};
+thread_local PlanCache g_plan_cache;
+}  // namespace
+
+static uint64_t plan_digest(const int32_t *xyz, int64_t n, const int32_t *part) {
+    uint64_t h = 1469598103934665603ull;
+    for (int64_t i = 0; i < n; i++) {
+        const uint64_t a = ((uint64_t)(uint32_t)xyz[3 * i] << 32) ^ (uint32_t)xyz[3 * i + 1];
+        const uint64_t b = ((uint64_t)(uint32_t)xyz[3 * i + 2] << 32) ^ (uint32_t)part[i];
+        h = (h ^ a) * 1099511628211ull;
+        h = (h ^ b) * 1099511628211ull;
+    }
+    return h;
+}
+
+static bool get_shard_plan(const int32_t *xyz, int64_t n, const vol_dist *d, ShardPlan &out) {
+    const uint64_t dg = plan_digest(xyz, n, d->part);
+    PlanCache &c = g_plan_cache;
+    if (c.valid && c.n == n && c.world == d->world && c.rank == d->rank && c.digest == dg) {
+        out = c.plan;
+        return true;
+    }
+    if (!make_shard_plan(xyz, n, d->part, d->world, d->rank, out)) return false;
+    c.valid = true;
+    c.n = n;
+    c.world = d->world;
+    c.rank = d->rank;
+    c.digest = dg;
+    c.plan = out;
+    return true;
+}
+
 extern "C" size_t vol_workspace_bytes(const int32_t *block_xyz, int64_t n_global, const vol_dist *dist) {
     if (n_global < 1) return 0;
     Layout L{};
     L.n_global = n_global;
     L.T = table_size(n_global);
-    if (!dist || dist->world <= 1) {
+    if (!dist || (dist->world <= 1 && !dist->nccl_id)) {
         L.S = n_global;
         L.n_local = n_global;
         return layout_bytes(L);
@@ -139,7 +180,7 @@ extern "C" size_t vol_workspace_bytes(const int32_t *block_xyz, int64_t n_global
         xyz = hxyz.data();
     }
     ShardPlan plan;
-    if (!make_shard_plan(xyz, n_global, dist->part, dist->world, dist->rank, plan)) return 0;
+    if (!get_shard_plan(xyz, n_global, dist, plan)) return 0;
     L.n_local = plan.n_local();
     L.S = plan.n_local() + plan.n_ghost();
     return layout_bytes(L) + shard_extra_bytes(plan);
@@ -158,7 +199,9 @@ extern "C" vol_status vol_create(const int32_t *block_xyz, int64_t n_global, con
     if (n_global < 1) return fail(VOL_EINVAL, "vol_create: n_global must be >= 1 (got %lld)", (long long)n_global);
     if (n_global > (int64_t)1 << 30) return fail(VOL_EINVAL, "vol_create: n_global too large");
     if (!block_xyz || !f || !W) return fail(VOL_EINVAL, "vol_create: NULL input pointer");
-    const bool sharded = dist && dist->world > 1;
+    // a dist with world > 1, or any dist carrying an NCCL id (world 1 runs the sharded runtime with no
+    // peers, which exercises the NCCL set-up and the two-launch schedule on a single GPU)
+    const bool sharded = dist && (dist->world > 1 || dist->nccl_id != nullptr);
     if (dist && (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world))
         return fail(VOL_EINVAL, "vol_create: bad rank/world");
     if (sharded && !dist->part) return fail(VOL_EINVAL, "vol_create: dist->part is NULL");
@@ -187,7 +230,7 @@ extern "C" vol_status vol_create(const int32_t *block_xyz, int64_t n_global, con
     L.n_global = n_global;
     L.T = table_size(n_global);
     if (sharded) {
-        if (!make_shard_plan(hxyz.data(), n_global, dist->part, dist->world, dist->rank, plan))
+        if (!get_shard_plan(hxyz.data(), n_global, dist, plan))
             return bail(fail(VOL_EDATA, "vol_create: shard plan failed: %s", plan.error.c_str()));
         L.n_local = plan.n_local();
         L.S = plan.n_local() + plan.n_ghost();

@@ -11,12 +11,20 @@ from synth import scenes  # noqa: E402
 
 
 def main():
+    sharded = "--sharded" in sys.argv
+    kw = {}
+    if sharded:
+        import torch.distributed as dist
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29541", RANK="0", WORLD_SIZE="1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", 0))
     s = scenes.street(0, device="cuda", chunk_blocks=4096)
+    if sharded:
+        kw = dict(part=torch.zeros(s.n_blocks, dtype=torch.int32), group=dist.group.WORLD)
     out = torch.empty(s.n_blocks, 512, device="cuda")
     for rep in range(4):
         torch.cuda.synchronize()
         t = [time.perf_counter()]
-        v = Volume(s.coords, s.f, s.W)
+        v = Volume(s.coords, s.f, s.W, **kw)
         torch.cuda.synchronize(); t.append(time.perf_counter())
         v.regularise(s.lam, s.eps, s.tau, s.sigma, 0)
         torch.cuda.synchronize(); t.append(time.perf_counter())

@@ -280,3 +280,33 @@ def test_freeze_is_bit_identical(V, tiny_scene):
         outs.append(vol.state())
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+def test_nccl_runtime_world1(V):
+    # the NCCL transport end to end on one GPU: communicator from a torch.distributed NCCL group of one
+    # rank, the sharded two-launch schedule (no peers), the Ω-count and energy all-reduces
+    import socket
+    import torch.distributed as dist
+    from paper_1604_03734_b200 import Volume
+    s = random_instance(300, seed=14, extent=5, w_density=0.7, lam=0.4, eps=0.01, iters=30)
+    _, u1 = run_gpu(V, s)
+    single = V(s.coords.cuda(), s.f.cuda(), s.W.cuda())
+    single.regularise_scene(s)
+    E1 = single.energy(s.lam, s.eps, s.data_term)
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        part = torch.zeros(len(s.coords), dtype=torch.int32)
+        vol = Volume(s.coords.cuda(), s.f.cuda(), s.W.cuda(), part=part, group=dist.group.WORLD)
+        assert vol.n_ghost == 0 and vol.n_local == len(s.coords)
+        vol.regularise_scene(s)
+        assert np.array_equal(vol.u().cpu().numpy(), u1)
+        E = vol.energy(s.lam, s.eps, s.data_term)
+        assert abs(E[0] - E1[0]) <= 1e-9 * abs(E1[0]) and abs(E[1] - E1[1]) <= 1e-9 * abs(E1[0])
+        vol.close()
+    finally:
+        dist.destroy_process_group()
