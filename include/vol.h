@@ -79,7 +79,8 @@ void vol_default_opts(vol_opts *opts);
 size_t vol_workspace_bytes(const int32_t *block_xyz, int64_t n_global, const vol_dist *dist);
 
 /* Build a volume:
- *   block_xyz [n_global][3] int32 block coordinates (host or device), all distinct;
+ *   block_xyz [n_global][3] int32 block coordinates (host or device), all distinct, each in
+ *             (−2^30, 2^30);
  *   f, W      [n_local][512] float32 (host or device): the blocks this rank owns, in global order
  *             (n_local = n_global when dist == NULL); f finite, W finite and >= 0;
  *   dist      NULL (single GPU) or the sharding description;
@@ -89,7 +90,8 @@ size_t vol_workspace_bytes(const int32_t *block_xyz, int64_t n_global, const vol
  * (u32)z·83492791) mod T with T = next power of two >= 2n, a CSR bucket table ordered by caller
  * index (reading c-14), and the 6-neighbour block table (−x,+x,−y,+y,−z,+z; −1 = unallocated).
  * Errors: VOL_EINVAL (n_global < 1, NULL pointers), VOL_EDATA (duplicate coordinates — the first
- * repeated pair is named in vol_last_error —, non-finite f/W, W < 0), VOL_ENOMEM, VOL_ECUDA.     */
+ * repeated pair is named in vol_last_error —, coordinates out of range, non-finite f/W, W < 0),
+ * VOL_ENOMEM, VOL_ECUDA.                                                                          */
 vol_status vol_create(const int32_t *block_xyz, int64_t n_global, const float *f, const float *W,
                       const vol_dist *dist, void *workspace, size_t workspace_bytes, void *stream,
                       vol_t *out);

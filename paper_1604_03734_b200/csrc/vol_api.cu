@@ -224,6 +224,10 @@ extern "C" vol_status vol_create(const int32_t *block_xyz, int64_t n_global, con
     } else {
         memcpy(hxyz.data(), block_xyz, hxyz.size() * 4);
     }
+    // block coordinates must leave room for the ±1 neighbour offsets in int32 arithmetic
+    for (size_t k = 0; k < hxyz.size(); k++)
+        if (hxyz[k] <= -(1 << 30) || hxyz[k] >= (1 << 30))
+            return bail(fail(VOL_EDATA, "block %lld: coordinate %d outside (-2^30, 2^30)", (long long)(k / 3), hxyz[k]));
 
     ShardPlan plan;
     Layout L{};

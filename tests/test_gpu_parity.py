@@ -310,3 +310,33 @@ def test_nccl_runtime_world1(V):
         vol.close()
     finally:
         dist.destroy_process_group()
+
+
+def test_coordinate_range_and_degenerate_parameters(V):
+    from paper_1604_03734_b200._native import VolError, VOL_EDATA
+    s = random_instance(40, seed=15, extent=3)
+    c = s.coords.clone()
+    c[5, 1] = 2 ** 30
+    with pytest.raises(VolError) as e:
+        V(c, s.f, s.W)
+    assert e.value.status == VOL_EDATA
+    # far-away coordinates (hash wrap-around), strong Huber damping, θ = 0, tiny σ
+    s = random_instance(200, seed=16, extent=4, w_density=0.8, lam=0.3, eps=1.0, iters=25)
+    s.coords = s.coords + torch.tensor([2 ** 29, -(2 ** 29), 12345], dtype=torch.int32)
+    s.theta = 0.0
+    _, u = run_gpu(V, s)
+    check_against_oracle(s, u)
+    s2 = random_instance(200, seed=17, extent=4, w_density=0.8, lam=50.0, eps=0.0, iters=25)
+    s2.sigma, s2.tau = 0.01, 0.5
+    _, u2 = run_gpu(V, s2)
+    check_against_oracle(s2, u2)
+
+
+def test_mostly_unobserved_blocks(V):
+    # blocks whose every voxel is Ω̄ next to blocks with a single observed voxel
+    s = random_instance(120, seed=18, extent=4, w_density=0.02, lam=0.5, eps=0.01, iters=30)
+    W = s.W.clone()
+    W[::3] = 0
+    s.W = W
+    _, u = run_gpu(V, s)
+    check_against_oracle(s, u)
