@@ -17,6 +17,9 @@ Parity status per function:
                           isotropic TV-L1 at finite iterations has no closed form ("parity unpinned
                           beyond these", SURVEY §8(c) last pin row)
   energy ................ pinned (worked examples, brute force, weak duality)
+  fusion (Eq. 1) ........ pinned (SPEC worked examples, fronto-parallel plane closed form under random
+                          rigid poses, running-average closed form, block walk vs exact segment-box
+                          intersection, dense numpy brute force O2-fusion) — ``fusion_oracle.c``
 """
 from __future__ import annotations
 
@@ -28,7 +31,8 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
-_SRC = [os.path.join(_HERE, "hvg_oracle.c"), os.path.join(_HERE, "hvg_oracle_real.inc")]
+_SRC = [os.path.join(_HERE, "hvg_oracle.c"), os.path.join(_HERE, "fusion_oracle.c"),
+        os.path.join(_HERE, "hvg_oracle_real.inc")]
 
 
 def build(force: bool = False) -> str:
@@ -37,7 +41,7 @@ def build(force: bool = False) -> str:
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < newest:
         tmp = _SO + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-std=c99", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
-                               "-Wall", "-o", tmp, _SRC[0], "-lm"])
+                               "-Wall", "-o", tmp, _SRC[0], _SRC[1], "-lm"])
         os.replace(tmp, _SO)
     return _SO
 
@@ -73,6 +77,19 @@ def lib():
             r.argtypes = [i64, P, P, P, real, real, real, real, real, cint, cint, i64, P, P, P, cint]
         L.orc_energy.restype = None
         L.orc_energy.argtypes = [i64, P, P, P, P, P, dbl, dbl, cint, P, P]
+        # fusion (fusion_oracle.c)
+        L.orc_tsdf_update.restype = cint
+        L.orc_tsdf_update.argtypes = [P, P, flt, flt, flt]
+        L.orc_project.restype = cint
+        L.orc_project.argtypes = [P, P, i32, i32, flt, flt, flt, P, P, P]
+        L.orc_block_walk.restype = i64
+        L.orc_block_walk.argtypes = [P, P, flt, P, i64]
+        L.orc_fuse.restype = i64
+        L.orc_fuse.argtypes = [P, i32, i32, i32, P, P, flt, flt, flt, flt, i64, P, P, P, P]
+        L.orc_fuse_alloc.restype = i64
+        L.orc_fuse_alloc.argtypes = [P, i32, i32, i32, P, P, flt, flt, flt, i64, P, P]
+        L.orc_fuse_update_blocks.restype = None
+        L.orc_fuse_update_blocks.argtypes = [P, i32, i32, i32, P, P, flt, flt, flt, flt, P, P, i64, P, P]
         _lib = L
     return _lib
 
@@ -207,3 +224,92 @@ def energy(nbr, f, W, u, lam, eps, data_term=0, p=None):
     lib().orc_energy(n, _ptr(nbr), _ptr(ff), _ptr(Wf), _ptr(uu), _ptr(pp) if pp is not None else None,
                      r32(lam), r32(eps), int(data_term), _ptr(out[0:1]), _ptr(out[1:2]))
     return float(out[0]), (float(out[1]) if p is not None else None)
+
+
+# ---------------------------------------------------------------------------------------------------
+# TSDF fusion (paper §III-A, Eq. 1; fusion_oracle.c).  All arithmetic is fp32 in the written order.
+# ---------------------------------------------------------------------------------------------------
+
+def tsdf_update(f, w, sdf, mu, w_max=1e30):
+    """Eq. 1 for one voxel: returns (f, w, updated)."""
+    ff = np.array([f], np.float32)
+    ww = np.array([w], np.float32)
+    up = lib().orc_tsdf_update(_ptr(ff), _ptr(ww), float(np.float32(sdf)), float(np.float32(mu)),
+                               float(np.float32(w_max)))
+    return float(ff[0]), float(ww[0]), bool(up)
+
+
+def project(pose, intr, H, Wd, p):
+    """Steps 1-2 of P:160-164: (i, j, z_c) of the nearest pixel of global point p, or None."""
+    ps = _np(pose, np.float32).reshape(12)
+    it = _np(intr, np.float32).reshape(4)
+    i, j = np.zeros(1, np.int32), np.zeros(1, np.int32)
+    z = np.zeros(1, np.float32)
+    ok = lib().orc_project(_ptr(ps), _ptr(it), int(H), int(Wd), float(np.float32(p[0])), float(np.float32(p[1])),
+                           float(np.float32(p[2])), _ptr(i), _ptr(j), _ptr(z))
+    return (int(i[0]), int(j[0]), float(z[0])) if ok else None
+
+
+def block_walk(a, b, Bm, max_cells=100000) -> np.ndarray:
+    """Reading F-7 lattice walk of blocks from point a to point b (metres); [m, 3] int32."""
+    aa = _np(a, np.float32).reshape(3)
+    bb = _np(b, np.float32).reshape(3)
+    cells = np.zeros((max_cells, 3), np.int32)
+    m = lib().orc_block_walk(_ptr(aa), _ptr(bb), float(np.float32(Bm)), _ptr(cells), max_cells)
+    assert m <= max_cells
+    return cells[:m].copy()
+
+
+def _fusion_inputs(depth, intr, poses):
+    D = _np(depth, np.float32)
+    if D.ndim == 2:
+        D = D[None]
+    K, H, Wd = D.shape
+    return D, K, H, Wd, _np(intr, np.float32).reshape(4), _np(poses, np.float32).reshape(K, 12)
+
+
+def fuse(depth, intr, poses, voxel, mu, max_range, w_max):
+    """Sequential fusion of K depth maps (allocation then update, frame by frame).
+    Returns (xyz [n,3] int32 sorted by (x,y,z), first [n] int32, f [n,512], W [n,512])."""
+    D, K, H, Wd, it, ps = _fusion_inputs(depth, intr, poses)
+    r = lambda x: float(np.float32(x))
+    n = lib().orc_fuse(_ptr(D), K, H, Wd, _ptr(it), _ptr(ps), r(voxel), r(mu), r(max_range), r(w_max), 0,
+                       None, None, None, None)
+    if n < 0:
+        raise ValueError("fusion oracle: block walk out of range")
+    xyz = np.zeros((max(n, 1), 3), np.int32)
+    first = np.zeros(max(n, 1), np.int32)
+    f = np.zeros((max(n, 1), 512), np.float32)
+    W = np.zeros((max(n, 1), 512), np.float32)
+    n2 = lib().orc_fuse(_ptr(D), K, H, Wd, _ptr(it), _ptr(ps), r(voxel), r(mu), r(max_range), r(w_max), n,
+                        _ptr(xyz), _ptr(first), _ptr(f), _ptr(W))
+    assert n2 == n
+    return xyz[:n], first[:n], f[:n], W[:n]
+
+
+def fuse_alloc(depth, intr, poses, voxel, mu, max_range):
+    """Allocation passes only: (xyz [n,3] sorted by (x,y,z), first [n])."""
+    D, K, H, Wd, it, ps = _fusion_inputs(depth, intr, poses)
+    r = lambda x: float(np.float32(x))
+    n = lib().orc_fuse_alloc(_ptr(D), K, H, Wd, _ptr(it), _ptr(ps), r(voxel), r(mu), r(max_range), 0, None, None)
+    if n < 0:
+        raise ValueError("fusion oracle: block walk out of range")
+    xyz = np.zeros((max(n, 1), 3), np.int32)
+    first = np.zeros(max(n, 1), np.int32)
+    lib().orc_fuse_alloc(_ptr(D), K, H, Wd, _ptr(it), _ptr(ps), r(voxel), r(mu), r(max_range), n, _ptr(xyz),
+                         _ptr(first))
+    return xyz[:n], first[:n]
+
+
+def fuse_update_blocks(depth, intr, poses, voxel, mu, max_range, w_max, xyz, first):
+    """Update passes for a subset of blocks (each from its allocating frame on): (f, W) [nb, 512]."""
+    D, K, H, Wd, it, ps = _fusion_inputs(depth, intr, poses)
+    c = _np(xyz, np.int32).reshape(-1, 3)
+    fr = _np(first, np.int32).reshape(-1)
+    nb = c.shape[0]
+    f = np.zeros((max(nb, 1), 512), np.float32)
+    W = np.zeros((max(nb, 1), 512), np.float32)
+    r = lambda x: float(np.float32(x))
+    lib().orc_fuse_update_blocks(_ptr(D), K, H, Wd, _ptr(it), _ptr(ps), r(voxel), r(mu), r(max_range), r(w_max),
+                                 _ptr(c), _ptr(fr), nb, _ptr(f), _ptr(W))
+    return f[:nb], W[:nb]
