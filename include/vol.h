@@ -179,6 +179,57 @@ vol_status vol_plan_shard(const int32_t *block_xyz, int64_t n_global, const int3
                           int64_t *ghost_global, int64_t *send_global, int64_t *peer_send,
                           int64_t *peer_recv);
 
+/* TSDF fusion of posed depth maps (paper §III-A, Eq. 1) ----------
+ * Readings F-1 … F-10.  For every depth map k = 0 … K−1 in sequence the paper
+ * allocates the blocks where frame k observes a surface and then updates every voxel of
+ * every allocated block:
+ *   allocation  every valid pixel (i, j) (depth d finite, 0 < d <= max_range) allocates the blocks met
+ *               by its viewing ray between camera depths max(d − μ, 0) and d + μ (F-5), visited by a
+ *               6-connected walk over the block lattice (F-7);
+ *   update      p_c = R^T (p_g − t) (F-2) for the voxel centre p_g = (8B + i + ½)·v; nearest
+ *               pixel (floor(fx·x_c/z_c + cx + ½), floor(fy·y_c/z_c + cy + ½)) (F-1); if z_c > 0,
+ *               the pixel is inside and its depth valid: u_SDF = d − z_c; Eq. 1: if
+ *               u_SDF >= −μ then u_TSDF = clamp(u_SDF, −μ, μ)/μ (F-3), f = (u_TSDF + w·f)/(w + 1),
+ *               w = min(w + 1, w_max) (F-4).  Unobserved voxels keep f = 0, W = 0.
+ * All arithmetic is IEEE fp32 in that written order (F-10).                                         */
+typedef struct {
+    float fx, fy;       /* focal lengths in pixels (> 0)                                            */
+    float cx, cy;       /* principal point in pixels; pixel (i, j) is the unit square centred at (i, j) */
+    int32_t width;      /* W: columns of every depth map                                            */
+    int32_t height;     /* H: rows                                                                  */
+} vol_camera;
+
+typedef struct {
+    float voxel;        /* voxel edge v in metres (blocks are 8v)                                   */
+    float mu;           /* truncation distance μ in metres (Eq. 1)                                  */
+    float max_range;    /* depths > max_range are invalid (F-9)                                     */
+    float w_max;        /* weight cap (F-4); >= 1, a huge value gives the paper's uncapped w         */
+} vol_fusion_params;
+
+/* Device bytes vol_fuse needs for up to max_blocks allocated blocks (worst case: host inputs and
+ * host outputs).  Returns 0 on invalid arguments.                                                 */
+size_t vol_fuse_workspace_bytes(int64_t max_blocks, int32_t n_frames, const vol_camera *cam);
+
+/* Fuse K = n_frames depth maps into a new set of blocks:
+ *   depth     [K][H][W] float32 metres (host or device); non-finite, <= 0 or > max_range = invalid;
+ *   poses     [K][12] float32 row-major T_gc = [R | t] (camera-to-global, p_g = R p_c + t), host or
+ *             device;
+ *   max_blocks capacity of the outputs; workspace device buffer of >= vol_fuse_workspace_bytes(...)
+ *             or NULL (the library allocates and frees its own); stream cudaStream_t or NULL;
+ *   outputs   (all host or all device) block_xyz [max_blocks][3] int32, first_frame [max_blocks]
+ *             int32 (frame that allocated the block; may be NULL), f, W [max_blocks][512] float32;
+ *             rows 0 … n−1 hold the n allocated blocks sorted by (x, y, z) (F-9); *n_blocks (host)
+ *             receives n.
+ * Synchronous with respect to the host for *n_blocks (the count is read back); device outputs are
+ * complete when the stream reaches that point.  Errors: VOL_EINVAL (arguments), VOL_EDATA (a block
+ * walk leaves the coordinate range (−2^20, 2^20) or is longer than 4096 blocks), VOL_ENOMEM (more
+ * than max_blocks blocks: *n_blocks then holds the count reached, retry with a larger capacity; or
+ * workspace too small), VOL_ECUDA.                                                                  */
+vol_status vol_fuse(const float *depth, int32_t n_frames, const vol_camera *cam, const float *poses,
+                    const vol_fusion_params *params, int64_t max_blocks, void *workspace, size_t workspace_bytes,
+                    void *stream, int32_t *block_xyz, int32_t *first_frame, float *f, float *W,
+                    int64_t *n_blocks);
+
 #ifdef __cplusplus
 }
 #endif

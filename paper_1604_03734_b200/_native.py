@@ -24,6 +24,16 @@ class vol_opts(ctypes.Structure):
                 ("resume", ctypes.c_int), ("kernel", ctypes.c_int), ("freeze", ctypes.c_int)]
 
 
+class vol_camera(ctypes.Structure):
+    _fields_ = [("fx", ctypes.c_float), ("fy", ctypes.c_float), ("cx", ctypes.c_float), ("cy", ctypes.c_float),
+                ("width", ctypes.c_int32), ("height", ctypes.c_int32)]
+
+
+class vol_fusion_params(ctypes.Structure):
+    _fields_ = [("voxel", ctypes.c_float), ("mu", ctypes.c_float), ("max_range", ctypes.c_float),
+                ("w_max", ctypes.c_float)]
+
+
 class vol_dist(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int), ("world", ctypes.c_int), ("part", ctypes.c_void_p),
                 ("nccl_id", ctypes.c_void_p)]
@@ -33,7 +43,8 @@ EXPORTS = [
     "vol_default_opts", "vol_workspace_bytes", "vol_create", "vol_regularise", "vol_read_u", "vol_energy",
     "vol_read_state", "vol_load_state", "vol_read_tables", "vol_info", "vol_last_launches", "vol_sync",
     "vol_destroy", "vol_last_error", "vol_nccl_unique_id", "vol_group_connect", "vol_regularise_group",
-    "vol_group_energy", "vol_block_hash", "vol_plan_shard", "vol_total_launches",
+    "vol_group_energy", "vol_block_hash", "vol_plan_shard", "vol_total_launches", "vol_fuse_workspace_bytes",
+    "vol_fuse",
 ]
 
 _lib = None
@@ -71,6 +82,9 @@ def lib() -> ctypes.CDLL:
         "vol_block_hash": (u32, [i32, i32, i32, u32]),
         "vol_plan_shard": (st, [P, i64, P, c_int, c_int, P, P, P, P, P, P, P]),
         "vol_total_launches": (i64, []),
+        "vol_fuse_workspace_bytes": (ctypes.c_size_t, [i64, i32, ctypes.POINTER(vol_camera)]),
+        "vol_fuse": (st, [P, i32, ctypes.POINTER(vol_camera), P, ctypes.POINTER(vol_fusion_params), i64, P,
+                          ctypes.c_size_t, P, P, P, P, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

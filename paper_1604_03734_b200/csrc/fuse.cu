@@ -1,0 +1,477 @@
+// fuse.cu — TSDF fusion of posed depth maps into the hashed voxel-block grid on the device
+// (arXiv 1604.03734 §III-A, Eq. 1).  Readings F-1 … F-10: DESIGN.md §11.
+//
+// The paper fuses frame by frame: allocate the blocks where frame k observes a surface,
+// then update every voxel of every allocated block with frame k (P:152-176 steps 1-4, Eq. 1).
+// The update of one voxel depends only on its own (f, w) and the frame, so the sequential result is
+// reproduced exactly by (i) one allocation launch over all pixels of all frames that records, per
+// block, the FIRST frame that allocates it (atomicMin — order-independent), and (ii) one update
+// launch in which every voxel runs its Eq. 1 recurrence over frames first(b) … K−1 in order, in
+// registers, writing f and W once.  The block set, the canonical (x, y, z) order (radix sort of the
+// packed keys) and every value are therefore independent of thread scheduling.
+//
+//   k_fuse_alloc      one thread per (frame, pixel): the pixel ray between camera depths
+//                     max(d − μ, 0) and d + μ (the truncation band, reading F-5) walked over the
+//                     block lattice (reading F-7), each block inserted into an open-addressing
+//                     device hash set of packed keys (atomicCAS) with atomicMin of the frame;
+//   k_fuse_compact    occupied slots → (key, first frame) list;  CUB radix sort by key;
+//   k_fuse_integrate  one 128-thread CTA per block, 4 voxels per thread: for k = first … K−1, a
+//                     conservative block-level frustum / range cull (never skips a voxel the exact
+//                     per-voxel test would update), then steps 1-4 and Eq. 1 per voxel.
+//
+// Every floating-point decision and value follows the written order of the readings (compiled
+// with --fmad=false, IEEE division): bit-identical to the oracle in the same precision.
+#include <cuda_runtime.h>
+
+#include <cub/device/device_radix_sort.cuh>
+
+#include <climits>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+
+#include "../../include/vol.h"
+#include "handle.h"
+#include "internal.h"
+
+namespace hvg {
+
+constexpr unsigned long long kEmpty = ~0ull;
+constexpr int kWalkMax = 4096;        // longest accepted block walk (cells)
+constexpr int32_t kCoordLim = 1 << 20;
+
+// packed key: (x + 2^20, y + 2^20, z + 2^20) in 21 bits each, x most significant → sorting the keys
+// sorts blocks by (x, y, z) lexicographically (reading F-9)
+__device__ __forceinline__ unsigned long long pack_key(int32_t x, int32_t y, int32_t z) {
+    return ((unsigned long long)(uint32_t)(x + kCoordLim) << 42) | ((unsigned long long)(uint32_t)(y + kCoordLim) << 21) |
+           (unsigned long long)(uint32_t)(z + kCoordLim);
+}
+
+struct FuseSet {
+    unsigned long long *keys;   // [cap], kEmpty = free
+    int32_t *first;             // [cap], INT_MAX = none
+    unsigned long long *count;  // [0] inserted keys, [1] error flags (bit0 table full, bit1 coordinate range / walk)
+    uint32_t mask;              // cap − 1
+};
+
+__device__ __forceinline__ void set_insert(const FuseSet &S, int32_t x, int32_t y, int32_t z, int32_t frame) {
+    if (x <= -kCoordLim || x >= kCoordLim || y <= -kCoordLim || y >= kCoordLim || z <= -kCoordLim || z >= kCoordLim) {
+        atomicOr(&S.count[1], 2ull);
+        return;
+    }
+    const unsigned long long key = pack_key(x, y, z);
+    uint32_t h = ((uint32_t)x * 73856093u ^ (uint32_t)y * 19349669u ^ (uint32_t)z * 83492791u) & S.mask;
+    for (uint32_t probe = 0; probe <= S.mask; probe++) {
+        unsigned long long cur = *((volatile unsigned long long *)&S.keys[h]);
+        if (cur == kEmpty) {
+            cur = atomicCAS(&S.keys[h], kEmpty, key);
+            if (cur == kEmpty) {
+                atomicAdd(&S.count[0], 1ull);
+                atomicMin(&S.first[h], frame);
+                return;
+            }
+        }
+        if (cur == key) {
+            if (*((volatile int32_t *)&S.first[h]) > frame) atomicMin(&S.first[h], frame);
+            return;
+        }
+        h = (h + 1) & S.mask;
+    }
+    atomicOr(&S.count[1], 1ull);
+}
+
+__device__ __forceinline__ bool depth_ok(float d, float max_range) {
+    return isfinite(d) && d > 0.0f && d <= max_range;
+}
+
+// Reading F-6: p_c = ((i − cx)/fx · z, (j − cy)/fy · z, z), p_g = R p_c + t, row sums left to right.
+__device__ __forceinline__ void ray_point(const float *T, float fx, float fy, float cx, float cy, int32_t i, int32_t j,
+                                          float z, float &gx, float &gy, float &gz) {
+    const float xc = __fmul_rn(__fdiv_rn(__fsub_rn((float)i, cx), fx), z);
+    const float yc = __fmul_rn(__fdiv_rn(__fsub_rn((float)j, cy), fy), z);
+    const float zc = z;
+    gx = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(T[0], xc), __fmul_rn(T[1], yc)), __fmul_rn(T[2], zc)), T[3]);
+    gy = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(T[4], xc), __fmul_rn(T[5], yc)), __fmul_rn(T[6], zc)), T[7]);
+    gz = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(T[8], xc), __fmul_rn(T[9], yc)), __fmul_rn(T[10], zc)), T[11]);
+}
+
+// One axis of the reading F-7 walk set-up.
+__device__ __forceinline__ void walk_axis(float a, float b, float Bm, int32_t &c, int32_t &n, int32_t &step,
+                                          float &tmax, float &tdel) {
+    const float sa = __fdiv_rn(a, Bm);
+    const float sb = __fdiv_rn(b, Bm);
+    const float fa = floorf(sa);
+    const float fb = floorf(sb);
+    const float dir = __fsub_rn(sb, sa);
+    // coordinates far outside the packable range are clamped here and rejected by set_insert
+    const float lim = 2.0e9f;
+    c = (int32_t)fminf(fmaxf(fa, -lim), lim);
+    const int32_t e = (int32_t)fminf(fmaxf(fb, -lim), lim);
+    if (dir > 0.0f) {
+        step = 1;
+        tdel = __fdiv_rn(1.0f, dir);
+        tmax = __fdiv_rn(__fsub_rn(__fadd_rn(fa, 1.0f), sa), dir);
+    } else if (dir < 0.0f) {
+        step = -1;
+        tdel = __fdiv_rn(1.0f, -dir);
+        tmax = __fdiv_rn(__fsub_rn(sa, fa), -dir);
+    } else {
+        step = 0;
+        tdel = INFINITY;
+        tmax = INFINITY;
+    }
+    const long long dn = (long long)e - (long long)c;
+    n = (int32_t)(dn < 0 ? (-dn > kWalkMax ? kWalkMax + 1 : -dn) : (dn > kWalkMax ? kWalkMax + 1 : dn));
+}
+
+struct FuseArgs {
+    const float *depth;   // [K][H][W]
+    const float *poses;   // [K][12] T_gc row-major
+    int32_t K, H, W;
+    float fx, fy, cx, cy;
+    float voxel, mu, max_range, w_max;
+};
+
+__global__ void __launch_bounds__(256) k_fuse_alloc(FuseArgs A, FuseSet S) {
+    const long long HW = (long long)A.H * A.W;
+    const long long total = HW * A.K;
+    const float Bm = __fmul_rn(8.0f, A.voxel);
+    for (long long pix = (long long)blockIdx.x * blockDim.x + threadIdx.x; pix < total;
+         pix += (long long)gridDim.x * blockDim.x) {
+        const float d = __ldg(A.depth + pix);
+        if (!depth_ok(d, A.max_range)) continue;
+        const int32_t k = (int32_t)(pix / HW);
+        const long long rem = pix - (long long)k * HW;
+        const int32_t j = (int32_t)(rem / A.W);
+        const int32_t i = (int32_t)(rem - (long long)j * A.W);
+        float T[12];
+#pragma unroll
+        for (int q = 0; q < 12; q++) T[q] = __ldg(A.poses + 12 * k + q);
+        float za = __fsub_rn(d, A.mu);
+        if (za < 0.0f) za = 0.0f;
+        const float zb = __fadd_rn(d, A.mu);
+        float ax, ay, az, bx, by, bz;
+        ray_point(T, A.fx, A.fy, A.cx, A.cy, i, j, za, ax, ay, az);
+        ray_point(T, A.fx, A.fy, A.cx, A.cy, i, j, zb, bx, by, bz);
+        int32_t cx_, cy_, cz_, nx, ny, nz, sx, sy, sz;
+        float tx, ty, tz, dx, dy, dz;
+        walk_axis(ax, bx, Bm, cx_, nx, sx, tx, dx);
+        walk_axis(ay, by, Bm, cy_, ny, sy, ty, dy);
+        walk_axis(az, bz, Bm, cz_, nz, sz, tz, dz);
+        if (nx + ny + nz + 1 > kWalkMax) {
+            atomicOr(&S.count[1], 2ull);
+            continue;
+        }
+        set_insert(S, cx_, cy_, cz_, k);
+        while (nx + ny + nz > 0) {
+            // the axis with remaining steps and the smallest tMax; ties → lowest axis (reading F-7)
+            if (nx > 0 && (ny == 0 || tx <= ty) && (nz == 0 || tx <= tz)) {
+                cx_ += sx;
+                tx = __fadd_rn(tx, dx);
+                nx--;
+            } else if (ny > 0 && (nz == 0 || ty <= tz)) {
+                cy_ += sy;
+                ty = __fadd_rn(ty, dy);
+                ny--;
+            } else {
+                cz_ += sz;
+                tz = __fadd_rn(tz, dz);
+                nz--;
+            }
+            set_insert(S, cx_, cy_, cz_, k);
+        }
+    }
+}
+
+__global__ void k_fuse_compact(FuseSet S, uint32_t cap, unsigned long long *out_keys, int32_t *out_first,
+                               unsigned long long *cursor, unsigned long long limit) {
+    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= cap) return;
+    const unsigned long long key = S.keys[s];
+    if (key == kEmpty) return;
+    const unsigned long long r = atomicAdd(cursor, 1ull);
+    if (r < limit) {
+        out_keys[r] = key;
+        out_first[r] = S.first[s];
+    }
+}
+
+// Conservative cull of one block against one frame: true only if no voxel of the block can pass the
+// per-voxel test (z_c > 0, nearest pixel inside the image, u_SDF >= −μ with d <= max_range).  The
+// block's voxel centres lie in the sphere of centre c (block centre) and radius 3.5·v·√3; the
+// margins below absorb the fp32 rounding of the per-voxel path (relative ~1e-6) many times over.
+__device__ __forceinline__ bool block_culled(const float *T, const FuseArgs &A, float cxg, float cyg, float czg) {
+    const float d0 = cxg - T[3], d1 = cyg - T[7], d2 = czg - T[11];
+    const float xc = (T[0] * d0 + T[4] * d1) + T[8] * d2;
+    const float yc = (T[1] * d0 + T[5] * d1) + T[9] * d2;
+    const float zc = (T[2] * d0 + T[6] * d1) + T[10] * d2;
+    const float ext = fabsf(d0) + fabsf(d1) + fabsf(d2);
+    const float r = 3.5f * 1.7320508f * A.voxel * 1.001f + 1e-3f + 1e-5f * ext;
+    if (zc + r <= 0.0f) return true;                            // behind the camera
+    if (zc - r > A.max_range + A.mu) return true;               // behind every admissible surface by > μ
+    const float pad = 2.0f;                                     // pixels
+    // in-image half-spaces for z_c > 0:  fx·x + (cx + ½ + pad)·z >= 0,  −fx·x + (W − cx − ½ + pad)·z > 0
+    const float l0 = A.cx + 0.5f + pad, r0 = (float)A.W - A.cx - 0.5f + pad;
+    const float t0 = A.cy + 0.5f + pad, b0 = (float)A.H - A.cy - 0.5f + pad;
+    if (A.fx * xc + l0 * zc + sqrtf(A.fx * A.fx + l0 * l0) * r < 0.0f) return true;
+    if (-A.fx * xc + r0 * zc + sqrtf(A.fx * A.fx + r0 * r0) * r < 0.0f) return true;
+    if (A.fy * yc + t0 * zc + sqrtf(A.fy * A.fy + t0 * t0) * r < 0.0f) return true;
+    if (-A.fy * yc + b0 * zc + sqrtf(A.fy * A.fy + b0 * b0) * r < 0.0f) return true;
+    return false;
+}
+
+__global__ void __launch_bounds__(128) k_fuse_integrate(FuseArgs A, const unsigned long long *__restrict__ keys,
+                                                        const int32_t *__restrict__ first, int64_t n,
+                                                        int32_t *__restrict__ xyz_out, int32_t *__restrict__ first_out,
+                                                        float *__restrict__ f_out, float *__restrict__ w_out,
+                                                        int cull) {
+    const int64_t b = blockIdx.x;
+    if (b >= n) return;
+    const unsigned long long key = keys[b];
+    const int32_t bx = (int32_t)((key >> 42) & 0x1FFFFF) - kCoordLim;
+    const int32_t by = (int32_t)((key >> 21) & 0x1FFFFF) - kCoordLim;
+    const int32_t bz = (int32_t)(key & 0x1FFFFF) - kCoordLim;
+    const int32_t k0 = first[b];
+    if (threadIdx.x == 0) {
+        xyz_out[3 * b] = bx;
+        xyz_out[3 * b + 1] = by;
+        xyz_out[3 * b + 2] = bz;
+        if (first_out) first_out[b] = k0;
+    }
+    // voxels 4t … 4t+3: x = 4(t&1) + q, y = (t>>1)&7, z = t>>4
+    const int t = threadIdx.x;
+    const int lx0 = 4 * (t & 1), ly = (t >> 1) & 7, lz = t >> 4;
+    // voxel centre (8B + i + ½)·v (SURVEY §8(d) frame convention)
+    float px[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) px[q] = __fmul_rn(__fadd_rn((float)(8 * bx + lx0 + q), 0.5f), A.voxel);
+    const float py = __fmul_rn(__fadd_rn((float)(8 * by + ly), 0.5f), A.voxel);
+    const float pz = __fmul_rn(__fadd_rn((float)(8 * bz + lz), 0.5f), A.voxel);
+    const float cxg = (8.0f * (float)bx + 4.0f) * A.voxel;
+    const float cyg = (8.0f * (float)by + 4.0f) * A.voxel;
+    const float czg = (8.0f * (float)bz + 4.0f) * A.voxel;
+    float f[4] = {0.f, 0.f, 0.f, 0.f}, w[4] = {0.f, 0.f, 0.f, 0.f};
+    const long long HW = (long long)A.H * A.W;
+    for (int32_t k = k0; k < A.K; k++) {
+        float T[12];
+#pragma unroll
+        for (int q = 0; q < 12; q++) T[q] = __ldg(A.poses + 12 * k + q);
+        if (cull && block_culled(T, A, cxg, cyg, czg)) continue;
+        const float *D = A.depth + (long long)k * HW;
+        // step 1: p_c = R^T (p_g − t); the y and z parts of p_g − t are shared by the 4 voxels
+        const float d1 = __fsub_rn(py, T[7]);
+        const float d2 = __fsub_rn(pz, T[11]);
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const float d0 = __fsub_rn(px[q], T[3]);
+            const float xc = __fadd_rn(__fadd_rn(__fmul_rn(T[0], d0), __fmul_rn(T[4], d1)), __fmul_rn(T[8], d2));
+            const float yc = __fadd_rn(__fadd_rn(__fmul_rn(T[1], d0), __fmul_rn(T[5], d1)), __fmul_rn(T[9], d2));
+            const float zc = __fadd_rn(__fadd_rn(__fmul_rn(T[2], d0), __fmul_rn(T[6], d1)), __fmul_rn(T[10], d2));
+            if (!(zc > 0.0f)) continue;
+            // step 2: nearest pixel (reading F-1)
+            const float ix = __fadd_rn(__fmul_rn(A.fx, __fdiv_rn(xc, zc)), A.cx);
+            const float iy = __fadd_rn(__fmul_rn(A.fy, __fdiv_rn(yc, zc)), A.cy);
+            const float fi = floorf(__fadd_rn(ix, 0.5f));
+            const float fj = floorf(__fadd_rn(iy, 0.5f));
+            if (!(fi >= 0.0f && fi < (float)A.W && fj >= 0.0f && fj < (float)A.H)) continue;
+            const float d = __ldg(D + (long long)(int32_t)fj * A.W + (int32_t)fi);
+            if (!depth_ok(d, A.max_range)) continue;
+            // step 3: u_SDF = d − z_c;  step 4, Eq. 1, readings F-3/F-4
+            const float sdf = __fsub_rn(d, zc);
+            if (sdf < -A.mu) continue;
+            const float c = fminf(fmaxf(sdf, -A.mu), A.mu);
+            const float tsdf = __fdiv_rn(c, A.mu);
+            const float num = __fadd_rn(tsdf, __fmul_rn(w[q], f[q]));
+            const float den = __fadd_rn(w[q], 1.0f);
+            f[q] = __fdiv_rn(num, den);
+            w[q] = fminf(den, A.w_max);
+        }
+    }
+    const int64_t o = b * kBlockVox + 4 * t;
+    *reinterpret_cast<float4 *>(f_out + o) = make_float4(f[0], f[1], f[2], f[3]);
+    *reinterpret_cast<float4 *>(w_out + o) = make_float4(w[0], w[1], w[2], w[3]);
+}
+
+}  // namespace hvg
+
+using namespace hvg;
+
+namespace {
+
+uint32_t fuse_table_cap(int64_t max_blocks) {
+    uint64_t c = 1024;
+    while ((int64_t)c < 2 * max_blocks) c <<= 1;
+    return (uint32_t)c;
+}
+
+size_t cub_sort_bytes(int64_t n) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const unsigned long long *)nullptr, (unsigned long long *)nullptr,
+                                    (const int32_t *)nullptr, (int32_t *)nullptr, (int)(n > 0 ? n : 1), 0, 63);
+    return bytes;
+}
+
+struct FuseLayout {
+    float *depth;
+    float *poses;
+    unsigned long long *keys;
+    int32_t *first;
+    unsigned long long *count;
+    unsigned long long *ckeys[2];
+    int32_t *cfirst[2];
+    void *sort_tmp;
+    size_t sort_bytes;
+    int32_t *xyz;
+    int32_t *ofirst;
+    float *f, *w;
+};
+
+size_t fuse_layout(Carve &c, FuseLayout &L, int64_t max_blocks, int32_t K, int32_t H, int32_t W, bool dev_depth,
+                   bool dev_poses, bool dev_out) {
+    const uint32_t cap = fuse_table_cap(max_blocks);
+    L.depth = dev_depth ? nullptr : c.take<float>((size_t)K * H * W);
+    L.poses = dev_poses ? nullptr : c.take<float>((size_t)K * 12);
+    L.keys = c.take<unsigned long long>(cap);
+    L.first = c.take<int32_t>(cap);
+    L.count = c.take<unsigned long long>(4);
+    for (int q = 0; q < 2; q++) {
+        L.ckeys[q] = c.take<unsigned long long>(max_blocks);
+        L.cfirst[q] = c.take<int32_t>(max_blocks);
+    }
+    L.sort_bytes = cub_sort_bytes(max_blocks);
+    L.sort_tmp = c.take<char>(L.sort_bytes);
+    if (!dev_out) {
+        L.xyz = c.take<int32_t>(3 * max_blocks);
+        L.ofirst = c.take<int32_t>(max_blocks);
+        L.f = c.take<float>((size_t)max_blocks * kBlockVox);
+        L.w = c.take<float>((size_t)max_blocks * kBlockVox);
+    } else {
+        L.xyz = nullptr;
+        L.ofirst = nullptr;
+        L.f = L.w = nullptr;
+    }
+    return c.off + 256;
+}
+
+vol_status check_fuse_args(int32_t K, const vol_camera *cam, const vol_fusion_params *p, int64_t max_blocks) {
+    if (K < 1) return fail(VOL_EINVAL, "vol_fuse: n_frames must be >= 1 (got %d)", K);
+    if (!cam || !p) return fail(VOL_EINVAL, "vol_fuse: camera and params must not be NULL");
+    if (cam->width < 1 || cam->height < 1) return fail(VOL_EINVAL, "vol_fuse: image size must be positive");
+    if ((long long)K * cam->width * cam->height > (1ll << 40)) return fail(VOL_EINVAL, "vol_fuse: too many pixels");
+    if (!(cam->fx > 0.0f) || !(cam->fy > 0.0f) || !std::isfinite(cam->fx) || !std::isfinite(cam->fy) ||
+        !std::isfinite(cam->cx) || !std::isfinite(cam->cy))
+        return fail(VOL_EINVAL, "vol_fuse: intrinsics must be finite with fx, fy > 0");
+    if (!(p->voxel > 0.0f) || !std::isfinite(p->voxel)) return fail(VOL_EINVAL, "vol_fuse: voxel must be > 0");
+    if (!(p->mu > 0.0f) || !std::isfinite(p->mu)) return fail(VOL_EINVAL, "vol_fuse: mu must be > 0");
+    if (!(p->max_range > 0.0f)) return fail(VOL_EINVAL, "vol_fuse: max_range must be > 0");
+    if (!(p->w_max >= 1.0f)) return fail(VOL_EINVAL, "vol_fuse: w_max must be >= 1");
+    if (max_blocks < 1 || max_blocks > (1ll << 30)) return fail(VOL_EINVAL, "vol_fuse: max_blocks out of range");
+    return VOL_OK;
+}
+
+}  // namespace
+
+extern "C" size_t vol_fuse_workspace_bytes(int64_t max_blocks, int32_t n_frames, const vol_camera *cam) {
+    if (!cam || max_blocks < 1 || n_frames < 1) return 0;
+    Carve c;
+    FuseLayout L;
+    // worst case: host depth, host poses, host outputs
+    return fuse_layout(c, L, max_blocks, n_frames, cam->height, cam->width, false, false, false);
+}
+
+extern "C" vol_status vol_fuse(const float *depth, int32_t n_frames, const vol_camera *cam, const float *poses,
+                               const vol_fusion_params *prm, int64_t max_blocks, void *workspace,
+                               size_t workspace_bytes, void *stream, int32_t *block_xyz, int32_t *first_frame,
+                               float *f, float *W, int64_t *n_blocks) {
+    vol_status st = check_fuse_args(n_frames, cam, prm, max_blocks);
+    if (st != VOL_OK) return st;
+    if (!depth || !poses || !block_xyz || !f || !W || !n_blocks)
+        return fail(VOL_EINVAL, "vol_fuse: depth, poses, block_xyz, f, W and n_blocks must not be NULL");
+    *n_blocks = 0;
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool dev_depth = is_device_ptr(depth), dev_poses = is_device_ptr(poses);
+    const bool dev_out = is_device_ptr(block_xyz) && is_device_ptr(f) && is_device_ptr(W) &&
+                         (!first_frame || is_device_ptr(first_frame));
+    const bool any_dev_out = is_device_ptr(block_xyz) || is_device_ptr(f) || is_device_ptr(W) ||
+                             (first_frame && is_device_ptr(first_frame));
+    if (any_dev_out && !dev_out) return fail(VOL_EINVAL, "vol_fuse: outputs must be all device or all host pointers");
+    const int32_t K = n_frames, H = cam->height, Wd = cam->width;
+    Carve probe;
+    FuseLayout L;
+    const size_t need = fuse_layout(probe, L, max_blocks, K, H, Wd, dev_depth, dev_poses, dev_out);
+    void *ws = workspace;
+    bool owns = false;
+    if (ws) {
+        if (workspace_bytes < need)
+            return fail(VOL_ENOMEM, "vol_fuse: workspace of %zu bytes < %zu needed", workspace_bytes, need);
+    } else {
+        CK(cudaMalloc(&ws, need));
+        owns = true;
+    }
+    struct Free {
+        void *p;
+        bool own;
+        ~Free() {
+            if (own && p) cudaFree(p);
+        }
+    } guard{ws, owns};
+    Carve c;
+    c.base = (char *)ws;
+    fuse_layout(c, L, max_blocks, K, H, Wd, dev_depth, dev_poses, dev_out);
+    const float *d_depth = dev_depth ? depth : L.depth;
+    const float *d_poses = dev_poses ? poses : L.poses;
+    if (!dev_depth) CK(cudaMemcpyAsync(L.depth, depth, sizeof(float) * (size_t)K * H * Wd, cudaMemcpyDefault, s));
+    if (!dev_poses) CK(cudaMemcpyAsync(L.poses, poses, sizeof(float) * (size_t)K * 12, cudaMemcpyDefault, s));
+    const uint32_t cap = fuse_table_cap(max_blocks);
+    CK(cudaMemsetAsync(L.keys, 0xFF, sizeof(unsigned long long) * cap, s));
+    CK(cudaMemsetAsync(L.first, 0x7F, sizeof(int32_t) * cap, s));   // 0x7F7F7F7F > any frame index
+    CK(cudaMemsetAsync(L.count, 0, sizeof(unsigned long long) * 4, s));
+    FuseArgs A{d_depth, d_poses, K, H, Wd, cam->fx, cam->fy, cam->cx, cam->cy,
+               prm->voxel, prm->mu, prm->max_range, prm->w_max};
+    FuseSet S{L.keys, L.first, L.count, cap - 1};
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long long total = (long long)K * H * Wd;
+    long long grid = (total + 255) / 256;
+    if (grid > (long long)sms * 16) grid = (long long)sms * 16;
+    k_fuse_alloc<<<(unsigned)grid, 256, 0, s>>>(A, S);
+    CK(cudaPeekAtLastError());
+    counted(1);
+    unsigned long long hc[2];
+    CK(cudaMemcpyAsync(hc, L.count, sizeof hc, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    *n_blocks = (int64_t)hc[0];
+    if (hc[1] & 2ull)
+        return fail(VOL_EDATA, "vol_fuse: a block walk leaves the block-coordinate range (-2^20, 2^20) or is longer "
+                               "than %d blocks (check poses, voxel size and max_range)", kWalkMax);
+    if ((hc[1] & 1ull) || (int64_t)hc[0] > max_blocks)
+        return fail(VOL_ENOMEM, "vol_fuse: %lld blocks allocated (at least) > max_blocks = %lld",
+                    (long long)hc[0], (long long)max_blocks);
+    const int64_t n = (int64_t)hc[0];
+    if (n == 0) return VOL_OK;
+    CK(cudaMemsetAsync(L.count + 2, 0, sizeof(unsigned long long), s));
+    k_fuse_compact<<<(cap + 255) / 256, 256, 0, s>>>(S, cap, L.ckeys[0], L.cfirst[0], L.count + 2,
+                                                      (unsigned long long)max_blocks);
+    CK(cudaPeekAtLastError());
+    counted(1);
+    size_t sb = L.sort_bytes;
+    CK(cub::DeviceRadixSort::SortPairs(L.sort_tmp, sb, L.ckeys[0], L.ckeys[1], L.cfirst[0], L.cfirst[1], (int)n, 0, 63,
+                                       s));   // library sort (CUB): not counted as this library's launches
+    int32_t *oxyz = dev_out ? block_xyz : L.xyz;
+    int32_t *ofirst = dev_out ? first_frame : (first_frame ? L.ofirst : nullptr);
+    float *of = dev_out ? f : L.f;
+    float *ow = dev_out ? W : L.w;
+    const int cull = getenv("HVG_FUSE_NOCULL") ? 0 : 1;   // experiments only: the cull never changes results
+    k_fuse_integrate<<<(unsigned)n, 128, 0, s>>>(A, L.ckeys[1], L.cfirst[1], n, oxyz, ofirst, of, ow, cull);
+    CK(cudaPeekAtLastError());
+    counted(1);
+    if (!dev_out) {
+        CK(cudaMemcpyAsync(block_xyz, L.xyz, sizeof(int32_t) * 3 * n, cudaMemcpyDeviceToHost, s));
+        if (first_frame) CK(cudaMemcpyAsync(first_frame, L.ofirst, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(f, L.f, sizeof(float) * kBlockVox * n, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(W, L.w, sizeof(float) * kBlockVox * n, cudaMemcpyDeviceToHost, s));
+    }
+    if (owns || !dev_out) CK(cudaStreamSynchronize(s));
+    return VOL_OK;
+}

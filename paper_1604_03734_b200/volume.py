@@ -236,6 +236,55 @@ class Volume:
         self.close()
 
 
+# -- TSDF fusion (paper §III-A, Eq. 1) -----------------------------------------
+
+def fuse(depth, poses, intr, voxel: float, mu: float, max_range: float, w_max: float, *, max_blocks=None,
+         stream=None, return_first=True):
+    """Fuse K posed depth maps into hashed voxel blocks on the GPU (``vol_fuse``).
+
+    depth [K, H, W] float32 metres, poses [K, 12] float32 row-major T_gc (camera-to-global), intr
+    (fx, fy, cx, cy).  Returns CUDA tensors (coords int32 [n, 3] sorted by (x, y, z), first frame
+    int32 [n], f float32 [n, 512], W float32 [n, 512]) — ready for :class:`Volume`.
+    """
+    _require_cuda()
+    L = N.lib()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    depth = depth if isinstance(depth, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(depth, np.float32))
+    poses = poses if isinstance(poses, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(poses, np.float32))
+    depth = depth.to(torch.float32).contiguous()
+    if depth.dim() == 2:
+        depth = depth[None]
+    poses = poses.to(torch.float32).reshape(-1, 12).contiguous()
+    K, H, Wd = (int(v) for v in depth.shape)
+    if poses.shape[0] != K:
+        raise ValueError(f"{poses.shape[0]} poses for {K} depth maps")
+    it = [float(v) for v in (intr.tolist() if hasattr(intr, "tolist") else intr)]
+    cam = N.vol_camera(it[0], it[1], it[2], it[3], Wd, H)
+    prm = N.vol_fusion_params(float(voxel), float(mu), float(max_range), float(w_max))
+    s = torch.cuda.current_stream(dev) if stream is None else stream
+    cap = int(max_blocks) if max_blocks else 65536
+    while True:
+        xyz = torch.empty(cap, 3, dtype=torch.int32, device=dev)
+        first = torch.empty(cap, dtype=torch.int32, device=dev)
+        f = torch.empty(cap, 512, dtype=torch.float32, device=dev)
+        W = torch.empty(cap, 512, dtype=torch.float32, device=dev)
+        nbytes = L.vol_fuse_workspace_bytes(cap, K, ctypes.byref(cam))
+        ws = torch.empty(int(nbytes), dtype=torch.uint8, device=dev)
+        n = ctypes.c_int64()
+        st = L.vol_fuse(ctypes.c_void_p(depth.data_ptr()), K, ctypes.byref(cam), ctypes.c_void_p(poses.data_ptr()),
+                        ctypes.byref(prm), cap, ctypes.c_void_p(ws.data_ptr()), nbytes, ctypes.c_void_p(s.cuda_stream),
+                        ctypes.c_void_p(xyz.data_ptr()), ctypes.c_void_p(first.data_ptr()),
+                        ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(W.data_ptr()), ctypes.byref(n))
+        if st == N.VOL_ENOMEM and not max_blocks and n.value > cap:
+            cap = int(n.value * 1.25) + 1024
+            continue
+        N.check(st)
+        break
+    m = n.value
+    out = (xyz[:m], first[:m], f[:m], W[:m])
+    return out if return_first else (out[0], out[2], out[3])
+
+
 # -- loopback groups (one process, one GPU; tests of the sharded path) --------------------------------
 
 def _handles(vols):
