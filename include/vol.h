@@ -206,6 +206,15 @@ typedef struct {
     float w_max;        /* weight cap (F-4); >= 1, a huge value gives the paper's uncapped w         */
 } vol_fusion_params;
 
+/* Counters of one vol_fuse call ("Returns counts").                                   */
+typedef struct {
+    int64_t pixels_valid;   /* valid depth pixels over all frames (each allocates its band)          */
+    int64_t blocks;         /* allocated blocks                                                      */
+    int64_t block_frames;   /* (block, frame) pairs evaluated by the update pass after the
+                               conservative frustum/range cull (frames since the block's allocation) */
+    int64_t voxel_updates;  /* Eq. 1 updates applied (u_SDF >= −μ on a valid in-image pixel)          */
+} vol_fusion_stats;
+
 /* Device bytes vol_fuse needs for up to max_blocks allocated blocks (worst case: host inputs and
  * host outputs).  Returns 0 on invalid arguments.                                                 */
 size_t vol_fuse_workspace_bytes(int64_t max_blocks, int32_t n_frames, const vol_camera *cam);
@@ -219,7 +228,8 @@ size_t vol_fuse_workspace_bytes(int64_t max_blocks, int32_t n_frames, const vol_
  *   outputs   (all host or all device) block_xyz [max_blocks][3] int32, first_frame [max_blocks]
  *             int32 (frame that allocated the block; may be NULL), f, W [max_blocks][512] float32;
  *             rows 0 … n−1 hold the n allocated blocks sorted by (x, y, z) (F-9); *n_blocks (host)
- *             receives n.
+ *             receives n; stats (host, may be NULL) receives the counters above (reading them
+ *             synchronises the stream).
  * Synchronous with respect to the host for *n_blocks (the count is read back); device outputs are
  * complete when the stream reaches that point.  Errors: VOL_EINVAL (arguments), VOL_EDATA (a block
  * walk leaves the coordinate range (−2^20, 2^20) or is longer than 4096 blocks), VOL_ENOMEM (more
@@ -228,7 +238,7 @@ size_t vol_fuse_workspace_bytes(int64_t max_blocks, int32_t n_frames, const vol_
 vol_status vol_fuse(const float *depth, int32_t n_frames, const vol_camera *cam, const float *poses,
                     const vol_fusion_params *params, int64_t max_blocks, void *workspace, size_t workspace_bytes,
                     void *stream, int32_t *block_xyz, int32_t *first_frame, float *f, float *W,
-                    int64_t *n_blocks);
+                    int64_t *n_blocks, vol_fusion_stats *stats);
 
 #ifdef __cplusplus
 }

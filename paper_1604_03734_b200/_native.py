@@ -34,6 +34,11 @@ class vol_fusion_params(ctypes.Structure):
                 ("w_max", ctypes.c_float)]
 
 
+class vol_fusion_stats(ctypes.Structure):
+    _fields_ = [("pixels_valid", ctypes.c_int64), ("blocks", ctypes.c_int64), ("block_frames", ctypes.c_int64),
+                ("voxel_updates", ctypes.c_int64)]
+
+
 class vol_dist(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int), ("world", ctypes.c_int), ("part", ctypes.c_void_p),
                 ("nccl_id", ctypes.c_void_p)]
@@ -84,7 +89,7 @@ def lib() -> ctypes.CDLL:
         "vol_total_launches": (i64, []),
         "vol_fuse_workspace_bytes": (ctypes.c_size_t, [i64, i32, ctypes.POINTER(vol_camera)]),
         "vol_fuse": (st, [P, i32, ctypes.POINTER(vol_camera), P, ctypes.POINTER(vol_fusion_params), i64, P,
-                          ctypes.c_size_t, P, P, P, P, P, P]),
+                          ctypes.c_size_t, P, P, P, P, P, P, ctypes.POINTER(vol_fusion_stats)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

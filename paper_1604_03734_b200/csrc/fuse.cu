@@ -50,7 +50,9 @@ __device__ __forceinline__ unsigned long long pack_key(int32_t x, int32_t y, int
 struct FuseSet {
     unsigned long long *keys;   // [cap], kEmpty = free
     int32_t *first;             // [cap], INT_MAX = none
-    unsigned long long *count;  // [0] inserted keys, [1] error flags (bit0 table full, bit1 coordinate range / walk)
+    unsigned long long *count;  // [0] inserted keys, [1] error flags (bit0 table full, bit1 coordinate range /
+                                // walk), [2] compaction cursor, [3] valid pixels, [4] evaluated block-frames,
+                                // [5] Eq. 1 voxel updates
     uint32_t mask;              // cap − 1
 };
 
@@ -62,7 +64,9 @@ __device__ __forceinline__ void set_insert(const FuseSet &S, int32_t x, int32_t 
     const unsigned long long key = pack_key(x, y, z);
     uint32_t h = ((uint32_t)x * 73856093u ^ (uint32_t)y * 19349669u ^ (uint32_t)z * 83492791u) & S.mask;
     for (uint32_t probe = 0; probe <= S.mask; probe++) {
-        unsigned long long cur = *((volatile unsigned long long *)&S.keys[h]);
+        // plain load: a slot only ever goes EMPTY -> key and first only decreases, so a stale value is
+        // an older state — EMPTY falls through to the CAS, a larger first costs one extra atomicMin
+        unsigned long long cur = S.keys[h];
         if (cur == kEmpty) {
             cur = atomicCAS(&S.keys[h], kEmpty, key);
             if (cur == kEmpty) {
@@ -72,7 +76,7 @@ __device__ __forceinline__ void set_insert(const FuseSet &S, int32_t x, int32_t 
             }
         }
         if (cur == key) {
-            if (*((volatile int32_t *)&S.first[h]) > frame) atomicMin(&S.first[h], frame);
+            if (S.first[h] > frame) atomicMin(&S.first[h], frame);
             return;
         }
         h = (h + 1) & S.mask;
@@ -84,44 +88,44 @@ __device__ __forceinline__ bool depth_ok(float d, float max_range) {
     return isfinite(d) && d > 0.0f && d <= max_range;
 }
 
-// Reading F-6: p_c = ((i − cx)/fx · z, (j − cy)/fy · z, z), p_g = R p_c + t, row sums left to right.
-__device__ __forceinline__ void ray_point(const float *T, float fx, float fy, float cx, float cy, int32_t i, int32_t j,
-                                          float z, float &gx, float &gy, float &gz) {
-    const float xc = __fmul_rn(__fdiv_rn(__fsub_rn((float)i, cx), fx), z);
-    const float yc = __fmul_rn(__fdiv_rn(__fsub_rn((float)j, cy), fy), z);
+// Reading F-6: p_c = (xr·z, yr·z, z) with xr = (i − cx)/fx, yr = (j − cy)/fy; p_g = R p_c + t, row sums left
+// to right.  (xr, yr) are computed once per pixel (same operations as evaluating them per point.)
+__device__ __forceinline__ void ray_point(const float *T, float xr, float yr, float z, float &gx, float &gy, float &gz) {
+    const float xc = __fmul_rn(xr, z);
+    const float yc = __fmul_rn(yr, z);
     const float zc = z;
     gx = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(T[0], xc), __fmul_rn(T[1], yc)), __fmul_rn(T[2], zc)), T[3]);
     gy = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(T[4], xc), __fmul_rn(T[5], yc)), __fmul_rn(T[6], zc)), T[7]);
     gz = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(T[8], xc), __fmul_rn(T[9], yc)), __fmul_rn(T[10], zc)), T[11]);
 }
 
-// One axis of the reading F-7 walk set-up.
+// One axis of the reading F-7 walk set-up.  tMax and tDelta are only ever read for an axis with
+// remaining steps (n > 0), so they are computed only then (n > 0 implies dir != 0).
 __device__ __forceinline__ void walk_axis(float a, float b, float Bm, int32_t &c, int32_t &n, int32_t &step,
                                           float &tmax, float &tdel) {
     const float sa = __fdiv_rn(a, Bm);
     const float sb = __fdiv_rn(b, Bm);
     const float fa = floorf(sa);
     const float fb = floorf(sb);
-    const float dir = __fsub_rn(sb, sa);
     // coordinates far outside the packable range are clamped here and rejected by set_insert
     const float lim = 2.0e9f;
     c = (int32_t)fminf(fmaxf(fa, -lim), lim);
     const int32_t e = (int32_t)fminf(fmaxf(fb, -lim), lim);
-    if (dir > 0.0f) {
-        step = 1;
-        tdel = __fdiv_rn(1.0f, dir);
-        tmax = __fdiv_rn(__fsub_rn(__fadd_rn(fa, 1.0f), sa), dir);
-    } else if (dir < 0.0f) {
-        step = -1;
-        tdel = __fdiv_rn(1.0f, -dir);
-        tmax = __fdiv_rn(__fsub_rn(sa, fa), -dir);
-    } else {
-        step = 0;
-        tdel = INFINITY;
-        tmax = INFINITY;
-    }
     const long long dn = (long long)e - (long long)c;
     n = (int32_t)(dn < 0 ? (-dn > kWalkMax ? kWalkMax + 1 : -dn) : (dn > kWalkMax ? kWalkMax + 1 : dn));
+    step = dn > 0 ? 1 : (dn < 0 ? -1 : 0);
+    tmax = INFINITY;
+    tdel = INFINITY;
+    if (n > 0) {
+        const float dir = __fsub_rn(sb, sa);
+        if (dir > 0.0f) {
+            tdel = __fdiv_rn(1.0f, dir);
+            tmax = __fdiv_rn(__fsub_rn(__fadd_rn(fa, 1.0f), sa), dir);
+        } else {
+            tdel = __fdiv_rn(1.0f, -dir);
+            tmax = __fdiv_rn(__fsub_rn(sa, fa), -dir);
+        }
+    }
 }
 
 struct FuseArgs {
@@ -132,27 +136,34 @@ struct FuseArgs {
     float voxel, mu, max_range, w_max;
 };
 
+// One thread per pixel, grid-stride.  IDX is uint32_t when K·H·W < 2^32 (cheap index arithmetic), else
+// 64-bit.  A lane's walk is independent of its neighbours' (no lockstep): repeated inserts of a block
+// by neighbouring pixels mostly hit the block's slot in L1/L2 and skip the atomics (set_insert).
+template <class IDX>
 __global__ void __launch_bounds__(256) k_fuse_alloc(FuseArgs A, FuseSet S) {
-    const long long HW = (long long)A.H * A.W;
-    const long long total = HW * A.K;
+    const IDX HW = (IDX)A.H * (IDX)A.W;
+    const IDX total = HW * (IDX)A.K;
     const float Bm = __fmul_rn(8.0f, A.voxel);
-    for (long long pix = (long long)blockIdx.x * blockDim.x + threadIdx.x; pix < total;
-         pix += (long long)gridDim.x * blockDim.x) {
+    unsigned long long n_valid = 0;
+    for (IDX pix = (IDX)blockIdx.x * blockDim.x + threadIdx.x; pix < total; pix += (IDX)gridDim.x * blockDim.x) {
         const float d = __ldg(A.depth + pix);
         if (!depth_ok(d, A.max_range)) continue;
+        n_valid++;
         const int32_t k = (int32_t)(pix / HW);
-        const long long rem = pix - (long long)k * HW;
-        const int32_t j = (int32_t)(rem / A.W);
-        const int32_t i = (int32_t)(rem - (long long)j * A.W);
+        const IDX rem = pix - (IDX)k * HW;
+        const int32_t j = (int32_t)(rem / (IDX)A.W);
+        const int32_t i = (int32_t)(rem - (IDX)j * (IDX)A.W);
         float T[12];
 #pragma unroll
         for (int q = 0; q < 12; q++) T[q] = __ldg(A.poses + 12 * k + q);
         float za = __fsub_rn(d, A.mu);
         if (za < 0.0f) za = 0.0f;
         const float zb = __fadd_rn(d, A.mu);
+        const float xr = __fdiv_rn(__fsub_rn((float)i, A.cx), A.fx);
+        const float yr = __fdiv_rn(__fsub_rn((float)j, A.cy), A.fy);
         float ax, ay, az, bx, by, bz;
-        ray_point(T, A.fx, A.fy, A.cx, A.cy, i, j, za, ax, ay, az);
-        ray_point(T, A.fx, A.fy, A.cx, A.cy, i, j, zb, bx, by, bz);
+        ray_point(T, xr, yr, za, ax, ay, az);
+        ray_point(T, xr, yr, zb, bx, by, bz);
         int32_t cx_, cy_, cz_, nx, ny, nz, sx, sy, sz;
         float tx, ty, tz, dx, dy, dz;
         walk_axis(ax, bx, Bm, cx_, nx, sx, tx, dx);
@@ -181,6 +192,9 @@ __global__ void __launch_bounds__(256) k_fuse_alloc(FuseArgs A, FuseSet S) {
             set_insert(S, cx_, cy_, cz_, k);
         }
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) n_valid += __shfl_xor_sync(0xffffffffu, n_valid, o);
+    if ((threadIdx.x & 31) == 0 && n_valid) atomicAdd(&S.count[3], n_valid);
 }
 
 __global__ void k_fuse_compact(FuseSet S, uint32_t cap, unsigned long long *out_keys, int32_t *out_first,
@@ -220,11 +234,18 @@ __device__ __forceinline__ bool block_culled(const float *T, const FuseArgs &A, 
     return false;
 }
 
+// Frames are taken in chunks of 128 (one per thread): each thread loads one frame's pose into shared
+// memory and runs the block cull for it; the CTA then walks the surviving frames of the chunk in
+// increasing order (the Eq. 1 recurrence order is unchanged).
+constexpr int kFrameChunk = 128;
+
 __global__ void __launch_bounds__(128) k_fuse_integrate(FuseArgs A, const unsigned long long *__restrict__ keys,
                                                         const int32_t *__restrict__ first, int64_t n,
                                                         int32_t *__restrict__ xyz_out, int32_t *__restrict__ first_out,
                                                         float *__restrict__ f_out, float *__restrict__ w_out,
-                                                        int cull) {
+                                                        int cull, unsigned long long *stats) {
+    __shared__ float4 sT[kFrameChunk][3];
+    __shared__ uint32_t sMask[kFrameChunk / 32];
     const int64_t b = blockIdx.x;
     if (b >= n) return;
     const unsigned long long key = keys[b];
@@ -232,14 +253,14 @@ __global__ void __launch_bounds__(128) k_fuse_integrate(FuseArgs A, const unsign
     const int32_t by = (int32_t)((key >> 21) & 0x1FFFFF) - kCoordLim;
     const int32_t bz = (int32_t)(key & 0x1FFFFF) - kCoordLim;
     const int32_t k0 = first[b];
-    if (threadIdx.x == 0) {
+    const int t = threadIdx.x;
+    if (t == 0) {
         xyz_out[3 * b] = bx;
         xyz_out[3 * b + 1] = by;
         xyz_out[3 * b + 2] = bz;
         if (first_out) first_out[b] = k0;
     }
     // voxels 4t … 4t+3: x = 4(t&1) + q, y = (t>>1)&7, z = t>>4
-    const int t = threadIdx.x;
     const int lx0 = 4 * (t & 1), ly = (t >> 1) & 7, lz = t >> 4;
     // voxel centre (8B + i + ½)·v (SURVEY §8(d) frame convention)
     float px[4];
@@ -252,41 +273,73 @@ __global__ void __launch_bounds__(128) k_fuse_integrate(FuseArgs A, const unsign
     const float czg = (8.0f * (float)bz + 4.0f) * A.voxel;
     float f[4] = {0.f, 0.f, 0.f, 0.f}, w[4] = {0.f, 0.f, 0.f, 0.f};
     const long long HW = (long long)A.H * A.W;
-    for (int32_t k = k0; k < A.K; k++) {
-        float T[12];
+    unsigned n_frames = 0, n_upd = 0;
+    const float Wf = (float)A.W, Hf = (float)A.H;
+    for (int32_t kb = k0; kb < A.K; kb += kFrameChunk) {
+        {
+            const int32_t k = kb + t;
+            bool keep = false;
+            if (k < A.K) {
+                float T[12];
 #pragma unroll
-        for (int q = 0; q < 12; q++) T[q] = __ldg(A.poses + 12 * k + q);
-        if (cull && block_culled(T, A, cxg, cyg, czg)) continue;
-        const float *D = A.depth + (long long)k * HW;
-        // step 1: p_c = R^T (p_g − t); the y and z parts of p_g − t are shared by the 4 voxels
-        const float d1 = __fsub_rn(py, T[7]);
-        const float d2 = __fsub_rn(pz, T[11]);
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-            const float d0 = __fsub_rn(px[q], T[3]);
-            const float xc = __fadd_rn(__fadd_rn(__fmul_rn(T[0], d0), __fmul_rn(T[4], d1)), __fmul_rn(T[8], d2));
-            const float yc = __fadd_rn(__fadd_rn(__fmul_rn(T[1], d0), __fmul_rn(T[5], d1)), __fmul_rn(T[9], d2));
-            const float zc = __fadd_rn(__fadd_rn(__fmul_rn(T[2], d0), __fmul_rn(T[6], d1)), __fmul_rn(T[10], d2));
-            if (!(zc > 0.0f)) continue;
-            // step 2: nearest pixel (reading F-1)
-            const float ix = __fadd_rn(__fmul_rn(A.fx, __fdiv_rn(xc, zc)), A.cx);
-            const float iy = __fadd_rn(__fmul_rn(A.fy, __fdiv_rn(yc, zc)), A.cy);
-            const float fi = floorf(__fadd_rn(ix, 0.5f));
-            const float fj = floorf(__fadd_rn(iy, 0.5f));
-            if (!(fi >= 0.0f && fi < (float)A.W && fj >= 0.0f && fj < (float)A.H)) continue;
-            const float d = __ldg(D + (long long)(int32_t)fj * A.W + (int32_t)fi);
-            if (!depth_ok(d, A.max_range)) continue;
-            // step 3: u_SDF = d − z_c;  step 4, Eq. 1, readings F-3/F-4
-            const float sdf = __fsub_rn(d, zc);
-            if (sdf < -A.mu) continue;
-            const float c = fminf(fmaxf(sdf, -A.mu), A.mu);
-            const float tsdf = __fdiv_rn(c, A.mu);
-            const float num = __fadd_rn(tsdf, __fmul_rn(w[q], f[q]));
-            const float den = __fadd_rn(w[q], 1.0f);
-            f[q] = __fdiv_rn(num, den);
-            w[q] = fminf(den, A.w_max);
+                for (int q = 0; q < 12; q++) T[q] = __ldg(A.poses + 12 * k + q);
+                keep = !cull || !block_culled(T, A, cxg, cyg, czg);
+                sT[t][0] = make_float4(T[0], T[1], T[2], T[3]);
+                sT[t][1] = make_float4(T[4], T[5], T[6], T[7]);
+                sT[t][2] = make_float4(T[8], T[9], T[10], T[11]);
+            }
+            const uint32_t m = __ballot_sync(0xffffffffu, keep);
+            if ((t & 31) == 0) sMask[t >> 5] = m;
         }
+        __syncthreads();
+#pragma unroll 1
+        for (int wq = 0; wq < kFrameChunk / 32; wq++) {
+            uint32_t m = sMask[wq];
+            while (m) {
+                const int idx = 32 * wq + __ffs(m) - 1;
+                m &= m - 1;
+                n_frames++;
+                const float4 r0 = sT[idx][0], r1 = sT[idx][1], r2 = sT[idx][2];
+                const float *D = A.depth + (long long)(kb + idx) * HW;
+                // step 1: p_c = R^T (p_g − t); the y and z parts of p_g − t are shared by the 4 voxels
+                const float d1 = __fsub_rn(py, r1.w);
+                const float d2 = __fsub_rn(pz, r2.w);
+                const float e1x = __fmul_rn(r1.x, d1), e1y = __fmul_rn(r1.y, d1), e1z = __fmul_rn(r1.z, d1);
+                const float e2x = __fmul_rn(r2.x, d2), e2y = __fmul_rn(r2.y, d2), e2z = __fmul_rn(r2.z, d2);
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    const float d0 = __fsub_rn(px[q], r0.w);
+                    const float xc = __fadd_rn(__fadd_rn(__fmul_rn(r0.x, d0), e1x), e2x);
+                    const float yc = __fadd_rn(__fadd_rn(__fmul_rn(r0.y, d0), e1y), e2y);
+                    const float zc = __fadd_rn(__fadd_rn(__fmul_rn(r0.z, d0), e1z), e2z);
+                    if (!(zc > 0.0f)) continue;
+                    // step 2: nearest pixel (reading F-1)
+                    const float ix = __fadd_rn(__fmul_rn(A.fx, __fdiv_rn(xc, zc)), A.cx);
+                    const float iy = __fadd_rn(__fmul_rn(A.fy, __fdiv_rn(yc, zc)), A.cy);
+                    const float fi = floorf(__fadd_rn(ix, 0.5f));
+                    const float fj = floorf(__fadd_rn(iy, 0.5f));
+                    if (!(fi >= 0.0f && fi < Wf && fj >= 0.0f && fj < Hf)) continue;
+                    const float d = __ldg(D + (int32_t)fj * A.W + (int32_t)fi);
+                    if (!depth_ok(d, A.max_range)) continue;
+                    // step 3: u_SDF = d − z_c;  step 4, Eq. 1, readings F-3/F-4
+                    const float sdf = __fsub_rn(d, zc);
+                    if (sdf < -A.mu) continue;
+                    const float c = fminf(fmaxf(sdf, -A.mu), A.mu);
+                    const float tsdf = __fdiv_rn(c, A.mu);
+                    const float num = __fadd_rn(tsdf, __fmul_rn(w[q], f[q]));
+                    const float den = __fadd_rn(w[q], 1.0f);
+                    f[q] = __fdiv_rn(num, den);
+                    w[q] = fminf(den, A.w_max);
+                    n_upd++;
+                }
+            }
+        }
+        __syncthreads();
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) n_upd += __shfl_xor_sync(0xffffffffu, n_upd, o);
+    if ((t & 31) == 0 && n_upd) atomicAdd(&stats[1], (unsigned long long)n_upd);
+    if (t == 0 && n_frames) atomicAdd(&stats[0], (unsigned long long)n_frames);
     const int64_t o = b * kBlockVox + 4 * t;
     *reinterpret_cast<float4 *>(f_out + o) = make_float4(f[0], f[1], f[2], f[3]);
     *reinterpret_cast<float4 *>(w_out + o) = make_float4(w[0], w[1], w[2], w[3]);
@@ -333,7 +386,7 @@ size_t fuse_layout(Carve &c, FuseLayout &L, int64_t max_blocks, int32_t K, int32
     L.poses = dev_poses ? nullptr : c.take<float>((size_t)K * 12);
     L.keys = c.take<unsigned long long>(cap);
     L.first = c.take<int32_t>(cap);
-    L.count = c.take<unsigned long long>(4);
+    L.count = c.take<unsigned long long>(8);
     for (int q = 0; q < 2; q++) {
         L.ckeys[q] = c.take<unsigned long long>(max_blocks);
         L.cfirst[q] = c.take<int32_t>(max_blocks);
@@ -382,12 +435,13 @@ extern "C" size_t vol_fuse_workspace_bytes(int64_t max_blocks, int32_t n_frames,
 extern "C" vol_status vol_fuse(const float *depth, int32_t n_frames, const vol_camera *cam, const float *poses,
                                const vol_fusion_params *prm, int64_t max_blocks, void *workspace,
                                size_t workspace_bytes, void *stream, int32_t *block_xyz, int32_t *first_frame,
-                               float *f, float *W, int64_t *n_blocks) {
+                               float *f, float *W, int64_t *n_blocks, vol_fusion_stats *stats) {
     vol_status st = check_fuse_args(n_frames, cam, prm, max_blocks);
     if (st != VOL_OK) return st;
     if (!depth || !poses || !block_xyz || !f || !W || !n_blocks)
         return fail(VOL_EINVAL, "vol_fuse: depth, poses, block_xyz, f, W and n_blocks must not be NULL");
     *n_blocks = 0;
+    if (stats) memset(stats, 0, sizeof *stats);
     cudaStream_t s = (cudaStream_t)stream;
     const bool dev_depth = is_device_ptr(depth), dev_poses = is_device_ptr(poses);
     const bool dev_out = is_device_ptr(block_xyz) && is_device_ptr(f) && is_device_ptr(W) &&
@@ -425,7 +479,7 @@ extern "C" vol_status vol_fuse(const float *depth, int32_t n_frames, const vol_c
     const uint32_t cap = fuse_table_cap(max_blocks);
     CK(cudaMemsetAsync(L.keys, 0xFF, sizeof(unsigned long long) * cap, s));
     CK(cudaMemsetAsync(L.first, 0x7F, sizeof(int32_t) * cap, s));   // 0x7F7F7F7F > any frame index
-    CK(cudaMemsetAsync(L.count, 0, sizeof(unsigned long long) * 4, s));
+    CK(cudaMemsetAsync(L.count, 0, sizeof(unsigned long long) * 8, s));
     FuseArgs A{d_depth, d_poses, K, H, Wd, cam->fx, cam->fy, cam->cx, cam->cy,
                prm->voxel, prm->mu, prm->max_range, prm->w_max};
     FuseSet S{L.keys, L.first, L.count, cap - 1};
@@ -435,13 +489,20 @@ extern "C" vol_status vol_fuse(const float *depth, int32_t n_frames, const vol_c
     const long long total = (long long)K * H * Wd;
     long long grid = (total + 255) / 256;
     if (grid > (long long)sms * 16) grid = (long long)sms * 16;
-    k_fuse_alloc<<<(unsigned)grid, 256, 0, s>>>(A, S);
+    if (total < (1ll << 32) - 1 - (long long)grid * 256)
+        k_fuse_alloc<uint32_t><<<(unsigned)grid, 256, 0, s>>>(A, S);
+    else
+        k_fuse_alloc<unsigned long long><<<(unsigned)grid, 256, 0, s>>>(A, S);
     CK(cudaPeekAtLastError());
     counted(1);
-    unsigned long long hc[2];
+    unsigned long long hc[4];
     CK(cudaMemcpyAsync(hc, L.count, sizeof hc, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     *n_blocks = (int64_t)hc[0];
+    if (stats) {
+        stats->pixels_valid = (int64_t)hc[3];
+        stats->blocks = (int64_t)hc[0];
+    }
     if (hc[1] & 2ull)
         return fail(VOL_EDATA, "vol_fuse: a block walk leaves the block-coordinate range (-2^20, 2^20) or is longer "
                                "than %d blocks (check poses, voxel size and max_range)", kWalkMax);
@@ -463,7 +524,8 @@ extern "C" vol_status vol_fuse(const float *depth, int32_t n_frames, const vol_c
     float *of = dev_out ? f : L.f;
     float *ow = dev_out ? W : L.w;
     const int cull = getenv("HVG_FUSE_NOCULL") ? 0 : 1;   // experiments only: the cull never changes results
-    k_fuse_integrate<<<(unsigned)n, 128, 0, s>>>(A, L.ckeys[1], L.cfirst[1], n, oxyz, ofirst, of, ow, cull);
+    k_fuse_integrate<<<(unsigned)n, 128, 0, s>>>(A, L.ckeys[1], L.cfirst[1], n, oxyz, ofirst, of, ow, cull,
+                                                  L.count + 4);
     CK(cudaPeekAtLastError());
     counted(1);
     if (!dev_out) {
@@ -471,6 +533,13 @@ extern "C" vol_status vol_fuse(const float *depth, int32_t n_frames, const vol_c
         if (first_frame) CK(cudaMemcpyAsync(first_frame, L.ofirst, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(f, L.f, sizeof(float) * kBlockVox * n, cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(W, L.w, sizeof(float) * kBlockVox * n, cudaMemcpyDeviceToHost, s));
+    }
+    if (stats) {
+        unsigned long long hs[2];
+        CK(cudaMemcpyAsync(hs, L.count + 4, sizeof hs, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        stats->block_frames = (int64_t)hs[0];
+        stats->voxel_updates = (int64_t)hs[1];
     }
     if (owns || !dev_out) CK(cudaStreamSynchronize(s));
     return VOL_OK;

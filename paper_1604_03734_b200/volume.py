@@ -239,12 +239,14 @@ class Volume:
 # -- TSDF fusion (paper §III-A, Eq. 1) -----------------------------------------
 
 def fuse(depth, poses, intr, voxel: float, mu: float, max_range: float, w_max: float, *, max_blocks=None,
-         stream=None, return_first=True):
+         stream=None, return_first=True, stats=None):
     """Fuse K posed depth maps into hashed voxel blocks on the GPU (``vol_fuse``).
 
     depth [K, H, W] float32 metres, poses [K, 12] float32 row-major T_gc (camera-to-global), intr
     (fx, fy, cx, cy).  Returns CUDA tensors (coords int32 [n, 3] sorted by (x, y, z), first frame
-    int32 [n], f float32 [n, 512], W float32 [n, 512]) — ready for :class:`Volume`.
+    int32 [n], f float32 [n, 512], W float32 [n, 512]) — ready for :class:`Volume`.  Pass a dict as
+    `stats` to receive the call's counters (pixels_valid, blocks, block_frames, voxel_updates; this
+    synchronises the stream).
     """
     _require_cuda()
     L = N.lib()
@@ -271,16 +273,20 @@ def fuse(depth, poses, intr, voxel: float, mu: float, max_range: float, w_max: f
         nbytes = L.vol_fuse_workspace_bytes(cap, K, ctypes.byref(cam))
         ws = torch.empty(int(nbytes), dtype=torch.uint8, device=dev)
         n = ctypes.c_int64()
+        sts = N.vol_fusion_stats()
         st = L.vol_fuse(ctypes.c_void_p(depth.data_ptr()), K, ctypes.byref(cam), ctypes.c_void_p(poses.data_ptr()),
                         ctypes.byref(prm), cap, ctypes.c_void_p(ws.data_ptr()), nbytes, ctypes.c_void_p(s.cuda_stream),
                         ctypes.c_void_p(xyz.data_ptr()), ctypes.c_void_p(first.data_ptr()),
-                        ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(W.data_ptr()), ctypes.byref(n))
+                        ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(W.data_ptr()), ctypes.byref(n),
+                        ctypes.byref(sts) if stats is not None else None)
         if st == N.VOL_ENOMEM and not max_blocks and n.value > cap:
             cap = int(n.value * 1.25) + 1024
             continue
         N.check(st)
         break
     m = n.value
+    if stats is not None:
+        stats.update({k: int(getattr(sts, k)) for k, _ in N.vol_fusion_stats._fields_})
     out = (xyz[:m], first[:m], f[:m], W[:m])
     return out if return_first else (out[0], out[2], out[3])
 

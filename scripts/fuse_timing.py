@@ -13,7 +13,9 @@ ds = street_depth(device="cuda")
 torch.cuda.synchronize()
 print(f"render {time.time() - t0:.1f} s, depth {tuple(ds.depth.shape)}")
 intr = ds.intr.cpu().numpy()
-out = fuse(ds.depth, ds.poses, intr, ds.voxel, ds.mu, ds.max_range, ds.w_max)
+st = {}
+out = fuse(ds.depth, ds.poses, intr, ds.voxel, ds.mu, ds.max_range, ds.w_max, stats=st)
+print("stats", st)
 n = out[0].shape[0]
 print("blocks", n, "observed voxels", int((out[3] > 0).sum()), "max W", float(out[3].max()))
 for cap in (n, None):

@@ -125,9 +125,26 @@ def test_host_outputs_equal_device_outputs(fuse):
     nb = ctypes.c_int64()
     N.check(N.lib().vol_fuse(D.ctypes.data, ds.K, ctypes.byref(cam), P.ctypes.data, ctypes.byref(prm), cap, None, 0,
                              None, xyz.ctypes.data, first.ctypes.data, f.ctypes.data, W.ctypes.data,
-                             ctypes.byref(nb)))
+                             ctypes.byref(nb), None))
     assert nb.value == n
     _same(dev, (xyz[:n], first[:n], f[:n], W[:n]))
+
+
+def test_stats_counters(fuse):
+    """pixels_valid, blocks and voxel_updates are exact counts (the latter = number of Eq. 1 updates,
+    i.e. the sum of W for an uncapped fusion); block_frames lies between the frames that update some
+    voxel of a block and all frames since its allocation."""
+    ds = sphere_depth()
+    st = {}
+    xyz, first, f, W = fuse(ds.depth.cuda(), ds.poses.cuda(), ds.intr.numpy(), ds.voxel, ds.mu, ds.max_range, 1e30,
+                            stats=st)
+    D = ds.depth.numpy()
+    assert st["pixels_valid"] == int((np.isfinite(D) & (D > 0) & (D <= ds.max_range)).sum())
+    assert st["blocks"] == xyz.shape[0]
+    assert st["voxel_updates"] == int(W.sum().item())
+    fr = first.cpu().numpy()
+    assert st["block_frames"] <= int((ds.K - fr).sum())
+    assert st["block_frames"] >= int(W.cpu().numpy().max(1).sum())
 
 
 def test_capacity_errors_and_retry(fuse):
