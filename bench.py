@@ -33,6 +33,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 ALG_BYTES_PER_VOXEL = 48  # 28 B read (f, W, u, ū, p×3) + 20 B written (u, ū, p×3)
+FUSE_OPS_PER_EVAL = 36    # fp32 operations of steps 1-4 + Eq. 1 for one voxel and one frame
 
 
 def parse():
@@ -49,6 +50,7 @@ def parse():
                     help="use the NCCL sharded runtime even at one rank (tests the N > 1 code path on one GPU)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fusion", action="store_true", help="skip the TSDF-fusion leg (SURVEY §8(f) NEXT-2)")
     ap.add_argument("--seed", type=int, default=0)
     return ap.parse_args()
 
@@ -149,6 +151,75 @@ def partition(coords, world):
     for r in range(world):
         part[order[r * n // world:(r + 1) * n // world].cpu()] = r
     return part
+
+
+def alu_peak():
+    """Issue-limited ALU peak in lane-operations/s: 148 SMs × 4 SMSPs × 32 lanes × 1 instruction per clock
+    × the max SM clock (MEASURED_PEAKS.json sm_max_mhz, else 1965 MHz) — DESIGN.md §11."""
+    mhz = 1965.0
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            mhz = float(json.load(fh).get("sm_max_mhz", mhz))
+    except Exception:
+        pass
+    return 148 * 4 * 32 * mhz * 1e6, f"148 SMs x 4 SMSPs x 32 lanes x 1 inst/clk x {mhz:.0f} MHz"
+
+
+def fusion_leg(args, dev):
+    """TSDF fusion of the fusion-street depth maps (61 frames, 1240x376) through vol_fuse, inputs in HBM."""
+    import torch
+
+    from paper_1604_03734_b200 import fuse
+    from synth.depth import street_depth
+    ds = street_depth(seed=args.seed, device=dev)
+    intr = ds.intr.cpu().numpy()
+    st = {}
+    out = fuse(ds.depth, ds.poses, intr, ds.voxel, ds.mu, ds.max_range, ds.w_max, stats=st)
+    n = int(out[0].shape[0])
+    del out
+    call = lambda **kw: fuse(ds.depth, ds.poses, intr, ds.voxel, ds.mu, ds.max_range, ds.w_max, max_blocks=n + 16, **kw)
+    for _ in range(3):
+        call()
+    stream = torch.cuda.current_stream(dev)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    a.record(stream)
+    for _ in range(args.steps):
+        call()
+    b.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = a.elapsed_time(b) / args.steps
+    kst = []
+    for _ in range(5):
+        d = {}
+        call(stats=d)
+        kst.append(d)
+    t_int = statistics.median(d["ms_integrate"] for d in kst)
+    t_alloc = statistics.median(d["ms_alloc"] for d in kst)
+    evals = st["block_frames"] * 512
+    peak, peak_src = alu_peak()
+    ach = FUSE_OPS_PER_EVAL * evals / (t_int / 1e3)
+    res = {"workload": "fusion-street", "frames": ds.K, "image": [ds.H, ds.Wd], "voxel": ds.voxel, "mu": ds.mu,
+           "w_max": ds.w_max, "ms_per_call": ms, "frames_per_s": ds.K / (ms / 1e3),
+           "voxel_updates_per_s": st["voxel_updates"] / (ms / 1e3), "blocks": n,
+           "stats": {k: st[k] for k in ("pixels_valid", "blocks", "block_frames", "voxel_updates")},
+           "kernel_ms": {"k_fuse_alloc": t_alloc, "k_fuse_integrate": t_int},
+           "step": "vol_fuse (alloc + compact + radix sort + integrate), depth maps and poses resident in HBM",
+           "roofline": {"bound": "alu", "kernel": "k_fuse_integrate", "achieved": ach / 1e12, "peak": peak / 1e12,
+                        "unit": "Tops/s", "frac": ach / peak, "peak_source": peak_src,
+                        "alg_ops_per_launch": FUSE_OPS_PER_EVAL * evals, "avg_launch_ms": t_int,
+                        "traffic": None}}
+    if not args.no_cpu_baseline:
+        import oracle
+        k = 4
+        D, P = ds.depth[:k].cpu().numpy(), ds.poses[:k].cpu().numpy()
+        t0 = time.perf_counter()
+        oracle.fuse(D, intr, P, ds.voxel, ds.mu, ds.max_range, ds.w_max)
+        dt = time.perf_counter() - t0
+        res["cpu_baseline"] = {"value": k / dt, "unit": "frames/s", "cores": 1, "kind": "oracle",
+                               "sample": f"first {k} of the {ds.K} fusion-street frames, sequential fp32 oracle, "
+                                         f"{dt:.1f} s on one host core"}
+    return res
 
 
 # ------------------------------------------------------------------------------ CPU oracle timing
@@ -332,6 +403,10 @@ def main():
         e2e = {"value": n_alloc_total * iters / (ems / 1e3), "unit": "voxel-updates/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": ems}
 
+    fusion = None
+    if not args.no_fusion and world == 1:
+        fusion = fusion_leg(args, dev)
+
     if rank != 0:
         dist.destroy_process_group()
         return 0
@@ -378,7 +453,7 @@ def main():
                    "energy": {"primal": E[0], "dual": E[1]}},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
         "freeze": bool(args.freeze), "no_freeze": nf,
-        "clocks": clk,
+        "clocks": clk, "fusion": fusion,
     }
     print(json.dumps(line), flush=True)
     if sharded:

@@ -213,6 +213,8 @@ typedef struct {
     int64_t block_frames;   /* (block, frame) pairs evaluated by the update pass after the
                                conservative frustum/range cull (frames since the block's allocation) */
     int64_t voxel_updates;  /* Eq. 1 updates applied (u_SDF >= −μ on a valid in-image pixel)          */
+    float ms_alloc;         /* CUDA-event duration of the allocation kernel on the stream (ms)        */
+    float ms_integrate;     /* CUDA-event duration of the update kernel on the stream (ms)            */
 } vol_fusion_stats;
 
 /* Device bytes vol_fuse needs for up to max_blocks allocated blocks (worst case: host inputs and

@@ -36,7 +36,7 @@ class vol_fusion_params(ctypes.Structure):
 
 class vol_fusion_stats(ctypes.Structure):
     _fields_ = [("pixels_valid", ctypes.c_int64), ("blocks", ctypes.c_int64), ("block_frames", ctypes.c_int64),
-                ("voxel_updates", ctypes.c_int64)]
+                ("voxel_updates", ctypes.c_int64), ("ms_alloc", ctypes.c_float), ("ms_integrate", ctypes.c_float)]
 
 
 class vol_dist(ctypes.Structure):

@@ -489,12 +489,24 @@ extern "C" vol_status vol_fuse(const float *depth, int32_t n_frames, const vol_c
     const long long total = (long long)K * H * Wd;
     long long grid = (total + 255) / 256;
     if (grid > (long long)sms * 16) grid = (long long)sms * 16;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    if (stats)
+        for (auto &e : ev) CK(cudaEventCreate(&e));
+    struct EvFree {
+        cudaEvent_t *e;
+        ~EvFree() {
+            for (int q = 0; q < 4; q++)
+                if (e[q]) cudaEventDestroy(e[q]);
+        }
+    } ev_guard{ev};
+    if (stats) CK(cudaEventRecord(ev[0], s));
     if (total < (1ll << 32) - 1 - (long long)grid * 256)
         k_fuse_alloc<uint32_t><<<(unsigned)grid, 256, 0, s>>>(A, S);
     else
         k_fuse_alloc<unsigned long long><<<(unsigned)grid, 256, 0, s>>>(A, S);
     CK(cudaPeekAtLastError());
     counted(1);
+    if (stats) CK(cudaEventRecord(ev[1], s));
     unsigned long long hc[4];
     CK(cudaMemcpyAsync(hc, L.count, sizeof hc, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -524,10 +536,12 @@ extern "C" vol_status vol_fuse(const float *depth, int32_t n_frames, const vol_c
     float *of = dev_out ? f : L.f;
     float *ow = dev_out ? W : L.w;
     const int cull = getenv("HVG_FUSE_NOCULL") ? 0 : 1;   // experiments only: the cull never changes results
+    if (stats) CK(cudaEventRecord(ev[2], s));
     k_fuse_integrate<<<(unsigned)n, 128, 0, s>>>(A, L.ckeys[1], L.cfirst[1], n, oxyz, ofirst, of, ow, cull,
                                                   L.count + 4);
     CK(cudaPeekAtLastError());
     counted(1);
+    if (stats) CK(cudaEventRecord(ev[3], s));
     if (!dev_out) {
         CK(cudaMemcpyAsync(block_xyz, L.xyz, sizeof(int32_t) * 3 * n, cudaMemcpyDeviceToHost, s));
         if (first_frame) CK(cudaMemcpyAsync(first_frame, L.ofirst, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
@@ -540,6 +554,8 @@ extern "C" vol_status vol_fuse(const float *depth, int32_t n_frames, const vol_c
         CK(cudaStreamSynchronize(s));
         stats->block_frames = (int64_t)hs[0];
         stats->voxel_updates = (int64_t)hs[1];
+        CK(cudaEventElapsedTime(&stats->ms_alloc, ev[0], ev[1]));
+        CK(cudaEventElapsedTime(&stats->ms_integrate, ev[2], ev[3]));
     }
     if (owns || !dev_out) CK(cudaStreamSynchronize(s));
     return VOL_OK;

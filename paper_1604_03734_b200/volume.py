@@ -286,7 +286,7 @@ def fuse(depth, poses, intr, voxel: float, mu: float, max_range: float, w_max: f
         break
     m = n.value
     if stats is not None:
-        stats.update({k: int(getattr(sts, k)) for k, _ in N.vol_fusion_stats._fields_})
+        stats.update({k: getattr(sts, k) for k, _ in N.vol_fusion_stats._fields_})
     out = (xyz[:m], first[:m], f[:m], W[:m])
     return out if return_first else (out[0], out[2], out[3])
 
