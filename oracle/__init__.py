@@ -20,6 +20,9 @@ Parity status per function:
   fusion (Eq. 1) ........ pinned (SPEC worked examples, fronto-parallel plane closed form under random
                           rigid poses, running-average closed form, block walk vs exact segment-box
                           intersection, dense numpy brute force O2-fusion) — ``fusion_oracle.c``
+  extraction ............ pinned (planar fields: vertices on the plane, exact area, orientation; analytic
+                          sphere: closed 2-manifold, Euler characteristic 2, area/volume; Ω
+                          restriction) — ``extract_oracle.c``
 """
 from __future__ import annotations
 
@@ -32,7 +35,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
 _SRC = [os.path.join(_HERE, "hvg_oracle.c"), os.path.join(_HERE, "fusion_oracle.c"),
-        os.path.join(_HERE, "hvg_oracle_real.inc")]
+        os.path.join(_HERE, "extract_oracle.c"), os.path.join(_HERE, "hvg_oracle_real.inc")]
 
 
 def build(force: bool = False) -> str:
@@ -41,7 +44,7 @@ def build(force: bool = False) -> str:
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < newest:
         tmp = _SO + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-std=c99", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
-                               "-Wall", "-o", tmp, _SRC[0], _SRC[1], "-lm"])
+                               "-Wall", "-o", tmp, _SRC[0], _SRC[1], _SRC[2], "-lm"])
         os.replace(tmp, _SO)
     return _SO
 
@@ -88,6 +91,8 @@ def lib():
         L.orc_fuse.argtypes = [P, i32, i32, i32, P, P, flt, flt, flt, flt, i64, P, P, P, P]
         L.orc_fuse_alloc.restype = i64
         L.orc_fuse_alloc.argtypes = [P, i32, i32, i32, P, P, flt, flt, flt, i64, P, P]
+        L.orc_extract.restype = i64
+        L.orc_extract.argtypes = [P, i64, P, P, flt, flt, P, i64]
         L.orc_fuse_update_blocks.restype = None
         L.orc_fuse_update_blocks.argtypes = [P, i32, i32, i32, P, P, flt, flt, flt, flt, P, P, i64, P, P]
         _lib = L
@@ -313,3 +318,21 @@ def fuse_update_blocks(depth, intr, poses, voxel, mu, max_range, w_max, xyz, fir
     lib().orc_fuse_update_blocks(_ptr(D), K, H, Wd, _ptr(it), _ptr(ps), r(voxel), r(mu), r(max_range), r(w_max),
                                  _ptr(c), _ptr(fr), nb, _ptr(f), _ptr(W))
     return f[:nb], W[:nb]
+
+
+# ---------------------------------------------------------------------------------------------------
+# Ω-restricted isosurface extraction (marching tetrahedra; extract_oracle.c)
+# ---------------------------------------------------------------------------------------------------
+
+def extract(coords, u, W, voxel, w_min=0.0) -> np.ndarray:
+    """Triangle soup [m, 3, 3] float32 of the zero level set of u over the fully observed cells."""
+    c = _np(coords, np.int32).reshape(-1, 3)
+    n = c.shape[0]
+    uu = _np(u, np.float32).reshape(n, 512)
+    ww = _np(W, np.float32).reshape(n, 512)
+    r = lambda x: float(np.float32(x))
+    m = lib().orc_extract(_ptr(c), n, _ptr(uu), _ptr(ww), r(voxel), r(w_min), None, 0)
+    out = np.zeros((max(m, 1), 3, 3), np.float32)
+    m2 = lib().orc_extract(_ptr(c), n, _ptr(uu), _ptr(ww), r(voxel), r(w_min), _ptr(out), m)
+    assert m2 == m
+    return out[:m]
