@@ -179,6 +179,20 @@ vol_status vol_plan_shard(const int32_t *block_xyz, int64_t n_global, const int3
                           int64_t *ghost_global, int64_t *send_global, int64_t *peer_send,
                           int64_t *peer_recv);
 
+/* Isosurface extraction ("extract the surface", P:132-133 zero-crossing
+ * level set).  Readings X-1 … X-7: marching tetrahedra over the cells spanned by every
+ * voxel g and g + {0,1}^3 (voxel centres (g + ½)·voxel metres) whose 8 corners are allocated with
+ * W > 0 and W >= w_min (no geometry next to Ω̄); each cell split into the 6 Freudenthal tetrahedra;
+ * inside ⇔ value < 0; vertex on an edge with ends lo < hi (global coordinates, lexicographic)
+ * p = P_lo + t(P_hi − P_lo), t = v_lo/(v_lo − v_hi) in fp32; triangles oriented toward value > 0;
+ * triangles with two identical vertices dropped.  Output: triangle soup [m][3][3] float32 (x, y, z
+ * of 3 vertices), ordered by caller block, cell (voxel order), tetrahedron, triangle.
+ *   field   0: the current u (u = f from vol_create until the first vol_regularise), 1: the fused f;
+ *   tris    host or device buffer of max_tris triangles, or NULL to count only; *n_tris receives m.
+ * Synchronous.  Errors: VOL_EINVAL, VOL_ENOMEM (m > max_tris; *n_tris = m), VOL_ENOTSUP (sharded
+ * volume), VOL_ECUDA.                                                                               */
+vol_status vol_extract(vol_t v, int field, float voxel, float w_min, float *tris, int64_t max_tris, int64_t *n_tris);
+
 /* TSDF fusion of posed depth maps (paper §III-A, Eq. 1) ----------
  * Readings F-1 … F-10.  For every depth map k = 0 … K−1 in sequence the paper
  * allocates the blocks where frame k observes a surface and then updates every voxel of

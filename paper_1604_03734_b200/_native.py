@@ -49,7 +49,7 @@ EXPORTS = [
     "vol_read_state", "vol_load_state", "vol_read_tables", "vol_info", "vol_last_launches", "vol_sync",
     "vol_destroy", "vol_last_error", "vol_nccl_unique_id", "vol_group_connect", "vol_regularise_group",
     "vol_group_energy", "vol_block_hash", "vol_plan_shard", "vol_total_launches", "vol_fuse_workspace_bytes",
-    "vol_fuse",
+    "vol_fuse", "vol_extract",
 ]
 
 _lib = None
@@ -87,6 +87,7 @@ def lib() -> ctypes.CDLL:
         "vol_block_hash": (u32, [i32, i32, i32, u32]),
         "vol_plan_shard": (st, [P, i64, P, c_int, c_int, P, P, P, P, P, P, P]),
         "vol_total_launches": (i64, []),
+        "vol_extract": (st, [P, c_int, f32, f32, P, i64, P]),
         "vol_fuse_workspace_bytes": (ctypes.c_size_t, [i64, i32, ctypes.POINTER(vol_camera)]),
         "vol_fuse": (st, [P, i32, ctypes.POINTER(vol_camera), P, ctypes.POINTER(vol_fusion_params), i64, P,
                           ctypes.c_size_t, P, P, P, P, P, P, ctypes.POINTER(vol_fusion_stats)]),

@@ -1,0 +1,302 @@
+// extract.cu — Ω-restricted isosurface extraction of the regularised TSDF (paper
+// P:102 "regularise the model in 3D space, extract the surface", P:132-133 zero-crossing level set).
+// Readings X-1 … X-7: marching tetrahedra over the cells of fully observed voxels.
+//
+//   k_extract<false>  one 128-thread CTA per store row: stage the 9×9×9 tile of values and
+//                     "usable" flags (allocated ∧ W > 0 ∧ W >= w_min) of the block and its +x/+y/+z
+//                     neighbours (face, edge and corner blocks reached by neighbour-table chains: if an
+//                     intermediate block is missing, every cell needing the chained block has a corner
+//                     in the missing one, so it is skipped anyway); each thread counts the triangles of
+//                     its 4 cells; per-thread counts go to scratch, the block total to counts[caller].
+//   exclusive scan of the per-block totals in caller order → triangle offsets (deterministic output
+//   order X-7: caller block order, cell order, tetrahedron order, triangle order).
+//   k_extract<true>   same CTA layout: block scan of the per-thread counts, then each thread writes
+//                     its triangles at offset[caller] + prefix.
+// Vertex arithmetic is fp32 in the written order of X-4 (bit-identical to the oracle).
+#include <cuda_runtime.h>
+
+#include "../../include/vol.h"
+#include "handle.h"
+#include "internal.h"
+
+namespace hvg {
+
+namespace {
+
+constexpr int kT = 9;             // tile edge: 8 own voxels + 1 from the + neighbours
+constexpr int kTile = kT * kT * kT;
+
+struct ExArgs {
+    const float *val;      // [S][512] field (u or f), store rows
+    const float *W;        // [S][512]
+    const int32_t *nbr;    // [S][12]
+    const int32_t *perm;   // [n] caller index of store row
+    const int32_t *xyz;    // [n][3] caller order
+    float voxel, w_min;
+};
+
+// X-4: vertex on the tet edge between tile corners i and j (tile coordinates; same block origin so the
+// lexicographic order of global coordinates is that of tile coordinates).
+__device__ __forceinline__ void edge_vertex(int gx, int gy, int gz, const int *ci, float ui, const int *cj, float uj,
+                                            float voxel, float *p) {
+    bool swap = false;
+    if (cj[0] != ci[0]) swap = cj[0] < ci[0];
+    else if (cj[1] != ci[1]) swap = cj[1] < ci[1];
+    else swap = cj[2] < ci[2];
+    const int *lo = swap ? cj : ci;
+    const int *hi = swap ? ci : cj;
+    const float ulo = swap ? uj : ui, uhi = swap ? ui : uj;
+    const float t = __fdiv_rn(ulo, __fsub_rn(ulo, uhi));
+    const int g0[3] = {gx, gy, gz};
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+        const float plo = __fmul_rn(__fadd_rn((float)(g0[k] + lo[k]), 0.5f), voxel);
+        const float phi = __fmul_rn(__fadd_rn((float)(g0[k] + hi[k]), 0.5f), voxel);
+        p[k] = __fadd_rn(plo, __fmul_rn(t, __fsub_rn(phi, plo)));
+    }
+}
+
+__device__ __forceinline__ bool same3(const float *a, const float *b) {
+    return a[0] == b[0] && a[1] == b[1] && a[2] == b[2];
+}
+
+template <bool EMIT>
+__device__ __forceinline__ void put(float *out, unsigned &m, const float *p0, const float *p1, const float *p2) {
+    if (same3(p0, p1) || same3(p1, p2) || same3(p0, p2)) return;   // X-6
+    if (EMIT) {
+        float *o = out + 9ull * m;
+#pragma unroll
+        for (int k = 0; k < 3; k++) {
+            o[k] = p0[k];
+            o[3 + k] = p1[k];
+            o[6 + k] = p2[k];
+        }
+    }
+    m++;
+}
+
+// All triangles of one cell (corner values cu[i + 2j + 4k], tile origin (cx, cy, cz), global voxel
+// origin of the block g0).  Returns the count; writes them from out[9·m0] when EMIT.
+template <bool EMIT>
+__device__ unsigned cell_triangles(const float *cu, int cx, int cy, int cz, int gx, int gy, int gz, float voxel,
+                                   float *out, unsigned m) {
+    // X-2: permutations of the axes in lexicographic order and their parity
+    const int P0[6] = {0, 0, 1, 1, 2, 2}, P1[6] = {1, 2, 0, 2, 0, 1};
+    const bool EVEN[6] = {true, false, false, true, true, false};
+#pragma unroll 1
+    for (int q = 0; q < 6; q++) {
+        int off[4][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {1, 1, 1}};
+        off[1][P0[q]] = 1;
+        off[2][P0[q]] = 1;
+        off[2][P1[q]] = 1;
+        int ord[4] = {0, 1, 2, 3};
+        if (!EVEN[q]) {
+            ord[2] = 3;
+            ord[3] = 2;
+        }
+        int c[4][3];
+        float val[4];
+        bool in[4];
+        int nin = 0;
+#pragma unroll
+        for (int r = 0; r < 4; r++) {
+            const int *o = off[ord[r]];
+            c[r][0] = cx + o[0];
+            c[r][1] = cy + o[1];
+            c[r][2] = cz + o[2];
+            val[r] = cu[o[0] + 2 * o[1] + 4 * o[2]];
+            in[r] = val[r] < 0.0f;   // X-3
+            nin += in[r];
+        }
+        if (nin == 0 || nin == 4) continue;
+        int p[4], np = 0;
+        if (nin == 2) {
+#pragma unroll
+            for (int r = 0; r < 4; r++)
+                if (in[r]) p[np++] = r;
+#pragma unroll
+            for (int r = 0; r < 4; r++)
+                if (!in[r]) p[np++] = r;
+        } else {
+            const bool sel = nin == 1;   // the lone vertex has in == sel
+#pragma unroll
+            for (int r = 0; r < 4; r++)
+                if (in[r] == sel) p[np++] = r;
+#pragma unroll
+            for (int r = 0; r < 4; r++)
+                if (in[r] != sel) p[np++] = r;
+        }
+        int inv = 0;
+#pragma unroll
+        for (int x = 0; x < 4; x++)
+#pragma unroll
+            for (int y = x + 1; y < 4; y++) inv += p[x] > p[y];
+        if (inv & 1) {
+            const int t = p[2];
+            p[2] = p[3];
+            p[3] = t;
+        }
+        const int a = p[0], b = p[1], cc = p[2], d = p[3];
+        float e1[3], e2[3], e3[3], e4[3];
+        if (nin != 2) {
+            edge_vertex(gx, gy, gz, c[a], val[a], c[b], val[b], voxel, e1);
+            edge_vertex(gx, gy, gz, c[a], val[a], c[cc], val[cc], voxel, e2);
+            edge_vertex(gx, gy, gz, c[a], val[a], c[d], val[d], voxel, e3);
+            if (nin == 1) put<EMIT>(out, m, e1, e2, e3);
+            else put<EMIT>(out, m, e1, e3, e2);
+        } else {
+            edge_vertex(gx, gy, gz, c[a], val[a], c[cc], val[cc], voxel, e1);   // E_ac
+            edge_vertex(gx, gy, gz, c[a], val[a], c[d], val[d], voxel, e2);     // E_ad
+            edge_vertex(gx, gy, gz, c[b], val[b], c[d], val[d], voxel, e3);     // E_bd
+            edge_vertex(gx, gy, gz, c[b], val[b], c[cc], val[cc], voxel, e4);   // E_bc
+            put<EMIT>(out, m, e1, e2, e3);
+            put<EMIT>(out, m, e1, e3, e4);
+        }
+    }
+    return m;
+}
+
+template <bool EMIT>
+__global__ void __launch_bounds__(128) k_extract(ExArgs A, int64_t n_rows, uint32_t *__restrict__ block_counts,
+                                                 uint32_t *__restrict__ thread_counts,
+                                                 const uint32_t *__restrict__ offsets, float *__restrict__ out) {
+    __shared__ float su[kTile];
+    __shared__ uint8_t sok[kTile];
+    __shared__ int32_t srow[8];
+    __shared__ uint32_t swarp[4];
+    const int64_t r = blockIdx.x;
+    if (r >= n_rows) return;
+    const int t = threadIdx.x;
+    if (t == 0) {
+        // blocks of the tile: index dx + 2dy + 4dz; chains +x → +y → +z (reading X-1 note above)
+        const int32_t *N = A.nbr;
+        const int32_t bx = N[12 * r + 1], by = N[12 * r + 3], bz = N[12 * r + 5];
+        const int32_t bxy = bx >= 0 ? N[12 * bx + 3] : -1;
+        const int32_t bxz = bx >= 0 ? N[12 * bx + 5] : -1;
+        const int32_t byz = by >= 0 ? N[12 * by + 5] : -1;
+        const int32_t bxyz = bxy >= 0 ? N[12 * bxy + 5] : -1;
+        srow[0] = (int32_t)r;
+        srow[1] = bx;
+        srow[2] = by;
+        srow[3] = bxy;
+        srow[4] = bz;
+        srow[5] = bxz;
+        srow[6] = byz;
+        srow[7] = bxyz;
+    }
+    __syncthreads();
+    for (int i = t; i < kTile; i += 128) {
+        const int x = i % kT, y = (i / kT) % kT, z = i / (kT * kT);
+        const int blk = srow[(x >> 3) + 2 * (y >> 3) + 4 * (z >> 3)];
+        float uv = 0.0f;
+        uint8_t ok = 0;
+        if (blk >= 0) {
+            const int64_t o = (int64_t)blk * kBlockVox + (x & 7) + 8 * (y & 7) + 64 * (z & 7);
+            const float w = A.W[o];
+            uv = A.val[o];
+            ok = (w > 0.0f && w >= A.w_min) ? 1 : 0;   // X-1
+        }
+        su[i] = uv;
+        sok[i] = ok;
+    }
+    __syncthreads();
+    const int32_t ci = A.perm[r];
+    const int gx = 8 * A.xyz[3 * ci], gy = 8 * A.xyz[3 * ci + 1], gz = 8 * A.xyz[3 * ci + 2];
+    // cells 4t … 4t+3 in voxel order: x = 4(t&1) + q, y = (t>>1)&7, z = t>>4
+    const int cy = (t >> 1) & 7, cz = t >> 4;
+    unsigned base = 0;
+    float *dst = nullptr;
+    if (EMIT) {
+        // block-exclusive prefix of the per-thread counts (cell order = thread order)
+        const uint32_t mine = thread_counts[(size_t)r * 128 + t];
+        uint32_t x = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if ((t & 31) >= o) x += y;
+        }
+        if ((t & 31) == 31) swarp[t >> 5] = x;
+        __syncthreads();
+        uint32_t wbase = 0;
+        for (int w = 0; w < (t >> 5); w++) wbase += swarp[w];
+        base = wbase + x - mine;
+        dst = out + 9ull * ((unsigned long long)offsets[ci] + base);
+        if (mine == 0) return;
+    }
+    unsigned m = 0;
+#pragma unroll 1
+    for (int q = 0; q < 4; q++) {
+        const int cx = 4 * (t & 1) + q;
+        float cu[8];
+        bool ok = true;
+#pragma unroll
+        for (int k = 0; k < 2; k++)
+#pragma unroll
+            for (int j = 0; j < 2; j++)
+#pragma unroll
+                for (int i = 0; i < 2; i++) {
+                    const int idx = (cx + i) + kT * (cy + j) + kT * kT * (cz + k);
+                    ok = ok && sok[idx];
+                    cu[i + 2 * j + 4 * k] = su[idx];
+                }
+        if (!ok) continue;
+        m = cell_triangles<EMIT>(cu, cx, cy, cz, gx, gy, gz, A.voxel, dst, m);
+    }
+    if (!EMIT) {
+        thread_counts[(size_t)r * 128 + t] = m;
+        uint32_t s = m;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if ((t & 31) == 0) swarp[t >> 5] = s;
+        __syncthreads();
+        if (t == 0) block_counts[ci] = swarp[0] + swarp[1] + swarp[2] + swarp[3];
+    }
+}
+
+}  // namespace
+
+}  // namespace hvg
+
+using namespace hvg;
+
+extern "C" vol_status vol_extract(vol_t v, int field, float voxel, float w_min, float *tris, int64_t max_tris,
+                                  int64_t *n_tris) {
+    if (!v || !n_tris) return fail(VOL_EINVAL, "vol_extract: NULL argument");
+    *n_tris = 0;
+    if (v->shard) return fail(VOL_ENOTSUP, "vol_extract: sharded volumes are not supported (extract per GPU volume)");
+    if (field != 0 && field != 1) return fail(VOL_EINVAL, "vol_extract: field must be 0 (u) or 1 (f)");
+    if (!(voxel > 0.0f) || !(voxel < 1e30f)) return fail(VOL_EINVAL, "vol_extract: voxel must be > 0");
+    if (!(w_min >= 0.0f) || !(w_min < 1e30f)) return fail(VOL_EINVAL, "vol_extract: w_min must be finite and >= 0");
+    if (tris && max_tris < 0) return fail(VOL_EINVAL, "vol_extract: max_tris < 0");
+    const int64_t n = v->L.n_local;
+    cudaStream_t s = v->stream;
+    uint32_t *counts = v->d_count;                                   // [n] (build scratch, T >= 2n)
+    uint32_t *offs = v->d_hash;                                      // [n + 1] (build scratch)
+    uint32_t *tcounts = reinterpret_cast<uint32_t *>(v->d_tmp);      // [n][128]
+    ExArgs A{field == 0 ? v->F.u : v->F.f, v->F.W, v->d_nbr, v->d_perm, v->d_xyz, voxel, w_min};
+    k_extract<false><<<(unsigned)n, 128, 0, s>>>(A, n, counts, tcounts, nullptr, nullptr);
+    CK(cudaPeekAtLastError());
+    counted(1);
+    CKL(launch_exclusive_scan_u32(counts, offs, n, v->d_scan, s));
+    uint32_t total = 0;
+    CK(cudaMemcpyAsync(&total, offs + n, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    *n_tris = (int64_t)total;
+    if (!tris) return VOL_OK;
+    if ((int64_t)total > max_tris)
+        return fail(VOL_ENOMEM, "vol_extract: %lld triangles > max_tris = %lld", (long long)total, (long long)max_tris);
+    if (total == 0) return VOL_OK;
+    const bool dev = is_device_ptr(tris);
+    float *out = tris;
+    if (!dev) CK(cudaMallocAsync((void **)&out, (size_t)total * 36, s));
+    k_extract<true><<<(unsigned)n, 128, 0, s>>>(A, n, nullptr, tcounts, offs, out);
+    cudaError_t e = cudaPeekAtLastError();
+    if (e == cudaSuccess) counted(1);
+    if (!dev) {
+        if (e == cudaSuccess) e = cudaMemcpyAsync(tris, out, (size_t)total * 36, cudaMemcpyDeviceToHost, s);
+        cudaFreeAsync(out, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    }
+    if (e != cudaSuccess) return fail(VOL_ECUDA, "vol_extract: %s", cudaGetErrorString(e));
+    return VOL_OK;
+}

@@ -218,6 +218,18 @@ class Volume:
         N.check(self._lib.vol_read_tables(self._h, None, bs.ctypes.data, be.ctypes.data, nbr.ctypes.data))
         return T.value, bs, be, nbr
 
+    # -- surface -----------------------------------------------------------
+    def extract(self, voxel: float, w_min: float = 0.0, field: str = "u", device=None) -> torch.Tensor:
+        """Ω-restricted zero level set of u (or f) as a triangle soup [m, 3, 3] float32 (vol_extract)."""
+        fid = {"u": 0, "f": 1}[field]
+        n = ctypes.c_int64()
+        N.check(self._lib.vol_extract(self._h, fid, float(voxel), float(w_min), None, 0, ctypes.byref(n)))
+        out = torch.empty(max(n.value, 1), 3, 3, dtype=torch.float32, device=self.device if device is None else device)
+        m = ctypes.c_int64()
+        N.check(self._lib.vol_extract(self._h, fid, float(voxel), float(w_min), ctypes.c_void_p(out.data_ptr()),
+                                      n.value, ctypes.byref(m)))
+        return out[:m.value]
+
     def close(self):
         if getattr(self, "_h", None):
             self._lib.vol_destroy(self._h)
