@@ -222,6 +222,43 @@ def fusion_leg(args, dev):
     return res
 
 
+def extraction_leg(args, dev, scene, iters, stream):
+    """vol_extract of the regularised street u (count pass + scan + ordered emit pass), inputs in HBM."""
+    import torch
+
+    from paper_1604_03734_b200 import Volume
+    vol = Volume(scene.coords, scene.f, scene.W, stream=stream)
+    vol.regularise(scene.lam, scene.eps, scene.tau, scene.sigma, iters, theta=scene.theta, data_term=scene.data_term,
+                   init=scene.init)
+    v = scene.meta["voxel"]
+    T = vol.extract(v)
+    cap = int(T.shape[0]) + 1024
+    out = torch.empty(cap, 3, 3, dtype=torch.float32, device=dev)
+    for _ in range(3):
+        vol.extract(v, out=out)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    a.record(stream)
+    for _ in range(args.steps):
+        T = vol.extract(v, out=out)
+    b.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = a.elapsed_time(b) / args.steps
+    ntri = int(T.shape[0])
+    nvox = scene.n_alloc
+    alg = 8 * nvox + 36 * ntri          # read u and W once, write the triangles (DESIGN.md §12)
+    peak, peak_src = load_peaks()
+    res = {"workload": scene.name + " (regularised u, " + str(iters) + " iterations)", "field": "u", "w_min": 0.0,
+           "triangles": ntri, "cells": nvox, "ms_per_call": ms, "cells_per_s": nvox / (ms / 1e3),
+           "triangles_per_s": ntri / (ms / 1e3),
+           "step": "vol_extract: count kernel + exclusive scan + ordered emit kernel, output in HBM",
+           "roofline": {"bound": "hbm", "kernel": "k_extract (count + emit)", "achieved": alg / (ms / 1e3) / 1e9,
+                        "peak": peak, "unit": "GB/s", "frac": alg / (ms / 1e3) / 1e9 / peak, "peak_source": peak_src,
+                        "alg_bytes_per_call": alg, "traffic": None}}
+    vol.close()
+    return res
+
+
 # ------------------------------------------------------------------------------ CPU oracle timing
 
 def time_oracle(scene, iters: int):
@@ -406,6 +443,9 @@ def main():
     fusion = None
     if not args.no_fusion and world == 1:
         fusion = fusion_leg(args, dev)
+    extraction = None
+    if not args.no_fusion and world == 1:
+        extraction = extraction_leg(args, dev, scene, iters, stream)
 
     if rank != 0:
         dist.destroy_process_group()
@@ -453,7 +493,7 @@ def main():
                    "energy": {"primal": E[0], "dual": E[1]}},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
         "freeze": bool(args.freeze), "no_freeze": nf,
-        "clocks": clk, "fusion": fusion,
+        "clocks": clk, "fusion": fusion, "extraction": extraction,
     }
     print(json.dumps(line), flush=True)
     if sharded:

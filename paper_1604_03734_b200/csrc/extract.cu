@@ -35,23 +35,24 @@ struct ExArgs {
     float voxel, w_min;
 };
 
-// X-4: vertex on the tet edge between tile corners i and j (tile coordinates; same block origin so the
-// lexicographic order of global coordinates is that of tile coordinates).
-__device__ __forceinline__ void edge_vertex(int gx, int gy, int gz, const int *ci, float ui, const int *cj, float uj,
-                                            float voxel, float *p) {
-    bool swap = false;
-    if (cj[0] != ci[0]) swap = cj[0] < ci[0];
-    else if (cj[1] != ci[1]) swap = cj[1] < ci[1];
-    else swap = cj[2] < ci[2];
-    const int *lo = swap ? cj : ci;
-    const int *hi = swap ? ci : cj;
-    const float ulo = swap ? uj : ui, uhi = swap ? ui : uj;
+// Cube corners are coded c = i + 2j + 4k for the offset (i, j, k) ∈ {0,1}^3 from the cell origin.
+
+// X-4: vertex on the edge between cell corners ca and cb (values ua, ub).  The ends are ordered by global
+// voxel coordinate, lexicographically in (x, y, z); inside one cell that is the order of the offsets.
+__device__ __forceinline__ void edge_vertex(int ox, int oy, int oz, int ca, float ua, int cb, float ub, float voxel,
+                                            float *p) {
+    const int ax = ca & 1, ay = (ca >> 1) & 1, az = ca >> 2;
+    const int bx = cb & 1, by = (cb >> 1) & 1, bz = cb >> 2;
+    const bool swap = ax != bx ? bx < ax : (ay != by ? by < ay : bz < az);
+    const int lx = swap ? bx : ax, ly = swap ? by : ay, lz = swap ? bz : az;
+    const int hx = swap ? ax : bx, hy = swap ? ay : by, hz = swap ? az : bz;
+    const float ulo = swap ? ub : ua, uhi = swap ? ua : ub;
     const float t = __fdiv_rn(ulo, __fsub_rn(ulo, uhi));
-    const int g0[3] = {gx, gy, gz};
+    const int lo[3] = {ox + lx, oy + ly, oz + lz}, hi[3] = {ox + hx, oy + hy, oz + hz};
 #pragma unroll
     for (int k = 0; k < 3; k++) {
-        const float plo = __fmul_rn(__fadd_rn((float)(g0[k] + lo[k]), 0.5f), voxel);
-        const float phi = __fmul_rn(__fadd_rn((float)(g0[k] + hi[k]), 0.5f), voxel);
+        const float plo = __fmul_rn(__fadd_rn((float)lo[k], 0.5f), voxel);
+        const float phi = __fmul_rn(__fadd_rn((float)hi[k], 0.5f), voxel);
         p[k] = __fadd_rn(plo, __fmul_rn(t, __fsub_rn(phi, plo)));
     }
 }
@@ -75,84 +76,79 @@ __device__ __forceinline__ void put(float *out, unsigned &m, const float *p0, co
     m++;
 }
 
-// All triangles of one cell (corner values cu[i + 2j + 4k], tile origin (cx, cy, cz), global voxel
-// origin of the block g0).  Returns the count; writes them from out[9·m0] when EMIT.
+__device__ __forceinline__ int sel4(int i, int a0, int a1, int a2, int a3) {
+    return i == 0 ? a0 : (i == 1 ? a1 : (i == 2 ? a2 : a3));
+}
+__device__ __forceinline__ float sel4f(int i, float a0, float a1, float a2, float a3) {
+    return i == 0 ? a0 : (i == 1 ? a1 : (i == 2 ? a2 : a3));
+}
+
+// One tetrahedron with corner codes (k0, k1, k2, k3) in positively oriented order (X-2) and values
+// (v0 … v3).  X-5: the lone corner (nin = 1: the inside one, nin = 3: the outside one) or the inside pair
+// goes first, the remaining corners follow in tetrahedron order, and the last two are swapped when that
+// permutation is odd, so (a, b, c, d) stays positively oriented.
 template <bool EMIT>
-__device__ unsigned cell_triangles(const float *cu, int cx, int cy, int cz, int gx, int gy, int gz, float voxel,
-                                   float *out, unsigned m) {
-    // X-2: permutations of the axes in lexicographic order and their parity
-    const int P0[6] = {0, 0, 1, 1, 2, 2}, P1[6] = {1, 2, 0, 2, 0, 1};
-    const bool EVEN[6] = {true, false, false, true, true, false};
-#pragma unroll 1
-    for (int q = 0; q < 6; q++) {
-        int off[4][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {1, 1, 1}};
-        off[1][P0[q]] = 1;
-        off[2][P0[q]] = 1;
-        off[2][P1[q]] = 1;
-        int ord[4] = {0, 1, 2, 3};
-        if (!EVEN[q]) {
-            ord[2] = 3;
-            ord[3] = 2;
-        }
-        int c[4][3];
-        float val[4];
-        bool in[4];
-        int nin = 0;
-#pragma unroll
-        for (int r = 0; r < 4; r++) {
-            const int *o = off[ord[r]];
-            c[r][0] = cx + o[0];
-            c[r][1] = cy + o[1];
-            c[r][2] = cz + o[2];
-            val[r] = cu[o[0] + 2 * o[1] + 4 * o[2]];
-            in[r] = val[r] < 0.0f;   // X-3
-            nin += in[r];
-        }
-        if (nin == 0 || nin == 4) continue;
-        int p[4], np = 0;
-        if (nin == 2) {
-#pragma unroll
-            for (int r = 0; r < 4; r++)
-                if (in[r]) p[np++] = r;
-#pragma unroll
-            for (int r = 0; r < 4; r++)
-                if (!in[r]) p[np++] = r;
-        } else {
-            const bool sel = nin == 1;   // the lone vertex has in == sel
-#pragma unroll
-            for (int r = 0; r < 4; r++)
-                if (in[r] == sel) p[np++] = r;
-#pragma unroll
-            for (int r = 0; r < 4; r++)
-                if (in[r] != sel) p[np++] = r;
-        }
-        int inv = 0;
-#pragma unroll
-        for (int x = 0; x < 4; x++)
-#pragma unroll
-            for (int y = x + 1; y < 4; y++) inv += p[x] > p[y];
-        if (inv & 1) {
-            const int t = p[2];
-            p[2] = p[3];
-            p[3] = t;
-        }
-        const int a = p[0], b = p[1], cc = p[2], d = p[3];
-        float e1[3], e2[3], e3[3], e4[3];
-        if (nin != 2) {
-            edge_vertex(gx, gy, gz, c[a], val[a], c[b], val[b], voxel, e1);
-            edge_vertex(gx, gy, gz, c[a], val[a], c[cc], val[cc], voxel, e2);
-            edge_vertex(gx, gy, gz, c[a], val[a], c[d], val[d], voxel, e3);
-            if (nin == 1) put<EMIT>(out, m, e1, e2, e3);
-            else put<EMIT>(out, m, e1, e3, e2);
-        } else {
-            edge_vertex(gx, gy, gz, c[a], val[a], c[cc], val[cc], voxel, e1);   // E_ac
-            edge_vertex(gx, gy, gz, c[a], val[a], c[d], val[d], voxel, e2);     // E_ad
-            edge_vertex(gx, gy, gz, c[b], val[b], c[d], val[d], voxel, e3);     // E_bd
-            edge_vertex(gx, gy, gz, c[b], val[b], c[cc], val[cc], voxel, e4);   // E_bc
-            put<EMIT>(out, m, e1, e2, e3);
-            put<EMIT>(out, m, e1, e3, e4);
-        }
+__device__ __forceinline__ void tet(int k0, int k1, int k2, int k3, float v0, float v1, float v2, float v3, int ox,
+                                    int oy, int oz, float voxel, float *out, unsigned &m) {
+    const int mask = (v0 < 0.0f) | ((v1 < 0.0f) << 1) | ((v2 < 0.0f) << 2) | ((v3 < 0.0f) << 3);   // X-3
+    if (mask == 0 || mask == 15) return;
+    const int nin = __popc(mask);
+    int pa, pb, pc, pd;
+    if (nin == 2) {
+        // inside positions i < j first, then outside k < l; parity = inversions between the two groups
+        const int i = __ffs(mask) - 1, j = 31 - __clz(mask);
+        const int om = (~mask) & 15;
+        const int k = __ffs(om) - 1, l = 31 - __clz(om);
+        const int inv = (k < i) + (l < i) + (k < j) + (l < j);
+        pa = i;
+        pb = j;
+        pc = (inv & 1) ? l : k;
+        pd = (inv & 1) ? k : l;
+    } else {
+        const int lone = nin == 1 ? mask : ((~mask) & 15);
+        const int a = __ffs(lone) - 1;
+        // remaining positions in order; moving a to the front costs a transpositions
+        const int r0 = a == 0 ? 1 : 0, r1 = a <= 1 ? 2 : 1, r2 = a <= 2 ? 3 : 2;
+        pa = a;
+        pb = r0;
+        pc = (a & 1) ? r2 : r1;
+        pd = (a & 1) ? r1 : r2;
     }
+    const int ca = sel4(pa, k0, k1, k2, k3), cb = sel4(pb, k0, k1, k2, k3);
+    const int cc = sel4(pc, k0, k1, k2, k3), cd = sel4(pd, k0, k1, k2, k3);
+    const float ua = sel4f(pa, v0, v1, v2, v3), ub = sel4f(pb, v0, v1, v2, v3);
+    const float uc = sel4f(pc, v0, v1, v2, v3), ud = sel4f(pd, v0, v1, v2, v3);
+    float e1[3], e2[3], e3[3];
+    if (nin != 2) {
+        edge_vertex(ox, oy, oz, ca, ua, cb, ub, voxel, e1);
+        edge_vertex(ox, oy, oz, ca, ua, cc, uc, voxel, e2);
+        edge_vertex(ox, oy, oz, ca, ua, cd, ud, voxel, e3);
+        if (nin == 1) put<EMIT>(out, m, e1, e2, e3);
+        else put<EMIT>(out, m, e1, e3, e2);
+    } else {
+        float e4[3];
+        edge_vertex(ox, oy, oz, ca, ua, cc, uc, voxel, e1);   // E_ac
+        edge_vertex(ox, oy, oz, ca, ua, cd, ud, voxel, e2);   // E_ad
+        edge_vertex(ox, oy, oz, cb, ub, cd, ud, voxel, e3);   // E_bd
+        edge_vertex(ox, oy, oz, cb, ub, cc, uc, voxel, e4);   // E_bc
+        put<EMIT>(out, m, e1, e2, e3);
+        put<EMIT>(out, m, e1, e3, e4);
+    }
+}
+
+// All triangles of one cell: corner values cu[code], global voxel coordinate of the cell origin
+// (ox, oy, oz).  X-2: the 6 Freudenthal tetrahedra 000 → e_a → e_a + e_b → 111 for the permutations
+// (a, b, c) in lexicographic order; odd permutations list their last two corners swapped.
+template <bool EMIT>
+__device__ __forceinline__ unsigned cell_triangles(const float (&cu)[8], int ox, int oy, int oz, float voxel,
+                                                   float *out, unsigned m) {
+    // (0,1,2): 0 1 3 7   (0,2,1): 0 1 7 5   (1,0,2): 0 2 7 3   (1,2,0): 0 2 6 7   (2,0,1): 0 4 5 7   (2,1,0): 0 4 7 6
+    tet<EMIT>(0, 1, 3, 7, cu[0], cu[1], cu[3], cu[7], ox, oy, oz, voxel, out, m);
+    tet<EMIT>(0, 1, 7, 5, cu[0], cu[1], cu[7], cu[5], ox, oy, oz, voxel, out, m);
+    tet<EMIT>(0, 2, 7, 3, cu[0], cu[2], cu[7], cu[3], ox, oy, oz, voxel, out, m);
+    tet<EMIT>(0, 2, 6, 7, cu[0], cu[2], cu[6], cu[7], ox, oy, oz, voxel, out, m);
+    tet<EMIT>(0, 4, 5, 7, cu[0], cu[4], cu[5], cu[7], ox, oy, oz, voxel, out, m);
+    tet<EMIT>(0, 4, 7, 6, cu[0], cu[4], cu[7], cu[6], ox, oy, oz, voxel, out, m);
     return m;
 }
 
@@ -240,7 +236,15 @@ __global__ void __launch_bounds__(128) k_extract(ExArgs A, int64_t n_rows, uint3
                     cu[i + 2 * j + 4 * k] = su[idx];
                 }
         if (!ok) continue;
-        m = cell_triangles<EMIT>(cu, cx, cy, cz, gx, gy, gz, A.voxel, dst, m);
+        // a cell whose corners are all inside or all outside has no triangle in any tetrahedron
+        bool any_in = false, any_out = false;
+#pragma unroll
+        for (int c8 = 0; c8 < 8; c8++) {
+            any_in |= cu[c8] < 0.0f;
+            any_out |= !(cu[c8] < 0.0f);
+        }
+        if (!(any_in && any_out)) continue;
+        m = cell_triangles<EMIT>(cu, gx + cx, gy + cy, gz + cz, A.voxel, dst, m);
     }
     if (!EMIT) {
         thread_counts[(size_t)r * 128 + t] = m;

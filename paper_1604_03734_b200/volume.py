@@ -219,9 +219,18 @@ class Volume:
         return T.value, bs, be, nbr
 
     # -- surface -----------------------------------------------------------
-    def extract(self, voxel: float, w_min: float = 0.0, field: str = "u", device=None) -> torch.Tensor:
-        """Ω-restricted zero level set of u (or f) as a triangle soup [m, 3, 3] float32 (vol_extract)."""
+    def extract(self, voxel: float, w_min: float = 0.0, field: str = "u", device=None, out=None) -> torch.Tensor:
+        """Ω-restricted zero level set of u (or f) as a triangle soup [m, 3, 3] float32 (vol_extract).
+        With `out` (a float32 [cap, 3, 3] tensor) the triangles go into it in one call if they fit."""
         fid = {"u": 0, "f": 1}[field]
+        if out is not None:
+            m = ctypes.c_int64()
+            st = self._lib.vol_extract(self._h, fid, float(voxel), float(w_min), ctypes.c_void_p(out.data_ptr()),
+                                       int(out.shape[0]), ctypes.byref(m))
+            if st == N.VOL_OK:
+                return out[:m.value]
+            if st != N.VOL_ENOMEM:
+                N.check(st)
         n = ctypes.c_int64()
         N.check(self._lib.vol_extract(self._h, fid, float(voxel), float(w_min), None, 0, ctypes.byref(n)))
         out = torch.empty(max(n.value, 1), 3, 3, dtype=torch.float32, device=self.device if device is None else device)
