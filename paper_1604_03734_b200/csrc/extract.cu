@@ -136,35 +136,45 @@ __device__ __forceinline__ void tet(int k0, int k1, int k2, int k3, float v0, fl
     }
 }
 
-// All triangles of one cell: corner values cu[code], global voxel coordinate of the cell origin
-// (ox, oy, oz).  X-2: the 6 Freudenthal tetrahedra 000 → e_a → e_a + e_b → 111 for the permutations
-// (a, b, c) in lexicographic order; odd permutations list their last two corners swapped.
-template <bool EMIT>
-__device__ __forceinline__ unsigned cell_triangles(const float (&cu)[8], int ox, int oy, int oz, float voxel,
-                                                   float *out, unsigned m) {
-    // (0,1,2): 0 1 3 7   (0,2,1): 0 1 7 5   (1,0,2): 0 2 7 3   (1,2,0): 0 2 6 7   (2,0,1): 0 4 5 7   (2,1,0): 0 4 7 6
-    tet<EMIT>(0, 1, 3, 7, cu[0], cu[1], cu[3], cu[7], ox, oy, oz, voxel, out, m);
-    tet<EMIT>(0, 1, 7, 5, cu[0], cu[1], cu[7], cu[5], ox, oy, oz, voxel, out, m);
-    tet<EMIT>(0, 2, 7, 3, cu[0], cu[2], cu[7], cu[3], ox, oy, oz, voxel, out, m);
-    tet<EMIT>(0, 2, 6, 7, cu[0], cu[2], cu[6], cu[7], ox, oy, oz, voxel, out, m);
-    tet<EMIT>(0, 4, 5, 7, cu[0], cu[4], cu[5], cu[7], ox, oy, oz, voxel, out, m);
-    tet<EMIT>(0, 4, 7, 6, cu[0], cu[4], cu[7], cu[6], ox, oy, oz, voxel, out, m);
-    return m;
+// X-2: the 6 Freudenthal tetrahedra 000 → e_a → e_a + e_b → 111 for the axis permutations (a, b, c) in
+// lexicographic order; odd permutations list their last two corners swapped (positive orientation):
+//   (0,1,2): 0 1 3 7   (0,2,1): 0 1 7 5   (1,0,2): 0 2 7 3   (1,2,0): 0 2 6 7   (2,0,1): 0 4 5 7   (2,1,0): 0 4 7 6
+// corner codes k1 k2 k3 of tetrahedron q, 4 bits each (k1 lowest), 12 bits per tetrahedron
+constexpr unsigned long long kTetLo = 0x731ull | (0x571ull << 12) | (0x372ull << 24);
+constexpr unsigned long long kTetHi = 0x762ull | (0x754ull << 12) | (0x674ull << 24);
+__device__ __forceinline__ int tet_code(int q, int r) {   // r = 1, 2, 3
+    const unsigned long long w = q < 3 ? kTetLo : kTetHi;
+    return (int)((w >> (12 * (q < 3 ? q : q - 3) + 4 * (r - 1))) & 0xF);
 }
 
+__device__ __forceinline__ int tile_index(int cx, int cy, int cz, int code) {
+    return (cx + (code & 1)) + kT * (cy + ((code >> 1) & 1)) + kT * kT * (cz + (code >> 2));
+}
+
+constexpr int kMaxItems = 512 * 6;   // (cell, tetrahedron) pairs of one block
+constexpr int kItemWords = 2 * kMaxItems / 32;   // 2 count bits per item
+
+// Two phases per CTA: (A) every thread tests its 4 cells (all corners usable, mixed signs) and their
+// 6 tetrahedra (mixed signs) and appends the crossing (cell, tetrahedron) items to a shared list in
+// cell, tetrahedron order; (B) the 128 threads process the items round-robin — the same code path for
+// every lane, instead of each lane walking its own cells' varying tetrahedra.  The count pass stores
+// the triangles of every item (0, 1 or 2 after the X-6 drop) for the emit pass as 2 bits per item:
+// item_bits[row][2·(4·round + warp) + b] = bit b of the counts of the warp's 32 items (ballots).
 template <bool EMIT>
 __global__ void __launch_bounds__(128) k_extract(ExArgs A, int64_t n_rows, uint32_t *__restrict__ block_counts,
-                                                 uint32_t *__restrict__ thread_counts,
+                                                 uint32_t *__restrict__ item_bits,
                                                  const uint32_t *__restrict__ offsets, float *__restrict__ out) {
     __shared__ float su[kTile];
     __shared__ uint8_t sok[kTile];
+    __shared__ uint16_t sitem[kMaxItems];   // cell (9 bits) << 3 | tetrahedron (3 bits)
     __shared__ int32_t srow[8];
     __shared__ uint32_t swarp[4];
     const int64_t r = blockIdx.x;
     if (r >= n_rows) return;
-    const int t = threadIdx.x;
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
     if (t == 0) {
-        // blocks of the tile: index dx + 2dy + 4dz; chains +x → +y → +z (reading X-1 note above)
+        // blocks of the tile: index dx + 2dy + 4dz; chains +x → +y → +z (a missing intermediate block
+        // holds a corner of every cell that needs the chained block, so such cells are skipped anyway)
         const int32_t *N = A.nbr;
         const int32_t bx = N[12 * r + 1], by = N[12 * r + 3], bz = N[12 * r + 5];
         const int32_t bxy = bx >= 0 ? N[12 * bx + 3] : -1;
@@ -198,60 +208,105 @@ __global__ void __launch_bounds__(128) k_extract(ExArgs A, int64_t n_rows, uint3
     __syncthreads();
     const int32_t ci = A.perm[r];
     const int gx = 8 * A.xyz[3 * ci], gy = 8 * A.xyz[3 * ci + 1], gz = 8 * A.xyz[3 * ci + 2];
-    // cells 4t … 4t+3 in voxel order: x = 4(t&1) + q, y = (t>>1)&7, z = t>>4
+    // (A) cells 4t … 4t+3 (voxel order): x = 4(t&1) + q, y = (t>>1)&7, z = t>>4
     const int cy = (t >> 1) & 7, cz = t >> 4;
-    unsigned base = 0;
-    float *dst = nullptr;
-    if (EMIT) {
-        // block-exclusive prefix of the per-thread counts (cell order = thread order)
-        const uint32_t mine = thread_counts[(size_t)r * 128 + t];
-        uint32_t x = mine;
+    uint32_t tets = 0;   // bit 6q + k: tetrahedron k of cell q crosses the level set
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if ((t & 31) >= o) x += y;
-        }
-        if ((t & 31) == 31) swarp[t >> 5] = x;
-        __syncthreads();
-        uint32_t wbase = 0;
-        for (int w = 0; w < (t >> 5); w++) wbase += swarp[w];
-        base = wbase + x - mine;
-        dst = out + 9ull * ((unsigned long long)offsets[ci] + base);
-        if (mine == 0) return;
-    }
-    unsigned m = 0;
-#pragma unroll 1
     for (int q = 0; q < 4; q++) {
         const int cx = 4 * (t & 1) + q;
-        float cu[8];
         bool ok = true;
-#pragma unroll
-        for (int k = 0; k < 2; k++)
-#pragma unroll
-            for (int j = 0; j < 2; j++)
-#pragma unroll
-                for (int i = 0; i < 2; i++) {
-                    const int idx = (cx + i) + kT * (cy + j) + kT * kT * (cz + k);
-                    ok = ok && sok[idx];
-                    cu[i + 2 * j + 4 * k] = su[idx];
-                }
-        if (!ok) continue;
-        // a cell whose corners are all inside or all outside has no triangle in any tetrahedron
-        bool any_in = false, any_out = false;
+        int neg = 0;
 #pragma unroll
         for (int c8 = 0; c8 < 8; c8++) {
-            any_in |= cu[c8] < 0.0f;
-            any_out |= !(cu[c8] < 0.0f);
+            const int idx = tile_index(cx, cy, cz, c8);
+            ok = ok && sok[idx];
+            neg |= (su[idx] < 0.0f) << c8;   // X-3
         }
-        if (!(any_in && any_out)) continue;
-        m = cell_triangles<EMIT>(cu, gx + cx, gy + cy, gz + cz, A.voxel, dst, m);
+        if (!ok || neg == 0 || neg == 255) continue;
+        uint32_t tm = 0;
+#pragma unroll
+        for (int k = 0; k < 6; k++) {
+            const int m4 = (neg & 1) | (((neg >> tet_code(k, 1)) & 1) << 1) | (((neg >> tet_code(k, 2)) & 1) << 2) |
+                           (((neg >> tet_code(k, 3)) & 1) << 3);
+            tm |= (uint32_t)(m4 != 0 && m4 != 15) << k;
+        }
+        tets |= tm << (6 * q);
+    }
+    const uint32_t mine = __popc(tets);
+    uint32_t x = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) swarp[wid] = x;
+    __syncthreads();
+    uint32_t pos = x - mine;
+    for (int w = 0; w < wid; w++) pos += swarp[w];
+    const uint32_t n_items = swarp[0] + swarp[1] + swarp[2] + swarp[3];
+    while (tets) {
+        const int bit = __ffs(tets) - 1;
+        tets &= tets - 1;
+        const int q = bit / 6, k = bit - 6 * q;
+        sitem[pos++] = (uint16_t)(((4 * t + q) << 3) | k);
+    }
+    __syncthreads();
+    // (B) items round-robin: item i = t + 128·round, in list order
+    uint32_t run = 0;            // EMIT: triangles written by the earlier rounds
+    uint32_t block_total = 0;    // count pass: triangles of this thread's items
+    float *base_out = EMIT ? out + 9ull * offsets[ci] : nullptr;
+    for (uint32_t i0 = 0; i0 < n_items; i0 += 128) {
+        const uint32_t i = i0 + t;
+        int cell = 0, k = 0;
+        if (i < n_items) {
+            cell = sitem[i] >> 3;
+            k = sitem[i] & 7;
+        }
+        const int cx = cell & 7, cyy = (cell >> 3) & 7, czz = cell >> 6;
+        const int k1 = tet_code(k, 1), k2 = tet_code(k, 2), k3 = tet_code(k, 3);
+        if (EMIT) {
+            const uint32_t *wb = item_bits + (size_t)r * kItemWords + 2 * ((i0 >> 5) + wid);
+            const uint32_t cnt = i < n_items ? (((wb[0] >> lane) & 1u) | (((wb[1] >> lane) & 1u) << 1)) : 0u;
+            // block-exclusive scan of this round's counts (list order = thread order)
+            uint32_t y = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t z = __shfl_up_sync(0xffffffffu, y, o);
+                if (lane >= o) y += z;
+            }
+            __syncthreads();
+            if (lane == 31) swarp[wid] = y;
+            __syncthreads();
+            uint32_t before = y - cnt;
+            for (int w = 0; w < wid; w++) before += swarp[w];
+            const uint32_t round_total = swarp[0] + swarp[1] + swarp[2] + swarp[3];
+            if (cnt) {
+                unsigned m = 0;
+                tet<true>(0, k1, k2, k3, su[tile_index(cx, cyy, czz, 0)], su[tile_index(cx, cyy, czz, k1)],
+                          su[tile_index(cx, cyy, czz, k2)], su[tile_index(cx, cyy, czz, k3)], gx + cx, gy + cyy,
+                          gz + czz, A.voxel, base_out + 9ull * (run + before), m);
+            }
+            run += round_total;
+        } else {
+            unsigned m = 0;
+            if (i < n_items)
+                tet<false>(0, k1, k2, k3, su[tile_index(cx, cyy, czz, 0)], su[tile_index(cx, cyy, czz, k1)],
+                           su[tile_index(cx, cyy, czz, k2)], su[tile_index(cx, cyy, czz, k3)], gx + cx, gy + cyy,
+                           gz + czz, A.voxel, nullptr, m);
+            const uint32_t b0 = __ballot_sync(0xffffffffu, m & 1u), b1 = __ballot_sync(0xffffffffu, (m >> 1) & 1u);
+            if (lane == 0 && i0 + 32 * wid < n_items) {
+                uint32_t *wb = item_bits + (size_t)r * kItemWords + 2 * ((i0 >> 5) + wid);
+                wb[0] = b0;
+                wb[1] = b1;
+            }
+            block_total += m;
+        }
     }
     if (!EMIT) {
-        thread_counts[(size_t)r * 128 + t] = m;
-        uint32_t s = m;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if ((t & 31) == 0) swarp[t >> 5] = s;
+        for (int o = 16; o > 0; o >>= 1) block_total += __shfl_xor_sync(0xffffffffu, block_total, o);
+        __syncthreads();
+        if (lane == 0) swarp[wid] = block_total;
         __syncthreads();
         if (t == 0) block_counts[ci] = swarp[0] + swarp[1] + swarp[2] + swarp[3];
     }
@@ -276,7 +331,8 @@ extern "C" vol_status vol_extract(vol_t v, int field, float voxel, float w_min, 
     cudaStream_t s = v->stream;
     uint32_t *counts = v->d_count;                                   // [n] (build scratch, T >= 2n)
     uint32_t *offs = v->d_hash;                                      // [n + 1] (build scratch)
-    uint32_t *tcounts = reinterpret_cast<uint32_t *>(v->d_tmp);      // [n][128]
+    // [n][192] words: 2 bits per (cell, tetrahedron) item (768 B per block <= the 2 KiB per block of d_tmp)
+    uint32_t *tcounts = reinterpret_cast<uint32_t *>(v->d_tmp);
     ExArgs A{field == 0 ? v->F.u : v->F.f, v->F.W, v->d_nbr, v->d_perm, v->d_xyz, voxel, w_min};
     k_extract<false><<<(unsigned)n, 128, 0, s>>>(A, n, counts, tcounts, nullptr, nullptr);
     CK(cudaPeekAtLastError());
