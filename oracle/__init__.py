@@ -20,6 +20,9 @@ Parity status per function:
   fusion (Eq. 1) ........ pinned (SPEC worked examples, fronto-parallel plane closed form under random
                           rigid poses, running-average closed form, block walk vs exact segment-box
                           intersection, dense numpy brute force O2-fusion) — ``fusion_oracle.c``
+  stereo (§IV) .......... pinned (census worked example, strict-order invariance, shifted-pair WTA, tensor
+                          closed forms and eigen-structure, K/Kᵀ adjointness, dual feasibility,
+                          constant and slanted-plane disparities, λ → ∞ gives WTA) — ``stereo_oracle.c``
   extraction ............ pinned (planar fields: vertices on the plane, exact area, orientation; analytic
                           sphere: closed 2-manifold, Euler characteristic 2, area/volume; Ω
                           restriction) — ``extract_oracle.c``
@@ -35,7 +38,8 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
 _SRC = [os.path.join(_HERE, "hvg_oracle.c"), os.path.join(_HERE, "fusion_oracle.c"),
-        os.path.join(_HERE, "extract_oracle.c"), os.path.join(_HERE, "hvg_oracle_real.inc")]
+        os.path.join(_HERE, "extract_oracle.c"), os.path.join(_HERE, "stereo_oracle.c"),
+        os.path.join(_HERE, "hvg_oracle_real.inc")]
 
 
 def build(force: bool = False) -> str:
@@ -44,7 +48,7 @@ def build(force: bool = False) -> str:
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < newest:
         tmp = _SO + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-std=c99", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
-                               "-Wall", "-o", tmp, _SRC[0], _SRC[1], _SRC[2], "-lm"])
+                               "-Wall", "-o", tmp, _SRC[0], _SRC[1], _SRC[2], _SRC[3], "-lm"])
         os.replace(tmp, _SO)
     return _SO
 
@@ -93,6 +97,22 @@ def lib():
         L.orc_fuse_alloc.argtypes = [P, i32, i32, i32, P, P, flt, flt, flt, i64, P, P]
         L.orc_extract.restype = i64
         L.orc_extract.argtypes = [P, i64, P, P, flt, flt, P, i64]
+        L.orc_census.restype = None
+        L.orc_census.argtypes = [P, cint, cint, cint, P]
+        L.orc_cost.restype = None
+        L.orc_cost.argtypes = [P, P, cint, cint, cint, cint, P]
+        L.orc_tensor.restype = None
+        L.orc_tensor.argtypes = [P, cint, cint, flt, flt, P]
+        L.orc_tgv_K.restype = None
+        L.orc_tgv_K.argtypes = [P, P, P, cint, cint, P, P]
+        L.orc_tgv_KT.restype = None
+        L.orc_tgv_KT.argtypes = [P, P, P, cint, cint, P, P, P]
+        L.orc_data_step.restype = flt
+        L.orc_data_step.argtypes = [flt, P, cint, flt, flt]
+        L.orc_stereo_theta.restype = flt
+        L.orc_stereo_theta.argtypes = [P, cint]
+        L.orc_stereo.restype = cint
+        L.orc_stereo.argtypes = [P, P, cint, cint, P, P, P, P]
         L.orc_fuse_update_blocks.restype = None
         L.orc_fuse_update_blocks.argtypes = [P, i32, i32, i32, P, P, flt, flt, flt, flt, P, P, i64, P, P]
         _lib = L
@@ -336,3 +356,91 @@ def extract(coords, u, W, voxel, w_min=0.0) -> np.ndarray:
     m2 = lib().orc_extract(_ptr(c), n, _ptr(uu), _ptr(ww), r(voxel), r(w_min), _ptr(out), m)
     assert m2 == m
     return out[:m]
+
+
+# ---------------------------------------------------------------------------------------------------
+# Depth-map estimation (paper §IV: census data term + tensor TGV; stereo_oracle.c, DESIGN.md §13)
+# ---------------------------------------------------------------------------------------------------
+
+class orc_stereo_params(ctypes.Structure):
+    _fields_ = [("win", ctypes.c_int), ("D", ctypes.c_int), ("outer", ctypes.c_int), ("inner", ctypes.c_int),
+                ("lam", ctypes.c_float), ("alpha1", ctypes.c_float), ("alpha2", ctypes.c_float),
+                ("beta", ctypes.c_float), ("gamma", ctypes.c_float), ("theta0", ctypes.c_float),
+                ("theta_end", ctypes.c_float), ("tau", ctypes.c_float), ("sigma", ctypes.c_float)]
+
+
+def stereo_params(D=64, win=5, outer=10, inner=10, lam=0.5, alpha1=1.0, alpha2=5.0, beta=1.0, gamma=4.0,
+                  theta0=1.0, theta_end=0.01, tau=None, sigma=None):
+    t = float(np.float32(1.0 / np.sqrt(12.0)))
+    return orc_stereo_params(win, D, outer, inner, lam, alpha1, alpha2, beta, gamma, theta0, theta_end,
+                             t if tau is None else tau, t if sigma is None else sigma)
+
+
+def census(I, win=5) -> np.ndarray:
+    A = _np(I, np.float32)
+    H, W = A.shape
+    out = np.zeros((H, W), np.uint32)
+    lib().orc_census(_ptr(A), H, W, win, _ptr(out))
+    return out
+
+
+def cost_volume(sigL, sigR, D, win=5) -> np.ndarray:
+    """[H, W, D] uint8 Hamming distances (win² − 1 where x + d leaves the image)."""
+    L_ = _np(sigL, np.uint32)
+    R_ = _np(sigR, np.uint32)
+    H, W = L_.shape
+    out = np.zeros((H, W, D), np.uint8)
+    lib().orc_cost(_ptr(L_), _ptr(R_), H, W, D, win, _ptr(out))
+    return out
+
+
+def tensor(I, beta=1.0, gamma=4.0) -> np.ndarray:
+    A = _np(I, np.float32)
+    H, W = A.shape
+    out = np.zeros((H, W, 3), np.float32)
+    lib().orc_tensor(_ptr(A), H, W, float(np.float32(beta)), float(np.float32(gamma)), _ptr(out))
+    return out
+
+
+def tgv_K(T, d, w):
+    T_ = _np(T, np.float32)
+    d_ = _np(d, np.float32)
+    w_ = _np(w, np.float32)
+    H, W = d_.shape
+    u = np.zeros((2, H, W), np.float32)
+    v = np.zeros((4, H, W), np.float32)
+    lib().orc_tgv_K(_ptr(T_), _ptr(d_), _ptr(w_), H, W, _ptr(u), _ptr(v))
+    return u, v
+
+
+def tgv_KT(T, p, q):
+    T_ = _np(T, np.float32)
+    p_ = _np(p, np.float32)
+    q_ = _np(q, np.float32)
+    H, W = p_.shape[1:]
+    kd = np.zeros((H, W), np.float32)
+    kw = np.zeros((2, H, W), np.float32)
+    tp = np.zeros((2, H, W), np.float32)
+    lib().orc_tgv_KT(_ptr(T_), _ptr(p_), _ptr(q_), H, W, _ptr(kd), _ptr(kw), _ptr(tp))
+    return kd, kw
+
+
+def data_step(d, rho, c, lam) -> float:
+    r = _np(rho, np.float32)
+    return float(lib().orc_data_step(float(np.float32(d)), _ptr(r), r.shape[0], float(np.float32(c)),
+                                     float(np.float32(lam))))
+
+
+def stereo(IL, IR, params=None, **kw):
+    """Solve one rectified pair; returns (d [H, W], w [2, H, W], a [H, W]) float32."""
+    P = params if params is not None else stereo_params(**kw)
+    L_ = _np(IL, np.float32)
+    R_ = _np(IR, np.float32)
+    H, W = L_.shape
+    d = np.zeros((H, W), np.float32)
+    w = np.zeros((2, H, W), np.float32)
+    a = np.zeros((H, W), np.float32)
+    rc = lib().orc_stereo(_ptr(L_), _ptr(R_), H, W, ctypes.byref(P), _ptr(d), _ptr(w), _ptr(a))
+    if rc != 0:
+        raise ValueError("stereo oracle: bad parameters")
+    return d, w, a
