@@ -193,6 +193,53 @@ vol_status vol_plan_shard(const int32_t *block_xyz, int64_t n_global, const int3
  * volume), VOL_ECUDA.                                                                               */
 vol_status vol_extract(vol_t v, int field, float voxel, float w_min, float *tris, int64_t max_tris, int64_t *n_tris);
 
+/* Depth-map estimation from rectified stereo (paper §IV) ----------
+ * Readings S-1 … S-12.  Batched: images are [F][H][W] float32 intensities in [0, 1].
+ *   census   window 3 or 5, bit k (row-major, centre skipped) = neighbour < centre,
+ *            clamp-to-edge borders;
+ *   cost     ρ(x, y, d) = Hamming(sig_R(x, y), sig_L(x + d, y)) (bits), d = 0 … n_disp−1, the right
+ *            image is the reference; x + d outside the image → win² − 1;
+ *   tensor   T = exp(−γ|∇I_R|^β) n nᵀ + n⊥ n⊥ᵀ, central differences, identity where |∇I| < 1e-6,
+ *            evaluated in fp64 and rounded to fp32;
+ *   solver   E = α₁Σ|T∇d − w|₂ + α₂Σ|∇w|_F + 1/(2θ)Σ(d − a)² + λΣρ(a) (P:526 + quadratic relaxation):
+ *            init a = d = winner-take-all; `outer` rounds of `inner` Chambolle–Pock iterations on (d, w)
+ *            (steps τ, σ with 12τσ <= 1), then a ← argmin over integer d of the coupling + data term
+ *            with a parabola sub-pixel step; θ from theta0 to theta_end geometrically.              */
+typedef struct {
+    int32_t width, height;   /* W, H of every image                                                */
+    int32_t n_disp;          /* D: candidate disparities 0 … D−1 (pixels)                          */
+    int32_t window;          /* census window: 3 or 5                                              */
+    int32_t outer, inner;    /* data-step rounds; Chambolle–Pock iterations per round               */
+    float lambda;            /* λ_2D (Table I: 0.5)                                                */
+    float alpha1, alpha2;    /* α₁, α₂ (Table I: 1.0, 5.0)                                         */
+    float beta, gamma;       /* β, γ (Table I: 1.0, 4.0)                                           */
+    float theta0, theta_end; /* coupling schedule (default 1.0 → 0.01)                             */
+    float tau, sigma;        /* primal / dual steps (default 1/√12 each)                           */
+} vol_stereo_params;
+
+void vol_stereo_default_params(vol_stereo_params *params);
+
+/* Device bytes vol_stereo needs for n_frames pairs (inputs on the host included). */
+size_t vol_stereo_workspace_bytes(int32_t n_frames, const vol_stereo_params *params);
+
+/* Solve n_frames rectified pairs.  left, right [F][H][W] (both host or both device); outputs (all host
+ * or all device): disparity d [F][H][W], w [F][2][H][W] per frame-major plane order [2][F][H][W]
+ * (may be NULL), a [F][H][W] (last data step, may be NULL).  workspace >= vol_stereo_workspace_bytes
+ * or NULL (library allocates).  Synchronous for host pointers, else asynchronous on `stream`.
+ * Errors: VOL_EINVAL (parameters: sizes, window, 12τσ > 1 …), VOL_ENOMEM, VOL_ECUDA.              */
+vol_status vol_stereo(const float *left, const float *right, int32_t n_frames, const vol_stereo_params *params,
+                      void *workspace, size_t workspace_bytes, void *stream, float *disparity, float *w, float *a);
+
+/* Census signatures [F][H][W] uint32 of img [F][H][W] (device pointers; for checks).               */
+vol_status vol_stereo_census(const float *img, int32_t n_frames, int32_t height, int32_t width, int32_t window,
+                             void *stream, uint32_t *sig);
+/* Tensor fields T [3][F][H][W] = (T11, T12, T22) of img (device pointers; for checks).              */
+vol_status vol_stereo_tensor(const float *img, int32_t n_frames, int32_t height, int32_t width, float beta,
+                             float gamma, void *stream, float *T);
+/* depth = fx_baseline / d for d > d_min, else 0 (invalid); device pointers.                 */
+vol_status vol_disparity_to_depth(const float *disparity, int64_t n, float fx_baseline, float d_min, void *stream,
+                                  float *depth);
+
 /* TSDF fusion of posed depth maps (paper §III-A, Eq. 1) ----------
  * Readings F-1 … F-10.  For every depth map k = 0 … K−1 in sequence the paper
  * allocates the blocks where frame k observes a surface and then updates every voxel of

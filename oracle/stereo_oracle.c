@@ -16,8 +16,9 @@
  *             row-major window order without the centre, bit k = (k-th neighbour < centre), borders
  *             clamp to the edge;
  *   data term P:510-513: ρ(d, x, y) = Sim(I_L(x + d, y), I_R(x, y)) — the right image is the reference;
- *             Sim = Hamming distance of the signatures; x + d outside the image → maximal cost
- *             w² − 1; ρ is normalised to [0, 1] by w² − 1 (S-3);
+ *             Sim = Hamming distance of the signatures, used as is (reading S-3: not normalised,
+ *             so λ_2D = 0.5 of Table I weighs bit counts); x + d outside the image → maximal cost
+ *             w² − 1;
  *   tensor    P:540-546: T = exp(−γ|∇I|^β) n nᵀ + n⊥ n⊥ᵀ, n = ∇I/|∇I|, ∇I by central differences of I_R
  *             (clamp to edge), T = identity if |∇I| < 1e-6;
  *   TGV       P:524-529, Eq. reg_2D: α₁ Σ|T∇d − w|₂ + α₂ Σ|∇w|_F (S-6), forward differences with
@@ -211,7 +212,7 @@ int orc_stereo(const float *IL, const float *IR, int H, int W, const orc_stereo_
 {
     if (H < 1 || W < 1 || P->D < 1 || (P->win != 3 && P->win != 5)) return -1;   /* 24-bit signatures at most */
     size_t n = (size_t)H * W;
-    int D = P->D, maxc = P->win * P->win - 1;
+    int D = P->D;
     uint32_t *sL = malloc(n * 4), *sR = malloc(n * 4);
     uint8_t *cost = malloc(n * (size_t)D);
     float *T = malloc(n * 12), *rho = malloc(n * (size_t)D * 4);
@@ -224,7 +225,7 @@ int orc_stereo(const float *IL, const float *IR, int H, int W, const orc_stereo_
     orc_census(IR, H, W, P->win, sR);
     orc_cost(sL, sR, H, W, D, P->win, cost);
     orc_tensor(IR, H, W, P->beta, P->gamma, T);
-    for (size_t i = 0; i < n * (size_t)D; i++) rho[i] = (float)cost[i] / (float)maxc;   /* S-3 */
+    for (size_t i = 0; i < n * (size_t)D; i++) rho[i] = (float)cost[i];   /* S-3: the Hamming distance */
     /* init (S-8): winner-take-all a = d = argmin ρ (ties: smallest), w = p = q = 0 */
     for (size_t i = 0; i < n; i++) {
         int best = 0;

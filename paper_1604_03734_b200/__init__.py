@@ -3,6 +3,7 @@
 The product path is libvol.so (C ABI in include/vol.h, CUDA kernels for sm_100a in csrc/);
 this package is its thin Python binding.  It never imports the CPU oracle and has no CPU fallback.
 """
+from . import stereo  # noqa: F401
 from .volume import Volume, block_hash, connect_group, fuse, group_energy, nccl_unique_id, plan_shard, regularise_group  # noqa: F401
 
 __all__ = ["Volume", "fuse", "block_hash", "plan_shard", "nccl_unique_id", "connect_group", "regularise_group", "group_energy"]

@@ -39,6 +39,14 @@ class vol_fusion_stats(ctypes.Structure):
                 ("voxel_updates", ctypes.c_int64), ("ms_alloc", ctypes.c_float), ("ms_integrate", ctypes.c_float)]
 
 
+class vol_stereo_params(ctypes.Structure):
+    _fields_ = [("width", ctypes.c_int32), ("height", ctypes.c_int32), ("n_disp", ctypes.c_int32),
+                ("window", ctypes.c_int32), ("outer", ctypes.c_int32), ("inner", ctypes.c_int32),
+                ("lam", ctypes.c_float), ("alpha1", ctypes.c_float), ("alpha2", ctypes.c_float),
+                ("beta", ctypes.c_float), ("gamma", ctypes.c_float), ("theta0", ctypes.c_float),
+                ("theta_end", ctypes.c_float), ("tau", ctypes.c_float), ("sigma", ctypes.c_float)]
+
+
 class vol_dist(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int), ("world", ctypes.c_int), ("part", ctypes.c_void_p),
                 ("nccl_id", ctypes.c_void_p)]
@@ -49,7 +57,8 @@ EXPORTS = [
     "vol_read_state", "vol_load_state", "vol_read_tables", "vol_info", "vol_last_launches", "vol_sync",
     "vol_destroy", "vol_last_error", "vol_nccl_unique_id", "vol_group_connect", "vol_regularise_group",
     "vol_group_energy", "vol_block_hash", "vol_plan_shard", "vol_total_launches", "vol_fuse_workspace_bytes",
-    "vol_fuse", "vol_extract",
+    "vol_fuse", "vol_extract", "vol_stereo_default_params", "vol_stereo_workspace_bytes", "vol_stereo",
+    "vol_stereo_census", "vol_stereo_tensor", "vol_disparity_to_depth",
 ]
 
 _lib = None
@@ -88,6 +97,12 @@ def lib() -> ctypes.CDLL:
         "vol_plan_shard": (st, [P, i64, P, c_int, c_int, P, P, P, P, P, P, P]),
         "vol_total_launches": (i64, []),
         "vol_extract": (st, [P, c_int, f32, f32, P, i64, P]),
+        "vol_stereo_default_params": (None, [ctypes.POINTER(vol_stereo_params)]),
+        "vol_stereo_workspace_bytes": (ctypes.c_size_t, [i32, ctypes.POINTER(vol_stereo_params)]),
+        "vol_stereo": (st, [P, P, i32, ctypes.POINTER(vol_stereo_params), P, ctypes.c_size_t, P, P, P, P]),
+        "vol_stereo_census": (st, [P, i32, i32, i32, i32, P, P]),
+        "vol_stereo_tensor": (st, [P, i32, i32, i32, f32, f32, P, P]),
+        "vol_disparity_to_depth": (st, [P, i64, f32, f32, P, P]),
         "vol_fuse_workspace_bytes": (ctypes.c_size_t, [i64, i32, ctypes.POINTER(vol_camera)]),
         "vol_fuse": (st, [P, i32, ctypes.POINTER(vol_camera), P, ctypes.POINTER(vol_fusion_params), i64, P,
                           ctypes.c_size_t, P, P, P, P, P, P, ctypes.POINTER(vol_fusion_stats)]),

@@ -55,10 +55,14 @@ def value_noise2(x, y, seed=0, cells=(2.0, 5.0, 13.0, 31.0)):
     return out / wsum
 
 
-def value_noise3(P, seed=0, cells=(0.02, 0.05, 0.15, 0.5)):
-    """Solid 3-D value noise (trilinear octaves, cell sizes in metres) at points P [..., 3], in [0, 1]."""
+def value_noise3(P, seed=0, cells=(0.03, 0.08, 0.2, 0.5, 1.2), footprint=None):
+    """Solid 3-D value noise (trilinear octaves, cell sizes in metres) at points P [..., 3], in [0, 1].
+
+    `footprint` (metres per pixel at each point) band-limits the texture like a mip-map: an octave fades
+    out as its cell shrinks below two pixels, so point-sampled views of the same surface stay
+    correlated (a real camera integrates over the pixel)."""
     out = torch.zeros(P.shape[:-1], dtype=P.dtype, device=P.device)
-    wsum = 0.0
+    wsum = torch.zeros_like(out) if footprint is not None else 0.0
     for o, cs in enumerate(cells):
         key = rng.stream_key(seed, 200 + o, S_TEX3)
         U = P / cs
@@ -73,8 +77,12 @@ def value_noise3(P, seed=0, cells=(0.02, 0.05, 0.15, 0.5)):
                          (F[..., 2] if dz else 1 - F[..., 2])
                     acc = acc + wv * _lattice(key, I0[..., 0] + dx, I0[..., 1] + dy, I0[..., 2] + dz)
         wgt = 1.0 / (1 + o)
+        if footprint is not None:
+            wgt = wgt * torch.clamp(cs / (2.0 * footprint) - 1.0, 0.0, 1.0)
         out = out + wgt * acc
-        wsum += wgt
+        wsum = wsum + wgt
+    if footprint is not None:
+        return torch.where(wsum > 0, out / torch.clamp(wsum, min=1e-12), torch.full_like(out, 0.5))
     return out / wsum
 
 
@@ -109,7 +117,7 @@ def street_pair(seed: int = 0, frames=(0,), H: int = 376, Wd: int = 1240, fpx: f
             t = _street_hit(o, dirs, boxes, STREET_H)
             hit = torch.isfinite(t)
             pts = o + dirs * torch.where(hit, t, torch.zeros_like(t))[..., None]
-            tex = value_noise3(pts, seed)
+            tex = value_noise3(pts, seed, footprint=torch.where(hit, t, torch.ones_like(t)) / fpx)
             imgs.append((torch.where(hit, tex, torch.full_like(tex, 0.85)), t))   # sky: flat bright
         L.append(imgs[0][0])
         R.append(imgs[1][0])

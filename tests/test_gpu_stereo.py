@@ -1,0 +1,106 @@
+"""GPU parity of the depth-map estimation (vol_stereo and its stages)
+against the stereo oracle (oracle/stereo_oracle.c).
+
+Bar: census signatures are integers — bit-exact; the tensor is evaluated in fp64 and rounded to fp32 on
+both sides — bit-exact; the solver runs the same written fp32 order with the argmin decisions taken in
+fp32 on both sides — d, w and a compared bit for bit.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from synth.stereo import plane_pair, street_pair
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def S():
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    from paper_1604_03734_b200 import stereo as S_
+    return S_
+
+
+def _bits_equal(a, b):
+    a = np.ascontiguousarray(a, np.float32)
+    b = np.ascontiguousarray(b, np.float32)
+    assert a.shape == b.shape
+    bad = int((a.view(np.uint32) != b.view(np.uint32)).sum())
+    assert bad == 0, f"{bad} values differ (max |diff| {np.nanmax(np.abs(a - b))})"
+
+
+@pytest.mark.parametrize("win", [3, 5])
+def test_census_bit_exact(S, win):
+    rng = np.random.default_rng(win)
+    I = rng.uniform(size=(2, 37, 53)).astype(np.float32)
+    I[0, 5:9, 5:9] = 0.5                     # ties with the centre (strict <)
+    g = S.census(torch.from_numpy(I).cuda(), window=win).cpu().numpy().view(np.uint32)
+    for f in range(2):
+        assert np.array_equal(g[f], oracle.census(I[f], win=win))
+
+
+def test_tensor_bit_exact(S):
+    rng = np.random.default_rng(3)
+    I = rng.uniform(size=(2, 31, 45)).astype(np.float32)
+    I[1, :, :20] = 0.25                      # flat region: identity tensor
+    T = S.tensor(torch.from_numpy(I).cuda(), beta=1.0, gamma=4.0).cpu().numpy()
+    for f in range(2):
+        To = oracle.tensor(I[f], 1.0, 4.0)
+        _bits_equal(np.moveaxis(T[:, f], 0, -1), To)
+    T2 = S.tensor(torch.from_numpy(I).cuda(), beta=0.7, gamma=2.5).cpu().numpy()
+    _bits_equal(np.moveaxis(T2[:, 0], 0, -1), oracle.tensor(I[0], 0.7, 2.5))
+
+
+@pytest.mark.parametrize("abc", [(0.0, 0.0, 7.0), (0.05, 0.02, 5.0), (-0.04, 0.01, 12.0)])
+def test_solve_plane_bit_exact(S, abc):
+    IL, IR, dt = plane_pair(48, 96, *abc)
+    kw = dict(n_disp=32, outer=6, inner=15)
+    d, w, a = S.stereo(IL, IR, return_all=True, **kw)
+    do, wo, ao = oracle.stereo(IL, IR, D=32, outer=6, inner=15)
+    _bits_equal(d.cpu().numpy(), do)
+    _bits_equal(w.cpu().numpy(), wo)
+    _bits_equal(a.cpu().numpy(), ao)
+
+
+def test_batch_frames_independent(S):
+    pairs = [plane_pair(40, 80, 0.03, 0.0, 6.0, seed=1), plane_pair(40, 80, -0.02, 0.03, 9.0, seed=2)]
+    IL = torch.stack([p[0] for p in pairs])
+    IR = torch.stack([p[1] for p in pairs])
+    d = S.stereo(IL, IR, n_disp=24, outer=4, inner=10, window=3).cpu().numpy()
+    for f, (l, r, _) in enumerate(pairs):
+        do, _, _ = oracle.stereo(l, r, D=24, outer=4, inner=10, win=3)
+        _bits_equal(d[f], do)
+
+
+def test_parameters_and_edge_cases(S):
+    from paper_1604_03734_b200._native import VolError
+    IL, IR, _ = plane_pair(16, 32, c=3.0)
+    with pytest.raises(VolError):
+        S.stereo(IL, IR, window=7)
+    with pytest.raises(VolError):
+        S.stereo(IL, IR, tau=0.5, sigma=0.5)           # 12τσ > 1
+    # no iterations: winner-take-all
+    d = S.stereo(IL, IR, n_disp=8, outer=0, inner=0).cpu().numpy()
+    cv = oracle.cost_volume(oracle.census(IL), oracle.census(IR), 8)
+    assert np.array_equal(d, cv.argmin(-1).astype(np.float32))
+    # one disparity: everything 0
+    assert (S.stereo(IL, IR, n_disp=1, outer=2, inner=2).cpu().numpy() == 0).all()
+
+
+def test_disparity_to_depth(S):
+    d = torch.tensor([72.0, 36.0, 0.0, 0.05], device="cuda")
+    z = S.disparity_to_depth(d, 720.0 * 0.54, d_min=0.1).cpu().numpy()
+    assert abs(z[0] - 5.4) <= 1e-6 and abs(z[1] - 10.8) <= 2e-6    # S:406 example, reciprocal law
+    assert z[2] == 0 and z[3] == 0
+
+
+def test_street_full_size_bit_exact(S):
+    """One street stereo pair at full size (1240×376, 128 disparities, 10 × 20 iterations)."""
+    IL, IR, dt = street_pair(frames=(25,), device="cuda")
+    d = S.stereo(IL, IR, n_disp=128).cpu().numpy()[0]
+    do, _, _ = oracle.stereo(IL[0].cpu().numpy(), IR[0].cpu().numpy(), D=128, outer=10, inner=20)
+    _bits_equal(d, do)
+    valid = (dt[0].cpu().numpy() > 1) & (dt[0].cpu().numpy() < 120)
+    assert np.median(np.abs(d - dt[0].cpu().numpy())[valid]) < 1.0
