@@ -50,7 +50,8 @@ def parse():
                     help="use the NCCL sharded runtime even at one rank (tests the N > 1 code path on one GPU)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-fusion", action="store_true", help="skip the TSDF-fusion leg (SURVEY §8(f) NEXT-2)")
+    ap.add_argument("--no-fusion", action="store_true",
+                    help="skip the widened rows (SURVEY §8(f) NEXT-2/3/4: fusion, extraction, stereo legs)")
     ap.add_argument("--seed", type=int, default=0)
     return ap.parse_args()
 
@@ -259,6 +260,60 @@ def extraction_leg(args, dev, scene, iters, stream):
     return res
 
 
+STEREO_BYTES_PER_PIXEL_ITER = 112   # 16 fields read + 12 written (fp32) per pixel-iteration
+
+
+def stereo_leg(args, dev):
+    """Depth-map estimation (§IV) of 8 street stereo pairs (1240x376, 128 disparities, 10 x 20 iterations)."""
+    import torch
+
+    from paper_1604_03734_b200 import stereo
+    from synth.stereo import street_pair
+    F = 8
+    IL, IR, dt = street_pair(seed=args.seed, frames=tuple(range(20, 20 + F)), device=dev)
+    kw = dict(n_disp=128, outer=10, inner=20)
+    stream = torch.cuda.current_stream(dev)
+
+    def timed(n, **k):
+        for _ in range(2):
+            stereo.stereo(IL, IR, **k)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        a.record(stream)
+        for _ in range(n):
+            out = stereo.stereo(IL, IR, **k)
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        return a.elapsed_time(b) / n, out
+
+    ms, d = timed(args.steps, **kw)
+    ms_half, _ = timed(max(2, args.steps // 2), **dict(kw, inner=10))
+    it_ms = (ms - ms_half) / (10 * kw["outer"])            # one k_tgv_iter launch over the batch
+    valid = (dt > 1) & (dt < 120)
+    err = float((d - dt).abs()[valid].median())
+    npx = F * IL.shape[1] * IL.shape[2]
+    peak, peak_src = load_peaks()
+    ach = STEREO_BYTES_PER_PIXEL_ITER * npx / (it_ms / 1e3) / 1e9
+    res = {"workload": f"stereo-street ({F} pairs 1240x376, D=128, 10 x 20 iterations)", "frames": F,
+           "ms_per_call": ms, "frames_per_s": F / (ms / 1e3),
+           "pixel_iterations_per_s": npx * kw["outer"] * kw["inner"] / (ms / 1e3),
+           "median_abs_disparity_error_px": err,
+           "step": "vol_stereo: census x2, tensor, WTA init, 200 fused TGV iterations, 10 data steps (CUDA graph)",
+           "roofline": {"bound": "hbm", "kernel": "k_tgv_iter", "achieved": ach, "peak": peak, "unit": "GB/s",
+                        "frac": ach / peak, "peak_source": peak_src, "avg_launch_ms": it_ms,
+                        "alg_bytes_per_launch": STEREO_BYTES_PER_PIXEL_ITER * npx, "traffic": None}}
+    if not args.no_cpu_baseline:
+        import time as _t
+
+        import oracle
+        t0 = _t.perf_counter()
+        oracle.stereo(IL[0].cpu().numpy(), IR[0].cpu().numpy(), D=128, outer=10, inner=20)
+        dt_cpu = _t.perf_counter() - t0
+        res["cpu_baseline"] = {"value": 1.0 / dt_cpu, "unit": "frames/s", "cores": 1, "kind": "oracle",
+                               "sample": f"one 1240x376 pair, full solve, {dt_cpu:.1f} s on one host core"}
+    return res
+
+
 # ------------------------------------------------------------------------------ CPU oracle timing
 
 def time_oracle(scene, iters: int):
@@ -446,6 +501,9 @@ def main():
     extraction = None
     if not args.no_fusion and world == 1:
         extraction = extraction_leg(args, dev, scene, iters, stream)
+    stereo_res = None
+    if not args.no_fusion and world == 1:
+        stereo_res = stereo_leg(args, dev)
 
     if rank != 0:
         dist.destroy_process_group()
@@ -493,7 +551,7 @@ def main():
                    "energy": {"primal": E[0], "dual": E[1]}},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
         "freeze": bool(args.freeze), "no_freeze": nf,
-        "clocks": clk, "fusion": fusion, "extraction": extraction,
+        "clocks": clk, "fusion": fusion, "extraction": extraction, "stereo": stereo_res,
     }
     print(json.dumps(line), flush=True)
     if sharded:

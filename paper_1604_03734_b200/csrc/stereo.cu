@@ -17,7 +17,9 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "../../include/vol.h"
@@ -208,6 +210,183 @@ __global__ void k_primal(State S, Img g, Steps P) {
     S.w2[i] = wn2;
 }
 
+// Fused iteration: dual then primal in one launch.  A CTA owns a TX×TY tile; it recomputes the dual
+// update of the −x column and −y row next to the tile (same function, same inputs ⇒ bit-identical to
+// the owner's), so the primal step needs no grid-wide synchronisation.  Ping-pong buffers: every field
+// another CTA may read (d̄, w̄, p, q) is read from set `in` and written to set `out`; d, w, a are only
+// touched by their owner and stay in place.
+constexpr int TX = 32, TY = 8;
+constexpr int SX = TX + 2, SY = TY + 2;   // staged box x0−1 … x0+TX, y0−1 … y0+TY
+
+struct PP {
+    const float *db, *wb1, *wb2, *p1, *p2, *q1, *q2, *q3, *q4;   // in
+    float *dbo, *wb1o, *wb2o, *p1o, *p2o, *q1o, *q2o, *q3o, *q4o;  // out
+    float *d, *w1, *w2;
+    const float *a, *T11, *T12, *T22;
+};
+
+__global__ void __launch_bounds__(TX * TY) k_tgv_iter(PP S, Img g, Steps P) {
+    __shared__ float s_db[SY][SX], s_w1[SY][SX], s_w2[SY][SX];
+    __shared__ float s_p1[SY][SX], s_p2[SY][SX], s_q1[SY][SX], s_q2[SY][SX], s_q3[SY][SX], s_q4[SY][SX];
+    __shared__ float s_t11[SY][SX], s_t12[SY][SX], s_t22[SY][SX];
+    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+    const long long fo = (long long)blockIdx.z * g.H * g.W;
+    const int tid = threadIdx.x;
+    // stage d̄, w̄ over the whole box, T, p, q over the box (−1 … +TX/TY is enough for the dual region)
+    for (int k = tid; k < SX * SY; k += TX * TY) {
+        const int sx = k % SX, sy = k / SX;
+        const int x = x0 - 1 + sx, y = y0 - 1 + sy;
+        float db = 0.f, w1 = 0.f, w2 = 0.f, p1 = 0.f, p2 = 0.f, q1 = 0.f, q2 = 0.f, q3 = 0.f, q4 = 0.f;
+        float t11 = 0.f, t12 = 0.f, t22 = 0.f;
+        if (x >= 0 && x < g.W && y >= 0 && y < g.H) {
+            const long long i = fo + (long long)y * g.W + x;
+            db = S.db[i];
+            w1 = S.wb1[i];
+            w2 = S.wb2[i];
+            p1 = S.p1[i];
+            p2 = S.p2[i];
+            q1 = S.q1[i];
+            q2 = S.q2[i];
+            q3 = S.q3[i];
+            q4 = S.q4[i];
+            t11 = S.T11[i];
+            t12 = S.T12[i];
+            t22 = S.T22[i];
+        }
+        s_db[sy][sx] = db;
+        s_w1[sy][sx] = w1;
+        s_w2[sy][sx] = w2;
+        s_p1[sy][sx] = p1;
+        s_p2[sy][sx] = p2;
+        s_q1[sy][sx] = q1;
+        s_q2[sy][sx] = q2;
+        s_q3[sy][sx] = q3;
+        s_q4[sy][sx] = q4;
+        s_t11[sy][sx] = t11;
+        s_t12[sy][sx] = t12;
+        s_t22[sy][sx] = t22;
+    }
+    __syncthreads();
+    // dual step on the tile, its −x column and its −y row (reading order of k_dual); results overwrite
+    // p, q in shared memory only after every thread has read its inputs
+    float np1[2], np2[2], nq1[2], nq2[2], nq3[2], nq4[2];
+    int ssx[2], ssy[2];
+    const int n_dual = TX * TY + TX + TY;
+#pragma unroll
+    for (int r = 0; r < 2; r++) {
+        const int k = tid + r * TX * TY;
+        ssx[r] = -1;
+        if (k >= n_dual) continue;
+        int sx, sy;
+        if (k < TX * TY) {
+            sx = 1 + k % TX;
+            sy = 1 + k / TX;
+        } else if (k < TX * TY + TX) {
+            sx = 1 + (k - TX * TY);
+            sy = 0;
+        } else {
+            sx = 0;
+            sy = 1 + (k - TX * TY - TX);
+        }
+        const int x = x0 - 1 + sx, y = y0 - 1 + sy;
+        if (x < 0 || x >= g.W || y < 0 || y >= g.H) continue;
+        ssx[r] = sx;
+        ssy[r] = sy;
+        const bool hx = x < g.W - 1, hy = y < g.H - 1;
+        const float gx = hx ? __fsub_rn(s_db[sy][sx + 1], s_db[sy][sx]) : 0.0f;
+        const float gy = hy ? __fsub_rn(s_db[sy + 1][sx], s_db[sy][sx]) : 0.0f;
+        const float t11 = s_t11[sy][sx], t12 = s_t12[sy][sx], t22 = s_t22[sy][sx];
+        const float tx = __fadd_rn(__fmul_rn(t11, gx), __fmul_rn(t12, gy));
+        const float ty = __fadd_rn(__fmul_rn(t12, gx), __fmul_rn(t22, gy));
+        const float u1 = __fsub_rn(tx, s_w1[sy][sx]), u2 = __fsub_rn(ty, s_w2[sy][sx]);
+        float p1 = __fadd_rn(s_p1[sy][sx], __fmul_rn(P.sigma, u1));
+        float p2 = __fadd_rn(s_p2[sy][sx], __fmul_rn(P.sigma, u2));
+        const float sc = __fdiv_rn(__fsqrt_rn(__fadd_rn(__fmul_rn(p1, p1), __fmul_rn(p2, p2))), P.alpha1);
+        if (sc > 1.0f) {
+            p1 = __fdiv_rn(p1, sc);
+            p2 = __fdiv_rn(p2, sc);
+        }
+        const float v1 = hx ? __fsub_rn(s_w1[sy][sx + 1], s_w1[sy][sx]) : 0.0f;
+        const float v2 = hy ? __fsub_rn(s_w1[sy + 1][sx], s_w1[sy][sx]) : 0.0f;
+        const float v3 = hx ? __fsub_rn(s_w2[sy][sx + 1], s_w2[sy][sx]) : 0.0f;
+        const float v4 = hy ? __fsub_rn(s_w2[sy + 1][sx], s_w2[sy][sx]) : 0.0f;
+        float q1 = __fadd_rn(s_q1[sy][sx], __fmul_rn(P.sigma, v1));
+        float q2 = __fadd_rn(s_q2[sy][sx], __fmul_rn(P.sigma, v2));
+        float q3 = __fadd_rn(s_q3[sy][sx], __fmul_rn(P.sigma, v3));
+        float q4 = __fadd_rn(s_q4[sy][sx], __fmul_rn(P.sigma, v4));
+        const float n2 = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(q1, q1), __fmul_rn(q2, q2)), __fmul_rn(q3, q3)),
+                                   __fmul_rn(q4, q4));
+        const float sq = __fdiv_rn(__fsqrt_rn(n2), P.alpha2);
+        if (sq > 1.0f) {
+            q1 = __fdiv_rn(q1, sq);
+            q2 = __fdiv_rn(q2, sq);
+            q3 = __fdiv_rn(q3, sq);
+            q4 = __fdiv_rn(q4, sq);
+        }
+        np1[r] = p1;
+        np2[r] = p2;
+        nq1[r] = q1;
+        nq2[r] = q2;
+        nq3[r] = q3;
+        nq4[r] = q4;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 2; r++) {
+        if (ssx[r] < 0) continue;
+        const int sx = ssx[r], sy = ssy[r];
+        s_p1[sy][sx] = np1[r];
+        s_p2[sy][sx] = np2[r];
+        s_q1[sy][sx] = nq1[r];
+        s_q2[sy][sx] = nq2[r];
+        s_q3[sy][sx] = nq3[r];
+        s_q4[sy][sx] = nq4[r];
+    }
+    __syncthreads();
+    // primal step on the tile pixel of this thread (reading order of k_primal)
+    const int tx_ = tid % TX, ty_ = tid / TX;
+    const int x = x0 + tx_, y = y0 + ty_;
+    if (x >= g.W || y >= g.H) return;
+    const int sx = tx_ + 1, sy = ty_ + 1;
+    const long long i = fo + (long long)y * g.W + x;
+    auto tp = [&](int cx, int cy, float &a1, float &a2) {
+        const float p1 = s_p1[cy][cx], p2 = s_p2[cy][cx];
+        a1 = __fadd_rn(__fmul_rn(s_t11[cy][cx], p1), __fmul_rn(s_t12[cy][cx], p2));
+        a2 = __fadd_rn(__fmul_rn(s_t12[cy][cx], p1), __fmul_rn(s_t22[cy][cx], p2));
+    };
+    float h1, h2, l1 = 0.f, l2 = 0.f, u1 = 0.f, u2 = 0.f;
+    tp(sx, sy, h1, h2);
+    const bool hx = x < g.W - 1, bx = x > 0, hy = y < g.H - 1, by = y > 0;
+    if (bx) tp(sx - 1, sy, l1, l2);
+    if (by) tp(sx, sy - 1, u1, u2);
+    (void)l2;
+    (void)u1;
+    const float kd = -__fadd_rn(bd(h1, l1, hx, bx), bd(h2, u2, hy, by));
+    const float dq1 = __fadd_rn(bd(s_q1[sy][sx], bx ? s_q1[sy][sx - 1] : 0.f, hx, bx),
+                                bd(s_q2[sy][sx], by ? s_q2[sy - 1][sx] : 0.f, hy, by));
+    const float dq2 = __fadd_rn(bd(s_q3[sy][sx], bx ? s_q3[sy][sx - 1] : 0.f, hx, bx),
+                                bd(s_q4[sy][sx], by ? s_q4[sy - 1][sx] : 0.f, hy, by));
+    const float kw1 = -__fadd_rn(s_p1[sy][sx], dq1);
+    const float kw2 = -__fadd_rn(s_p2[sy][sx], dq2);
+    const float d = S.d[i], w1 = S.w1[i], w2 = S.w2[i];
+    const float dn = __fdiv_rn(__fadd_rn(__fsub_rn(d, __fmul_rn(P.tau, kd)), __fmul_rn(P.tt, S.a[i])),
+                               __fadd_rn(1.0f, P.tt));
+    const float wn1 = __fsub_rn(w1, __fmul_rn(P.tau, kw1));
+    const float wn2 = __fsub_rn(w2, __fmul_rn(P.tau, kw2));
+    S.dbo[i] = __fadd_rn(dn, __fsub_rn(dn, d));
+    S.wb1o[i] = __fadd_rn(wn1, __fsub_rn(wn1, w1));
+    S.wb2o[i] = __fadd_rn(wn2, __fsub_rn(wn2, w2));
+    S.d[i] = dn;
+    S.w1[i] = wn1;
+    S.w2[i] = wn2;
+    S.p1o[i] = s_p1[sy][sx];
+    S.p2o[i] = s_p2[sy][sx];
+    S.q1o[i] = s_q1[sy][sx];
+    S.q2o[i] = s_q2[sy][sx];
+    S.q3o[i] = s_q3[sy][sx];
+    S.q4o[i] = s_q4[sy][sx];
+}
+
 __global__ void k_data(State S, Img g, int D, int maxc, float c, float lambda) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= g.n()) return;
@@ -257,6 +436,7 @@ struct StereoLayout {
     uint32_t *sL, *sR;
     float *T[3];
     float *f[13];
+    float *g2[9];      // second buffer of d̄, w̄1, w̄2, p1, p2, q1 … q4 (fused kernel ping-pong)
     size_t bytes;
 };
 
@@ -270,6 +450,7 @@ StereoLayout stereo_layout(char *base, long long n, bool stage_in) {
     L.sR = c.take<uint32_t>(n);
     for (auto &t : L.T) t = c.take<float>(n);
     for (auto &f : L.f) f = c.take<float>(n);
+    for (auto &f : L.g2) f = c.take<float>(n);
     L.bytes = c.off + 256;
     return L;
 }
@@ -326,6 +507,85 @@ static float theta_of(const vol_stereo_params *P, int o) {
     return (float)((double)P->theta0 * std::pow((double)P->theta_end / (double)P->theta0, r));
 }
 
+namespace {
+
+// The whole solve of frames [c0, c0 + C) of the batch, for each chunk of `chunk` frames in turn: a chunk's
+// state (~116 B per pixel) is sized to stay resident in the 126 MB L2 across its iterations.
+void enqueue_solve(const StereoLayout &L, const vol_stereo_params *prm, int32_t F, int chunk, bool two_kernel,
+                   cudaStream_t s, long long &launches) {
+    const long long HW = (long long)prm->width * prm->height;
+    const int maxc = prm->window * prm->window - 1;
+    const int TPB = 256;
+    for (int c0 = 0; c0 < F; c0 += chunk) {
+        const int C = F - c0 < chunk ? F - c0 : chunk;
+        const long long o = (long long)c0 * HW, n = (long long)C * HW;
+        const unsigned nb = blocks_for(n, TPB);
+        Img g{C, prm->height, prm->width};
+        State S{L.f[0] + o, L.f[1] + o, L.f[2] + o, L.f[3] + o, L.f[4] + o, L.f[5] + o, L.f[6] + o, L.f[7] + o,
+                L.f[8] + o, L.f[9] + o, L.f[10] + o, L.f[11] + o, L.f[12] + o, L.T[0] + o, L.T[1] + o, L.T[2] + o,
+                L.sL + o, L.sR + o};
+        k_census<<<nb, TPB, 0, s>>>(L.IL + o, g, prm->window, L.sL + o);
+        k_census<<<nb, TPB, 0, s>>>(L.IR + o, g, prm->window, L.sR + o);
+        k_tensor<<<nb, TPB, 0, s>>>(L.IR + o, g, prm->beta, prm->gamma, L.T[0] + o, L.T[1] + o, L.T[2] + o);
+        k_wta<<<nb, TPB, 0, s>>>(S, g, prm->n_disp, maxc);
+        launches += 4;
+        // set 0 = the State fields (k_wta / k_dual / k_primal), set 1 = L.g2; d, w, a single
+        float *set[2][9] = {{S.db, S.wb1, S.wb2, S.p1, S.p2, S.q1, S.q2, S.q3, S.q4},
+                            {L.g2[0] + o, L.g2[1] + o, L.g2[2] + o, L.g2[3] + o, L.g2[4] + o, L.g2[5] + o,
+                             L.g2[6] + o, L.g2[7] + o, L.g2[8] + o}};
+        const dim3 tgrid((prm->width + TX - 1) / TX, (prm->height + TY - 1) / TY, C);
+        int cur = 0;
+        for (int oi = 0; oi < prm->outer; oi++) {
+            const float theta = theta_of(prm, oi);
+            Steps P{prm->sigma, prm->tau, prm->alpha1, prm->alpha2, prm->tau / theta};
+            for (int it = 0; it < prm->inner; it++) {
+                if (two_kernel) {
+                    k_dual<<<nb, TPB, 0, s>>>(S, g, P);
+                    k_primal<<<nb, TPB, 0, s>>>(S, g, P);
+                    launches += 2;
+                } else {
+                    float *const *in = set[cur], *const *out = set[cur ^ 1];
+                    PP pp{in[0], in[1], in[2], in[3], in[4], in[5], in[6], in[7], in[8],
+                          out[0], out[1], out[2], out[3], out[4], out[5], out[6], out[7], out[8],
+                          S.d, S.w1, S.w2, S.a, S.T11, S.T12, S.T22};
+                    k_tgv_iter<<<tgrid, TX * TY, 0, s>>>(pp, g, P);
+                    cur ^= 1;
+                    launches++;
+                }
+            }
+            const float c = 1.0f / (2.0f * theta);
+            k_data<<<nb, TPB, 0, s>>>(S, g, prm->n_disp, maxc, c, prm->lambda);
+            launches++;
+        }
+    }
+}
+
+struct GraphKey {
+    void *ws;
+    int32_t F;
+    int chunk;
+    bool two;
+    int device;
+    vol_stereo_params p;
+};
+
+struct GraphEntry {
+    GraphKey key;
+    cudaGraphExec_t exec;
+    long long launches;
+};
+
+std::mutex g_graph_mu;
+std::vector<GraphEntry> g_graphs;   // most recent last; at most 8
+
+bool same_key(const GraphKey &a, const GraphKey &b) {
+    return a.ws == b.ws && a.F == b.F && a.chunk == b.chunk && a.two == b.two && a.device == b.device &&
+           memcmp(&a.p, &b.p, sizeof a.p) == 0;
+}
+
+}  // namespace
+
+// θ of outer round o is evaluated on the host (theta_of), so a captured graph holds the same values.
 extern "C" vol_status vol_stereo(const float *left, const float *right, int32_t n_frames,
                                  const vol_stereo_params *prm, void *workspace, size_t workspace_bytes, void *stream,
                                  float *disparity, float *w_out, float *a_out) {
@@ -333,13 +593,10 @@ extern "C" vol_status vol_stereo(const float *left, const float *right, int32_t 
     if (st != VOL_OK) return st;
     if (!left || !right || !disparity) return fail(VOL_EINVAL, "vol_stereo: NULL image or output pointer");
     const long long n = (long long)n_frames * prm->width * prm->height;
-    const bool dev_in = is_device_ptr(left) && is_device_ptr(right);
-    if (!dev_in && (is_device_ptr(left) || is_device_ptr(right)))
-        return fail(VOL_EINVAL, "vol_stereo: both images must be host or both device pointers");
     const bool dev_out = is_device_ptr(disparity);
     if ((w_out && is_device_ptr(w_out) != dev_out) || (a_out && is_device_ptr(a_out) != dev_out))
         return fail(VOL_EINVAL, "vol_stereo: outputs must be all host or all device pointers");
-    const size_t need = stereo_layout(nullptr, n, !dev_in).bytes;
+    const size_t need = stereo_layout(nullptr, n, true).bytes;
     void *ws = workspace;
     bool owns = false;
     if (ws) {
@@ -356,50 +613,67 @@ extern "C" vol_status vol_stereo(const float *left, const float *right, int32_t 
             if (own && p) cudaFree(p);
         }
     } guard{ws, owns};
-    StereoLayout L = stereo_layout((char *)ws, n, !dev_in);
+    StereoLayout L = stereo_layout((char *)ws, n, true);
     cudaStream_t s = (cudaStream_t)stream;
-    const float *IL = left, *IR = right;
-    if (!dev_in) {
-        CK(cudaMemcpyAsync(L.IL, left, n * 4, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(L.IR, right, n * 4, cudaMemcpyHostToDevice, s));
-        IL = L.IL;
-        IR = L.IR;
-    }
-    Img g{n_frames, prm->height, prm->width};
-    const int TPB = 256;
-    const unsigned nb = blocks_for(n, TPB);
-    State S{L.f[0], L.f[1], L.f[2], L.f[3], L.f[4], L.f[5], L.f[6], L.f[7], L.f[8], L.f[9], L.f[10], L.f[11], L.f[12],
-            L.T[0], L.T[1], L.T[2], L.sL, L.sR};
-    const int maxc = prm->window * prm->window - 1;
+    // inputs are always staged into the workspace, so a captured solve depends only on the workspace
+    CK(cudaMemcpyAsync(L.IL, left, n * 4, cudaMemcpyDefault, s));
+    CK(cudaMemcpyAsync(L.IR, right, n * 4, cudaMemcpyDefault, s));
+    const bool two_kernel = getenv("HVG_STEREO_TWO_KERNEL") != nullptr;   // baseline, experiments only
+    const long long per_frame = (long long)prm->width * prm->height * 116;
+    int chunk = (int)((96ll << 20) / (per_frame > 0 ? per_frame : 1));
+    if (const char *e = getenv("HVG_STEREO_CHUNK")) chunk = atoi(e);      // experiments only
+    if (chunk < 1) chunk = 1;
+    if (chunk > n_frames) chunk = n_frames;
     long long launches = 0;
-    k_census<<<nb, TPB, 0, s>>>(IL, g, prm->window, L.sL);
-    k_census<<<nb, TPB, 0, s>>>(IR, g, prm->window, L.sR);
-    k_tensor<<<nb, TPB, 0, s>>>(IR, g, prm->beta, prm->gamma, L.T[0], L.T[1], L.T[2]);
-    k_wta<<<nb, TPB, 0, s>>>(S, g, prm->n_disp, maxc);
-    launches += 4;
-    CK(cudaPeekAtLastError());
-    for (int o = 0; o < prm->outer; o++) {
-        const float theta = theta_of(prm, o);
-        Steps P{prm->sigma, prm->tau, prm->alpha1, prm->alpha2, prm->tau / theta};
-        for (int it = 0; it < prm->inner; it++) {
-            k_dual<<<nb, TPB, 0, s>>>(S, g, P);
-            k_primal<<<nb, TPB, 0, s>>>(S, g, P);
-            launches += 2;
-        }
-        const float c = 1.0f / (2.0f * theta);
-        k_data<<<nb, TPB, 0, s>>>(S, g, prm->n_disp, maxc, c, prm->lambda);
-        launches++;
+    if (owns || getenv("HVG_STEREO_NO_GRAPH")) {
+        enqueue_solve(L, prm, n_frames, chunk, two_kernel, s, launches);
         CK(cudaPeekAtLastError());
+    } else {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        GraphKey key{ws, n_frames, chunk, two_kernel, dev, *prm};
+        cudaGraphExec_t exec = nullptr;
+        {
+            std::lock_guard<std::mutex> lk(g_graph_mu);
+            for (auto &e : g_graphs)
+                if (same_key(e.key, key)) {
+                    exec = e.exec;
+                    launches = e.launches;
+                }
+        }
+        if (!exec) {
+            cudaStream_t cs;
+            CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+            cudaGraph_t graph;
+            cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+            if (e == cudaSuccess) {
+                enqueue_solve(L, prm, n_frames, chunk, two_kernel, cs, launches);
+                e = cudaStreamEndCapture(cs, &graph);
+            }
+            if (e == cudaSuccess) {
+                e = cudaGraphInstantiate(&exec, graph, 0);
+                cudaGraphDestroy(graph);
+            }
+            cudaStreamDestroy(cs);
+            if (e != cudaSuccess) return fail(VOL_ECUDA, "vol_stereo: graph capture failed: %s", cudaGetErrorString(e));
+            std::lock_guard<std::mutex> lk(g_graph_mu);
+            if (g_graphs.size() >= 8) {
+                cudaGraphExecDestroy(g_graphs.front().exec);
+                g_graphs.erase(g_graphs.begin());
+            }
+            g_graphs.push_back(GraphEntry{key, exec, launches});
+        }
+        CK(cudaGraphLaunch(exec, s));
     }
     counted((int)launches);
     const cudaMemcpyKind kind = dev_out ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-    CK(cudaMemcpyAsync(disparity, S.d, n * 4, kind, s));
+    CK(cudaMemcpyAsync(disparity, L.f[0], n * 4, kind, s));
     if (w_out) {
-        CK(cudaMemcpyAsync(w_out, S.w1, n * 4, kind, s));
-        CK(cudaMemcpyAsync(w_out + n, S.w2, n * 4, kind, s));
+        CK(cudaMemcpyAsync(w_out, L.f[3], n * 4, kind, s));
+        CK(cudaMemcpyAsync(w_out + n, L.f[4], n * 4, kind, s));
     }
-    if (a_out) CK(cudaMemcpyAsync(a_out, S.a, n * 4, kind, s));
-    if (owns || !dev_out || !dev_in) CK(cudaStreamSynchronize(s));
+    if (a_out) CK(cudaMemcpyAsync(a_out, L.f[2], n * 4, kind, s));
+    if (owns || !dev_out) CK(cudaStreamSynchronize(s));
     return VOL_OK;
 }
 

@@ -25,6 +25,9 @@ def params(width, height, **kw) -> N.vol_stereo_params:
     return p
 
 
+_WS = {}
+
+
 def _f32(x, dev):
     t = x if isinstance(x, torch.Tensor) else torch.as_tensor(x)
     return t.to(device=dev, dtype=torch.float32).contiguous()
@@ -45,8 +48,15 @@ def stereo(left, right, *, stream=None, return_all=False, **kw):
     w = torch.empty(2, F, H, W, device=dev) if return_all else None
     a = torch.empty(F, H, W, device=dev) if return_all else None
     s = torch.cuda.current_stream(dev) if stream is None else stream
-    nbytes = N.lib().vol_stereo_workspace_bytes(F, ctypes.byref(p))
-    ws = torch.empty(int(nbytes), dtype=torch.uint8, device=dev)
+    nbytes = int(N.lib().vol_stereo_workspace_bytes(F, ctypes.byref(p)))
+    # one workspace per (device, size), reused across calls: the library caches the captured solve
+    # (a CUDA graph) per workspace and parameter set
+    key = (dev.index, nbytes)
+    ws = _WS.get(key)
+    if ws is None:
+        if len(_WS) >= 4:
+            _WS.pop(next(iter(_WS)))
+        ws = _WS[key] = torch.empty(nbytes, dtype=torch.uint8, device=dev)
     ptr = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None
     N.check(N.lib().vol_stereo(ptr(L), ptr(R), F, ctypes.byref(p), ptr(ws), nbytes, ctypes.c_void_p(s.cuda_stream),
                                ptr(d), ptr(w), ptr(a)))
