@@ -99,13 +99,15 @@ def plane_pair(H=48, W=96, a=0.0, b=0.0, c=7.0, seed=0, device="cpu"):
 
 
 def street_pair(seed: int = 0, frames=(0,), H: int = 376, Wd: int = 1240, fpx: float = 720.0,
-                baseline: float = 0.54, length: float = 60.0, device="cpu"):
-    """(I_L, I_R, d_true) float32 [F, H, W] of the street canyon from a forward stereo rig at 1 m steps."""
+                baseline: float = 0.54, length: float = 60.0, device="cpu", return_rig: bool = False):
+    """(I_L, I_R, d_true) float32 [F, H, W] of the street canyon from a forward stereo rig at 1 m steps;
+    with return_rig also the right (reference) cameras' poses T_gc [F, 12] float32, the intrinsics
+    (fx, fy, cx, cy) and the baseline."""
     cfg = CONFIG_IDS["street"]
     seg = Segment(0.0, 0.0, 1.0, 0.0, length)
     boxes = _make_boxes(seed, cfg, [seg], 20.0 / 60.0, device)[0].to(torch.float64)
     intr = np.array([fpx, fpx, (Wd - 1) / 2.0, (H - 1) / 2.0])
-    L, R, D = [], [], []
+    L, R, D, poses = [], [], [], []
     for k in frames:
         cam = np.array([float(k), 0.0, CAM_Z])
         Rm = look_at(cam, cam + np.array([1.0, 0.0, 0.0]))
@@ -119,9 +121,12 @@ def street_pair(seed: int = 0, frames=(0,), H: int = 376, Wd: int = 1240, fpx: f
             pts = o + dirs * torch.where(hit, t, torch.zeros_like(t))[..., None]
             tex = value_noise3(pts, seed, footprint=torch.where(hit, t, torch.ones_like(t)) / fpx)
             imgs.append((torch.where(hit, tex, torch.full_like(tex, 0.85)), t))   # sky: flat bright
+        poses.append(_pose12(Rm, right_cam).astype(np.float32))
         L.append(imgs[0][0])
         R.append(imgs[1][0])
         z = imgs[1][1]
         D.append(torch.where(torch.isfinite(z), fpx * baseline / z, torch.zeros_like(z)))
     st = lambda xs: torch.stack(xs).to(torch.float32).contiguous()
+    if return_rig:
+        return st(L), st(R), st(D), torch.tensor(np.stack(poses), device=device), intr.astype(np.float32), baseline
     return st(L), st(R), st(D)
