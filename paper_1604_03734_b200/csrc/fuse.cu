@@ -54,6 +54,7 @@ struct FuseSet {
                                 // walk), [2] compaction cursor, [3] valid pixels, [4] evaluated block-frames,
                                 // [5] Eq. 1 voxel updates
     uint32_t mask;              // cap − 1
+    unsigned long long limit;   // max_blocks: past it the call fails with VOL_ENOMEM, so inserting stops
 };
 
 __device__ __forceinline__ void set_insert(const FuseSet &S, int32_t x, int32_t y, int32_t z, int32_t frame) {
@@ -64,6 +65,13 @@ __device__ __forceinline__ void set_insert(const FuseSet &S, int32_t x, int32_t 
     const unsigned long long key = pack_key(x, y, z);
     uint32_t h = ((uint32_t)x * 73856093u ^ (uint32_t)y * 19349669u ^ (uint32_t)z * 83492791u) & S.mask;
     for (uint32_t probe = 0; probe <= S.mask; probe++) {
+        // capacity reached: the call will fail (VOL_ENOMEM), so stop probing a table that keeps filling
+        if (probe == 0 || (probe & 15) == 0) {
+            if (*((volatile unsigned long long *)&S.count[0]) > S.limit) {
+                atomicOr(&S.count[1], 1ull);
+                return;
+            }
+        }
         // plain load: a slot only ever goes EMPTY -> key and first only decreases, so a stale value is
         // an older state — EMPTY falls through to the CAS, a larger first costs one extra atomicMin
         unsigned long long cur = S.keys[h];
@@ -482,7 +490,7 @@ extern "C" vol_status vol_fuse(const float *depth, int32_t n_frames, const vol_c
     CK(cudaMemsetAsync(L.count, 0, sizeof(unsigned long long) * 8, s));
     FuseArgs A{d_depth, d_poses, K, H, Wd, cam->fx, cam->fy, cam->cx, cam->cy,
                prm->voxel, prm->mu, prm->max_range, prm->w_max};
-    FuseSet S{L.keys, L.first, L.count, cap - 1};
+    FuseSet S{L.keys, L.first, L.count, cap - 1, (unsigned long long)max_blocks};
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

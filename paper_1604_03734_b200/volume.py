@@ -301,7 +301,7 @@ def fuse(depth, poses, intr, voxel: float, mu: float, max_range: float, w_max: f
                         ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(W.data_ptr()), ctypes.byref(n),
                         ctypes.byref(sts) if stats is not None else None)
         if st == N.VOL_ENOMEM and not max_blocks and n.value > cap:
-            cap = int(n.value * 1.25) + 1024
+            cap = 4 * cap      # the count reached is only a lower bound once the capacity is exceeded
             continue
         N.check(st)
         break
