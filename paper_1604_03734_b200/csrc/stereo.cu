@@ -399,9 +399,23 @@ __global__ void k_data(State S, Img g, int D, int maxc, float c, float lambda) {
         const float diff = __fsub_rn(d, (float)k);
         return __fadd_rn(__fmul_rn(c, __fmul_rn(diff, diff)), __fmul_rn(lambda, rho));
     };
-    int best = 0;
-    float eb = energy(0);
-    for (int k = 1; k < D; k++) {
+    // Exact pruning of the scan: E(k) = fl(fl(c·fl((d−k)²)) + fl(λρ)) >= fl(c·fl((d−k)²)) (λρ >= 0,
+    // rounding is monotone), so every k with c(d−k)² > E(k₀) for the nearest integer k₀ has
+    // E(k) > E(k₀) >= min E and can be neither the minimiser nor tied with it.  The window below
+    // contains every other k with a margin of two disparities; scanning it in increasing k with the
+    // strict < keeps the "smallest k among equal minima" rule of the full scan.
+    int lo = 0, hi = D - 1;
+    if (c > 0.0f) {
+        const int k0 = (int)fminf(fmaxf(rintf(d), 0.0f), (float)(D - 1));
+        const float r = __fmul_rn(sqrtf(__fdiv_rn(energy(k0), c)), 1.001f) + 2.0f;
+        if (r < (float)D) {
+            lo = (int)fmaxf(floorf(d - r), 0.0f);
+            hi = (int)fminf(ceilf(d + r), (float)(D - 1));
+        }
+    }
+    int best = lo;
+    float eb = energy(lo);
+    for (int k = lo + 1; k <= hi; k++) {
         const float e = energy(k);
         if (e < eb) {
             eb = e;
