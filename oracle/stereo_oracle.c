@@ -28,7 +28,9 @@
  *             relaxation E = TGV(d, w) + 1/(2θ) Σ(d − a)² + λ Σ ρ(a); `outer` rounds of `inner`
  *             Chambolle–Pock iterations on (d, w) with a fixed, then the exact point-wise minimisation
  *             of 1/(2θ)(d − a)² + λρ(a) over the integer disparities with a 3-point parabola sub-pixel
- *             step; θ decreases geometrically from θ₀ to θ_end.
+ *             step; θ decreases geometrically from θ₀ to θ_end.  Reading S-13: the ball
+ *             projections are p·fl(α/‖p‖) when ‖p‖ > α and the coupling prox divides by (1 + τ/θ) as a
+ *             product with fl(1/(1 + τ/θ)) — the same real numbers as Eq.'s prox steps.
  */
 #include <math.h>
 #include <stdint.h>
@@ -236,25 +238,27 @@ int orc_stereo(const float *IL, const float *IR, int H, int W, const orc_stereo_
     for (int o = 0; o < P->outer; o++) {
         float theta = orc_stereo_theta(P, o);
         float tt = P->tau / theta;                 /* τ/θ */
+        float kd_inv = 1.0f / (1.0f + tt);         /* the prox divisor as a reciprocal (reading S-13) */
         for (int it = 0; it < P->inner; it++) {
             /* dual ascent on the frozen relaxed primal (d̄, w̄), projections onto the α-balls */
             orc_tgv_K(T, db, wb, H, W, u, v);
             for (size_t i = 0; i < n; i++) {
                 float p1 = p[i] + P->sigma * u[i], p2 = p[n + i] + P->sigma * u[n + i];
-                float s = sqrtf(p1 * p1 + p2 * p2) / P->alpha1;
-                if (s > 1.0f) { p1 = p1 / s; p2 = p2 / s; }
+                /* projection onto the α₁-ball, p·(α₁/‖p‖) when ‖p‖ > α₁ (reading S-13) */
+                float nrm = sqrtf(p1 * p1 + p2 * p2);
+                if (nrm > P->alpha1) { float r = P->alpha1 / nrm; p1 = p1 * r; p2 = p2 * r; }
                 p[i] = p1;
                 p[n + i] = p2;
                 float q1 = q[i] + P->sigma * v[i], q2 = q[n + i] + P->sigma * v[n + i];
                 float q3 = q[2 * n + i] + P->sigma * v[2 * n + i], q4 = q[3 * n + i] + P->sigma * v[3 * n + i];
-                float sq = sqrtf(((q1 * q1 + q2 * q2) + q3 * q3) + q4 * q4) / P->alpha2;
-                if (sq > 1.0f) { q1 = q1 / sq; q2 = q2 / sq; q3 = q3 / sq; q4 = q4 / sq; }
+                float nq = sqrtf(((q1 * q1 + q2 * q2) + q3 * q3) + q4 * q4);
+                if (nq > P->alpha2) { float r = P->alpha2 / nq; q1 = q1 * r; q2 = q2 * r; q3 = q3 * r; q4 = q4 * r; }
                 q[i] = q1; q[n + i] = q2; q[2 * n + i] = q3; q[3 * n + i] = q4;
             }
             /* primal descent: prox of the coupling for d, plain step for w; over-relaxation θ = 1 */
             orc_tgv_KT(T, p, q, H, W, kd, kw, tp);
             for (size_t i = 0; i < n; i++) {
-                dn[i] = ((d[i] - P->tau * kd[i]) + tt * a[i]) / (1.0f + tt);
+                dn[i] = ((d[i] - P->tau * kd[i]) + tt * a[i]) * kd_inv;
                 wn[i] = w[i] - P->tau * kw[i];
                 wn[n + i] = w[n + i] - P->tau * kw[n + i];
             }

@@ -64,6 +64,18 @@ def test_solve_plane_bit_exact(S, abc):
     _bits_equal(a.cpu().numpy(), ao)
 
 
+def test_fused_iteration_kernel_bit_exact(S, monkeypatch):
+    """The fused halo-recompute iteration kernel (selectable) computes the same bits as the product path."""
+    IL, IR, dt = plane_pair(40, 100, 0.04, -0.02, 8.0)
+    monkeypatch.setenv("HVG_STEREO_FUSED", "1")
+    d1 = S.stereo(IL, IR, n_disp=32, outer=5, inner=12).cpu().numpy()
+    monkeypatch.delenv("HVG_STEREO_FUSED")
+    d0 = S.stereo(IL, IR, n_disp=32, outer=5, inner=12).cpu().numpy()
+    _bits_equal(d1, d0)
+    do, _, _ = oracle.stereo(IL, IR, D=32, outer=5, inner=12)
+    _bits_equal(d0, do)
+
+
 def test_batch_frames_independent(S):
     pairs = [plane_pair(40, 80, 0.03, 0.0, 6.0, seed=1), plane_pair(40, 80, -0.02, 0.03, 9.0, seed=2)]
     IL = torch.stack([p[0] for p in pairs])
