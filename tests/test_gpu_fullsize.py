@@ -120,3 +120,56 @@ def test_street_outlier_components_full_iterations(V):
         assert np.array_equal(u[blocks][m], uo32[m])
         checked += int(m.sum())
     assert checked >= 100
+
+
+# ------------------------------------------------------------------ city (configs[3], 1 km route)
+
+def _city():
+    """The first 375 m of the configs[3] route (configs[4] weak-scaling prefix for 3 GPUs: two 90° turns,
+    city voxel size and solver): the full 1 km takes minutes to generate, the prefix ~1/3 of that."""
+    if "city" not in _cache:
+        from synth import scenes
+        _cache["city"] = scenes.by_name("city-weak:3", device="cuda").to("cpu")
+    return _cache["city"]
+
+
+def test_city_first_iterations_match_oracle(V):
+    """configs[3] geometry (staircase route, v = 10 cm, μ = 0.5 m, Huber-TV): the whole volume after
+    2 iterations, bitwise against the fp32 oracle and within 1e-5 of fp64."""
+    s = _city()
+    assert s.n_alloc > 2e7
+    vol = V(s.coords.cuda(), s.f.cuda(), s.W.cuda())
+    vol.regularise_scene(s, iters=2)
+    u = vol.u().cpu().numpy()
+    nbr = oracle.neighbours(s.coords)
+    u32, _, _ = oracle.regularise_scene(s, precision="f32", iters=2, nbr=nbr)
+    assert np.array_equal(u, u32)
+    u64, _, _ = oracle.regularise_scene(s, precision="f64", iters=2, nbr=nbr)
+    assert float(np.abs(u - u64).max()) <= 1e-5
+
+
+def test_city_route_shards_bitwise_equal_single(V):
+    """The sharded runtime on the city route prefix (8 route-axis shards, loopback transport on one GPU, the same
+    plan, pack/unpack and two-launch schedule as NCCL) equals the single-GPU result bit for bit after
+    the config's 200 iterations (SURVEY §8(e) correctness gate)."""
+    from paper_1604_03734_b200 import connect_group, group_energy, regularise_group
+    import bench
+    s = _city()
+    world = 8
+    part = bench.partition(s.coords, world)
+    vols = []
+    for r in range(world):
+        mine = (part == r).nonzero().squeeze(1)
+        vols.append(V(s.coords.cuda(), s.f[mine].cuda(), s.W[mine].cuda(), part=part, loopback=(r, world)))
+    assert all(v.n_ghost > 0 for v in vols)
+    connect_group(vols)
+    regularise_group(vols, s.lam, s.eps, s.tau, s.sigma, s.iters, data_term=s.data_term)
+    single = V(s.coords.cuda(), s.f.cuda(), s.W.cuda())
+    single.regularise_scene(s)
+    u1 = single.u().cpu()
+    for r, v in enumerate(vols):
+        mine = (part == r).nonzero().squeeze(1)
+        assert torch.equal(v.u().cpu(), u1[mine])
+    P1, D1 = single.energy(s.lam, s.eps, s.data_term)
+    Pg, Dg = group_energy(vols, s.lam, s.eps, s.data_term)
+    assert abs(P1 - Pg) <= 1e-9 * abs(P1) and abs(D1 - Dg) <= 1e-9 * abs(P1)
