@@ -66,7 +66,8 @@ __device__ __forceinline__ void set_insert(const FuseSet &S, int32_t x, int32_t 
     uint32_t h = ((uint32_t)x * 73856093u ^ (uint32_t)y * 19349669u ^ (uint32_t)z * 83492791u) & S.mask;
     for (uint32_t probe = 0; probe <= S.mask; probe++) {
         // capacity reached: the call will fail (VOL_ENOMEM), so stop probing a table that keeps filling
-        if (probe == 0 || (probe & 15) == 0) {
+        // (checked only on long probe sequences: below the capacity the load factor is <= 1/2)
+        if (probe >= 32 && (probe & 15) == 0) {
             if (*((volatile unsigned long long *)&S.count[0]) > S.limit) {
                 atomicOr(&S.count[1], 1ull);
                 return;
