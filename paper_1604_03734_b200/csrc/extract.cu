@@ -320,6 +320,7 @@ using namespace hvg;
 
 extern "C" vol_status vol_extract(vol_t v, int field, float voxel, float w_min, float *tris, int64_t max_tris,
                                   int64_t *n_tris) {
+    NvtxRange nvtx_range_("vol_extract");
     if (!v || !n_tris) return fail(VOL_EINVAL, "vol_extract: NULL argument");
     *n_tris = 0;
     if (v->shard) return fail(VOL_ENOTSUP, "vol_extract: sharded volumes are not supported (extract per GPU volume)");

@@ -445,6 +445,7 @@ extern "C" vol_status vol_fuse(const float *depth, int32_t n_frames, const vol_c
                                const vol_fusion_params *prm, int64_t max_blocks, void *workspace,
                                size_t workspace_bytes, void *stream, int32_t *block_xyz, int32_t *first_frame,
                                float *f, float *W, int64_t *n_blocks, vol_fusion_stats *stats) {
+    NvtxRange nvtx_range_("vol_fuse");
     vol_status st = check_fuse_args(n_frames, cam, prm, max_blocks);
     if (st != VOL_OK) return st;
     if (!depth || !poses || !block_xyz || !f || !W || !n_blocks)

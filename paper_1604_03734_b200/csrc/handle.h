@@ -6,6 +6,8 @@
 
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX 3: ranges show up in nsys / ncu timelines
+
 #include "../../include/vol.h"
 #include "internal.h"
 
@@ -31,6 +33,14 @@ vol_status fail(vol_status st, const char *fmt, ...) __attribute__((format(print
                         __FILE__, __LINE__);                                                   \
         }                                                                                      \
     } while (0)
+
+// NVTX range for the lifetime of a scope (one per ABI call; SURVEY §5 tracing)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 // ------------------------------------------------------------------------------ workspace carving
 struct Carve {

@@ -283,6 +283,7 @@ static vol_status unpack(vol_s *v, float *a, float *b, float *c, float *d, cudaS
     } while (0)
 
 static vol_status nccl_exchange(vol_s *v, cudaStream_t s) {
+    NvtxRange nvtx_range_("halo_exchange");
     ShardRuntime *R = v->shard;
     const ShardPlan &P = R->plan;
     NCK(ncclGroupStart());
@@ -428,6 +429,10 @@ vol_status shard_iterate(vol_s *v, const IterParams &P, int32_t iters) {
         if (st != VOL_OK) return st;
     }
     v->last_launches = launches;
+    // asynchronous NCCL failures of earlier work (SURVEY §5 failure detection)
+    ncclResult_t async = ncclSuccess;
+    if (ncclCommGetAsyncError(R->comm, &async) == ncclSuccess && async != ncclSuccess && async != ncclInProgress)
+        return fail(VOL_ENCCL, "NCCL asynchronous error: %s", ncclGetErrorString(async));
     return VOL_OK;
 }
 
@@ -527,6 +532,7 @@ extern "C" vol_status vol_group_connect(vol_t *h, int world) {
 
 extern "C" vol_status vol_regularise_group(vol_t *h, int world, float lambda, float eps, float tau, float sigma,
                                            int32_t iters, const vol_opts *opts) {
+    NvtxRange nvtx_range_("vol_regularise_group");
     vol_status st = check_group(h, world);
     if (st != VOL_OK) return st;
     for (int r = 0; r < world; r++)

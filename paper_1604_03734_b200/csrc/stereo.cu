@@ -601,6 +601,7 @@ bool same_key(const GraphKey &a, const GraphKey &b) {
 extern "C" vol_status vol_stereo(const float *left, const float *right, int32_t n_frames,
                                  const vol_stereo_params *prm, void *workspace, size_t workspace_bytes, void *stream,
                                  float *disparity, float *w_out, float *a_out) {
+    NvtxRange nvtx_range_("vol_stereo");
     vol_status st = check_params(n_frames, prm);
     if (st != VOL_OK) return st;
     if (!left || !right || !disparity) return fail(VOL_EINVAL, "vol_stereo: NULL image or output pointer");

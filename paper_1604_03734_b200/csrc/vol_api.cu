@@ -194,6 +194,7 @@ static vol_status copy_in(void *dst, const void *src, size_t bytes, cudaStream_t
 extern "C" vol_status vol_create(const int32_t *block_xyz, int64_t n_global, const float *f, const float *W,
                                  const vol_dist *dist, void *workspace, size_t workspace_bytes, void *stream,
                                  vol_t *out) {
+    NvtxRange nvtx_range_("vol_create");
     if (!out) return fail(VOL_EINVAL, "vol_create: out is NULL");
     *out = nullptr;
     if (n_global < 1) return fail(VOL_EINVAL, "vol_create: n_global must be >= 1 (got %lld)", (long long)n_global);
@@ -484,6 +485,7 @@ vol_status vol_regularise_prepare(vol_s *v, float lambda, float eps, float tau, 
 
 extern "C" vol_status vol_regularise(vol_t v, float lambda, float eps, float tau, float sigma, int32_t iters,
                                      const vol_opts *opts) {
+    NvtxRange nvtx_range_("vol_regularise");
     vol_status st = vol_regularise_prepare(v, lambda, eps, tau, sigma, iters, opts);
     if (st != VOL_OK) return st;
     if (iters == 0) return VOL_OK;
@@ -529,11 +531,13 @@ static vol_status write_field(vol_s *v, float *dst, const float *src) {
 }
 
 extern "C" vol_status vol_read_u(vol_t v, float *u_out) {
+    NvtxRange nvtx_range_("vol_read_u");
     if (!v || !u_out) return fail(VOL_EINVAL, "vol_read_u: NULL argument");
     return read_field(v, u_out, v->F.u);
 }
 
 extern "C" vol_status vol_read_state(vol_t v, float *u, float *ubar, float *p) {
+    NvtxRange nvtx_range_("vol_read_state");
     if (!v) return fail(VOL_EINVAL, "vol_read_state: NULL handle");
     const size_t nv = (size_t)v->L.n_local * kBlockVox;
     const int c = v->cur;
@@ -549,6 +553,7 @@ extern "C" vol_status vol_read_state(vol_t v, float *u, float *ubar, float *p) {
 }
 
 extern "C" vol_status vol_load_state(vol_t v, const float *u, const float *ubar, const float *p) {
+    NvtxRange nvtx_range_("vol_load_state");
     if (!v) return fail(VOL_EINVAL, "vol_load_state: NULL handle");
     if (v->shard) return fail(VOL_ENOTSUP, "vol_load_state: single-GPU volumes only");
     const size_t nv = (size_t)v->L.n_local * kBlockVox;
@@ -567,6 +572,7 @@ extern "C" vol_status vol_load_state(vol_t v, const float *u, const float *ubar,
 }
 
 extern "C" vol_status vol_energy(vol_t v, float lambda, float eps, int data_term, double *primal, double *dual) {
+    NvtxRange nvtx_range_("vol_energy");
     if (!v || !primal) return fail(VOL_EINVAL, "vol_energy: NULL argument");
     if (!(lambda > 0.0f) || !(eps >= 0.0f) || (data_term != 0 && data_term != 1))
         return fail(VOL_EINVAL, "vol_energy: bad parameters");

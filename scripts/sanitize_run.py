@@ -1,5 +1,6 @@
 """Small end-to-end run for compute-sanitizer (memcheck / racecheck / synccheck): the fused and two-kernel
-paths, state I/O, energy and a 2-shard loopback group, on the tiny sphere and a random instance."""
+paths, state I/O, energy and a 2-shard loopback group, on the tiny sphere and a random instance; then
+the widened rows on small inputs: vol_fuse, vol_extract, vol_stereo (two-kernel and fused iteration)."""
 import os
 import sys
 
@@ -29,6 +30,22 @@ def main():
     connect_group(vols)
     regularise_group(vols, 0.5, 0.01, r.tau, r.sigma, 3)
     print("group energy", group_energy(vols, 0.5, 0.01))
+    # widened rows: fusion, extraction, stereo
+    from paper_1604_03734_b200 import fuse, stereo
+    from synth.depth import sphere_depth
+    from synth.stereo import plane_pair
+    ds = sphere_depth(n_cams=3, H=40, Wd=56)
+    xyz, first, f, W = fuse(ds.depth.cuda(), ds.poses.cuda(), ds.intr.numpy(), ds.voxel, ds.mu, ds.max_range,
+                            ds.w_max, stats={})
+    fv = Volume(xyz, f, W)
+    fv.regularise(1.0, 0.0, s.tau, s.sigma, 3)
+    print("triangles", fv.extract(ds.voxel).shape[0], fv.extract(ds.voxel, field="f", w_min=2.0).shape[0])
+    IL, IR, _ = plane_pair(24, 72, 0.03, 0.01, 5.0)
+    d = stereo.stereo(IL, IR, n_disp=16, outer=2, inner=3)
+    os.environ["HVG_STEREO_FUSED"] = "1"
+    d2 = stereo.stereo(IL, IR, n_disp=16, outer=2, inner=3)
+    del os.environ["HVG_STEREO_FUSED"]
+    print("stereo equal", bool(torch.equal(d, d2)), float(stereo.disparity_to_depth(d, 388.8, 0.5).mean()))
     torch.cuda.synchronize()
     print("sanitize run ok")
 
