@@ -129,3 +129,20 @@ def test_street_full_size_f(Vol):
     To = oracle.extract(s.coords.cpu().numpy(), s.f.cpu().numpy(), s.W.cpu().numpy(), s.meta["voxel"])
     assert To.shape[0] > 1_000_000
     _same(T, To)
+
+
+def test_degenerate_and_tiny_t_bit_exact(Vol):
+    """Exact zeros at corners (X-6 drops) and values that make t round to 0 or 1: GPU == oracle."""
+    s = dense_box(2, 2, 2)
+    c = s.coords.numpy()
+    i = np.arange(512)
+    loc = np.stack([i % 8, (i // 8) % 8, i // 64], 1)
+    g = c[:, None, :].astype(np.int64) * 8 + loc[None]
+    u = (g[..., 0] + g[..., 1] - g[..., 2] - 3).astype(np.float32)
+    u[(g[..., 0] % 3) == 0] *= np.float32(1e-30)                 # tiny values next to O(1) ones
+    W = np.ones_like(u)
+    vol = Vol(torch.from_numpy(c).cuda(), torch.from_numpy(u).cuda(), torch.from_numpy(W).cuda())
+    T = vol.extract(V, field="f").cpu().numpy()
+    To = oracle.extract(c, u, W, V)
+    assert To.shape[0] > 0
+    _same(T, To)

@@ -205,3 +205,18 @@ def test_street_fusion_full_size(fuse):
     assert np.array_equal(W.cpu().numpy()[sel], Ws)
     assert np.array_equal(f.cpu().numpy()[sel], fs)
     assert xo.shape[0] > 20000
+
+
+def test_edge_cases_bit_exact(fuse):
+    """Weight cap 1, an all-invalid frame inside the sequence, depths below μ (band clamped at the camera,
+    z_c → 0), negative coordinates and a camera looking back along −z: GPU == oracle bit for bit."""
+    g = np.random.default_rng(11)
+    K = 5
+    P = np.stack([_rand_pose(200 + k, 0.3) for k in range(K)])
+    P[:, 3] -= 7.0                                   # negative x everywhere
+    P[2, :3] = -P[2, :3]                             # an improper (reflected) rotation: still just numbers
+    D = g.uniform(0.05, 4.0, size=(K, HH, WW)).astype(np.float32)
+    D[1] = np.nan                                    # whole frame invalid
+    D[3, :, :10] = 0.1                               # < μ: band starts at the camera
+    args = (D, INTR, P, 0.05, 0.3, 6.0, 1.0)
+    _same(_gpu(fuse, *args), oracle.fuse(*args))

@@ -152,3 +152,21 @@ def test_caller_block_order_only_permutes_blocks():
     T2 = oracle.extract(c[perm], u[perm], np.ones_like(u), V)
     key = lambda A: sorted(map(bytes, A.view(np.uint8).reshape(A.shape[0], -1)))
     assert key(T) == key(T2)
+
+
+def test_degenerate_triangles_dropped():
+    """X-6: corners with u exactly 0 collapse edge vertices onto the corner; such triangles are
+    dropped, every emitted triangle has three distinct vertices, and the surface stays manifold."""
+    s = dense_box(2, 2, 2)
+    c = s.coords.numpy()
+    g = _grid(c)
+    # integer-valued field on the voxel lattice: many corners exactly 0
+    u = (g[..., 0] + g[..., 1] - g[..., 2] - 3).astype(np.float32)
+    assert (u == 0).sum() > 100
+    T = oracle.extract(c, u, np.ones_like(u), V)
+    assert T.shape[0] > 0
+    b = T.view(np.uint32).reshape(-1, 3, 3)
+    same = lambda i, j: (b[:, i] == b[:, j]).all(-1)
+    assert not (same(0, 1) | same(1, 2) | same(0, 2)).any()
+    E = _edges(T)
+    assert len(set(E)) == len(E)
