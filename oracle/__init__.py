@@ -93,6 +93,8 @@ def lib():
         L.orc_block_walk.argtypes = [P, P, flt, P, i64]
         L.orc_fuse.restype = i64
         L.orc_fuse.argtypes = [P, i32, i32, i32, P, P, flt, flt, flt, flt, i64, P, P, P, P]
+        L.orc_fuse_incremental.restype = i64
+        L.orc_fuse_incremental.argtypes = [P, P, P, i64, P, i32, i32, i32, P, P, flt, flt, flt, flt, i64, P, P, P, P]
         L.orc_fuse_alloc.restype = i64
         L.orc_fuse_alloc.argtypes = [P, i32, i32, i32, P, P, flt, flt, flt, i64, P, P]
         L.orc_extract.restype = i64
@@ -309,6 +311,31 @@ def fuse(depth, intr, poses, voxel, mu, max_range, w_max):
     n2 = lib().orc_fuse(_ptr(D), K, H, Wd, _ptr(it), _ptr(ps), r(voxel), r(mu), r(max_range), r(w_max), n,
                         _ptr(xyz), _ptr(first), _ptr(f), _ptr(W))
     assert n2 == n
+    return xyz[:n], first[:n], f[:n], W[:n]
+
+
+def fuse_incremental(prev, depth, intr, poses, voxel, mu, max_range, w_max):
+    """Continue a fusion: prev = (xyz [m,3], f [m,512], W [m,512]) of earlier frames, then the new depth
+    maps in sequence (reading F-11).  Returns (xyz, first, f, W) like :func:`fuse` (first = −1 for the
+    previous blocks)."""
+    px = _np(prev[0], np.int32).reshape(-1, 3)
+    m = px.shape[0]
+    pf = _np(prev[1], np.float32).reshape(m, 512)
+    pw = _np(prev[2], np.float32).reshape(m, 512)
+    D, K, H, Wd, it, ps = _fusion_inputs(depth, intr, poses)
+    r = lambda x: float(np.float32(x))
+    args = (_ptr(px), _ptr(pf), _ptr(pw), m, _ptr(D), K, H, Wd, _ptr(it), _ptr(ps), r(voxel), r(mu), r(max_range),
+            r(w_max))
+    n = lib().orc_fuse_incremental(*args, 0, None, None, None, None)
+    if n == -2:
+        raise ValueError("fusion oracle: repeated block in prev")
+    if n < 0:
+        raise ValueError("fusion oracle: block walk out of range")
+    xyz = np.zeros((max(n, 1), 3), np.int32)
+    first = np.zeros(max(n, 1), np.int32)
+    f = np.zeros((max(n, 1), 512), np.float32)
+    W = np.zeros((max(n, 1), 512), np.float32)
+    lib().orc_fuse_incremental(*args, n, _ptr(xyz), _ptr(first), _ptr(f), _ptr(W))
     return xyz[:n], first[:n], f[:n], W[:n]
 
 

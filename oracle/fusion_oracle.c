@@ -326,18 +326,30 @@ static void emit_sorted(const blockset *s, int32_t *xyz, int32_t *first, float *
 
 /* ------------------------------------------------------------------ entry points */
 
-/* The whole fusion, frame by frame (allocation then update).
+/* The whole fusion, frame by frame (allocation then update), continuing from an existing
+ * set of fused blocks ("New incoming data can be added at any time"; reading F-11): the
+ * n_prev blocks prev_xyz with their (f, W) are in the set before frame 0 (allocating frame −1), and
+ * new depth maps update them exactly as they would have after the frames that produced them.
  *   depth [K][H][Wd] metres (invalid: non-finite, <= 0 or > max_range);  intr = (fx, fy, cx, cy);
  *   pose [K][12] row-major T_gc (camera-to-global).
- * Returns the number of allocated blocks n (or -1 if a block walk leaves the coordinate range or is
- * longer than the oracle's walk buffer).  Outputs (sorted by (x, y, z)) are written only when
- * n <= max_blocks: xyz [n][3], first [n] (allocating frame), f, W [n][512].                      */
-int64_t orc_fuse(const float *depth, int32_t K, int32_t H, int32_t Wd, const float *intr, const float *pose,
-                 float voxel, float mu, float max_range, float w_max, int64_t max_blocks, int32_t *xyz,
-                 int32_t *first, float *f, float *W)
+ * Returns the number of blocks n (or -1 if a block walk leaves the coordinate range or is longer than
+ * the oracle's walk buffer, -2 if prev_xyz repeats a block).  Outputs (sorted by (x, y, z)) are
+ * written only when n <= max_blocks: xyz [n][3], first [n] (allocating frame, −1 for the previous
+ * blocks), f, W [n][512].                                                                          */
+int64_t orc_fuse_incremental(const int32_t *prev_xyz, const float *prev_f, const float *prev_W, int64_t n_prev,
+                             const float *depth, int32_t K, int32_t H, int32_t Wd, const float *intr,
+                             const float *pose, float voxel, float mu, float max_range, float w_max,
+                             int64_t max_blocks, int32_t *xyz, int32_t *first, float *f, float *W)
 {
     blockset s;
     set_init(&s);
+    for (int64_t b = 0; b < n_prev; b++) {
+        int64_t before = s.n;
+        set_insert(&s, prev_xyz[3 * b], prev_xyz[3 * b + 1], prev_xyz[3 * b + 2], -1, 1);
+        if (s.n == before) { set_free(&s); return -2; }
+        memcpy(s.f + 512 * before, prev_f + 512 * b, 512 * sizeof(float));
+        memcpy(s.w + 512 * before, prev_W + 512 * b, 512 * sizeof(float));
+    }
     for (int32_t k = 0; k < K; k++) {
         const float *D = depth + (int64_t)k * H * Wd;
         if (alloc_frame(&s, D, k, H, Wd, intr, pose + 12 * k, voxel, mu, max_range, 1)) { set_free(&s); return -1; }
@@ -347,6 +359,14 @@ int64_t orc_fuse(const float *depth, int32_t K, int32_t H, int32_t Wd, const flo
     if (n <= max_blocks) emit_sorted(&s, xyz, first, f, W, 1);
     set_free(&s);
     return n;
+}
+
+int64_t orc_fuse(const float *depth, int32_t K, int32_t H, int32_t Wd, const float *intr, const float *pose,
+                 float voxel, float mu, float max_range, float w_max, int64_t max_blocks, int32_t *xyz,
+                 int32_t *first, float *f, float *W)
+{
+    return orc_fuse_incremental(NULL, NULL, NULL, 0, depth, K, H, Wd, intr, pose, voxel, mu, max_range, w_max,
+                                max_blocks, xyz, first, f, W);
 }
 
 /* Allocation passes only (every frame in sequence): the allocated blocks sorted by (x, y, z) and the

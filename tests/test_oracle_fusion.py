@@ -325,3 +325,25 @@ def test_alloc_and_block_updates_compose_to_fuse():
     rows = [tuple(r) for r in xyz.tolist()]
     assert rows == sorted(set(rows))
     assert torch.is_tensor(ds.depth)
+
+
+def test_incremental_equals_batch():
+    """Reading F-11: fusing frames 0..K−1 at once equals fusing 0..k−1 and then continuing with k..K−1 from
+    the resulting blocks, bit for bit (each voxel's Eq. 1 recurrence only sees its own (f, w))."""
+    from synth.depth import sphere_depth
+    ds = sphere_depth()
+    D, I, P = ds.depth.numpy(), ds.intr.numpy(), ds.poses.numpy()
+    prm = (ds.voxel, ds.mu, ds.max_range, ds.w_max)
+    xa, fa, f_all, W_all = oracle.fuse(D, I, P, *prm)
+    for k in (1, 3, 7):
+        x1, _, f1, W1 = oracle.fuse(D[:k], I, P[:k], *prm)
+        x2, fr2, f2, W2 = oracle.fuse_incremental((x1, f1, W1), D[k:], I, P[k:], *prm)
+        assert np.array_equal(x2, xa)
+        assert np.array_equal(f2, f_all) and np.array_equal(W2, W_all)
+        # blocks from the first call carry −1, the others their frame shifted by k
+        old = {tuple(r) for r in x1}
+        is_old = np.array([tuple(r) in old for r in x2])
+        assert (fr2[is_old] == -1).all() and np.array_equal(fr2[~is_old] + k, fa[~is_old])
+    with pytest.raises(ValueError):
+        oracle.fuse_incremental((np.concatenate([x1, x1[:1]]), np.concatenate([f1, f1[:1]]),
+                                 np.concatenate([W1, W1[:1]])), D, I, P, *prm)
