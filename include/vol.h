@@ -303,6 +303,18 @@ vol_status vol_fuse(const float *depth, int32_t n_frames, const vol_camera *cam,
                     void *stream, int32_t *block_xyz, int32_t *first_frame, float *f, float *W,
                     int64_t *n_blocks, vol_fusion_stats *stats);
 
+/* Continue a fusion (reading F-11; "New incoming data can be added at any time"): the n_prev
+ * blocks prev_xyz [n_prev][3] with their prev_f, prev_W [n_prev][512] (host or device; e.g. the
+ * outputs of an earlier call) are in the set before the first new frame (allocating frame −1) and are
+ * updated by the new depth maps exactly as if all frames had been fused in one call — the output is
+ * bit-identical to fusing the old and new frames together.  Other arguments as vol_fuse; max_blocks
+ * counts the previous blocks too.  Errors as vol_fuse, plus VOL_EDATA when prev_xyz repeats a block. */
+vol_status vol_fuse_incremental(const int32_t *prev_xyz, const float *prev_f, const float *prev_W, int64_t n_prev,
+                                const float *depth, int32_t n_frames, const vol_camera *cam, const float *poses,
+                                const vol_fusion_params *params, int64_t max_blocks, void *workspace,
+                                size_t workspace_bytes, void *stream, int32_t *block_xyz, int32_t *first_frame,
+                                float *f, float *W, int64_t *n_blocks, vol_fusion_stats *stats);
+
 #ifdef __cplusplus
 }
 #endif

@@ -57,7 +57,7 @@ EXPORTS = [
     "vol_read_state", "vol_load_state", "vol_read_tables", "vol_info", "vol_last_launches", "vol_sync",
     "vol_destroy", "vol_last_error", "vol_nccl_unique_id", "vol_group_connect", "vol_regularise_group",
     "vol_group_energy", "vol_block_hash", "vol_plan_shard", "vol_total_launches", "vol_fuse_workspace_bytes",
-    "vol_fuse", "vol_extract", "vol_stereo_default_params", "vol_stereo_workspace_bytes", "vol_stereo",
+    "vol_fuse", "vol_fuse_incremental", "vol_extract", "vol_stereo_default_params", "vol_stereo_workspace_bytes", "vol_stereo",
     "vol_stereo_census", "vol_stereo_tensor", "vol_disparity_to_depth",
 ]
 
@@ -97,6 +97,9 @@ def lib() -> ctypes.CDLL:
         "vol_plan_shard": (st, [P, i64, P, c_int, c_int, P, P, P, P, P, P, P]),
         "vol_total_launches": (i64, []),
         "vol_extract": (st, [P, c_int, f32, f32, P, i64, P]),
+        "vol_fuse_incremental": (st, [P, P, P, i64, P, i32, ctypes.POINTER(vol_camera), P,
+                                      ctypes.POINTER(vol_fusion_params), i64, P, ctypes.c_size_t, P, P, P, P, P, P,
+                                      ctypes.POINTER(vol_fusion_stats)]),
         "vol_stereo_default_params": (None, [ctypes.POINTER(vol_stereo_params)]),
         "vol_stereo_workspace_bytes": (ctypes.c_size_t, [i32, ctypes.POINTER(vol_stereo_params)]),
         "vol_stereo": (st, [P, P, i32, ctypes.POINTER(vol_stereo_params), P, ctypes.c_size_t, P, P, P, P]),

@@ -55,6 +55,7 @@ struct FuseSet {
                                 // [5] Eq. 1 voxel updates
     uint32_t mask;              // cap − 1
     unsigned long long limit;   // max_blocks: past it the call fails with VOL_ENOMEM, so inserting stops
+    int32_t *prev;              // [cap] row of the block in the previous fusion's arrays, −1 = new (F-11)
 };
 
 __device__ __forceinline__ void set_insert(const FuseSet &S, int32_t x, int32_t y, int32_t z, int32_t frame) {
@@ -86,6 +87,35 @@ __device__ __forceinline__ void set_insert(const FuseSet &S, int32_t x, int32_t 
         }
         if (cur == key) {
             if (S.first[h] > frame) atomicMin(&S.first[h], frame);
+            return;
+        }
+        h = (h + 1) & S.mask;
+    }
+    atomicOr(&S.count[1], 1ull);
+}
+
+// Reading F-11: the blocks of an earlier fusion enter the set before frame 0 (first frame −1) and
+// remember their row in the caller's previous arrays.  Flags: bit1 coordinate range, bit2 repeated block.
+__global__ void k_fuse_seed(const int32_t *__restrict__ xyz, int64_t n, FuseSet S) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int32_t x = xyz[3 * i], y = xyz[3 * i + 1], z = xyz[3 * i + 2];
+    if (x <= -kCoordLim || x >= kCoordLim || y <= -kCoordLim || y >= kCoordLim || z <= -kCoordLim || z >= kCoordLim) {
+        atomicOr(&S.count[1], 2ull);
+        return;
+    }
+    const unsigned long long key = pack_key(x, y, z);
+    uint32_t h = ((uint32_t)x * 73856093u ^ (uint32_t)y * 19349669u ^ (uint32_t)z * 83492791u) & S.mask;
+    for (uint32_t probe = 0; probe <= S.mask; probe++) {
+        const unsigned long long cur = atomicCAS(&S.keys[h], kEmpty, key);
+        if (cur == kEmpty) {
+            atomicAdd(&S.count[0], 1ull);
+            S.first[h] = -1;
+            S.prev[h] = (int32_t)i;
+            return;
+        }
+        if (cur == key) {
+            atomicOr(&S.count[1], 4ull);
             return;
         }
         h = (h + 1) & S.mask;
@@ -206,7 +236,7 @@ __global__ void __launch_bounds__(256) k_fuse_alloc(FuseArgs A, FuseSet S) {
     if ((threadIdx.x & 31) == 0 && n_valid) atomicAdd(&S.count[3], n_valid);
 }
 
-__global__ void k_fuse_compact(FuseSet S, uint32_t cap, unsigned long long *out_keys, int32_t *out_first,
+__global__ void k_fuse_compact(FuseSet S, uint32_t cap, unsigned long long *out_keys, unsigned long long *out_val,
                                unsigned long long *cursor, unsigned long long limit) {
     const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= cap) return;
@@ -215,7 +245,8 @@ __global__ void k_fuse_compact(FuseSet S, uint32_t cap, unsigned long long *out_
     const unsigned long long r = atomicAdd(cursor, 1ull);
     if (r < limit) {
         out_keys[r] = key;
-        out_first[r] = S.first[s];
+        // value: (first frame, previous row), both int32, first in the high half
+        out_val[r] = ((unsigned long long)(uint32_t)S.first[s] << 32) | (uint32_t)S.prev[s];
     }
 }
 
@@ -249,7 +280,9 @@ __device__ __forceinline__ bool block_culled(const float *T, const FuseArgs &A, 
 constexpr int kFrameChunk = 128;
 
 __global__ void __launch_bounds__(128) k_fuse_integrate(FuseArgs A, const unsigned long long *__restrict__ keys,
-                                                        const int32_t *__restrict__ first, int64_t n,
+                                                        const unsigned long long *__restrict__ vals, int64_t n,
+                                                        const float *__restrict__ prev_f,
+                                                        const float *__restrict__ prev_w,
                                                         int32_t *__restrict__ xyz_out, int32_t *__restrict__ first_out,
                                                         float *__restrict__ f_out, float *__restrict__ w_out,
                                                         int cull, unsigned long long *stats) {
@@ -261,13 +294,16 @@ __global__ void __launch_bounds__(128) k_fuse_integrate(FuseArgs A, const unsign
     const int32_t bx = (int32_t)((key >> 42) & 0x1FFFFF) - kCoordLim;
     const int32_t by = (int32_t)((key >> 21) & 0x1FFFFF) - kCoordLim;
     const int32_t bz = (int32_t)(key & 0x1FFFFF) - kCoordLim;
-    const int32_t k0 = first[b];
+    const unsigned long long val = vals[b];
+    const int32_t kfirst = (int32_t)(uint32_t)(val >> 32);
+    const int32_t prow = (int32_t)(uint32_t)(val & 0xFFFFFFFFull);
+    const int32_t k0 = kfirst < 0 ? 0 : kfirst;
     const int t = threadIdx.x;
     if (t == 0) {
         xyz_out[3 * b] = bx;
         xyz_out[3 * b + 1] = by;
         xyz_out[3 * b + 2] = bz;
-        if (first_out) first_out[b] = k0;
+        if (first_out) first_out[b] = kfirst;
     }
     // voxels 4t … 4t+3: x = 4(t&1) + q, y = (t>>1)&7, z = t>>4
     const int lx0 = 4 * (t & 1), ly = (t >> 1) & 7, lz = t >> 4;
@@ -281,6 +317,12 @@ __global__ void __launch_bounds__(128) k_fuse_integrate(FuseArgs A, const unsign
     const float cyg = (8.0f * (float)by + 4.0f) * A.voxel;
     const float czg = (8.0f * (float)bz + 4.0f) * A.voxel;
     float f[4] = {0.f, 0.f, 0.f, 0.f}, w[4] = {0.f, 0.f, 0.f, 0.f};
+    if (prow >= 0) {   // a block of the previous fusion continues from its (f, W) (reading F-11)
+        const float4 pf = *reinterpret_cast<const float4 *>(prev_f + (int64_t)prow * kBlockVox + 4 * t);
+        const float4 pw = *reinterpret_cast<const float4 *>(prev_w + (int64_t)prow * kBlockVox + 4 * t);
+        f[0] = pf.x; f[1] = pf.y; f[2] = pf.z; f[3] = pf.w;
+        w[0] = pw.x; w[1] = pw.y; w[2] = pw.z; w[3] = pw.w;
+    }
     const long long HW = (long long)A.H * A.W;
     unsigned n_frames = 0, n_upd = 0;
     const float Wf = (float)A.W, Hf = (float)A.H;
@@ -369,7 +411,8 @@ uint32_t fuse_table_cap(int64_t max_blocks) {
 size_t cub_sort_bytes(int64_t n) {
     size_t bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const unsigned long long *)nullptr, (unsigned long long *)nullptr,
-                                    (const int32_t *)nullptr, (int32_t *)nullptr, (int)(n > 0 ? n : 1), 0, 63);
+                                    (const unsigned long long *)nullptr, (unsigned long long *)nullptr,
+                                    (int)(n > 0 ? n : 1), 0, 63);
     return bytes;
 }
 
@@ -378,9 +421,10 @@ struct FuseLayout {
     float *poses;
     unsigned long long *keys;
     int32_t *first;
+    int32_t *prev;
     unsigned long long *count;
     unsigned long long *ckeys[2];
-    int32_t *cfirst[2];
+    unsigned long long *cval[2];
     void *sort_tmp;
     size_t sort_bytes;
     int32_t *xyz;
@@ -395,10 +439,11 @@ size_t fuse_layout(Carve &c, FuseLayout &L, int64_t max_blocks, int32_t K, int32
     L.poses = dev_poses ? nullptr : c.take<float>((size_t)K * 12);
     L.keys = c.take<unsigned long long>(cap);
     L.first = c.take<int32_t>(cap);
+    L.prev = c.take<int32_t>(cap);
     L.count = c.take<unsigned long long>(8);
     for (int q = 0; q < 2; q++) {
         L.ckeys[q] = c.take<unsigned long long>(max_blocks);
-        L.cfirst[q] = c.take<int32_t>(max_blocks);
+        L.cval[q] = c.take<unsigned long long>(max_blocks);
     }
     L.sort_bytes = cub_sort_bytes(max_blocks);
     L.sort_tmp = c.take<char>(L.sort_bytes);
@@ -441,13 +486,17 @@ extern "C" size_t vol_fuse_workspace_bytes(int64_t max_blocks, int32_t n_frames,
     return fuse_layout(c, L, max_blocks, n_frames, cam->height, cam->width, false, false, false);
 }
 
-extern "C" vol_status vol_fuse(const float *depth, int32_t n_frames, const vol_camera *cam, const float *poses,
-                               const vol_fusion_params *prm, int64_t max_blocks, void *workspace,
-                               size_t workspace_bytes, void *stream, int32_t *block_xyz, int32_t *first_frame,
-                               float *f, float *W, int64_t *n_blocks, vol_fusion_stats *stats) {
+extern "C" vol_status vol_fuse_incremental(const int32_t *prev_xyz, const float *prev_f, const float *prev_W,
+                                           int64_t n_prev, const float *depth, int32_t n_frames, const vol_camera *cam,
+                                           const float *poses, const vol_fusion_params *prm, int64_t max_blocks,
+                                           void *workspace, size_t workspace_bytes, void *stream, int32_t *block_xyz,
+                                           int32_t *first_frame, float *f, float *W, int64_t *n_blocks,
+                                           vol_fusion_stats *stats) {
     NvtxRange nvtx_range_("vol_fuse");
     vol_status st = check_fuse_args(n_frames, cam, prm, max_blocks);
     if (st != VOL_OK) return st;
+    if (n_prev < 0 || (n_prev > 0 && (!prev_xyz || !prev_f || !prev_W)))
+        return fail(VOL_EINVAL, "vol_fuse: n_prev < 0 or NULL previous arrays");
     if (!depth || !poses || !block_xyz || !f || !W || !n_blocks)
         return fail(VOL_EINVAL, "vol_fuse: depth, poses, block_xyz, f, W and n_blocks must not be NULL");
     *n_blocks = 0;
@@ -489,10 +538,40 @@ extern "C" vol_status vol_fuse(const float *depth, int32_t n_frames, const vol_c
     const uint32_t cap = fuse_table_cap(max_blocks);
     CK(cudaMemsetAsync(L.keys, 0xFF, sizeof(unsigned long long) * cap, s));
     CK(cudaMemsetAsync(L.first, 0x7F, sizeof(int32_t) * cap, s));   // 0x7F7F7F7F > any frame index
+    CK(cudaMemsetAsync(L.prev, 0xFF, sizeof(int32_t) * cap, s));    // −1: a new block
     CK(cudaMemsetAsync(L.count, 0, sizeof(unsigned long long) * 8, s));
     FuseArgs A{d_depth, d_poses, K, H, Wd, cam->fx, cam->fy, cam->cx, cam->cy,
                prm->voxel, prm->mu, prm->max_range, prm->w_max};
-    FuseSet S{L.keys, L.first, L.count, cap - 1, (unsigned long long)max_blocks};
+    FuseSet S{L.keys, L.first, L.count, cap - 1, (unsigned long long)max_blocks, L.prev};
+    // previous blocks (reading F-11), staged to the device if they are host arrays
+    const int32_t *d_pxyz = prev_xyz;
+    const float *d_pf = prev_f, *d_pw = prev_W;
+    struct Stage {
+        void *p = nullptr;
+        cudaStream_t s;
+        ~Stage() {
+            if (p) cudaFreeAsync(p, s);
+        }
+    } pstage{nullptr, s};
+    if (n_prev > 0) {
+        if (n_prev > max_blocks) return fail(VOL_ENOMEM, "vol_fuse: n_prev = %lld > max_blocks", (long long)n_prev);
+        if (!(is_device_ptr(prev_xyz) && is_device_ptr(prev_f) && is_device_ptr(prev_W))) {
+            const size_t bx = (size_t)n_prev * 12, bf = (size_t)n_prev * kBlockVox * 4;
+            CK(cudaMallocAsync(&pstage.p, bx + 2 * bf + 512, s));
+            char *base = (char *)pstage.p;
+            float *sf = (float *)(base + ((bx + 255) & ~(size_t)255));
+            float *sw = sf + (size_t)n_prev * kBlockVox;
+            CK(cudaMemcpyAsync(base, prev_xyz, bx, cudaMemcpyDefault, s));
+            CK(cudaMemcpyAsync(sf, prev_f, bf, cudaMemcpyDefault, s));
+            CK(cudaMemcpyAsync(sw, prev_W, bf, cudaMemcpyDefault, s));
+            d_pxyz = (const int32_t *)base;
+            d_pf = sf;
+            d_pw = sw;
+        }
+        k_fuse_seed<<<(unsigned)((n_prev + 255) / 256), 256, 0, s>>>(d_pxyz, n_prev, S);
+        CK(cudaPeekAtLastError());
+        counted(1);
+    }
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -525,6 +604,7 @@ extern "C" vol_status vol_fuse(const float *depth, int32_t n_frames, const vol_c
         stats->pixels_valid = (int64_t)hc[3];
         stats->blocks = (int64_t)hc[0];
     }
+    if (hc[1] & 4ull) return fail(VOL_EDATA, "vol_fuse: the previous blocks repeat a block coordinate");
     if (hc[1] & 2ull)
         return fail(VOL_EDATA, "vol_fuse: a block walk leaves the block-coordinate range (-2^20, 2^20) or is longer "
                                "than %d blocks (check poses, voxel size and max_range)", kWalkMax);
@@ -534,12 +614,12 @@ extern "C" vol_status vol_fuse(const float *depth, int32_t n_frames, const vol_c
     const int64_t n = (int64_t)hc[0];
     if (n == 0) return VOL_OK;
     CK(cudaMemsetAsync(L.count + 2, 0, sizeof(unsigned long long), s));
-    k_fuse_compact<<<(cap + 255) / 256, 256, 0, s>>>(S, cap, L.ckeys[0], L.cfirst[0], L.count + 2,
+    k_fuse_compact<<<(cap + 255) / 256, 256, 0, s>>>(S, cap, L.ckeys[0], L.cval[0], L.count + 2,
                                                       (unsigned long long)max_blocks);
     CK(cudaPeekAtLastError());
     counted(1);
     size_t sb = L.sort_bytes;
-    CK(cub::DeviceRadixSort::SortPairs(L.sort_tmp, sb, L.ckeys[0], L.ckeys[1], L.cfirst[0], L.cfirst[1], (int)n, 0, 63,
+    CK(cub::DeviceRadixSort::SortPairs(L.sort_tmp, sb, L.ckeys[0], L.ckeys[1], L.cval[0], L.cval[1], (int)n, 0, 63,
                                        s));   // library sort (CUB): not counted as this library's launches
     int32_t *oxyz = dev_out ? block_xyz : L.xyz;
     int32_t *ofirst = dev_out ? first_frame : (first_frame ? L.ofirst : nullptr);
@@ -547,7 +627,7 @@ extern "C" vol_status vol_fuse(const float *depth, int32_t n_frames, const vol_c
     float *ow = dev_out ? W : L.w;
     const int cull = getenv("HVG_FUSE_NOCULL") ? 0 : 1;   // experiments only: the cull never changes results
     if (stats) CK(cudaEventRecord(ev[2], s));
-    k_fuse_integrate<<<(unsigned)n, 128, 0, s>>>(A, L.ckeys[1], L.cfirst[1], n, oxyz, ofirst, of, ow, cull,
+    k_fuse_integrate<<<(unsigned)n, 128, 0, s>>>(A, L.ckeys[1], L.cval[1], n, d_pf, d_pw, oxyz, ofirst, of, ow, cull,
                                                   L.count + 4);
     CK(cudaPeekAtLastError());
     counted(1);
@@ -569,4 +649,12 @@ extern "C" vol_status vol_fuse(const float *depth, int32_t n_frames, const vol_c
     }
     if (owns || !dev_out) CK(cudaStreamSynchronize(s));
     return VOL_OK;
+}
+
+extern "C" vol_status vol_fuse(const float *depth, int32_t n_frames, const vol_camera *cam, const float *poses,
+                               const vol_fusion_params *prm, int64_t max_blocks, void *workspace,
+                               size_t workspace_bytes, void *stream, int32_t *block_xyz, int32_t *first_frame,
+                               float *f, float *W, int64_t *n_blocks, vol_fusion_stats *stats) {
+    return vol_fuse_incremental(nullptr, nullptr, nullptr, 0, depth, n_frames, cam, poses, prm, max_blocks, workspace,
+                                workspace_bytes, stream, block_xyz, first_frame, f, W, n_blocks, stats);
 }

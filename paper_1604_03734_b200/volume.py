@@ -260,14 +260,15 @@ class Volume:
 # -- TSDF fusion (paper §III-A, Eq. 1) -----------------------------------------
 
 def fuse(depth, poses, intr, voxel: float, mu: float, max_range: float, w_max: float, *, max_blocks=None,
-         stream=None, return_first=True, stats=None):
+         stream=None, return_first=True, stats=None, prev=None):
     """Fuse K posed depth maps into hashed voxel blocks on the GPU (``vol_fuse``).
 
     depth [K, H, W] float32 metres, poses [K, 12] float32 row-major T_gc (camera-to-global), intr
     (fx, fy, cx, cy).  Returns CUDA tensors (coords int32 [n, 3] sorted by (x, y, z), first frame
     int32 [n], f float32 [n, 512], W float32 [n, 512]) — ready for :class:`Volume`.  Pass a dict as
     `stats` to receive the call's counters (pixels_valid, blocks, block_frames, voxel_updates; this
-    synchronises the stream).
+    synchronises the stream).  `prev` = (coords, f, W) of an earlier fusion continues it with the new depth
+    maps (vol_fuse_incremental, reading F-11): the result equals fusing all frames in one call.
     """
     _require_cuda()
     L = N.lib()
@@ -285,7 +286,15 @@ def fuse(depth, poses, intr, voxel: float, mu: float, max_range: float, w_max: f
     cam = N.vol_camera(it[0], it[1], it[2], it[3], Wd, H)
     prm = N.vol_fusion_params(float(voxel), float(mu), float(max_range), float(w_max))
     s = torch.cuda.current_stream(dev) if stream is None else stream
-    cap = int(max_blocks) if max_blocks else 65536
+    if prev is not None:
+        pxyz = _as(prev[0], torch.int32, np.int32)
+        pf = _as(prev[1], torch.float32, np.float32)
+        pW = _as(prev[2], torch.float32, np.float32)
+        n_prev = int(pxyz.shape[0])
+        (pxp, pxk), (pfp, pfk), (pwp, pwk) = _ptr(pxyz), _ptr(pf), _ptr(pW)
+    else:
+        n_prev, pxp, pfp, pwp = 0, None, None, None
+    cap = int(max_blocks) if max_blocks else max(65536, 2 * n_prev)
     while True:
         xyz = torch.empty(cap, 3, dtype=torch.int32, device=dev)
         first = torch.empty(cap, dtype=torch.int32, device=dev)
@@ -295,7 +304,8 @@ def fuse(depth, poses, intr, voxel: float, mu: float, max_range: float, w_max: f
         ws = torch.empty(int(nbytes), dtype=torch.uint8, device=dev)
         n = ctypes.c_int64()
         sts = N.vol_fusion_stats()
-        st = L.vol_fuse(ctypes.c_void_p(depth.data_ptr()), K, ctypes.byref(cam), ctypes.c_void_p(poses.data_ptr()),
+        st = L.vol_fuse_incremental(pxp, pfp, pwp, n_prev, ctypes.c_void_p(depth.data_ptr()), K, ctypes.byref(cam),
+                        ctypes.c_void_p(poses.data_ptr()),
                         ctypes.byref(prm), cap, ctypes.c_void_p(ws.data_ptr()), nbytes, ctypes.c_void_p(s.cuda_stream),
                         ctypes.c_void_p(xyz.data_ptr()), ctypes.c_void_p(first.data_ptr()),
                         ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(W.data_ptr()), ctypes.byref(n),

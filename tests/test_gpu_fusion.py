@@ -220,3 +220,26 @@ def test_edge_cases_bit_exact(fuse):
     D[3, :, :10] = 0.1                               # < μ: band starts at the camera
     args = (D, INTR, P, 0.05, 0.3, 6.0, 1.0)
     _same(_gpu(fuse, *args), oracle.fuse(*args))
+
+
+@pytest.mark.parametrize("k", [1, 4])
+def test_incremental_equals_batch_bit_exact(fuse, k):
+    """vol_fuse_incremental (reading F-11): frames 0..k−1, then k..K−1 continued from those blocks, equals
+    the one-call fusion of all frames and the oracle's incremental fusion, bit for bit."""
+    ds = sphere_depth()
+    D, P, I = ds.depth.cuda(), ds.poses.cuda(), ds.intr.numpy()
+    prm = (ds.voxel, ds.mu, ds.max_range, ds.w_max)
+    xa, fa, f_all, W_all = fuse(D, P, I, *prm)
+    x1, _, f1, W1 = fuse(D[:k], P[:k], I, *prm)
+    x2, fr2, f2, W2 = fuse(D[k:], P[k:], I, *prm, prev=(x1, f1, W1))
+    assert torch.equal(x2, xa) and torch.equal(f2, f_all) and torch.equal(W2, W_all)
+    xo, fro, fo, Wo = oracle.fuse_incremental((x1.cpu().numpy(), f1.cpu().numpy(), W1.cpu().numpy()),
+                                              ds.depth[k:], I, ds.poses[k:], *prm)
+    _same((x2.cpu().numpy(), fr2.cpu().numpy(), f2.cpu().numpy(), W2.cpu().numpy()), (xo, fro, fo, Wo))
+    # host-resident previous blocks take the staging path
+    x3, fr3, f3, W3 = fuse(D[k:], P[k:], I, *prm, prev=(x1.cpu(), f1.cpu(), W1.cpu()))
+    assert torch.equal(f3, f2) and torch.equal(fr3, fr2)
+    from paper_1604_03734_b200._native import VolError, VOL_EDATA
+    with pytest.raises(VolError) as e:
+        fuse(D[k:], P[k:], I, *prm, prev=(torch.cat([x1, x1[:1]]), torch.cat([f1, f1[:1]]), torch.cat([W1, W1[:1]])))
+    assert e.value.status == VOL_EDATA
