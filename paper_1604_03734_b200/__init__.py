@@ -4,6 +4,7 @@ The product path is libvol.so (C ABI in include/vol.h, CUDA kernels for sm_100a 
 this package is its thin Python binding.  It never imports the CPU oracle and has no CPU fallback.
 """
 from . import stereo  # noqa: F401
+from .stream import Reconstruction  # noqa: F401
 from .volume import Volume, block_hash, connect_group, fuse, group_energy, nccl_unique_id, plan_shard, regularise_group  # noqa: F401
 
-__all__ = ["Volume", "fuse", "block_hash", "plan_shard", "nccl_unique_id", "connect_group", "regularise_group", "group_energy"]
+__all__ = ["Volume", "fuse", "Reconstruction", "block_hash", "plan_shard", "nccl_unique_id", "connect_group", "regularise_group", "group_energy"]

@@ -195,13 +195,15 @@ class Volume:
         N.check(self._lib.vol_energy(self._h, lam, eps, data_term, ctypes.byref(P), ctypes.byref(D)))
         return P.value, D.value
 
-    def state(self):
-        """(u, ū, p[3]) as CPU tensors."""
-        u = torch.empty(self.n_local, 512)
-        ub = torch.empty(self.n_local, 512)
-        p = torch.empty(3, self.n_local, 512)
+    def state(self, device="cpu"):
+        """(u, ū, p[3]) in the caller's block order, as tensors on `device` (CPU by default)."""
+        u = torch.empty(self.n_local, 512, device=device)
+        ub = torch.empty(self.n_local, 512, device=device)
+        p = torch.empty(3, self.n_local, 512, device=device)
         N.check(self._lib.vol_read_state(self._h, ctypes.c_void_p(u.data_ptr()), ctypes.c_void_p(ub.data_ptr()),
                                          ctypes.c_void_p(p.data_ptr())))
+        if u.device.type == "cuda":
+            self.sync()
         return u, ub, p
 
     def load_state(self, u, ub, p):
