@@ -45,8 +45,9 @@ def fuse_dense(depth, intr, poses, voxel, mu, max_range, w_max, lo, hi):
         zs = np.where(front, zc, F(1))
         # step 2: nearest pixel
         with np.errstate(over="ignore", invalid="ignore"):
-            ix = fx * (xc / zs) + cx
-            iy = fy * (yc / zs) + cy
+            rz = F(1) / zs                              # reading F-12: one reciprocal of z_c
+            ix = fx * (xc * rz) + cx
+            iy = fy * (yc * rz) + cy
             fi = np.floor(ix + F(0.5))
             fj = np.floor(iy + F(0.5))
         inside = front & (fi >= 0) & (fi < F(Wd)) & (fj >= 0) & (fj < F(H))
@@ -58,7 +59,7 @@ def fuse_dense(depth, intr, poses, voxel, mu, max_range, w_max, lo, hi):
         sdf = np.where(valid, d, F(0)) - zc
         # step 4, Eq. 1
         upd = valid & (sdf >= -mu)
-        tsdf = np.minimum(np.maximum(sdf, -mu), mu) / mu
+        tsdf = np.minimum(np.maximum(sdf, -mu), mu) * (F(1) / mu)
         fn = (tsdf + w * f) / (w + F(1))
         wn = np.minimum(w + F(1), wmax)
         f = np.where(upd, fn, f).astype(F)

@@ -24,7 +24,8 @@
  *                  f = (u_TSDF + w·f)/(w + 1), w = min(w + 1, w_max) (F-4); else unchanged.
  *
  * Every floating-point decision (pixel choice, block walk) and every value is evaluated in IEEE
- * fp32 in the order written here (reading F-10, "where floating point decides an integer, both sides
+ * fp32 in the order written here; divisions by per-call constants (1/fx, 1/fy, 1/Bm, 1/μ) and the two
+ * divisions by z_c are products with a correctly rounded reciprocal (reading F-12) (reading F-10, "where floating point decides an integer, both sides
  * take that decision in the same precision"); compile with -ffp-contract=off.
  */
 #include <math.h>
@@ -42,7 +43,7 @@ int orc_tsdf_update(float *f, float *w, float sdf, float mu, float w_max)
     float c = sdf;
     if (c < -mu) c = -mu;
     if (c > mu) c = mu;
-    float tsdf = c / mu;                             /* reading F-3: u_TSDF in [−1, 1]       */
+    float tsdf = c * (1.0f / mu);                    /* reading F-3 (F-12: ·fl(1/μ)), in [−1, 1] */
     float num = tsdf + (*w) * (*f);                  /* u_TSDF + w_{k−1} f_{k−1}              */
     float den = (*w) + 1.0f;                         /* w_{k−1} + 1                           */
     *f = num / den;
@@ -70,8 +71,9 @@ int orc_project(const float *pose, const float *intr, int32_t H, int32_t Wd, flo
     float yc = (pose[1] * d0 + pose[5] * d1) + pose[9] * d2;
     float zc = (pose[2] * d0 + pose[6] * d1) + pose[10] * d2;
     if (!(zc > 0.0f)) return 0;
-    float a = xc / zc;
-    float b = yc / zc;
+    float rz = 1.0f / zc;                            /* reading F-12: one reciprocal of z_c  */
+    float a = xc * rz;
+    float b = yc * rz;
     float ix = intr[0] * a + intr[2];
     float iy = intr[1] * b + intr[3];
     float fi = floorf(ix + 0.5f);
@@ -87,8 +89,8 @@ int orc_project(const float *pose, const float *intr, int32_t H, int32_t Wd, flo
  * p_c = ((i − cx)/fx · z, (j − cy)/fy · z, z);  p_g = R p_c + t (row sums left to right).        */
 static void ray_point(const float *pose, const float *intr, int32_t i, int32_t j, float z, float *g)
 {
-    float xc = (((float)i - intr[2]) / intr[0]) * z;
-    float yc = (((float)j - intr[3]) / intr[1]) * z;
+    float xc = (((float)i - intr[2]) * (1.0f / intr[0])) * z;   /* reading F-12: ·fl(1/fx) */
+    float yc = (((float)j - intr[3]) * (1.0f / intr[1])) * z;
     float zc = z;
     for (int r = 0; r < 3; r++) g[r] = ((pose[4 * r + 0] * xc + pose[4 * r + 1] * yc) + pose[4 * r + 2] * zc) + pose[4 * r + 3];
 }
@@ -96,7 +98,7 @@ static void ray_point(const float *pose, const float *intr, int32_t i, int32_t j
 /* ------------------------------------------------------------------ block walk (reading F-7) */
 
 /* 6-connected lattice walk from the block of point a to the block of point b (points in metres,
- * block edge Bm metres).  s = p / Bm; start cell floor(s_a), end cell floor(s_b); per axis
+ * block edge Bm metres).  s = p·fl(1/Bm) (F-12); start cell floor(s_a), end cell floor(s_b); per axis
  * dir = s_b − s_a, tMax = distance in t to the first face crossing, tDelta = 1/|dir|; each step
  * advances the axis with remaining steps and the smallest tMax (ties: lowest axis), exactly
  * |Δcell|_1 steps.  Writes up to max_cells cells [.][3]; returns the number of cells of the walk. */
@@ -104,9 +106,10 @@ int64_t orc_block_walk(const float *a, const float *b, float Bm, int32_t *cells,
 {
     float sa[3], sb[3], tmax[3], tdel[3];
     int64_t c[3], n[3], step[3];
+    const float inv = 1.0f / Bm;                     /* reading F-12: s = p·fl(1/Bm) */
     for (int k = 0; k < 3; k++) {
-        sa[k] = a[k] / Bm;
-        sb[k] = b[k] / Bm;
+        sa[k] = a[k] * inv;
+        sb[k] = b[k] * inv;
         float fa = floorf(sa[k]);
         float fb = floorf(sb[k]);
         c[k] = (int64_t)fa;
@@ -115,11 +118,11 @@ int64_t orc_block_walk(const float *a, const float *b, float Bm, int32_t *cells,
         if (dir > 0.0f) {
             step[k] = 1;
             tdel[k] = 1.0f / dir;
-            tmax[k] = ((fa + 1.0f) - sa[k]) / dir;
+            tmax[k] = ((fa + 1.0f) - sa[k]) * tdel[k];
         } else if (dir < 0.0f) {
             step[k] = -1;
             tdel[k] = 1.0f / (-dir);
-            tmax[k] = (sa[k] - fa) / (-dir);
+            tmax[k] = (sa[k] - fa) * tdel[k];
         } else {
             step[k] = 0;
             tdel[k] = INFINITY;

@@ -140,10 +140,10 @@ __device__ __forceinline__ void ray_point(const float *T, float xr, float yr, fl
 
 // One axis of the reading F-7 walk set-up.  tMax and tDelta are only ever read for an axis with
 // remaining steps (n > 0), so they are computed only then (n > 0 implies dir != 0).
-__device__ __forceinline__ void walk_axis(float a, float b, float Bm, int32_t &c, int32_t &n, int32_t &step,
+__device__ __forceinline__ void walk_axis(float a, float b, float inv_bm, int32_t &c, int32_t &n, int32_t &step,
                                           float &tmax, float &tdel) {
-    const float sa = __fdiv_rn(a, Bm);
-    const float sb = __fdiv_rn(b, Bm);
+    const float sa = __fmul_rn(a, inv_bm);   // reading F-12: s = p·fl(1/Bm)
+    const float sb = __fmul_rn(b, inv_bm);
     const float fa = floorf(sa);
     const float fb = floorf(sb);
     // coordinates far outside the packable range are clamped here and rejected by set_insert
@@ -159,10 +159,10 @@ __device__ __forceinline__ void walk_axis(float a, float b, float Bm, int32_t &c
         const float dir = __fsub_rn(sb, sa);
         if (dir > 0.0f) {
             tdel = __fdiv_rn(1.0f, dir);
-            tmax = __fdiv_rn(__fsub_rn(__fadd_rn(fa, 1.0f), sa), dir);
+            tmax = __fmul_rn(__fsub_rn(__fadd_rn(fa, 1.0f), sa), tdel);
         } else {
             tdel = __fdiv_rn(1.0f, -dir);
-            tmax = __fdiv_rn(__fsub_rn(sa, fa), -dir);
+            tmax = __fmul_rn(__fsub_rn(sa, fa), tdel);
         }
     }
 }
@@ -182,7 +182,8 @@ template <class IDX>
 __global__ void __launch_bounds__(256) k_fuse_alloc(FuseArgs A, FuseSet S) {
     const IDX HW = (IDX)A.H * (IDX)A.W;
     const IDX total = HW * (IDX)A.K;
-    const float Bm = __fmul_rn(8.0f, A.voxel);
+    const float inv_bm = __fdiv_rn(1.0f, __fmul_rn(8.0f, A.voxel));   // fl(1/Bm), Bm = fl(8v)
+    const float inv_fx = __fdiv_rn(1.0f, A.fx), inv_fy = __fdiv_rn(1.0f, A.fy);
     unsigned long long n_valid = 0;
     for (IDX pix = (IDX)blockIdx.x * blockDim.x + threadIdx.x; pix < total; pix += (IDX)gridDim.x * blockDim.x) {
         const float d = __ldg(A.depth + pix);
@@ -198,16 +199,16 @@ __global__ void __launch_bounds__(256) k_fuse_alloc(FuseArgs A, FuseSet S) {
         float za = __fsub_rn(d, A.mu);
         if (za < 0.0f) za = 0.0f;
         const float zb = __fadd_rn(d, A.mu);
-        const float xr = __fdiv_rn(__fsub_rn((float)i, A.cx), A.fx);
-        const float yr = __fdiv_rn(__fsub_rn((float)j, A.cy), A.fy);
+        const float xr = __fmul_rn(__fsub_rn((float)i, A.cx), inv_fx);   // reading F-12
+        const float yr = __fmul_rn(__fsub_rn((float)j, A.cy), inv_fy);
         float ax, ay, az, bx, by, bz;
         ray_point(T, xr, yr, za, ax, ay, az);
         ray_point(T, xr, yr, zb, bx, by, bz);
         int32_t cx_, cy_, cz_, nx, ny, nz, sx, sy, sz;
         float tx, ty, tz, dx, dy, dz;
-        walk_axis(ax, bx, Bm, cx_, nx, sx, tx, dx);
-        walk_axis(ay, by, Bm, cy_, ny, sy, ty, dy);
-        walk_axis(az, bz, Bm, cz_, nz, sz, tz, dz);
+        walk_axis(ax, bx, inv_bm, cx_, nx, sx, tx, dx);
+        walk_axis(ay, by, inv_bm, cy_, ny, sy, ty, dy);
+        walk_axis(az, bz, inv_bm, cz_, nz, sz, tz, dz);
         if (nx + ny + nz + 1 > kWalkMax) {
             atomicOr(&S.count[1], 2ull);
             continue;
@@ -326,6 +327,7 @@ __global__ void __launch_bounds__(128) k_fuse_integrate(FuseArgs A, const unsign
     const long long HW = (long long)A.H * A.W;
     unsigned n_frames = 0, n_upd = 0;
     const float Wf = (float)A.W, Hf = (float)A.H;
+    const float inv_mu = __fdiv_rn(1.0f, A.mu);
     for (int32_t kb = k0; kb < A.K; kb += kFrameChunk) {
         {
             const int32_t k = kb + t;
@@ -365,8 +367,9 @@ __global__ void __launch_bounds__(128) k_fuse_integrate(FuseArgs A, const unsign
                     const float zc = __fadd_rn(__fadd_rn(__fmul_rn(r0.z, d0), e1z), e2z);
                     if (!(zc > 0.0f)) continue;
                     // step 2: nearest pixel (reading F-1)
-                    const float ix = __fadd_rn(__fmul_rn(A.fx, __fdiv_rn(xc, zc)), A.cx);
-                    const float iy = __fadd_rn(__fmul_rn(A.fy, __fdiv_rn(yc, zc)), A.cy);
+                    const float rz = __fdiv_rn(1.0f, zc);   // reading F-12: one reciprocal of z_c
+                    const float ix = __fadd_rn(__fmul_rn(A.fx, __fmul_rn(xc, rz)), A.cx);
+                    const float iy = __fadd_rn(__fmul_rn(A.fy, __fmul_rn(yc, rz)), A.cy);
                     const float fi = floorf(__fadd_rn(ix, 0.5f));
                     const float fj = floorf(__fadd_rn(iy, 0.5f));
                     if (!(fi >= 0.0f && fi < Wf && fj >= 0.0f && fj < Hf)) continue;
@@ -376,7 +379,7 @@ __global__ void __launch_bounds__(128) k_fuse_integrate(FuseArgs A, const unsign
                     const float sdf = __fsub_rn(d, zc);
                     if (sdf < -A.mu) continue;
                     const float c = fminf(fmaxf(sdf, -A.mu), A.mu);
-                    const float tsdf = __fdiv_rn(c, A.mu);
+                    const float tsdf = __fmul_rn(c, inv_mu);   // reading F-12: ·fl(1/μ)
                     const float num = __fadd_rn(tsdf, __fmul_rn(w[q], f[q]));
                     const float den = __fadd_rn(w[q], 1.0f);
                     f[q] = __fdiv_rn(num, den);
