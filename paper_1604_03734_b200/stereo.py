@@ -20,8 +20,12 @@ def params(width, height, **kw) -> N.vol_stereo_params:
     p = N.vol_stereo_params()
     N.lib().vol_stereo_default_params(ctypes.byref(p))
     p.width, p.height = int(width), int(height)
+    names = {name for name, _ in N.vol_stereo_params._fields_}
     for k, v in kw.items():
-        setattr(p, "lam" if k == "lam" else k, v)
+        k = "lam" if k == "lambda_" else k
+        if k not in names:
+            raise TypeError(f"unknown stereo parameter {k!r} (known: {sorted(names - {'width', 'height'})})")
+        setattr(p, k, v)
     return p
 
 
