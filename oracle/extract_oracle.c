@@ -23,7 +23,13 @@
  *   X-5 triangles 1 inside corner a (or 1 outside, orientation reversed) → triangle (E_ab, E_ac, E_ad);
  *                 2 inside a, b → (E_ac, E_ad, E_bd), (E_ac, E_bd, E_bc); with (a, b, c, d) a
  *                 positively oriented ordering of the tet — normals point toward u > 0 (free space);
- *   X-6 degenerate a triangle with two bit-identical vertices is dropped ("no degenerate");
+ *   X-6 degenerate a triangle whose area is zero in exact arithmetic is dropped ("no
+ *                 degenerate"): an edge vertex lies on its outside corner iff that corner's value is
+ *                 exactly 0 (the inside value is < 0), so two vertices coincide iff they share an
+ *                 outside corner of value 0 — the 1-outside triangle when that corner is 0, the quad's
+ *                 (E_ac, E_ad, E_bd) when u_d = 0 and (E_ac, E_bd, E_bc) when u_c = 0; the 1-inside
+ *                 triangle never degenerates.  A decision on the corner values alone, not on rounded
+ *                 vertices;
  *   X-7 order     blocks in caller order, cells in voxel order (x fastest), tets in X-2 order,
  *                 triangles in X-5 order.  Output: float [m][3][3] triangle soup (S:325 allows
  *                 duplicated seam vertices).
@@ -88,11 +94,10 @@ static void edge_vertex(const int64_t gi[3], float ui, const int64_t gj[3], floa
     }
 }
 
-static int same3(const float *a, const float *b) { return a[0] == b[0] && a[1] == b[1] && a[2] == b[2]; }
-
-static int64_t emit(float *out, int64_t m, int64_t max, const float *p0, const float *p1, const float *p2)
+static int64_t emit(float *out, int64_t m, int64_t max, const float *p0, const float *p1, const float *p2,
+                    int degenerate)
 {
-    if (same3(p0, p1) || same3(p1, p2) || same3(p0, p2)) return m;    /* X-6 */
+    if (degenerate) return m;    /* X-6 */
     if (out && m < max) {
         memcpy(out + 9 * m, p0, 3 * sizeof(float));
         memcpy(out + 9 * m + 3, p1, 3 * sizeof(float));
@@ -174,15 +179,17 @@ int64_t orc_extract(const int32_t *xyz, int64_t n, const float *u, const float *
                     edge_vertex(g[a], val[a], g[bb], val[bb], voxel, e1);
                     edge_vertex(g[a], val[a], g[c], val[c], voxel, e2);
                     edge_vertex(g[a], val[a], g[d], val[d], voxel, e3);
-                    if (!flip) m = emit(out, m, max_tris, e1, e2, e3);
-                    else m = emit(out, m, max_tris, e1, e3, e2);
+                    /* 1 inside: never degenerate; 1 outside (a): all three vertices at a iff u_a = 0 */
+                    int deg = flip && val[a] == 0.0f;
+                    if (!flip) m = emit(out, m, max_tris, e1, e2, e3, deg);
+                    else m = emit(out, m, max_tris, e1, e3, e2, deg);
                 } else {
                     edge_vertex(g[a], val[a], g[c], val[c], voxel, e1);   /* E_ac */
                     edge_vertex(g[a], val[a], g[d], val[d], voxel, e2);   /* E_ad */
                     edge_vertex(g[bb], val[bb], g[d], val[d], voxel, e3); /* E_bd */
                     edge_vertex(g[bb], val[bb], g[c], val[c], voxel, e4); /* E_bc */
-                    m = emit(out, m, max_tris, e1, e2, e3);
-                    m = emit(out, m, max_tris, e1, e3, e4);
+                    m = emit(out, m, max_tris, e1, e2, e3, val[d] == 0.0f);   /* E_ad = E_bd iff u_d = 0 */
+                    m = emit(out, m, max_tris, e1, e3, e4, val[c] == 0.0f);   /* E_ac = E_bc iff u_c = 0 */
                 }
             }
         }
