@@ -57,13 +57,12 @@ __device__ __forceinline__ void edge_vertex(int ox, int oy, int oz, int ca, floa
     }
 }
 
-__device__ __forceinline__ bool same3(const float *a, const float *b) {
-    return a[0] == b[0] && a[1] == b[1] && a[2] == b[2];
-}
-
+// X-6: a triangle is dropped iff its area is zero in exact arithmetic, decided on the corner values (an
+// edge vertex sits on its outside corner iff that corner's value is exactly 0), never on rounded vertices.
 template <bool EMIT>
-__device__ __forceinline__ void put(float *out, unsigned &m, const float *p0, const float *p1, const float *p2) {
-    if (same3(p0, p1) || same3(p1, p2) || same3(p0, p2)) return;   // X-6
+__device__ __forceinline__ void put(float *out, unsigned &m, const float *p0, const float *p1, const float *p2,
+                                    bool degenerate) {
+    if (degenerate) return;   // X-6
     if (EMIT) {
         float *o = out + 9ull * m;
 #pragma unroll
@@ -123,16 +122,17 @@ __device__ __forceinline__ void tet(int k0, int k1, int k2, int k3, float v0, fl
         edge_vertex(ox, oy, oz, ca, ua, cb, ub, voxel, e1);
         edge_vertex(ox, oy, oz, ca, ua, cc, uc, voxel, e2);
         edge_vertex(ox, oy, oz, ca, ua, cd, ud, voxel, e3);
-        if (nin == 1) put<EMIT>(out, m, e1, e2, e3);
-        else put<EMIT>(out, m, e1, e3, e2);
+        // 1 inside: never degenerate; 1 outside (a): all three vertices sit on a iff u_a = 0
+        if (nin == 1) put<EMIT>(out, m, e1, e2, e3, false);
+        else put<EMIT>(out, m, e1, e3, e2, ua == 0.0f);
     } else {
         float e4[3];
         edge_vertex(ox, oy, oz, ca, ua, cc, uc, voxel, e1);   // E_ac
         edge_vertex(ox, oy, oz, ca, ua, cd, ud, voxel, e2);   // E_ad
         edge_vertex(ox, oy, oz, cb, ub, cd, ud, voxel, e3);   // E_bd
         edge_vertex(ox, oy, oz, cb, ub, cc, uc, voxel, e4);   // E_bc
-        put<EMIT>(out, m, e1, e2, e3);
-        put<EMIT>(out, m, e1, e3, e4);
+        put<EMIT>(out, m, e1, e2, e3, ud == 0.0f);   // E_ad = E_bd iff u_d = 0
+        put<EMIT>(out, m, e1, e3, e4, uc == 0.0f);   // E_ac = E_bc iff u_c = 0
     }
 }
 
