@@ -62,6 +62,7 @@ struct IterParams {
     float theta;     // θ
     float kappa;     // fl(1 / fl(1 + σ·ε)) (Huber damping factor, reading c-18)
     int data_term;   // 0 L1, 1 L2
+    float one;       // 1.0f, as a runtime value: the paired sums a + b = fma(a, one, b) (see iterate.cu)
 };
 
 // Iteration launchers (return the number of kernel launches, or -1 on a launch error).

@@ -467,6 +467,7 @@ vol_status vol_regularise_prepare(vol_s *v, float lambda, float eps, float tau, 
     P.kappa = kp;
     P.theta = o.theta;
     P.data_term = o.data_term;
+    P.one = 1.0f;
     v->pending_kernel = o.kernel;
     v->last_launches = 0;
     if (!o.resume) {
