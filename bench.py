@@ -568,6 +568,10 @@ def main():
     if traffic:
         roofline["dram_gbs_actual"] = traffic / (it_ms / 1e3) / 1e9
         roofline["dram_frac_actual"] = roofline["dram_gbs_actual"] / peak
+    if args.freeze:
+        roofline["note"] = ("achieved counts SURVEY 8(d)'s 48 B per allocated voxel-iteration; with opts.freeze the kernel "
+                            "does not rewrite u/u-bar of frozen voxels (bit-identical result), so frac can exceed 1 - "
+                            "dram_frac_actual is the physical DRAM throughput, no_freeze the full-traffic run")
     if nf:
         nf_ach = ALG_BYTES_PER_VOXEL * n_local_vox / (nf["avg_launch_ms"] / 1e3) / 1e9
         nf.update({"achieved": nf_ach, "frac": nf_ach / peak})
