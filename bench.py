@@ -358,7 +358,17 @@ def pipeline_leg(args, dev):
 
 # ------------------------------------------------------------------------------ CPU oracle timing
 
-def time_oracle(scene, iters: int):
+def platform_cpu() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown CPU"
+
+
+def time_oracle(scene, iters: int, omp: bool = False):
     import numpy as np
 
     import oracle
@@ -366,7 +376,7 @@ def time_oracle(scene, iters: int):
     nbr = oracle.neighbours(coords)
     t0 = time.perf_counter()
     oracle.regularise(coords, f, W, scene.lam, scene.eps, scene.tau, scene.sigma, iters, theta=scene.theta,
-                      data_term=scene.data_term, init=scene.init, precision="f64", nbr=nbr)
+                      data_term=scene.data_term, init=scene.init, precision="f64", nbr=nbr, omp=omp)
     dt = time.perf_counter() - t0
     del np
     return dt
@@ -586,6 +596,20 @@ def main():
         cpu = {"value": sc.n_alloc * k / t, "unit": "voxel-updates/s", "cores": 1, "kind": "oracle",
                "sample": f"{k} fp64 oracle iteration(s) over the whole {scene.name} volume ({sc.n_alloc} voxels), "
                          f"{t:.1f} s on one host core"}
+    cpu_omp = None
+    if not args.no_cpu_baseline and world == 1:
+        # the same oracle with its phase loops over all host cores (OpenMP timing build,
+        # bitwise the plain oracle); a bounded sample like the single-core figure
+        sc = scene.to("cpu")
+        threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+        k = 1
+        t = time_oracle(sc, k, omp=True)
+        if t < 5.0:
+            k = max(1, int(10.0 / max(t, 1e-3)))
+            t = time_oracle(sc, k, omp=True)
+        cpu_omp = {"value": sc.n_alloc * k / t, "unit": "voxel-updates/s", "cores": threads, "kind": "oracle (OpenMP)",
+                   "sample": f"{k} fp64 oracle iteration(s) over the whole {scene.name} volume, {t:.1f} s on "
+                             f"{threads} host threads ({platform_cpu()})"}
     line = {
         "metric": "voxel-updates/s", "value": value, "unit": "voxel-updates/s", "n_gpus": world,
         "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
@@ -597,7 +621,7 @@ def main():
                    "l2": f"inputs larger than L2 ({n_alloc_total * 48 / 1e9:.2f} GB of state vs 126 MB L2)",
                    "parallelism": f"route-axis shards x{world}" if sharded else "single GPU",
                    "energy": {"primal": E[0], "dual": E[1]}},
-        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+        "roofline": roofline, "cpu_baseline": cpu, "cpu_baseline_omp": cpu_omp, "e2e": e2e, "gpu_launches": int(launches),
         "freeze": bool(args.freeze), "no_freeze": nf,
         "clocks": clk, "fusion": fusion, "extraction": extraction, "stereo": stereo_res, "pipeline": pipeline,
     }

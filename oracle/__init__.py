@@ -53,72 +53,97 @@ def build(force: bool = False) -> str:
     return _SO
 
 
+_SO_OMP = os.path.join(_HERE, "liboracle_omp.so")
+
+
+def build_omp(force: bool = False) -> str:
+    """The same sources with -fopenmp (ORC_PAR loops over all host cores): a TIMING build for
+    bench.py's cpu_baseline_omp only — identical arithmetic, checked bitwise against build() in
+    tests/test_oracle_iteration.py."""
+    newest = max(os.path.getmtime(s) for s in _SRC)
+    if force or not os.path.exists(_SO_OMP) or os.path.getmtime(_SO_OMP) < newest:
+        tmp = _SO_OMP + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC",
+                               "-shared", "-Wall", "-o", tmp, _SRC[0], _SRC[1], _SRC[2], _SRC[3], "-lm"])
+        os.replace(tmp, _SO_OMP)
+    return _SO_OMP
+
+
 _lib = None
+_lib_omp = None
 
 
-def lib():
-    global _lib
+def lib(omp: bool = False):
+    global _lib, _lib_omp
+    if omp:
+        if _lib_omp is None:
+            _lib_omp = _declare(ctypes.CDLL(build_omp()))
+        return _lib_omp
     if _lib is None:
-        L = ctypes.CDLL(build())
-        P = ctypes.c_void_p
-        i64, u32, i32, dbl, flt, cint = ctypes.c_int64, ctypes.c_uint32, ctypes.c_int32, ctypes.c_double, ctypes.c_float, ctypes.c_int
-        L.orc_hash.restype = u32
-        L.orc_hash.argtypes = [i32, i32, i32, u32]
-        L.orc_table_size.restype = u32
-        L.orc_table_size.argtypes = [i64]
-        L.orc_build_table.restype = i64
-        L.orc_build_table.argtypes = [P, i64, u32, P, P, P]
-        L.orc_lookup.restype = i64
-        L.orc_lookup.argtypes = [P, P, P, u32, i32, i32, i32]
-        L.orc_neighbours.restype = None
-        L.orc_neighbours.argtypes = [P, i64, u32, P, P, P]
-        for sfx, real in (("f64", dbl), ("f32", flt)):
-            g = getattr(L, f"orc_gradient_{sfx}")
-            g.restype = None
-            g.argtypes = [i64, P, P, P, P]
-            d = getattr(L, f"orc_divergence_{sfx}")
-            d.restype = None
-            d.argtypes = [i64, P, P, P, P]
-            r = getattr(L, f"orc_regularise_{sfx}")
-            r.restype = cint
-            r.argtypes = [i64, P, P, P, real, real, real, real, real, cint, cint, i64, P, P, P, cint]
-        L.orc_energy.restype = None
-        L.orc_energy.argtypes = [i64, P, P, P, P, P, dbl, dbl, cint, P, P]
-        # fusion (fusion_oracle.c)
-        L.orc_tsdf_update.restype = cint
-        L.orc_tsdf_update.argtypes = [P, P, flt, flt, flt]
-        L.orc_project.restype = cint
-        L.orc_project.argtypes = [P, P, i32, i32, flt, flt, flt, P, P, P]
-        L.orc_block_walk.restype = i64
-        L.orc_block_walk.argtypes = [P, P, flt, P, i64]
-        L.orc_fuse.restype = i64
-        L.orc_fuse.argtypes = [P, i32, i32, i32, P, P, flt, flt, flt, flt, i64, P, P, P, P]
-        L.orc_fuse_incremental.restype = i64
-        L.orc_fuse_incremental.argtypes = [P, P, P, i64, P, i32, i32, i32, P, P, flt, flt, flt, flt, i64, P, P, P, P]
-        L.orc_fuse_alloc.restype = i64
-        L.orc_fuse_alloc.argtypes = [P, i32, i32, i32, P, P, flt, flt, flt, i64, P, P]
-        L.orc_extract.restype = i64
-        L.orc_extract.argtypes = [P, i64, P, P, flt, flt, P, i64]
-        L.orc_census.restype = None
-        L.orc_census.argtypes = [P, cint, cint, cint, P]
-        L.orc_cost.restype = None
-        L.orc_cost.argtypes = [P, P, cint, cint, cint, cint, P]
-        L.orc_tensor.restype = None
-        L.orc_tensor.argtypes = [P, cint, cint, flt, flt, P]
-        L.orc_tgv_K.restype = None
-        L.orc_tgv_K.argtypes = [P, P, P, cint, cint, P, P]
-        L.orc_tgv_KT.restype = None
-        L.orc_tgv_KT.argtypes = [P, P, P, cint, cint, P, P, P]
-        L.orc_data_step.restype = flt
-        L.orc_data_step.argtypes = [flt, P, cint, flt, flt]
-        L.orc_stereo_theta.restype = flt
-        L.orc_stereo_theta.argtypes = [P, cint]
-        L.orc_stereo.restype = cint
-        L.orc_stereo.argtypes = [P, P, cint, cint, P, P, P, P]
-        L.orc_fuse_update_blocks.restype = None
-        L.orc_fuse_update_blocks.argtypes = [P, i32, i32, i32, P, P, flt, flt, flt, flt, P, P, i64, P, P]
-        _lib = L
+        _lib = _declare(ctypes.CDLL(build()))
     return _lib
+
+
+def _declare(L):
+    """ctypes signatures of every oracle entry point."""
+    P = ctypes.c_void_p
+    i64, u32, i32, dbl, flt, cint = ctypes.c_int64, ctypes.c_uint32, ctypes.c_int32, ctypes.c_double, ctypes.c_float, ctypes.c_int
+    L.orc_hash.restype = u32
+    L.orc_hash.argtypes = [i32, i32, i32, u32]
+    L.orc_table_size.restype = u32
+    L.orc_table_size.argtypes = [i64]
+    L.orc_build_table.restype = i64
+    L.orc_build_table.argtypes = [P, i64, u32, P, P, P]
+    L.orc_lookup.restype = i64
+    L.orc_lookup.argtypes = [P, P, P, u32, i32, i32, i32]
+    L.orc_neighbours.restype = None
+    L.orc_neighbours.argtypes = [P, i64, u32, P, P, P]
+    for sfx, real in (("f64", dbl), ("f32", flt)):
+        g = getattr(L, f"orc_gradient_{sfx}")
+        g.restype = None
+        g.argtypes = [i64, P, P, P, P]
+        d = getattr(L, f"orc_divergence_{sfx}")
+        d.restype = None
+        d.argtypes = [i64, P, P, P, P]
+        r = getattr(L, f"orc_regularise_{sfx}")
+        r.restype = cint
+        r.argtypes = [i64, P, P, P, real, real, real, real, real, cint, cint, i64, P, P, P, cint]
+    L.orc_energy.restype = None
+    L.orc_energy.argtypes = [i64, P, P, P, P, P, dbl, dbl, cint, P, P]
+    # fusion (fusion_oracle.c)
+    L.orc_tsdf_update.restype = cint
+    L.orc_tsdf_update.argtypes = [P, P, flt, flt, flt]
+    L.orc_project.restype = cint
+    L.orc_project.argtypes = [P, P, i32, i32, flt, flt, flt, P, P, P]
+    L.orc_block_walk.restype = i64
+    L.orc_block_walk.argtypes = [P, P, flt, P, i64]
+    L.orc_fuse.restype = i64
+    L.orc_fuse.argtypes = [P, i32, i32, i32, P, P, flt, flt, flt, flt, i64, P, P, P, P]
+    L.orc_fuse_incremental.restype = i64
+    L.orc_fuse_incremental.argtypes = [P, P, P, i64, P, i32, i32, i32, P, P, flt, flt, flt, flt, i64, P, P, P, P]
+    L.orc_fuse_alloc.restype = i64
+    L.orc_fuse_alloc.argtypes = [P, i32, i32, i32, P, P, flt, flt, flt, i64, P, P]
+    L.orc_extract.restype = i64
+    L.orc_extract.argtypes = [P, i64, P, P, flt, flt, P, i64]
+    L.orc_census.restype = None
+    L.orc_census.argtypes = [P, cint, cint, cint, P]
+    L.orc_cost.restype = None
+    L.orc_cost.argtypes = [P, P, cint, cint, cint, cint, P]
+    L.orc_tensor.restype = None
+    L.orc_tensor.argtypes = [P, cint, cint, flt, flt, P]
+    L.orc_tgv_K.restype = None
+    L.orc_tgv_K.argtypes = [P, P, P, cint, cint, P, P]
+    L.orc_tgv_KT.restype = None
+    L.orc_tgv_KT.argtypes = [P, P, P, cint, cint, P, P, P]
+    L.orc_data_step.restype = flt
+    L.orc_data_step.argtypes = [flt, P, cint, flt, flt]
+    L.orc_stereo_theta.restype = flt
+    L.orc_stereo_theta.argtypes = [P, cint]
+    L.orc_stereo.restype = cint
+    L.orc_stereo.argtypes = [P, P, cint, cint, P, P, P, P]
+    L.orc_fuse_update_blocks.restype = None
+    L.orc_fuse_update_blocks.argtypes = [P, i32, i32, i32, P, P, flt, flt, flt, flt, P, P, i64, P, P]
+    return L
 
 
 def _ptr(a: np.ndarray):
@@ -203,7 +228,7 @@ def divergence(nbr, W, p, precision="f64") -> np.ndarray:
 
 
 def regularise(coords, f, W, lam, eps, tau, sigma, iters, theta=1.0, data_term=0, init=0, precision="f64",
-               state=None, nbr=None):
+               state=None, nbr=None, omp=False):
     """Run `iters` CP iterations; returns (u, ubar, p) with u, ubar [n, 512] and p [3, n, 512].
 
     `state` = (u, ubar, p) resumes from a previous call.  Parameters are rounded to fp32 first
@@ -225,7 +250,7 @@ def regularise(coords, f, W, lam, eps, tau, sigma, iters, theta=1.0, data_term=0
         u, ub, p = (np.array(a, dtype=dt, copy=True) for a in state)
         resume = 1
     r32 = lambda x: float(np.float32(x))
-    getattr(lib(), f"orc_regularise_{sfx}")(n, _ptr(nbr), _ptr(ff), _ptr(Wf), r32(lam), r32(eps), r32(tau),
+    getattr(lib(omp), f"orc_regularise_{sfx}")(n, _ptr(nbr), _ptr(ff), _ptr(Wf), r32(lam), r32(eps), r32(tau),
                                             r32(sigma), r32(theta), int(data_term), int(init), int(iters),
                                             _ptr(u), _ptr(ub), _ptr(p), resume)
     return u, ub, p

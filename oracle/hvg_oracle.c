@@ -32,6 +32,15 @@
  */
 #include <math.h>
 #include <stdint.h>
+
+/* Voxel loops of one phase are independent (each phase reads a frozen snapshot of the previous one),
+ * so the timing build (liboracle_omp.so, -fopenmp; bench.py cpu_baseline_omp only) runs them over all
+ * host cores.  The parity build has no -fopenmp and the pragma is empty: same arithmetic either way. */
+#ifdef _OPENMP
+#define ORC_PAR _Pragma("omp parallel for schedule(static)")
+#else
+#define ORC_PAR
+#endif
 #include <stdlib.h>
 #include <string.h>
 

@@ -246,3 +246,15 @@ def test_l2_gap_shrinks(tiny_scene):
 def test_fp32_close_to_fp64(tiny_oracle):
     # reading c-18: fp32 drift after the config's 200 iterations stays below the 1e-5 parity budget
     assert np.abs(tiny_oracle["u32"] - tiny_oracle["u64"]).max() < 5e-6
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_openmp_timing_build_is_bitwise_the_plain_oracle(tiny_scene, prec):
+    """liboracle_omp.so (bench.py cpu_baseline_omp) runs the same phase loops over all host cores; every
+    phase reads a frozen snapshot, so the result must equal the plain build bit for bit."""
+    s = tiny_scene
+    a = oracle.regularise_scene(s, precision=prec, iters=25)
+    b = oracle.regularise(s.coords, s.f, s.W, s.lam, s.eps, s.tau, s.sigma, 25, theta=s.theta,
+                          data_term=s.data_term, init=s.init, precision=prec, omp=True)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
