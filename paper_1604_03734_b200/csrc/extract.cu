@@ -169,6 +169,10 @@ __global__ void __launch_bounds__(128) k_extract(ExArgs A, int64_t n_rows, uint3
     __shared__ uint16_t sitem[kMaxItems];   // cell (9 bits) << 3 | tetrahedron (3 bits)
     __shared__ int32_t srow[8];
     __shared__ uint32_t swarp[4];
+    // emit pass: one round's triangles (≤ 2 per item) staged here, then written out by the whole CTA
+    // with consecutive lanes on consecutive floats (coalesced) instead of 9 scattered 4-byte stores
+    // per triangle 36 B apart
+    __shared__ float sout[EMIT ? 2 * 128 * 9 : 1];
     const int64_t r = blockIdx.x;
     if (r >= n_rows) return;
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
@@ -284,8 +288,11 @@ __global__ void __launch_bounds__(128) k_extract(ExArgs A, int64_t n_rows, uint3
                 unsigned m = 0;
                 tet<true>(0, k1, k2, k3, su[tile_index(cx, cyy, czz, 0)], su[tile_index(cx, cyy, czz, k1)],
                           su[tile_index(cx, cyy, czz, k2)], su[tile_index(cx, cyy, czz, k3)], gx + cx, gy + cyy,
-                          gz + czz, A.voxel, base_out + 9ull * (run + before), m);
+                          gz + czz, A.voxel, sout + 9 * before, m);
             }
+            __syncthreads();
+            float *dst = base_out + 9ull * run;
+            for (uint32_t j = t; j < 9 * round_total; j += 128) dst[j] = sout[j];
             run += round_total;
         } else {
             unsigned m = 0;
