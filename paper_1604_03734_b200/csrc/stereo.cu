@@ -220,6 +220,147 @@ __global__ void k_primal(State S, Img g, Steps P) {
     S.w2[i] = wn2;
 }
 
+// Quad forms of k_dual / k_primal (widths divisible by 4): four consecutive pixels of a row per thread,
+// 128-bit loads and stores, 32-bit index arithmetic once per quad.  Per pixel the operations, their
+// operands and their order are exactly those of k_dual / k_primal (bit-identical results).
+__device__ __forceinline__ void ld4(const float *p, float (&a)[4]) {
+    const float4 v = *reinterpret_cast<const float4 *>(p);
+    a[0] = v.x; a[1] = v.y; a[2] = v.z; a[3] = v.w;
+}
+__device__ __forceinline__ void st4(float *p, const float (&a)[4]) {
+    *reinterpret_cast<float4 *>(p) = make_float4(a[0], a[1], a[2], a[3]);
+}
+
+struct Quad {
+    unsigned i;      // pixel index of the first pixel of the quad
+    int x0, y;
+    bool hasx;       // the quad's last pixel has a +x neighbour (x0 + 3 < W − 1)
+    bool hasy;       // y < H − 1
+};
+__device__ __forceinline__ bool quad_of(const Img &g, Quad &q) {
+    const unsigned Wq = (unsigned)g.W >> 2;
+    const unsigned qi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (qi >= (unsigned)(g.n() >> 2)) return false;
+    const unsigned row = qi / Wq;
+    q.x0 = 4 * (int)(qi - row * Wq);
+    q.y = (int)(row % (unsigned)g.H);
+    q.i = 4u * qi;
+    q.hasx = q.x0 + 4 < g.W;
+    q.hasy = q.y < g.H - 1;
+    return true;
+}
+
+__global__ void __launch_bounds__(256) k_dual4(State S, Img g, Steps P) {
+    Quad Q;
+    if (!quad_of(g, Q)) return;
+    const unsigned i = Q.i, W = (unsigned)g.W;
+    float db[5], dbd[4] = {0.f, 0.f, 0.f, 0.f}, wb1[5], wb2[5], wd1[4] = {0.f, 0.f, 0.f, 0.f},
+                 wd2[4] = {0.f, 0.f, 0.f, 0.f};
+    float t11[4], t12[4], t22[4], p1[4], p2[4], q1[4], q2[4], q3[4], q4[4];
+    ld4(S.db + i, reinterpret_cast<float(&)[4]>(db));
+    ld4(S.wb1 + i, reinterpret_cast<float(&)[4]>(wb1));
+    ld4(S.wb2 + i, reinterpret_cast<float(&)[4]>(wb2));
+    db[4] = Q.hasx ? S.db[i + 4] : 0.f;
+    wb1[4] = Q.hasx ? S.wb1[i + 4] : 0.f;
+    wb2[4] = Q.hasx ? S.wb2[i + 4] : 0.f;
+    if (Q.hasy) {
+        ld4(S.db + i + W, dbd);
+        ld4(S.wb1 + i + W, wd1);
+        ld4(S.wb2 + i + W, wd2);
+    }
+    ld4(S.T11 + i, t11); ld4(S.T12 + i, t12); ld4(S.T22 + i, t22);
+    ld4(S.p1 + i, p1); ld4(S.p2 + i, p2);
+    ld4(S.q1 + i, q1); ld4(S.q2 + i, q2); ld4(S.q3 + i, q3); ld4(S.q4 + i, q4);
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        const bool hx = j < 3 || Q.hasx;   // x < W − 1
+        // u = T∇d̄ − w̄
+        const float gx = hx ? __fsub_rn(db[j + 1], db[j]) : 0.0f;
+        const float gy = Q.hasy ? __fsub_rn(dbd[j], db[j]) : 0.0f;
+        const float tx = __fadd_rn(__fmul_rn(t11[j], gx), __fmul_rn(t12[j], gy));
+        const float ty = __fadd_rn(__fmul_rn(t12[j], gx), __fmul_rn(t22[j], gy));
+        const float u1 = __fsub_rn(tx, wb1[j]), u2 = __fsub_rn(ty, wb2[j]);
+        float a1 = __fadd_rn(p1[j], __fmul_rn(P.sigma, u1));
+        float a2 = __fadd_rn(p2[j], __fmul_rn(P.sigma, u2));
+        project2(a1, a2, P.alpha1);
+        p1[j] = a1;
+        p2[j] = a2;
+        // v = ∇w̄
+        float b1 = __fadd_rn(q1[j], __fmul_rn(P.sigma, hx ? __fsub_rn(wb1[j + 1], wb1[j]) : 0.0f));
+        float b2 = __fadd_rn(q2[j], __fmul_rn(P.sigma, Q.hasy ? __fsub_rn(wd1[j], wb1[j]) : 0.0f));
+        float b3 = __fadd_rn(q3[j], __fmul_rn(P.sigma, hx ? __fsub_rn(wb2[j + 1], wb2[j]) : 0.0f));
+        float b4 = __fadd_rn(q4[j], __fmul_rn(P.sigma, Q.hasy ? __fsub_rn(wd2[j], wb2[j]) : 0.0f));
+        project4(b1, b2, b3, b4, P.alpha2);
+        q1[j] = b1;
+        q2[j] = b2;
+        q3[j] = b3;
+        q4[j] = b4;
+    }
+    st4(S.p1 + i, p1); st4(S.p2 + i, p2);
+    st4(S.q1 + i, q1); st4(S.q2 + i, q2); st4(S.q3 + i, q3); st4(S.q4 + i, q4);
+}
+
+__global__ void __launch_bounds__(256) k_primal4(State S, Img g, Steps P) {
+    Quad Q;
+    if (!quad_of(g, Q)) return;
+    const unsigned i = Q.i, W = (unsigned)g.W;
+    const bool has_left = Q.x0 > 0, by = Q.y > 0;
+    // T p at the quad's pixels and at the pixel before it (index 0 = i − 1), a1 component
+    float p1[5], p2[5], t11[5], t12[5], t22[4];
+    ld4(S.p1 + i, reinterpret_cast<float(&)[4]>(p1[1]));
+    ld4(S.p2 + i, reinterpret_cast<float(&)[4]>(p2[1]));
+    ld4(S.T11 + i, reinterpret_cast<float(&)[4]>(t11[1]));
+    ld4(S.T12 + i, reinterpret_cast<float(&)[4]>(t12[1]));
+    ld4(S.T22 + i, t22);
+    p1[0] = has_left ? S.p1[i - 1] : 0.f;
+    p2[0] = has_left ? S.p2[i - 1] : 0.f;
+    t11[0] = has_left ? S.T11[i - 1] : 0.f;
+    t12[0] = has_left ? S.T12[i - 1] : 0.f;
+    float up1[4] = {0.f, 0.f, 0.f, 0.f}, up2[4] = {0.f, 0.f, 0.f, 0.f}, ut12[4] = {0.f, 0.f, 0.f, 0.f},
+          ut22[4] = {0.f, 0.f, 0.f, 0.f}, uq2[4] = {0.f, 0.f, 0.f, 0.f}, uq4[4] = {0.f, 0.f, 0.f, 0.f};
+    if (by) {
+        ld4(S.p1 + i - W, up1); ld4(S.p2 + i - W, up2);
+        ld4(S.T12 + i - W, ut12); ld4(S.T22 + i - W, ut22);
+        ld4(S.q2 + i - W, uq2); ld4(S.q4 + i - W, uq4);
+    }
+    float q1[5], q2[4], q3[5], q4[4];
+    ld4(S.q1 + i, reinterpret_cast<float(&)[4]>(q1[1]));
+    ld4(S.q3 + i, reinterpret_cast<float(&)[4]>(q3[1]));
+    ld4(S.q2 + i, q2);
+    ld4(S.q4 + i, q4);
+    q1[0] = has_left ? S.q1[i - 1] : 0.f;
+    q3[0] = has_left ? S.q3[i - 1] : 0.f;
+    float d[4], w1[4], w2[4], a[4];
+    ld4(S.d + i, d); ld4(S.w1 + i, w1); ld4(S.w2 + i, w2); ld4(S.a + i, a);
+    float h1[5];
+#pragma unroll
+    for (int j = 0; j < 5; j++) h1[j] = __fadd_rn(__fmul_rn(t11[j], p1[j]), __fmul_rn(t12[j], p2[j]));
+    float dbo[4], wbo1[4], wbo2[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        const bool hx = j < 3 || Q.hasx, bx = j > 0 || has_left, hy = Q.hasy;
+        const float h2 = __fadd_rn(__fmul_rn(t12[j + 1], p1[j + 1]), __fmul_rn(t22[j], p2[j + 1]));
+        const float l1 = bx ? h1[j] : 0.f;
+        const float u2 = by ? __fadd_rn(__fmul_rn(ut12[j], up1[j]), __fmul_rn(ut22[j], up2[j])) : 0.f;
+        const float kd = -__fadd_rn(bd(h1[j + 1], l1, hx, bx), bd(h2, u2, hy, by));
+        const float dq1 = __fadd_rn(bd(q1[j + 1], bx ? q1[j] : 0.f, hx, bx), bd(q2[j], by ? uq2[j] : 0.f, hy, by));
+        const float dq2 = __fadd_rn(bd(q3[j + 1], bx ? q3[j] : 0.f, hx, bx), bd(q4[j], by ? uq4[j] : 0.f, hy, by));
+        const float kw1 = -__fadd_rn(p1[j + 1], dq1);
+        const float kw2 = -__fadd_rn(p2[j + 1], dq2);
+        const float dn = __fmul_rn(__fadd_rn(__fsub_rn(d[j], __fmul_rn(P.tau, kd)), __fmul_rn(P.tt, a[j])), P.kinv);
+        const float wn1 = __fsub_rn(w1[j], __fmul_rn(P.tau, kw1));
+        const float wn2 = __fsub_rn(w2[j], __fmul_rn(P.tau, kw2));
+        dbo[j] = __fadd_rn(dn, __fsub_rn(dn, d[j]));
+        wbo1[j] = __fadd_rn(wn1, __fsub_rn(wn1, w1[j]));
+        wbo2[j] = __fadd_rn(wn2, __fsub_rn(wn2, w2[j]));
+        d[j] = dn;
+        w1[j] = wn1;
+        w2[j] = wn2;
+    }
+    st4(S.db + i, dbo); st4(S.wb1 + i, wbo1); st4(S.wb2 + i, wbo2);
+    st4(S.d + i, d); st4(S.w1 + i, w1); st4(S.w2 + i, w2);
+}
+
 // Fused iteration: dual then primal in one launch.  A CTA owns a TX×TY tile; it recomputes the dual
 // update of the −x column and −y row next to the tile (same function, same inputs ⇒ bit-identical to
 // the owner's), so the primal step needs no grid-wide synchronisation.  Ping-pong buffers: every field
@@ -522,7 +663,8 @@ namespace {
 
 // The whole solve of frames [c0, c0 + C) of the batch, for each chunk of `chunk` frames in turn: a chunk's
 // state (~116 B per pixel) is sized to stay resident in the 126 MB L2 across its iterations.
-void enqueue_solve(const StereoLayout &L, const vol_stereo_params *prm, int32_t F, int chunk, bool two_kernel,
+// mode: 0 fused k_tgv_iter, 1 k_dual + k_primal, 2 k_dual4 + k_primal4 where the width allows (product)
+void enqueue_solve(const StereoLayout &L, const vol_stereo_params *prm, int32_t F, int chunk, int mode,
                    cudaStream_t s, long long &launches) {
     const long long HW = (long long)prm->width * prm->height;
     const int maxc = prm->window * prm->window - 1;
@@ -531,6 +673,10 @@ void enqueue_solve(const StereoLayout &L, const vol_stereo_params *prm, int32_t 
         const int C = F - c0 < chunk ? F - c0 : chunk;
         const long long o = (long long)c0 * HW, n = (long long)C * HW;
         const unsigned nb = blocks_for(n, TPB);
+        // quad kernels: widths divisible by 4 (16-byte aligned rows) and 32-bit pixel indices
+        const bool two_kernel = mode != 0;
+        const bool quads = mode == 2 && prm->width % 4 == 0 && n < (1ll << 31);
+        const unsigned nq = blocks_for(n / 4, TPB);
         Img g{C, prm->height, prm->width};
         State S{L.f[0] + o, L.f[1] + o, L.f[2] + o, L.f[3] + o, L.f[4] + o, L.f[5] + o, L.f[6] + o, L.f[7] + o,
                 L.f[8] + o, L.f[9] + o, L.f[10] + o, L.f[11] + o, L.f[12] + o, L.T[0] + o, L.T[1] + o, L.T[2] + o,
@@ -551,7 +697,11 @@ void enqueue_solve(const StereoLayout &L, const vol_stereo_params *prm, int32_t 
             const float tt = prm->tau / theta;
             Steps P{prm->sigma, prm->tau, prm->alpha1, prm->alpha2, tt, 1.0f / (1.0f + tt)};
             for (int it = 0; it < prm->inner; it++) {
-                if (two_kernel) {
+                if (two_kernel && quads) {
+                    k_dual4<<<nq, TPB, 0, s>>>(S, g, P);
+                    k_primal4<<<nq, TPB, 0, s>>>(S, g, P);
+                    launches += 2;
+                } else if (two_kernel) {
                     k_dual<<<nb, TPB, 0, s>>>(S, g, P);
                     k_primal<<<nb, TPB, 0, s>>>(S, g, P);
                     launches += 2;
@@ -576,7 +726,7 @@ struct GraphKey {
     void *ws;
     int32_t F;
     int chunk;
-    bool two;
+    int mode;
     int device;
     vol_stereo_params p;
 };
@@ -591,7 +741,7 @@ std::mutex g_graph_mu;
 std::vector<GraphEntry> g_graphs;   // most recent last; at most 8
 
 bool same_key(const GraphKey &a, const GraphKey &b) {
-    return a.ws == b.ws && a.F == b.F && a.chunk == b.chunk && a.two == b.two && a.device == b.device &&
+    return a.ws == b.ws && a.F == b.F && a.chunk == b.chunk && a.mode == b.mode && a.device == b.device &&
            memcmp(&a.p, &b.p, sizeof a.p) == 0;
 }
 
@@ -635,7 +785,8 @@ extern "C" vol_status vol_stereo(const float *left, const float *right, int32_t 
     // working set (16 fp32 fields ≈ 64 B per pixel) stays in L2 — measured faster than the fused
     // halo-recompute kernel once the state is L2-resident.  The fused kernel stays
     // selectable (experiments only).
-    const bool two_kernel = getenv("HVG_STEREO_FUSED") == nullptr;
+    // HVG_STEREO_FUSED / HVG_STEREO_SCALAR select the other kernel forms (bit-identical; tests, experiments)
+    const int mode = getenv("HVG_STEREO_FUSED") ? 0 : (getenv("HVG_STEREO_SCALAR") ? 1 : 2);
     const long long per_frame = (long long)prm->width * prm->height * 64;
     int chunk = (int)((80ll << 20) / (per_frame > 0 ? per_frame : 1));
     if (const char *e = getenv("HVG_STEREO_CHUNK")) chunk = atoi(e);      // experiments only
@@ -643,12 +794,12 @@ extern "C" vol_status vol_stereo(const float *left, const float *right, int32_t 
     if (chunk > n_frames) chunk = n_frames;
     long long launches = 0;
     if (owns || getenv("HVG_STEREO_NO_GRAPH")) {
-        enqueue_solve(L, prm, n_frames, chunk, two_kernel, s, launches);
+        enqueue_solve(L, prm, n_frames, chunk, mode, s, launches);
         CK(cudaPeekAtLastError());
     } else {
         int dev = 0;
         cudaGetDevice(&dev);
-        GraphKey key{ws, n_frames, chunk, two_kernel, dev, *prm};
+        GraphKey key{ws, n_frames, chunk, mode, dev, *prm};
         cudaGraphExec_t exec = nullptr;
         {
             std::lock_guard<std::mutex> lk(g_graph_mu);
@@ -664,7 +815,7 @@ extern "C" vol_status vol_stereo(const float *left, const float *right, int32_t 
             cudaGraph_t graph;
             cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
             if (e == cudaSuccess) {
-                enqueue_solve(L, prm, n_frames, chunk, two_kernel, cs, launches);
+                enqueue_solve(L, prm, n_frames, chunk, mode, cs, launches);
                 e = cudaStreamEndCapture(cs, &graph);
             }
             if (e == cudaSuccess) {

@@ -116,3 +116,22 @@ def test_street_full_size_bit_exact(S):
     _bits_equal(d, do)
     valid = (dt[0].cpu().numpy() > 1) & (dt[0].cpu().numpy() < 120)
     assert np.median(np.abs(d - dt[0].cpu().numpy())[valid]) < 1.0
+
+
+@pytest.mark.parametrize("width", [98, 100])
+def test_quad_and_scalar_kernels_bit_exact(S, width, monkeypatch):
+    """The product iteration kernels work on quads of pixels (k_dual4 / k_primal4, widths divisible by 4);
+    the per-pixel kernels (HVG_STEREO_SCALAR, and every width not divisible by 4) compute the same bits,
+    and both equal the oracle.  Two frames, so the quad rows cross frame boundaries."""
+    pairs = [plane_pair(36, width, 0.03, -0.01, 7.0, seed=3), plane_pair(36, width, -0.02, 0.02, 9.0, seed=4)]
+    IL = torch.stack([p[0] for p in pairs])
+    IR = torch.stack([p[1] for p in pairs])
+    kw = dict(n_disp=24, outer=4, inner=12)
+    d_q = S.stereo(IL, IR, **kw).cpu().numpy()
+    monkeypatch.setenv("HVG_STEREO_SCALAR", "1")
+    d_s = S.stereo(IL, IR, **kw).cpu().numpy()
+    monkeypatch.delenv("HVG_STEREO_SCALAR")
+    _bits_equal(d_q, d_s)
+    for f, (l, r, _) in enumerate(pairs):
+        do, _, _ = oracle.stereo(l, r, D=24, outer=4, inner=12)
+        _bits_equal(d_q[f], do)
