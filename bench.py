@@ -463,14 +463,18 @@ def main():
     ev_b = torch.cuda.Event(enable_timing=True)
     iter_ms = []
 
-    def step(c, f, W, out, record, freeze=bool(args.freeze), rec=None):
+    shard_t = []
+
+    def step(c, f, W, out, record, freeze=bool(args.freeze), rec=None, exchange=True):
         vol = Volume(c, f, W, stream=stream, **kw)
         vol.regularise(scene.lam, scene.eps, scene.tau, scene.sigma, 0, theta=scene.theta,
                        data_term=scene.data_term, init=scene.init, kernel=args.kernel)
         ev_a.record(stream)
         vol.regularise(scene.lam, scene.eps, scene.tau, scene.sigma, iters, theta=scene.theta,
-                       data_term=scene.data_term, resume=True, kernel=args.kernel, freeze=freeze)
+                       data_term=scene.data_term, resume=True, kernel=args.kernel, freeze=freeze, exchange=exchange)
         ev_b.record(stream)
+        if sharded and record and rec is None:
+            shard_t.append(vol.shard_timing())   # last iteration: interior A, halo chain, boundary B
         E = vol.energy(scene.lam, scene.eps, scene.data_term)
         vol.read_u(out)
         if record:
@@ -524,6 +528,25 @@ def main():
             dist.all_reduce(nfm, op=dist.ReduceOp.MAX)
         nf = {"value": scene.n_alloc * iters / (float(nfm[0]) / 1e3), "ms_per_step": float(nfm[0]),
               "avg_launch_ms": float(nfm[1]), "steps": nsteps}
+
+    # SURVEY 8(d) multi-GPU: exposed halo = T_iter(exchange on) - T_iter(exchange replaced by a no-op with the
+    # same partition), and the per-stream durations of the last iteration (interior launch A, halo chain on
+    # the communication stream, boundary launch B), max over ranks
+    halo = None
+    if sharded:
+        off_ms = []
+        step(coords, f_loc, W_loc, u_out, False, exchange=False)
+        barrier()
+        for _ in range(max(2, args.steps // 2)):
+            step(coords, f_loc, W_loc, u_out, True, rec=off_ms, exchange=False)
+        barrier()
+        tt = torch.tensor([statistics.median(off_ms)] + [statistics.median(x[i] for x in shard_t) for i in range(3)],
+                          device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        halo = {"exposed_us_per_iter": 1e3 * (it_ms - float(tt[0])), "iter_ms_exchange_off": float(tt[0]),
+                "interior_ms": float(tt[1]), "exchange_chain_ms": float(tt[2]), "boundary_ms": float(tt[3]),
+                "transport": "NCCL send/recv per peer (comm stream), pack/unpack kernels",
+                "note": "max over ranks; chain overlaps the interior launch"}
 
     # end to end from pinned host buffers through the same API
     e2e = None
@@ -623,7 +646,7 @@ def main():
                    "l2": f"inputs larger than L2 ({n_alloc_total * 48 / 1e9:.2f} GB of state vs 126 MB L2)",
                    "parallelism": f"route-axis shards x{world}" if sharded else "single GPU",
                    "energy": {"primal": E[0], "dual": E[1]}},
-        "roofline": roofline, "cpu_baseline": cpu, "cpu_baseline_omp": cpu_omp, "e2e": e2e, "gpu_launches": int(launches),
+        "roofline": roofline, "cpu_baseline": cpu, "cpu_baseline_omp": cpu_omp, "e2e": e2e, "halo": halo, "gpu_launches": int(launches),
         "freeze": bool(args.freeze), "no_freeze": nf,
         "clocks": clk, "fusion": fusion, "extraction": extraction, "stereo": stereo_res, "pipeline": pipeline,
     }

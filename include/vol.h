@@ -58,6 +58,10 @@ typedef struct {
                         for the whole call (τλW >= τ(3+√3) plus rounding margin, and u = ū = f in both
                         buffers at the start of the call) are not recomputed nor rewritten — the result
                         is bit-identical; 0: every Ω voxel is updated every iteration               */
+    int exchange;    /* 1 (d): a sharded volume exchanges its halo every iteration;
+                        0: the exchange chain (pack, NCCL send/recv, unpack) is replaced by a no-op with
+                        the same partition and the same launches — the result is WRONG; for timing only
+                        (exposed halo µs/iteration = T(1) − T(0)).  Ignored when unsharded */
 } vol_opts;
 
 /* Multi-GPU description (route-axis spatial sharding).  NULL = single GPU.          */
@@ -131,6 +135,14 @@ vol_status vol_read_tables(vol_t v, uint32_t *T, uint32_t *bucket_start, int32_t
 
 /* Sizes: allocated blocks on this rank, ghost blocks held, total Ω voxels on this rank.           */
 vol_status vol_info(vol_t v, int64_t *n_local, int64_t *n_ghost, int64_t *n_omega);
+
+/* Per-stream durations of the LAST iteration of the last vol_regularise call on an NCCL-sharded volume
+ * (SURVEY §8(d) "boundary-chain vs interior-kernel durations from per-stream events"), in ms, from CUDA
+ * events: interior_ms = launch A (blocks without a remote neighbour, compute stream); exchange_ms = the
+ * halo chain pack → NCCL send/recv → unpack (communication stream, overlapping launch A); boundary_ms =
+ * launch B (blocks with a remote neighbour, after the halo).  Waits for those events.  Any output pointer
+ * may be NULL.  VOL_EINVAL if the volume is not NCCL-sharded or has not iterated yet.                  */
+vol_status vol_shard_timing(vol_t v, float *interior_ms, float *exchange_ms, float *boundary_ms);
 
 /* Number of kernel launches the last vol_regularise issued (counted on the host; graph nodes count). */
 int64_t vol_last_launches(vol_t v);

@@ -21,7 +21,8 @@ class VolError(RuntimeError):
 
 class vol_opts(ctypes.Structure):
     _fields_ = [("theta", ctypes.c_float), ("data_term", ctypes.c_int), ("init", ctypes.c_int),
-                ("resume", ctypes.c_int), ("kernel", ctypes.c_int), ("freeze", ctypes.c_int)]
+                ("resume", ctypes.c_int), ("kernel", ctypes.c_int), ("freeze", ctypes.c_int),
+                ("exchange", ctypes.c_int)]
 
 
 class vol_camera(ctypes.Structure):
@@ -58,7 +59,7 @@ EXPORTS = [
     "vol_destroy", "vol_last_error", "vol_nccl_unique_id", "vol_group_connect", "vol_regularise_group",
     "vol_group_energy", "vol_block_hash", "vol_plan_shard", "vol_total_launches", "vol_fuse_workspace_bytes",
     "vol_fuse", "vol_fuse_incremental", "vol_extract", "vol_stereo_default_params", "vol_stereo_workspace_bytes", "vol_stereo",
-    "vol_stereo_census", "vol_stereo_tensor", "vol_disparity_to_depth",
+    "vol_stereo_census", "vol_stereo_tensor", "vol_disparity_to_depth", "vol_shard_timing",
 ]
 
 _lib = None
@@ -96,6 +97,7 @@ def lib() -> ctypes.CDLL:
         "vol_block_hash": (u32, [i32, i32, i32, u32]),
         "vol_plan_shard": (st, [P, i64, P, c_int, c_int, P, P, P, P, P, P, P]),
         "vol_total_launches": (i64, []),
+        "vol_shard_timing": (st, [P, P, P, P]),
         "vol_extract": (st, [P, c_int, f32, f32, P, i64, P]),
         "vol_fuse_incremental": (st, [P, P, P, i64, P, i32, ctypes.POINTER(vol_camera), P,
                                       ctypes.POINTER(vol_fusion_params), i64, P, ctypes.c_size_t, P, P, P, P, P, P,

@@ -94,6 +94,7 @@ struct vol_s {
     bool shard_nccl() const;
     hvg::IterParams pending{};         // parameters of the current vol_regularise call
     int pending_kernel = 0;
+    int pending_exchange = 1;          // opts.exchange of the current call (sharded only)
 };
 
 // Validates the parameters, fills v->pending, initialises the state unless opts->resume.

@@ -218,6 +218,9 @@ struct ShardRuntime {
     ncclComm_t comm = nullptr;
     cudaStream_t cs = nullptr;       // communication stream
     cudaEvent_t ev_pack = nullptr, ev_halo = nullptr;
+    // timing events of the last iteration (vol_shard_timing): A start/end, chain start/end, B start/end
+    cudaEvent_t ev_t[6] = {};
+    bool timed = false;
     float *sendbuf = nullptr, *recvbuf = nullptr;
     int32_t *send_rows = nullptr;
     unsigned long long *omega = nullptr;  // [2] device scratch for the Ω count all-reduce
@@ -359,6 +362,7 @@ vol_status shard_setup(vol_s *v, const ShardPlan &plan, const vol_dist *dist) {
     CK(cudaStreamCreateWithFlags(&R->cs, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&R->ev_pack, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&R->ev_halo, cudaEventDisableTiming));
+    for (auto &e : R->ev_t) CK(cudaEventCreate(&e));
     if (dist->nccl_id) {
         R->nccl = true;
         vol_status st = comm_acquire(dist->nccl_id, P.world, P.rank, v->device, &R->comm);
@@ -395,28 +399,56 @@ vol_status shard_reset(vol_s *v) {
     return VOL_OK;
 }
 
-// One sharded iteration on one rank with the NCCL transport.
-static vol_status nccl_iteration(vol_s *v, const IterParams &P, int64_t &launches) {
+// One sharded iteration on one rank with the NCCL transport.  `timed`: record the per-stream timing
+// events (the last iteration of a call).  exchange == 0 replaces the halo chain by a no-op (timing only).
+static vol_status nccl_iteration(vol_s *v, const IterParams &P, int64_t &launches, bool timed) {
     ShardRuntime *R = v->shard;
     cudaStream_t s = v->stream;
     const int cur = v->cur;
-    vol_status st = pack(v, v->F.ub[cur], v->F.px[cur], v->F.py[cur], v->F.pz[cur], s);
-    if (st != VOL_OK) return st;
+    const bool xchg = v->pending_exchange != 0;
     CK(cudaEventRecord(R->ev_pack, s));
     CK(cudaStreamWaitEvent(R->cs, R->ev_pack, 0));
-    if ((st = nccl_exchange(v, R->cs)) != VOL_OK) return st;
-    if ((st = unpack(v, v->F.ub[cur], v->F.px[cur], v->F.py[cur], v->F.pz[cur], R->cs)) != VOL_OK) return st;
+    if (timed) CK(cudaEventRecord(R->ev_t[2], R->cs));
+    if (xchg) {
+        // pack on the communication stream: it reads ū^k, p^k, final once the previous iteration's
+        // launch B (ordered before ev_pack on the compute stream) has finished
+        vol_status st = pack(v, v->F.ub[cur], v->F.px[cur], v->F.py[cur], v->F.pz[cur], R->cs);
+        if (st != VOL_OK) return st;
+        if ((st = nccl_exchange(v, R->cs)) != VOL_OK) return st;
+        if ((st = unpack(v, v->F.ub[cur], v->F.px[cur], v->F.py[cur], v->F.pz[cur], R->cs)) != VOL_OK) return st;
+    }
+    if (timed) CK(cudaEventRecord(R->ev_t[3], R->cs));
     CK(cudaEventRecord(R->ev_halo, R->cs));
     View V = view_of(v->F, cur);
     V.frozen = v->pending_frozen;
     const ShardPlan &SP = R->plan;
+    if (timed) CK(cudaEventRecord(R->ev_t[0], s));
     int r = launch_fused(V, v->d_nbr, nullptr, 0, SP.nA, P, s);
     CKL(r);
+    if (timed) CK(cudaEventRecord(R->ev_t[1], s));
     CK(cudaStreamWaitEvent(s, R->ev_halo, 0));
+    if (timed) CK(cudaEventRecord(R->ev_t[4], s));
     int r2 = launch_fused(V, v->d_nbr, nullptr, SP.nA, SP.n_local() - SP.nA, P, s);
     CKL(r2);
-    launches += r + r2 + 2;  // + pack + unpack
+    if (timed) CK(cudaEventRecord(R->ev_t[5], s));
+    if (timed) R->timed = true;
+    launches += r + r2 + (xchg ? 2 : 0);  // + pack + unpack
     v->cur ^= 1;
+    return VOL_OK;
+}
+
+vol_status shard_timing(vol_s *v, float *interior_ms, float *exchange_ms, float *boundary_ms) {
+    ShardRuntime *R = v->shard;
+    if (!R || !R->nccl) return fail(VOL_EINVAL, "vol_shard_timing: the volume is not NCCL-sharded");
+    if (!R->timed) return fail(VOL_EINVAL, "vol_shard_timing: no sharded iteration has run yet");
+    CK(cudaEventSynchronize(R->ev_t[5]));
+    float a = 0.f, c = 0.f, b = 0.f;
+    CK(cudaEventElapsedTime(&a, R->ev_t[0], R->ev_t[1]));
+    CK(cudaEventElapsedTime(&c, R->ev_t[2], R->ev_t[3]));
+    CK(cudaEventElapsedTime(&b, R->ev_t[4], R->ev_t[5]));
+    if (interior_ms) *interior_ms = a;
+    if (exchange_ms) *exchange_ms = c;
+    if (boundary_ms) *boundary_ms = b;
     return VOL_OK;
 }
 
@@ -425,7 +457,7 @@ vol_status shard_iterate(vol_s *v, const IterParams &P, int32_t iters) {
     if (!R->nccl) return fail(VOL_EINVAL, "loopback-sharded volume: use vol_regularise_group");
     int64_t launches = 0;
     for (int32_t k = 0; k < iters; k++) {
-        vol_status st = nccl_iteration(v, P, launches);
+        vol_status st = nccl_iteration(v, P, launches, k == iters - 1);
         if (st != VOL_OK) return st;
     }
     v->last_launches = launches;
@@ -467,6 +499,8 @@ void shard_destroy(vol_s *v) {
     }
     if (R->ev_pack) cudaEventDestroy(R->ev_pack);
     if (R->ev_halo) cudaEventDestroy(R->ev_halo);
+    for (auto &e : R->ev_t)
+        if (e) cudaEventDestroy(e);
     // the communicator stays cached for later volumes of the same process group (comm_acquire)
     delete R;
     v->shard = nullptr;

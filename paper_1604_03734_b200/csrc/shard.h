@@ -47,6 +47,7 @@ vol_status shard_setup(vol_s *v, const hvg::ShardPlan &plan, const vol_dist *dis
 vol_status shard_after_create(vol_s *v);
 vol_status shard_reset(vol_s *v);
 vol_status shard_iterate(vol_s *v, const hvg::IterParams &P, int32_t iters);
+vol_status shard_timing(vol_s *v, float *interior_ms, float *exchange_ms, float *boundary_ms);
 vol_status shard_refresh_for_energy(vol_s *v);
 vol_status shard_allreduce_energy(vol_s *v, double *d_eout);
 void shard_destroy(vol_s *v);

@@ -47,6 +47,7 @@ extern "C" void vol_default_opts(vol_opts *o) {
     o->resume = 0;
     o->kernel = 0;
     o->freeze = 1;
+    o->exchange = 1;
 }
 
 extern "C" uint32_t vol_block_hash(int32_t x, int32_t y, int32_t z, uint32_t T) { return host_hash(x, y, z, T); }
@@ -450,6 +451,7 @@ vol_status vol_regularise_prepare(vol_s *v, float lambda, float eps, float tau, 
     if (o.init != 0 && o.init != 1) return fail(VOL_EINVAL, "init must be 0 (warm) or 1 (zero)");
     if (o.kernel != 0 && o.kernel != 1) return fail(VOL_EINVAL, "kernel must be 0 (fused) or 1 (two-kernel)");
     if (v->shard && o.kernel == 1) return fail(VOL_ENOTSUP, "two-kernel baseline is single-GPU only");
+    if (o.exchange != 0 && o.exchange != 1) return fail(VOL_EINVAL, "exchange must be 0 (no-op, timing only) or 1");
     if (v->shard) {
         vol_status st = shard_reset(v);
         if (st != VOL_OK) return st;
@@ -469,6 +471,7 @@ vol_status vol_regularise_prepare(vol_s *v, float lambda, float eps, float tau, 
     P.data_term = o.data_term;
     P.one = 1.0f;
     v->pending_kernel = o.kernel;
+    v->pending_exchange = o.exchange;
     v->last_launches = 0;
     if (!o.resume) {
         CKL(launch_init_state(v->F, v->L.S * kBlockVox, o.init, v->stream));
@@ -636,4 +639,9 @@ extern "C" vol_status vol_info(vol_t v, int64_t *n_local, int64_t *n_ghost, int6
     if (n_ghost) *n_ghost = v->L.S - v->L.n_local;
     if (n_omega) *n_omega = v->n_omega_local;
     return VOL_OK;
+}
+
+extern "C" vol_status vol_shard_timing(vol_t v, float *interior_ms, float *exchange_ms, float *boundary_ms) {
+    if (!v) return fail(VOL_EINVAL, "vol_shard_timing: NULL handle");
+    return shard_timing(v, interior_ms, exchange_ms, boundary_ms);
 }

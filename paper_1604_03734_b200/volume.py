@@ -147,17 +147,20 @@ class Volume:
 
     # -- solver ---------------------------------------------------------------------------------
     @staticmethod
-    def _opts(theta=1.0, data_term=0, init=0, resume=False, kernel=0, freeze=True):
+    def _opts(theta=1.0, data_term=0, init=0, resume=False, kernel=0, freeze=True, exchange=True):
         o = N.vol_opts()
         N.lib().vol_default_opts(ctypes.byref(o))
         o.theta, o.data_term, o.init, o.resume, o.kernel = float(theta), int(data_term), int(init), int(bool(resume)), int(kernel)
         o.freeze = int(bool(freeze))
+        o.exchange = int(bool(exchange))
         return o
 
     def regularise(self, lam: float, eps: float, tau: float, sigma: float, iters: int, *, theta: float = 1.0,
-                   data_term: int = 0, init: int = 0, resume: bool = False, kernel: int = 0, freeze: bool = True):
-        """`iters` Chambolle–Pock iterations (asynchronous on the volume's stream)."""
-        o = self._opts(theta, data_term, init, resume, kernel, freeze)
+                   data_term: int = 0, init: int = 0, resume: bool = False, kernel: int = 0, freeze: bool = True,
+                   exchange: bool = True):
+        """`iters` Chambolle–Pock iterations (asynchronous on the volume's stream).  `exchange=False`
+        (sharded volumes) replaces the halo exchange by a no-op: wrong results, timing only."""
+        o = self._opts(theta, data_term, init, resume, kernel, freeze, exchange)
         N.check(self._lib.vol_regularise(self._h, lam, eps, tau, sigma, int(iters), ctypes.byref(o)))
         return self
 
@@ -167,6 +170,13 @@ class Volume:
         kw.setdefault("data_term", scene.data_term)
         kw.setdefault("init", scene.init)
         return self.regularise(scene.lam, scene.eps, scene.tau, scene.sigma, it, **kw)
+
+    def shard_timing(self):
+        """(interior_ms, exchange_ms, boundary_ms) of the last iteration of the last sharded call: launch A,
+        the halo chain (pack → NCCL → unpack, communication stream) and launch B, from CUDA events."""
+        a, c, b = ctypes.c_float(), ctypes.c_float(), ctypes.c_float()
+        N.check(self._lib.vol_shard_timing(self._h, ctypes.byref(a), ctypes.byref(c), ctypes.byref(b)))
+        return a.value, c.value, b.value
 
     @property
     def last_launches(self) -> int:

@@ -307,6 +307,12 @@ def test_nccl_runtime_world1(V):
         assert np.array_equal(vol.u().cpu().numpy(), u1)
         E = vol.energy(s.lam, s.eps, s.data_term)
         assert abs(E[0] - E1[0]) <= 1e-9 * abs(E1[0]) and abs(E[1] - E1[1]) <= 1e-9 * abs(E1[0])
+        # per-stream timing of the last iteration: interior A, halo chain, boundary B
+        a, c, b = vol.shard_timing()
+        assert a >= 0 and c >= 0 and b >= 0
+        # no-op exchange (timing only): with no peers nothing is exchanged, so the bits are unchanged
+        vol.regularise_scene(s, exchange=False)
+        assert np.array_equal(vol.u().cpu().numpy(), u1)
         vol.close()
     finally:
         dist.destroy_process_group()
