@@ -93,7 +93,8 @@ size_t vol_workspace_bytes(const int32_t *block_xyz, int64_t n_global, const vol
  * Builds on the device: the spatial hash h(x,y,z) = ((u32)x·73856093 ⊕ (u32)y·19349669 ⊕
  * (u32)z·83492791) mod T with T = next power of two >= 2n, a CSR bucket table ordered by caller
  * index (reading c-14), and the 6-neighbour block table (−x,+x,−y,+y,−z,+z; −1 = unallocated).
- * Errors: VOL_EINVAL (n_global < 1, NULL pointers), VOL_EDATA (duplicate coordinates — the first
+ * Errors: VOL_EINVAL (n_global < 1, NULL pointers, 2^23 or more local + ghost blocks on one GPU —
+ * the iteration kernels index voxels with 32 bits), VOL_EDATA (duplicate coordinates — the first
  * repeated pair is named in vol_last_error —, coordinates out of range, non-finite f/W, W < 0),
  * VOL_ENOMEM, VOL_ECUDA.                                                                          */
 vol_status vol_create(const int32_t *block_xyz, int64_t n_global, const float *f, const float *W,

@@ -244,6 +244,12 @@ extern "C" vol_status vol_create(const int32_t *block_xyz, int64_t n_global, con
         L.n_local = n_global;
         L.S = n_global;
     }
+    // the iteration kernels index voxels with 32 bits (one GPU holds < 2^32 voxels: 2^23 blocks of
+    // 41 B per voxel are already 176 GB)
+    if (L.S >= ((int64_t)1 << 23))
+        return bail(fail(VOL_EINVAL, "vol_create: %lld store rows (local + ghost) on one GPU; at most 2^23 - 1 "
+                                     "(32-bit voxel indexing) — shard the volume over more GPUs",
+                         (long long)L.S));
     v->L = L;
     size_t need = layout_bytes(L) + (sharded ? shard_extra_bytes(plan) : 0);
     if (workspace) {
