@@ -271,6 +271,9 @@ class Volume:
 
 # -- TSDF fusion (paper §III-A, Eq. 1) -----------------------------------------
 
+_fuse_cap_hint = [65536]
+
+
 def fuse(depth, poses, intr, voxel: float, mu: float, max_range: float, w_max: float, *, max_blocks=None,
          stream=None, return_first=True, stats=None, prev=None):
     """Fuse K posed depth maps into hashed voxel blocks on the GPU (``vol_fuse``).
@@ -306,7 +309,10 @@ def fuse(depth, poses, intr, voxel: float, mu: float, max_range: float, w_max: f
         (pxp, pxk), (pfp, pfk), (pwp, pwk) = _ptr(pxyz), _ptr(pf), _ptr(pW)
     else:
         n_prev, pxp, pfp, pwp = 0, None, None, None
-    cap = int(max_blocks) if max_blocks else max(65536, 2 * n_prev)
+    # capacity: twice the block count of the previous call (a high-water hint like an allocator's, so a
+    # stream of similar fusions sizes its buffers right the first time), at least 2·n_prev and 65536;
+    # on overflow the call is retried with 4x the capacity
+    cap = int(max_blocks) if max_blocks else max(65536, 2 * n_prev, _fuse_cap_hint[0])
     while True:
         xyz = torch.empty(cap, 3, dtype=torch.int32, device=dev)
         first = torch.empty(cap, dtype=torch.int32, device=dev)
@@ -328,6 +334,8 @@ def fuse(depth, poses, intr, voxel: float, mu: float, max_range: float, w_max: f
         N.check(st)
         break
     m = n.value
+    if not max_blocks:
+        _fuse_cap_hint[0] = max(65536, 2 * m)
     if stats is not None:
         stats.update({k: getattr(sts, k) for k, _ in N.vol_fusion_stats._fields_})
     out = (xyz[:m], first[:m], f[:m], W[:m])
