@@ -138,6 +138,8 @@ def make_scene(cfg: str, world: int, seed: int, device):
         if world > 1:
             s.name = f"street-{int(length)}m"
         return s
+    if cfg.startswith("city"):
+        return scenes.by_name(cfg, seed=seed, device=device, chunk_blocks=4096)
     return scenes.by_name(cfg, seed=seed, device=device)
 
 

@@ -168,10 +168,30 @@ def _canyon_sd(seg: Segment, X, Y, Z, H):
     return torch.minimum(Z, torch.maximum(inner, Z - H))
 
 
-def _box_sd(X, Y, Z, boxes):
-    """min over axis-aligned boxes of the exterior signed distance (positive outside). boxes [k, 6]."""
+_BOX_SD_DIRECT = 1 << 28   # points x boxes evaluated in one tensor; above it, sub-chunks with box culling
+
+
+def _box_sd(X, Y, Z, boxes, cut=None):
+    """min over axis-aligned boxes of the exterior signed distance (positive outside). boxes [k, 6].
+
+    `cut`: callers only use min(sd, ·) clamped at or below `cut` (f = clamp(sd/μ), |sd| ≤ μ tests), so for
+    large problems (city-heavy: thousands of boxes) points are processed in spatially compact sub-chunks
+    and boxes farther than `cut` from a sub-chunk's bounding box are skipped: where the true minimum is
+    < cut its box is kept, elsewhere both values are >= cut — identical results downstream.  Street and
+    city stay below _BOX_SD_DIRECT and take the direct path."""
     if boxes.shape[0] == 0:
         return torch.full_like(X, float("inf"))
+    if cut is not None and X.numel() * boxes.shape[0] > _BOX_SD_DIRECT:
+        out = torch.empty_like(X)
+        step = 16384
+        for i in range(0, X.numel(), step):
+            x, y, z = X[i:i + step], Y[i:i + step], Z[i:i + step]
+            pmin = torch.stack([x.min(), y.min(), z.min()])
+            pmax = torch.stack([x.max(), y.max(), z.max()])
+            gap = torch.clamp(torch.maximum(boxes[:, 0:3] - pmax, pmin - boxes[:, 3:6]), min=0.0)
+            near = torch.linalg.norm(gap, dim=1) <= cut
+            out[i:i + step] = _box_sd(x, y, z, boxes[near]) if bool(near.any()) else float("inf")
+        return out
     lo = boxes[:, 0:3]
     hi = boxes[:, 3:6]
     P = torch.stack([X, Y, Z], -1)[..., None, :]              # [..., 1, 3]
@@ -183,11 +203,11 @@ def _box_sd(X, Y, Z, boxes):
     return (outside + inside).min(dim=-1).values
 
 
-def _scene_sd(X, Y, Z, segs, boxes, H):
+def _scene_sd(X, Y, Z, segs, boxes, H, cut=None):
     sd = _canyon_sd(segs[0], X, Y, Z, H)
     for seg in segs[1:]:
         sd = torch.maximum(sd, _canyon_sd(seg, X, Y, Z, H))
-    return torch.minimum(sd, _box_sd(X, Y, Z, boxes))
+    return torch.minimum(sd, _box_sd(X, Y, Z, boxes, cut))
 
 
 def _ray_first_hit(seg: Segment, cam, P, boxes, H):
@@ -311,7 +331,7 @@ def _route_scene(name, segs, boxes_per_seg, v, mu, H, seed, cfg, device, chunk_b
     for bx0 in range(lo[0], hi[0] + 1, 64):
         grid = _block_grid((bx0, lo[1], lo[2]), (min(bx0 + 63, hi[0]), hi[1], hi[2]), device)
         c = (grid.to(torch.float64) + 0.5) * B
-        sd = _scene_sd(c[:, 0], c[:, 1], c[:, 2], segs, allboxes, H)
+        sd = _scene_sd(c[:, 0], c[:, 1], c[:, 2], segs, allboxes, H, cut=mu + half_diag)
         m = sd.abs() <= mu + half_diag
         if near_pred is not None:
             m &= near_pred(c)
@@ -328,7 +348,7 @@ def _route_scene(name, segs, boxes_per_seg, v, mu, H, seed, cfg, device, chunk_b
     for i in range(0, cand.shape[0], chunk_blocks):
         cb = cand[i:i + chunk_blocks]
         P = voxel_centres(cb, v).reshape(-1, 3)
-        sd = _scene_sd(P[:, 0], P[:, 1], P[:, 2], segs, allboxes, H)
+        sd = _scene_sd(P[:, 0], P[:, 1], P[:, 2], segs, allboxes, H, cut=mu)
         # restrict observation work to segments whose samples can reach the chunk
         segs_i, cams_i, boxes_i = [], [], []
         pmin, pmax = P.min(0).values, P.max(0).values
