@@ -372,15 +372,24 @@ def _route_scene(name, segs, boxes_per_seg, v, mu, H, seed, cfg, device, chunk_b
     return coords, sd, W
 
 
-def _street_noise(coords, sd, W, v, mu, seed, cfg, path_dist):
-    """f = clamp(sd/μ, −1, 1) + N(0, 0.02·d²), d = distance to the camera path; f = 0 where unobserved."""
-    gv = global_voxel_coords(coords)
-    ctr = rng.pack_coords(gv[..., 0], gv[..., 1], gv[..., 2])
-    P = voxel_centres(coords, v)
-    d = path_dist(P)
-    f = (sd / mu).clamp(-1.0, 1.0) + 0.02 * d * d * _normal(seed, cfg, ctr)
-    f = torch.where(W > 0, f, torch.zeros_like(f))
-    return f, ctr
+def _street_noise(coords, sd, W, v, mu, seed, cfg, path_dist, want_ctr=True, chunk=65536):
+    """f = clamp(sd/μ, −1, 1) + N(0, 0.02·d²), d = distance to the camera path; f = 0 where unobserved.
+    Element-wise, evaluated in chunks of blocks (bounded temporaries for city-heavy); returns (f fp64,
+    the voxel counters or None)."""
+    n = coords.shape[0]
+    f = torch.empty(n, 512, dtype=torch.float64, device=coords.device)
+    ctr_all = torch.empty(n, 512, dtype=torch.int64, device=coords.device) if want_ctr else None
+    for i in range(0, n, chunk):
+        c = coords[i:i + chunk]
+        gv = global_voxel_coords(c)
+        ctr = rng.pack_coords(gv[..., 0], gv[..., 1], gv[..., 2])
+        P = voxel_centres(c, v)
+        d = path_dist(P)
+        fi = (sd[i:i + chunk] / mu).clamp(-1.0, 1.0) + 0.02 * d * d * _normal(seed, cfg, ctr)
+        f[i:i + chunk] = torch.where(W[i:i + chunk] > 0, fi, torch.zeros_like(fi))
+        if want_ctr:
+            ctr_all[i:i + chunk] = ctr
+    return f, ctr_all
 
 
 STREET_H = 25.0   # façade height (SURVEY §8(d) "calibrate so N_alloc ≈ 3e7 ± 30 %, then freeze")
@@ -485,7 +494,7 @@ def city(seed: int = 0, length: float = 1000.0, H: float = 20.0, device="cpu", c
             best = d if best is None else torch.minimum(best, d)
         return best
 
-    f, _ = _street_noise(coords, sd, W, v, mu, seed, cfg, path_dist)
+    f, _ = _street_noise(coords, sd, W, v, mu, seed, cfg, path_dist, want_ctr=False)
     meta = dict(voxel=v, mu=mu, H=H, length=length, seed=seed, segments=[(s.x0, s.y0, s.dx, s.dy, s.L) for s in all_segs])
     return Scene("city", coords, f.float().contiguous(), W.float().contiguous(), lam=0.8, eps=0.01, iters=200,
                  meta=meta)
