@@ -203,7 +203,37 @@ def _box_sd(X, Y, Z, boxes, cut=None):
     return (outside + inside).min(dim=-1).values
 
 
+def _near_segments(segs, X, Y, cut):
+    """Capped segments whose footprint rectangle (s ∈ [−4, L+4], |lat| ≤ 4) lies at Chebyshev distance
+    < cut from the points' xy bounding box; (kept, any_dropped).  A dropped segment has inner ≤ −cut at
+    every point, so its canyon sd there is exactly Z − H when Z − H > −cut and ≤ −cut otherwise."""
+    xmin, xmax, ymin, ymax = float(X.min()), float(X.max()), float(Y.min()), float(Y.max())
+    kept = []
+    for seg in segs:
+        if not seg.caps:
+            kept.append(seg)
+            continue
+        xs = [seg.x0 + a * seg.dx - b * seg.dy for a in (-HALF_WIDTH, seg.L + HALF_WIDTH) for b in (-HALF_WIDTH, HALF_WIDTH)]
+        ys = [seg.y0 + a * seg.dy + b * seg.dx for a in (-HALF_WIDTH, seg.L + HALF_WIDTH) for b in (-HALF_WIDTH, HALF_WIDTH)]
+        gx = max(min(xs) - xmax, xmin - max(xs), 0.0)
+        gy = max(min(ys) - ymax, ymin - max(ys), 0.0)
+        if max(gx, gy) < cut:
+            kept.append(seg)
+    return kept, len(kept) < len(segs)
+
+
 def _scene_sd(X, Y, Z, segs, boxes, H, cut=None):
+    """Union of the canyons' free space (max of their sd) minus the boxes (min).  With `cut` and many
+    segments (city-heavy) only the segments near the points are evaluated; the dropped ones contribute
+    exactly Z − H where that exceeds −cut (see _near_segments), so every value > −cut is unchanged and
+    every value ≤ −cut stays ≤ −cut — identical after the clamp and the |sd| ≤ cut tests downstream."""
+    if cut is not None and len(segs) > 8:
+        kept, dropped = _near_segments(segs, X, Y, cut)
+        sd = Z - H if dropped else None
+        for seg in kept:
+            c = _canyon_sd(seg, X, Y, Z, H)
+            sd = c if sd is None else torch.maximum(sd, c)
+        return torch.minimum(sd, _box_sd(X, Y, Z, boxes, cut))
     sd = _canyon_sd(segs[0], X, Y, Z, H)
     for seg in segs[1:]:
         sd = torch.maximum(sd, _canyon_sd(seg, X, Y, Z, H))
@@ -312,7 +342,7 @@ def _make_boxes(seed, cfg, segs, per_metre, device):
 
 
 def _route_scene(name, segs, boxes_per_seg, v, mu, H, seed, cfg, device, chunk_blocks, R=25.0,
-                 cam_step=1.0, near_pred=None):
+                 cam_step=1.0, near_pred=None, compact=False):
     """Shared body of street and city: candidate blocks → sd, W per voxel → allocation → f."""
     allboxes = torch.cat(boxes_per_seg, 0) if boxes_per_seg else torch.zeros(0, 6, dtype=torch.float64, device=device)
     B = 8 * v
@@ -337,6 +367,13 @@ def _route_scene(name, segs, boxes_per_seg, v, mu, H, seed, cfg, device, chunk_b
             m &= near_pred(c)
         cand_all.append(grid[m])
     cand = torch.cat(cand_all, 0)
+    if compact:
+        # spatially compact chunks (16³-block super cells in x, y, z order) so each chunk's observation
+        # work involves only the nearby segments and cameras (city-heavy: 13 parallel lanes); the
+        # per-voxel values do not depend on the chunking, only the output block order does
+        sc = (cand.to(torch.int64) >> 4) + (1 << 20)
+        key = (sc[:, 0] << 42) | (sc[:, 1] << 21) | sc[:, 2]
+        cand = cand[torch.argsort(key, stable=True)]
     # camera samples per segment
     seg_samples = []
     for seg in segs:
@@ -483,7 +520,8 @@ def city(seed: int = 0, length: float = 1000.0, H: float = 20.0, device="cpu", c
                   for k in range(lanes) for s in segs]
     all_segs = lanes_segs if lanes > 1 else segs
     boxes = _make_boxes(seed, cfg, all_segs, 20.0 / 60.0, device)
-    coords, sd, W = _route_scene("city", all_segs, boxes, v, mu, H, seed, cfg, device, chunk_blocks)
+    coords, sd, W = _route_scene("city", all_segs, boxes, v, mu, H, seed, cfg, device, chunk_blocks,
+                                 compact=lanes > 1)
 
     def path_dist(P):
         best = None
