@@ -293,6 +293,7 @@ def _observations(P, segs, seg_samples, boxes_of_seg, H, mu, R):
     distance ≥ dist − μ (paper Eq. 1: w is incremented iff u_SDF ≥ −μ).
     """
     cnt = torch.zeros(P.shape[0], dtype=torch.int32, device=P.device)
+    pmin, pmax = P.min(0).values, P.max(0).values
     for seg, cams, boxes in zip(segs, seg_samples, boxes_of_seg):
         for cam in cams:
             D = P - cam
@@ -300,7 +301,15 @@ def _observations(P, segs, seg_samples, boxes_of_seg, H, mu, R):
             inr = dist <= R
             if not bool(inr.any()):
                 continue
-            t = _ray_first_hit(seg, cam, P, boxes, H)
+            # a box can only cut a segment cam→P if it meets the bounding box of cam and the points:
+            # the others never register a hit in the slab test, so skipping them is exact
+            if boxes.shape[0] > 4:
+                lo, hi = torch.minimum(pmin, cam), torch.maximum(pmax, cam)
+                meet = ((boxes[:, 3:6] >= lo) & (boxes[:, 0:3] <= hi)).all(dim=1)
+                bx = boxes[meet]
+            else:
+                bx = boxes
+            t = _ray_first_hit(seg, cam, P, bx, H)
             obs = inr & (t * dist >= dist - mu)
             cnt += obs.to(torch.int32)
     return cnt.clamp(max=30)
