@@ -543,8 +543,8 @@ def city(seed: int = 0, length: float = 1000.0, H: float = 20.0, device="cpu", c
 
     f, _ = _street_noise(coords, sd, W, v, mu, seed, cfg, path_dist, want_ctr=False)
     meta = dict(voxel=v, mu=mu, H=H, length=length, seed=seed, segments=[(s.x0, s.y0, s.dx, s.dy, s.L) for s in all_segs])
-    return Scene("city", coords, f.float().contiguous(), W.float().contiguous(), lam=0.8, eps=0.01, iters=200,
-                 meta=meta)
+    return Scene("city" if lanes == 1 else "city-heavy", coords, f.float().contiguous(), W.float().contiguous(),
+                 lam=0.8, eps=0.01, iters=200, meta=meta)
 
 
 # ----------------------------------------------------------------------------------------------
