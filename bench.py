@@ -612,6 +612,11 @@ def main():
     if nf:
         nf_ach = ALG_BYTES_PER_VOXEL * n_local_vox / (nf["avg_launch_ms"] / 1e3) / 1e9
         nf.update({"achieved": nf_ach, "frac": nf_ach / peak})
+        nft = (tr or {}).get("no_freeze") if tr and tr.get("workload") == scene.name and args.kernel == 0 else None
+        if nft:
+            nf["traffic"] = nft["dram_bytes_per_launch"]
+            nf["dram_gbs_actual"] = nft["dram_bytes_per_launch"] / (nf["avg_launch_ms"] / 1e3) / 1e9
+            nf["dram_frac_actual"] = nf["dram_gbs_actual"] / peak
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         sc = scene.to("cpu")
