@@ -250,7 +250,13 @@ __device__ __forceinline__ bool quad_of(const Img &g, Quad &q) {
     return true;
 }
 
-__global__ void __launch_bounds__(256) k_dual4(State S, Img g, Steps P) {
+#ifndef HVG_DUAL4_MINB
+#define HVG_DUAL4_MINB 1
+#endif
+#ifndef HVG_PRIMAL4_MINB
+#define HVG_PRIMAL4_MINB 1
+#endif
+__global__ void __launch_bounds__(256, HVG_DUAL4_MINB) k_dual4(State S, Img g, Steps P) {
     Quad Q;
     if (!quad_of(g, Q)) return;
     const unsigned i = Q.i, W = (unsigned)g.W;
@@ -300,7 +306,7 @@ __global__ void __launch_bounds__(256) k_dual4(State S, Img g, Steps P) {
     st4(S.q1 + i, q1); st4(S.q2 + i, q2); st4(S.q3 + i, q3); st4(S.q4 + i, q4);
 }
 
-__global__ void __launch_bounds__(256) k_primal4(State S, Img g, Steps P) {
+__global__ void __launch_bounds__(256, HVG_PRIMAL4_MINB) k_primal4(State S, Img g, Steps P) {
     Quad Q;
     if (!quad_of(g, Q)) return;
     const unsigned i = Q.i, W = (unsigned)g.W;
