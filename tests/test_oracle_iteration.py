@@ -198,6 +198,53 @@ def test_rof_step_closed_form(c, w):
     assert np.abs(u - want).max() < 1e-4
 
 
+def _tvl1_dp_min(f, lw):
+    """Exact minimum of the 1-D TV-L1 energy Σ|u_{i+1} − u_i| + lw·Σ|u_i − f_i| (SURVEY §8(c) '1-D exact
+    minimiser'): a minimiser exists with every value in {f_j} (the energy is piecewise linear and its
+    breakpoints in each u_i are the data values), so dynamic programming over those levels is exact."""
+    levels = np.unique(f)
+    V = lw * np.abs(levels - f[0])
+    jump = np.abs(levels[:, None] - levels[None, :])
+    for fi in f[1:]:
+        V = lw * np.abs(levels - fi) + (V[None, :] + jump).min(axis=1)
+    return float(V.min())
+
+
+@pytest.mark.parametrize("seed,lam", [(1, 0.35), (2, 0.6), (3, 0.9)])
+def test_tvl1_1d_energy_reaches_exact_dp_minimum(seed, lam):
+    # random 1-D data (not a closed-form case): the CP iterate's energy must reach the exact minimum
+    rng = np.random.default_rng(seed)
+    n = 24
+    f = np.round(rng.normal(0.0, 1.0, n), 2).astype(np.float32).astype(np.float64)
+    lam = F32(lam)
+    s = line_scene(f, 1.0, axis=seed % 3, lam=lam, iters=30000)
+    u = _line_u(s)
+    E = float(np.abs(np.diff(u)).sum() + lam * np.abs(u - f).sum())
+    Emin = _tvl1_dp_min(f, lam)
+    assert Emin <= E + 1e-9                      # the DP value is a true lower bound
+    assert E - Emin <= 1e-4 * max(1.0, Emin)     # and the iterate attains it
+
+
+@pytest.mark.parametrize("seed,lam,w", [(4, 0.8, 1.0), (5, 2.0, 3.0)])
+def test_rof_1d_matches_exact_minimiser(seed, lam, w):
+    # 1-D weighted ROF (paper Eq. 8 data term (λW/2)(u − f)²) solved exactly through its dual, a
+    # box-constrained least-squares problem: u* = f − Dᵀp*/(λW), p* = argmin_{|p| ≤ 1} ‖Dᵀp/√(λW) − √(λW) f‖²
+    from scipy.optimize import lsq_linear
+    rng = np.random.default_rng(seed)
+    n = 24
+    f = rng.normal(0.0, 1.0, n).astype(np.float32).astype(np.float64)
+    lam = F32(lam)
+    lw = lam * w
+    D = np.zeros((n - 1, n))
+    D[np.arange(n - 1), np.arange(n - 1)] = -1.0
+    D[np.arange(n - 1), np.arange(1, n)] = 1.0
+    r = lsq_linear(D.T / np.sqrt(lw), np.sqrt(lw) * f, bounds=(-1.0, 1.0), tol=1e-14, lsmr_tol="auto", max_iter=10000)
+    u_star = f - D.T @ r.x / lw
+    s = line_scene(f, w, axis=seed % 3, lam=lam, data_term=1, iters=20000)
+    u = _line_u(s)
+    assert np.abs(u - u_star).max() < 1e-5
+
+
 def test_l2_zero_and_warm_init_reach_same_minimiser():
     s = random_instance(8, seed=7, extent=1, data_term=1, lam=2.0, iters=3000)
     a, _, _ = oracle.regularise_scene(s)
