@@ -37,23 +37,42 @@ struct ExArgs {
 
 // Cube corners are coded c = i + 2j + 4k for the offset (i, j, k) ∈ {0,1}^3 from the cell origin.
 
+// Voxel-centre coordinates of one cell: X[b][k] = fl(fl((float)(o_k + b) + ½)·v) for the cell origin o
+// and b ∈ {0, 1}, and dX[k] = fl(X[1][k] − X[0][k]).  Every quantity of X-4 is one of these: P_lo and
+// P_hi of an edge are corner coordinates, and P_hi − P_lo is ±dX[k] on an axis where the ends differ
+// (fl(a − b) = −fl(b − a)) and 0 where they agree — where p = P_lo + t·0 = P_lo exactly (P_lo ≠ 0).
+struct CellGeom {
+    float X[2][3];
+    float dX[3];
+};
+__device__ __forceinline__ CellGeom cell_geom(int ox, int oy, int oz, float voxel) {
+    CellGeom G;
+    const int o[3] = {ox, oy, oz};
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+        G.X[0][k] = __fmul_rn(__fadd_rn((float)o[k], 0.5f), voxel);
+        G.X[1][k] = __fmul_rn(__fadd_rn((float)(o[k] + 1), 0.5f), voxel);
+        G.dX[k] = __fsub_rn(G.X[1][k], G.X[0][k]);
+    }
+    return G;
+}
+
 // X-4: vertex on the edge between cell corners ca and cb (values ua, ub).  The ends are ordered by global
 // voxel coordinate, lexicographically in (x, y, z); inside one cell that is the order of the offsets.
-__device__ __forceinline__ void edge_vertex(int ox, int oy, int oz, int ca, float ua, int cb, float ub, float voxel,
-                                            float *p) {
+// t = u_lo/(u_lo − u_hi), p = P_lo + t·(P_hi − P_lo) per coordinate, in fp32 (the oracle's written order).
+__device__ __forceinline__ void edge_vertex(const CellGeom &G, int ca, float ua, int cb, float ub, float *p) {
     const int ax = ca & 1, ay = (ca >> 1) & 1, az = ca >> 2;
     const int bx = cb & 1, by = (cb >> 1) & 1, bz = cb >> 2;
     const bool swap = ax != bx ? bx < ax : (ay != by ? by < ay : bz < az);
-    const int lx = swap ? bx : ax, ly = swap ? by : ay, lz = swap ? bz : az;
-    const int hx = swap ? ax : bx, hy = swap ? ay : by, hz = swap ? az : bz;
+    const int cl = swap ? cb : ca, ch = swap ? ca : cb;
     const float ulo = swap ? ub : ua, uhi = swap ? ua : ub;
     const float t = __fdiv_rn(ulo, __fsub_rn(ulo, uhi));
-    const int lo[3] = {ox + lx, oy + ly, oz + lz}, hi[3] = {ox + hx, oy + hy, oz + hz};
 #pragma unroll
     for (int k = 0; k < 3; k++) {
-        const float plo = __fmul_rn(__fadd_rn((float)lo[k], 0.5f), voxel);
-        const float phi = __fmul_rn(__fadd_rn((float)hi[k], 0.5f), voxel);
-        p[k] = __fadd_rn(plo, __fmul_rn(t, __fsub_rn(phi, plo)));
+        const int al = (cl >> k) & 1, ah = (ch >> k) & 1;
+        const float plo = al ? G.X[1][k] : G.X[0][k];
+        const float d = ah ? G.dX[k] : -G.dX[k];
+        p[k] = al == ah ? plo : __fadd_rn(plo, __fmul_rn(t, d));
     }
 }
 
@@ -87,8 +106,8 @@ __device__ __forceinline__ float sel4f(int i, float a0, float a1, float a2, floa
 // goes first, the remaining corners follow in tetrahedron order, and the last two are swapped when that
 // permutation is odd, so (a, b, c, d) stays positively oriented.
 template <bool EMIT>
-__device__ __forceinline__ void tet(int k0, int k1, int k2, int k3, float v0, float v1, float v2, float v3, int ox,
-                                    int oy, int oz, float voxel, float *out, unsigned &m) {
+__device__ __forceinline__ void tet(int k0, int k1, int k2, int k3, float v0, float v1, float v2, float v3,
+                                    const CellGeom &G, float *out, unsigned &m) {
     const int mask = (v0 < 0.0f) | ((v1 < 0.0f) << 1) | ((v2 < 0.0f) << 2) | ((v3 < 0.0f) << 3);   // X-3
     if (mask == 0 || mask == 15) return;
     const int nin = __popc(mask);
@@ -119,18 +138,18 @@ __device__ __forceinline__ void tet(int k0, int k1, int k2, int k3, float v0, fl
     const float uc = sel4f(pc, v0, v1, v2, v3), ud = sel4f(pd, v0, v1, v2, v3);
     float e1[3], e2[3], e3[3];
     if (nin != 2) {
-        edge_vertex(ox, oy, oz, ca, ua, cb, ub, voxel, e1);
-        edge_vertex(ox, oy, oz, ca, ua, cc, uc, voxel, e2);
-        edge_vertex(ox, oy, oz, ca, ua, cd, ud, voxel, e3);
+        edge_vertex(G, ca, ua, cb, ub, e1);
+        edge_vertex(G, ca, ua, cc, uc, e2);
+        edge_vertex(G, ca, ua, cd, ud, e3);
         // 1 inside: never degenerate; 1 outside (a): all three vertices sit on a iff u_a = 0
         if (nin == 1) put<EMIT>(out, m, e1, e2, e3, false);
         else put<EMIT>(out, m, e1, e3, e2, ua == 0.0f);
     } else {
         float e4[3];
-        edge_vertex(ox, oy, oz, ca, ua, cc, uc, voxel, e1);   // E_ac
-        edge_vertex(ox, oy, oz, ca, ua, cd, ud, voxel, e2);   // E_ad
-        edge_vertex(ox, oy, oz, cb, ub, cd, ud, voxel, e3);   // E_bd
-        edge_vertex(ox, oy, oz, cb, ub, cc, uc, voxel, e4);   // E_bc
+        edge_vertex(G, ca, ua, cc, uc, e1);   // E_ac
+        edge_vertex(G, ca, ua, cd, ud, e2);   // E_ad
+        edge_vertex(G, cb, ub, cd, ud, e3);   // E_bd
+        edge_vertex(G, cb, ub, cc, uc, e4);   // E_bc
         put<EMIT>(out, m, e1, e2, e3, ud == 0.0f);   // E_ad = E_bd iff u_d = 0
         put<EMIT>(out, m, e1, e3, e4, uc == 0.0f);   // E_ac = E_bc iff u_c = 0
     }
@@ -286,9 +305,9 @@ __global__ void __launch_bounds__(128) k_extract(ExArgs A, int64_t n_rows, uint3
             const uint32_t round_total = swarp[0] + swarp[1] + swarp[2] + swarp[3];
             if (cnt) {
                 unsigned m = 0;
+                const CellGeom G = cell_geom(gx + cx, gy + cyy, gz + czz, A.voxel);
                 tet<true>(0, k1, k2, k3, su[tile_index(cx, cyy, czz, 0)], su[tile_index(cx, cyy, czz, k1)],
-                          su[tile_index(cx, cyy, czz, k2)], su[tile_index(cx, cyy, czz, k3)], gx + cx, gy + cyy,
-                          gz + czz, A.voxel, sout + 9 * before, m);
+                          su[tile_index(cx, cyy, czz, k2)], su[tile_index(cx, cyy, czz, k3)], G, sout + 9 * before, m);
             }
             __syncthreads();
             float *dst = base_out + 9ull * run;
@@ -298,8 +317,7 @@ __global__ void __launch_bounds__(128) k_extract(ExArgs A, int64_t n_rows, uint3
             unsigned m = 0;
             if (i < n_items)
                 tet<false>(0, k1, k2, k3, su[tile_index(cx, cyy, czz, 0)], su[tile_index(cx, cyy, czz, k1)],
-                           su[tile_index(cx, cyy, czz, k2)], su[tile_index(cx, cyy, czz, k3)], gx + cx, gy + cyy,
-                           gz + czz, A.voxel, nullptr, m);
+                           su[tile_index(cx, cyy, czz, k2)], su[tile_index(cx, cyy, czz, k3)], CellGeom{}, nullptr, m);
             const uint32_t b0 = __ballot_sync(0xffffffffu, m & 1u), b1 = __ballot_sync(0xffffffffu, (m >> 1) & 1u);
             if (lane == 0 && i0 + 32 * wid < n_items) {
                 uint32_t *wb = item_bits + (size_t)r * kItemWords + 2 * ((i0 >> 5) + wid);
