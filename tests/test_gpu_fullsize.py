@@ -106,6 +106,18 @@ def test_street_full_iterations_invariants(V):
     assert np.abs(u - f)[(W > 0) & ~pin].max() > 1e-3
 
 
+def test_street_outlier_full_size_full_iterations_bitwise(V):
+    """Config 3 at full size and all 500 TV-L1 iterations (≥ 30 % of the voxels unobserved in clumps, 5 %
+    impulse outliers): every voxel bit-identical to the fp32 oracle (OpenMP timing build)."""
+    s = _scene("street-outlier")
+    vol = V(s.coords.cuda(), s.f.cuda(), s.W.cuda())
+    vol.regularise_scene(s)
+    u = vol.u().cpu().numpy()
+    u32, _, _ = oracle.regularise(s.coords, s.f, s.W, s.lam, s.eps, s.tau, s.sigma, s.iters, theta=s.theta,
+                                  data_term=s.data_term, init=s.init, precision="f32", omp=True)
+    assert np.array_equal(u.view(np.uint32), u32.view(np.uint32))
+
+
 def _small_components(s, max_vox=150000, want=6):
     """Connected components (6-connectivity) of Ω with at most `max_vox` voxels, by block sets."""
     from scipy import ndimage
