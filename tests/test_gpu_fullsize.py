@@ -176,7 +176,8 @@ def _city():
 
 def test_city_first_iterations_match_oracle(V):
     """configs[3] geometry (staircase route, v = 10 cm, μ = 0.5 m, Huber-TV): the whole volume after
-    2 iterations, bitwise against the fp32 oracle and within 1e-5 of fp64."""
+    2 iterations, bitwise against the fp32 oracle and within 1e-5 of fp64; after all 200 iterations
+    bitwise against the fp32 oracle."""
     s = _city()
     assert s.n_alloc > 2e7
     vol = V(s.coords.cuda(), s.f.cuda(), s.W.cuda())
@@ -187,6 +188,12 @@ def test_city_first_iterations_match_oracle(V):
     assert np.array_equal(u, u32)
     u64, _, _ = oracle.regularise_scene(s, precision="f64", iters=2, nbr=nbr)
     assert float(np.abs(u - u64).max()) <= 1e-5
+    # and after the config's full 200 iterations, bit for bit (OpenMP timing build of the oracle)
+    vol.regularise_scene(s)
+    u = vol.u().cpu().numpy()
+    u32, _, _ = oracle.regularise(s.coords, s.f, s.W, s.lam, s.eps, s.tau, s.sigma, s.iters, theta=s.theta,
+                                  data_term=s.data_term, init=s.init, precision="f32", nbr=nbr, omp=True)
+    assert np.array_equal(u.view(np.uint32), u32.view(np.uint32))
 
 
 def test_city_route_shards_bitwise_equal_single(V):
