@@ -385,7 +385,85 @@ extern "C" void vol_destroy(vol_t v) {
 
 // ------------------------------------------------------------------------------- iterations
 
+// Skewed schedule (opts.kernel = 2, single GPU): k_dual (p^1 from ū^0), iters − 1 launches of k_skew
+// (primal k + dual k+1), k_primal (u^iters, ū^iters).  u is double-buffered through the caller-order
+// scratch field d_tmp (free during iterations); both buffers start equal to u^0 so voxels that are never
+// written (Ω̄, frozen) hold the same value in both, and the buffer order is chosen so that the epilogue
+// updates F.u in place.
+static vol_status run_iterations_skew(vol_s *v, const IterParams &P, int32_t iters) {
+    cudaStream_t s = v->stream;
+    const int cur = v->cur;
+    const int64_t n = v->L.n_local;
+    const size_t ubytes = (size_t)n * kBlockVox * 4;
+    int64_t launches = 0;
+    CK(cudaMemcpyAsync(v->d_tmp, v->F.u, ubytes, cudaMemcpyDeviceToDevice, s));
+    float *B[2];
+    B[(iters - 1) & 1] = v->F.u;
+    B[iters & 1] = v->d_tmp;
+    {
+        View V = view_of(v->F, cur);   // ū^0 = ub[cur], p^0 = p[cur] → p^1 = p[cur ^ 1]
+        int r = launch_dual_only(V, v->d_nbr, n, P, s);
+        CKL(r);
+        launches += r;
+    }
+    auto skew = [&](cudaStream_t st, int j) -> int {
+        return launch_skew(v->F, B[j & 1], B[(j + 1) & 1], cur ^ ((j + 1) & 1), v->pending_frozen, v->d_nbr, n, P, st);
+    };
+    int j = 0;
+    const int total = iters - 1;
+    const int m = std::min<int>(16, total / 2);
+    if (m >= 1) {   // a graph of 2m launches (buffer parities repeat every 2), replayed
+        cudaGraph_t g = nullptr;
+        cudaGraphExec_t ge = nullptr;
+        CK(cudaStreamBeginCapture(v->cap, cudaStreamCaptureModeThreadLocal));
+        int per = 0, bad = 0;
+        for (int k = 0; k < 2 * m; k++) {
+            int r = skew(v->cap, k);
+            if (r < 0) bad = 1;
+            per += r;
+        }
+        cudaError_t e = cudaStreamEndCapture(v->cap, &g);
+        if (bad || e != cudaSuccess) {
+            if (g) cudaGraphDestroy(g);
+            return fail(VOL_ECUDA, "graph capture failed: %s", cudaGetErrorString(e != cudaSuccess ? e : cudaGetLastError()));
+        }
+        g_launches.fetch_sub(per);
+        e = cudaGraphInstantiate(&ge, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) return fail(VOL_ECUDA, "graph instantiate failed: %s", cudaGetErrorString(e));
+        const int reps = total / (2 * m);
+        for (int r = 0; r < reps; r++) {
+            e = cudaGraphLaunch(ge, s);
+            if (e != cudaSuccess) {
+                cudaGraphExecDestroy(ge);
+                return fail(VOL_ECUDA, "graph launch failed: %s", cudaGetErrorString(e));
+            }
+            launches += per;
+            g_launches.fetch_add(per);
+        }
+        cudaGraphExecDestroy(ge);
+        j = reps * 2 * m;
+    }
+    for (; j < total; j++) {
+        int r = skew(s, j);
+        CKL(r);
+        launches += r;
+    }
+    {
+        const int c2 = cur ^ (iters & 1);   // p^iters and the final ū live at index c2
+        View V = view_of(v->F, c2 ^ 1);     // px_out = p[c2], ub_out = ub[c2]
+        V.u = B[(iters - 1) & 1];           // == F.u
+        int r = launch_primal_only(V, v->d_nbr, n, P, s);
+        CKL(r);
+        launches += r;
+        v->cur = c2;
+    }
+    v->last_launches += launches;
+    return VOL_OK;
+}
+
 static vol_status run_iterations_single(vol_s *v, const IterParams &P, int32_t iters, int kernel) {
+    if (kernel == 2) return run_iterations_skew(v, P, iters);
     cudaStream_t s = v->stream;
     int64_t launches = 0;
     auto one = [&](cudaStream_t st, int cur) -> int {
@@ -455,8 +533,9 @@ vol_status vol_regularise_prepare(vol_s *v, float lambda, float eps, float tau, 
     if (!(o.theta >= 0.0f) || !std::isfinite(o.theta)) return fail(VOL_EINVAL, "theta must be >= 0");
     if (o.data_term != 0 && o.data_term != 1) return fail(VOL_EINVAL, "data_term must be 0 (L1) or 1 (L2)");
     if (o.init != 0 && o.init != 1) return fail(VOL_EINVAL, "init must be 0 (warm) or 1 (zero)");
-    if (o.kernel != 0 && o.kernel != 1) return fail(VOL_EINVAL, "kernel must be 0 (fused) or 1 (two-kernel)");
-    if (v->shard && o.kernel == 1) return fail(VOL_ENOTSUP, "two-kernel baseline is single-GPU only");
+    if (o.kernel < 0 || o.kernel > 2)
+        return fail(VOL_EINVAL, "kernel must be 0 (fused), 1 (two-kernel) or 2 (skewed fused)");
+    if (v->shard && o.kernel != 0) return fail(VOL_ENOTSUP, "the two-kernel and skewed schedules are single-GPU only");
     if (o.exchange != 0 && o.exchange != 1) return fail(VOL_EINVAL, "exchange must be 0 (no-op, timing only) or 1");
     if (v->shard) {
         vol_status st = shard_reset(v);
@@ -485,7 +564,7 @@ vol_status vol_regularise_prepare(vol_s *v, float lambda, float eps, float tau, 
         v->last_launches = 1;
     }
     v->pending_frozen = nullptr;
-    if (o.freeze && o.data_term == 0 && o.kernel == 0 && iters > 0) {
+    if (o.freeze && o.data_term == 0 && o.kernel != 1 && iters > 0) {
         CKL(launch_freeze_mask(v->F, v->cur, P, v->L.n_local, v->d_frozen, v->stream));
         v->pending_frozen = v->d_frozen;
         v->last_launches += 1;

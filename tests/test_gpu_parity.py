@@ -346,3 +346,38 @@ def test_mostly_unobserved_blocks(V):
     s.W = W
     _, u = run_gpu(V, s)
     check_against_oracle(s, u)
+
+
+@pytest.mark.parametrize("iters", [1, 2, 3, 7, 40])
+@pytest.mark.parametrize("maker", [lambda: tiny(), lambda: random_instance(700, seed=31, extent=6, w_density=0.6),
+                                   lambda: random_instance(300, seed=32, extent=5, data_term=1, lam=0.7, eps=0.05),
+                                   lambda: dense_box(3, 2, 2, w_density=0.8)])
+def test_skewed_schedule_bit_identical(V, maker, iters):
+    """opts.kernel = 2 (primal k + dual k+1 per launch, +face primal recompute) gives the
+    same state (u, ū, p) as the fused kernel and the fp32 oracle, bit for bit."""
+    s = maker()
+    outs = []
+    for kernel in (0, 2):
+        vol = V(s.coords.cuda(), s.f.cuda(), s.W.cuda())
+        vol.regularise_scene(s, iters=iters, kernel=kernel)
+        outs.append(vol.state())
+        vol.close()
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+    check_against_oracle(s, outs[1][0].numpy(), iters=iters)
+
+
+def test_skewed_schedule_resume_and_mixed_calls(V, tiny_scene):
+    # calls alternate schedules and parameters; freeze on and off; zero init
+    s = tiny_scene
+    outs = []
+    for kernels in ((0, 0, 0), (2, 2, 2), (2, 0, 2)):
+        vol = V(s.coords.cuda(), s.f.cuda(), s.W.cuda())
+        vol.regularise(s.lam, 0.01, s.tau, s.sigma, 37, kernel=kernels[0], init=1)
+        vol.regularise(0.3, 0.0, s.tau, s.sigma, 21, resume=True, kernel=kernels[1], freeze=False)
+        vol.regularise(2.0, 0.0, s.tau, s.sigma, 16, resume=True, kernel=kernels[2])
+        outs.append(vol.state())
+        vol.close()
+    for other in outs[1:]:
+        for a, b in zip(outs[0], other):
+            assert torch.equal(a, b)
