@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--config", default="street")
     ap.add_argument("--iters", type=int, default=None, help="override the config's iteration count")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--kernel", type=int, default=0, help="0 fused (product), 1 two-kernel baseline")
+    ap.add_argument("--kernel", type=int, default=0, help="0 product (skewed on one GPU), 1 two-kernel baseline, 2 skewed, 3 one-pass fused")
     ap.add_argument("--freeze", type=int, default=1, help="opts.freeze (bit-identical skip of identity updates)")
     ap.add_argument("--sharded", action="store_true",
                     help="use the NCCL sharded runtime even at one rank (tests the N > 1 code path on one GPU)")
@@ -515,7 +515,7 @@ def main():
 
     # transparency: the same step with opts.freeze = 0 (every Ω voxel recomputed and rewritten)
     nf = None
-    if args.freeze and args.kernel == 0:
+    if args.freeze and args.kernel != 1:
         nf_ms = []
         step(coords, f_loc, W_loc, u_out, False, freeze=False)
         barrier()
@@ -594,12 +594,13 @@ def main():
     achieved = ALG_BYTES_PER_VOXEL * n_local_vox / (it_ms / 1e3) / 1e9
     tr = load_traffic()
     traffic = None
-    if tr and tr.get("workload") == scene.name and tr.get("kernel") == ("k_fused" if args.kernel == 0 else "k_dual+k_primal") \
+    kname = {0: "k_fused" if sharded else "k_skew", 1: "k_dual+k_primal", 2: "k_skew", 3: "k_fused"}[args.kernel]
+    if tr and tr.get("workload") == scene.name and tr.get("kernel") == kname \
             and bool(tr.get("freeze", True)) == bool(args.freeze):
         traffic = tr.get("dram_bytes_per_launch")
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "peak_source": peak_src,
-                "kernel": "k_fused" if args.kernel == 0 else "k_dual+k_primal",
+                "kernel": kname,
                 "alg_bytes_per_launch": ALG_BYTES_PER_VOXEL * n_local_vox,
                 "avg_launch_ms": it_ms, "frac_of_8TBps": achieved / 8000.0}
     if traffic:
@@ -612,7 +613,7 @@ def main():
     if nf:
         nf_ach = ALG_BYTES_PER_VOXEL * n_local_vox / (nf["avg_launch_ms"] / 1e3) / 1e9
         nf.update({"achieved": nf_ach, "frac": nf_ach / peak})
-        nft = (tr or {}).get("no_freeze") if tr and tr.get("workload") == scene.name and args.kernel == 0 else None
+        nft = (tr or {}).get("no_freeze") if tr and tr.get("workload") == scene.name and tr.get("kernel") == kname else None
         if nft:
             nf["traffic"] = nft["dram_bytes_per_launch"]
             nf["dram_gbs_actual"] = nft["dram_bytes_per_launch"] / (nf["avg_launch_ms"] / 1e3) / 1e9

@@ -463,7 +463,8 @@ static vol_status run_iterations_skew(vol_s *v, const IterParams &P, int32_t ite
 }
 
 static vol_status run_iterations_single(vol_s *v, const IterParams &P, int32_t iters, int kernel) {
-    if (kernel == 2) return run_iterations_skew(v, P, iters);
+    // kernel 0 (product): the skewed schedule on one GPU; 3: the one-pass fused kernel
+    if (kernel == 0 || kernel == 2) return run_iterations_skew(v, P, iters);
     cudaStream_t s = v->stream;
     int64_t launches = 0;
     auto one = [&](cudaStream_t st, int cur) -> int {
@@ -533,9 +534,10 @@ vol_status vol_regularise_prepare(vol_s *v, float lambda, float eps, float tau, 
     if (!(o.theta >= 0.0f) || !std::isfinite(o.theta)) return fail(VOL_EINVAL, "theta must be >= 0");
     if (o.data_term != 0 && o.data_term != 1) return fail(VOL_EINVAL, "data_term must be 0 (L1) or 1 (L2)");
     if (o.init != 0 && o.init != 1) return fail(VOL_EINVAL, "init must be 0 (warm) or 1 (zero)");
-    if (o.kernel < 0 || o.kernel > 2)
-        return fail(VOL_EINVAL, "kernel must be 0 (fused), 1 (two-kernel) or 2 (skewed fused)");
-    if (v->shard && o.kernel != 0) return fail(VOL_ENOTSUP, "the two-kernel and skewed schedules are single-GPU only");
+    if (o.kernel < 0 || o.kernel > 3)
+        return fail(VOL_EINVAL, "kernel must be 0 (product), 1 (two-kernel), 2 (skewed) or 3 (one-pass fused)");
+    if (v->shard && (o.kernel == 1 || o.kernel == 2))
+        return fail(VOL_ENOTSUP, "the two-kernel and skewed schedules are single-GPU only");
     if (o.exchange != 0 && o.exchange != 1) return fail(VOL_EINVAL, "exchange must be 0 (no-op, timing only) or 1");
     if (v->shard) {
         vol_status st = shard_reset(v);

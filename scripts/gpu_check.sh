@@ -18,7 +18,7 @@ for what in "$@"; do
       $P > gpurun_out/plain.log 2>&1 && \
       ncu --metrics gpu__time_duration.sum --clock-control none -k regex:^k_ -c 2000 --csv --log-file gpurun_out/launches.csv $P > gpurun_out/ncu_launch.log 2>&1
       echo "launch=$?" >> gpurun_out/status.txt
-      ncu --set full --clock-control none --import-source on -k regex:k_fused -s 100 -c 2 -o gpurun_out/prof_fused $P > gpurun_out/ncu_full.log 2>&1
+      ncu --set full --clock-control none --import-source on -k regex:"k_skew|k_fused" -s 100 -c 2 -o gpurun_out/prof_fused $P > gpurun_out/ncu_full.log 2>&1
       echo "full=$?" >> gpurun_out/status.txt ;;
   esac
 done

@@ -136,7 +136,7 @@ def test_random_instances_parity(V, case):
     check_against_oracle(s, u)
 
 
-@pytest.mark.parametrize("kernel", [0, 1])
+@pytest.mark.parametrize("kernel", [0, 1, 3])
 def test_dense_box_and_two_kernel_parity(V, kernel):
     s = dense_box(3, 3, 2, seed=5, w_density=0.85, lam=0.6, eps=0.02, iters=40)
     _, u = run_gpu(V, s, kernel=kernel)
@@ -147,7 +147,8 @@ def test_fused_equals_two_kernel_bitwise(V):
     s = random_instance(400, seed=9, extent=5, lam=0.3, eps=0.01, iters=50)
     _, a = run_gpu(V, s, kernel=0)
     _, b = run_gpu(V, s, kernel=1)
-    assert np.array_equal(a, b)
+    _, c = run_gpu(V, s, kernel=3)
+    assert np.array_equal(a, b) and np.array_equal(a, c)
 
 
 def test_single_block_and_odd_iteration_counts(V):
@@ -353,11 +354,11 @@ def test_mostly_unobserved_blocks(V):
                                    lambda: random_instance(300, seed=32, extent=5, data_term=1, lam=0.7, eps=0.05),
                                    lambda: dense_box(3, 2, 2, w_density=0.8)])
 def test_skewed_schedule_bit_identical(V, maker, iters):
-    """opts.kernel = 2 (primal k + dual k+1 per launch, +face primal recompute) gives the
-    same state (u, ū, p) as the fused kernel and the fp32 oracle, bit for bit."""
+    """opts.kernel = 2 (primal k + dual k+1 per launch, +face primal recompute; the single-GPU product
+    path) gives the same state (u, ū, p) as the one-pass fused kernel (3) and the fp32 oracle."""
     s = maker()
     outs = []
-    for kernel in (0, 2):
+    for kernel in (3, 2):
         vol = V(s.coords.cuda(), s.f.cuda(), s.W.cuda())
         vol.regularise_scene(s, iters=iters, kernel=kernel)
         outs.append(vol.state())
@@ -371,7 +372,7 @@ def test_skewed_schedule_resume_and_mixed_calls(V, tiny_scene):
     # calls alternate schedules and parameters; freeze on and off; zero init
     s = tiny_scene
     outs = []
-    for kernels in ((0, 0, 0), (2, 2, 2), (2, 0, 2)):
+    for kernels in ((3, 3, 3), (2, 2, 2), (2, 3, 0)):
         vol = V(s.coords.cuda(), s.f.cuda(), s.W.cuda())
         vol.regularise(s.lam, 0.01, s.tau, s.sigma, 37, kernel=kernels[0], init=1)
         vol.regularise(0.3, 0.0, s.tau, s.sigma, 21, resume=True, kernel=kernels[1], freeze=False)
