@@ -555,7 +555,11 @@ def main():
     if not args.no_e2e:
         hc = coords.cpu().pin_memory()
         hf = f_loc.cpu().pin_memory()
-        hW = W_loc.cpu().pin_memory()
+        Wc = W_loc.cpu()
+        # W is an observation count (Eq. 1): exact small integers go over PCIe as 8-bit counts
+        # (vol_create_w8, bit-identical to the fp32 call), a quarter of the weight bytes
+        w_u8 = bool(((Wc == Wc.round()) & (Wc >= 0) & (Wc <= 255)).all())
+        hW = (Wc.to(torch.uint8) if w_u8 else Wc).pin_memory()
         hu = torch.empty(u_out.shape, dtype=torch.float32).pin_memory()
         for _ in range(2):
             step(hc, hf, hW, hu, False)
@@ -569,10 +573,11 @@ def main():
         if sharded:
             dist.all_reduce(ems, op=dist.ReduceOp.MAX)
         ems = float(ems.item())
-        h2d = hc.numel() * 4 + hf.numel() * 4 + hW.numel() * 4
+        h2d = hc.numel() * 4 + hf.numel() * 4 + hW.numel() * hW.element_size()
         d2h = hu.numel() * 4 + 5 * 8
         e2e = {"value": n_alloc_total * iters / (ems / 1e3), "unit": "voxel-updates/s",
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": ems}
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": ems,
+               "w_host_dtype": "u8" if w_u8 else "f32"}
 
     fusion = None
     if not args.no_fusion and world == 1:

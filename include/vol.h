@@ -106,6 +106,13 @@ vol_status vol_create(const int32_t *block_xyz, int64_t n_global, const float *f
                       const vol_dist *dist, void *workspace, size_t workspace_bytes, void *stream,
                       vol_t *out);
 
+/* vol_create with the weights given as exact 8-bit observation counts (W is a count, Eq. 1: w_k = w_{k-1}
+ * + 1 capped at w_max): W8 [n_local][512] uint8 (host or device), otherwise as vol_create.
+ * Equivalent to vol_create with W = (float)W8 — bit for bit — with a quarter of the weight bytes to copy
+ * (the end-to-end bench passes host weights this way).  Errors as vol_create; VOL_EINVAL if W8 is NULL. */
+vol_status vol_create_w8(const int32_t *block_xyz, int64_t n_global, const float *f, const uint8_t *W8,
+                         const vol_dist *dist, void *workspace, size_t workspace_bytes, void *stream, vol_t *out);
+
 /* Run `iters` Chambolle–Pock iterations (SURVEY §8(a) rows a-2 … a-6):
  *   dual ascent with Huber damping + projection  q = (p + σ∇_Ω ū)/(1 + σε),  p = q / max(1, ‖q‖₂)
  *   primal step                                  ũ = u + τ·div_Ω p  (sign: reading c-2)

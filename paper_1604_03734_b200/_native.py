@@ -59,7 +59,7 @@ EXPORTS = [
     "vol_destroy", "vol_last_error", "vol_nccl_unique_id", "vol_group_connect", "vol_regularise_group",
     "vol_group_energy", "vol_block_hash", "vol_plan_shard", "vol_total_launches", "vol_fuse_workspace_bytes",
     "vol_fuse", "vol_fuse_incremental", "vol_extract", "vol_stereo_default_params", "vol_stereo_workspace_bytes", "vol_stereo",
-    "vol_stereo_census", "vol_stereo_tensor", "vol_disparity_to_depth", "vol_shard_timing",
+    "vol_stereo_census", "vol_stereo_tensor", "vol_disparity_to_depth", "vol_shard_timing", "vol_create_w8",
 ]
 
 _lib = None
@@ -79,6 +79,7 @@ def lib() -> ctypes.CDLL:
         "vol_default_opts": (None, [ctypes.POINTER(vol_opts)]),
         "vol_workspace_bytes": (ctypes.c_size_t, [P, i64, ctypes.POINTER(vol_dist)]),
         "vol_create": (st, [P, i64, P, P, ctypes.POINTER(vol_dist), P, ctypes.c_size_t, P, ctypes.POINTER(P)]),
+        "vol_create_w8": (st, [P, i64, P, P, ctypes.POINTER(vol_dist), P, ctypes.c_size_t, P, ctypes.POINTER(P)]),
         "vol_regularise": (st, [P, f32, f32, f32, f32, i32, ctypes.POINTER(vol_opts)]),
         "vol_read_u": (st, [P, P]),
         "vol_energy": (st, [P, f32, f32, c_int, P, P]),

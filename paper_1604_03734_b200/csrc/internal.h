@@ -102,6 +102,8 @@ int launch_freeze_mask(const Fields &F, int cur, const IterParams &P, int64_t n_
 int launch_pack_w8(const float *W, uint8_t *W8, int64_t nvox, unsigned *bad, cudaStream_t s);
 // gather: dst[r] = src[perm[r]] (caller → store order); scatter: dst[perm[r]] = src[r] (store → caller)
 int launch_permute_blocks(const float *src, float *dst, const int32_t *perm, int64_t n, bool gather, cudaStream_t s);
+// W given as 8-bit counts [n][512] in caller order → fp32 W in store order (gather by perm)
+int launch_permute_w8_to_f32(const uint8_t *src, float *dst, const int32_t *perm, int64_t n, cudaStream_t s);
 int launch_sanitize_state(const Fields &F, int cur, const int32_t *nbr, int64_t n_blocks, cudaStream_t s);
 
 // energy: per-block partial sums, then one deterministic final reduction into out[5]

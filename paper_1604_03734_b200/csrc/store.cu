@@ -336,6 +336,23 @@ int launch_permute_blocks(const float *src, float *dst, const int32_t *perm, int
     return cudaPeekAtLastError() == cudaSuccess ? counted(1) : -1;
 }
 
+// 8-bit weights given by the caller (vol_create_w8), gathered into store order and widened to fp32:
+// dst[r][i] = (float)src[perm[r]][i]
+__global__ void k_permute_w8_to_f32(const uint8_t *__restrict__ src, float *__restrict__ dst,
+                                    const int32_t *__restrict__ perm) {
+    const int64_t r = blockIdx.x;
+    const int64_t c = perm[r];
+    const uchar4 w = reinterpret_cast<const uchar4 *>(src + c * kBlockVox)[threadIdx.x];
+    reinterpret_cast<float4 *>(dst + r * kBlockVox)[threadIdx.x] = make_float4((float)w.x, (float)w.y, (float)w.z,
+                                                                               (float)w.w);
+}
+
+int launch_permute_w8_to_f32(const uint8_t *src, float *dst, const int32_t *perm, int64_t n, cudaStream_t s) {
+    if (n == 0) return 0;
+    k_permute_w8_to_f32<<<(unsigned)n, 128, 0, s>>>(src, dst, perm);
+    return cudaPeekAtLastError() == cudaSuccess ? counted(1) : -1;
+}
+
 // The fusion weight is an observation count (Eq. 1: w_k = w_{k-1} + 1), so it is usually an
 // exact small integer; then the fused kernel reads it as one byte instead of four (exact: the kernel
 // converts back to the same float).

@@ -192,15 +192,33 @@ static vol_status copy_in(void *dst, const void *src, size_t bytes, cudaStream_t
     return VOL_OK;
 }
 
+static vol_status create_impl(const int32_t *block_xyz, int64_t n_global, const float *f, const float *W,
+                              const uint8_t *W8in, const vol_dist *dist, void *workspace, size_t workspace_bytes,
+                              void *stream, vol_t *out);
+
 extern "C" vol_status vol_create(const int32_t *block_xyz, int64_t n_global, const float *f, const float *W,
                                  const vol_dist *dist, void *workspace, size_t workspace_bytes, void *stream,
                                  vol_t *out) {
     NvtxRange nvtx_range_("vol_create");
+    return create_impl(block_xyz, n_global, f, W, nullptr, dist, workspace, workspace_bytes, stream, out);
+}
+
+extern "C" vol_status vol_create_w8(const int32_t *block_xyz, int64_t n_global, const float *f, const uint8_t *W8,
+                                    const vol_dist *dist, void *workspace, size_t workspace_bytes, void *stream,
+                                    vol_t *out) {
+    NvtxRange nvtx_range_("vol_create_w8");
+    if (!W8) return fail(VOL_EINVAL, "vol_create_w8: W8 is NULL");
+    return create_impl(block_xyz, n_global, f, nullptr, W8, dist, workspace, workspace_bytes, stream, out);
+}
+
+static vol_status create_impl(const int32_t *block_xyz, int64_t n_global, const float *f, const float *W,
+                              const uint8_t *W8in, const vol_dist *dist, void *workspace, size_t workspace_bytes,
+                              void *stream, vol_t *out) {
     if (!out) return fail(VOL_EINVAL, "vol_create: out is NULL");
     *out = nullptr;
     if (n_global < 1) return fail(VOL_EINVAL, "vol_create: n_global must be >= 1 (got %lld)", (long long)n_global);
     if (n_global > (int64_t)1 << 30) return fail(VOL_EINVAL, "vol_create: n_global too large");
-    if (!block_xyz || !f || !W) return fail(VOL_EINVAL, "vol_create: NULL input pointer");
+    if (!block_xyz || !f || !(W || W8in)) return fail(VOL_EINVAL, "vol_create: NULL input pointer");
     // a dist with world > 1, or any dist carrying an NCCL id (world 1 runs the sharded runtime with no
     // peers, which exercises the NCCL set-up and the two-launch schedule on a single GPU)
     const bool sharded = dist && (dist->world > 1 || dist->nccl_id != nullptr);
@@ -293,10 +311,18 @@ extern "C" vol_status vol_create(const int32_t *block_xyz, int64_t n_global, con
     if (cudaMemcpyAsync(v->d_perm, row_caller.data(), (size_t)L.n_local * 4, cudaMemcpyHostToDevice, s) != cudaSuccess)
         return bail(fail(VOL_ECUDA, "permutation upload failed"));
     if ((st = copy_in(v->d_tmp, f, fbytes, s)) != VOL_OK) return bail(st);
-    if ((st = copy_in(v->F.u, W, fbytes, s)) != VOL_OK) return bail(st);
-    if (launch_permute_blocks(v->d_tmp, const_cast<float *>(v->F.f), v->d_perm, L.n_local, true, s) < 0 ||
-        launch_permute_blocks(v->F.u, const_cast<float *>(v->F.W), v->d_perm, L.n_local, true, s) < 0)
-        return bail(fail(VOL_ECUDA, "input permutation failed"));
+    if (W8in) {   // 8-bit counts: a quarter of the bytes to copy, widened on the device (exact)
+        if ((st = copy_in(v->F.u, W8in, (size_t)L.n_local * kBlockVox, s)) != VOL_OK) return bail(st);
+        if (launch_permute_blocks(v->d_tmp, const_cast<float *>(v->F.f), v->d_perm, L.n_local, true, s) < 0 ||
+            launch_permute_w8_to_f32(reinterpret_cast<const uint8_t *>(v->F.u), const_cast<float *>(v->F.W),
+                                     v->d_perm, L.n_local, s) < 0)
+            return bail(fail(VOL_ECUDA, "input permutation failed"));
+    } else {
+        if ((st = copy_in(v->F.u, W, fbytes, s)) != VOL_OK) return bail(st);
+        if (launch_permute_blocks(v->d_tmp, const_cast<float *>(v->F.f), v->d_perm, L.n_local, true, s) < 0 ||
+            launch_permute_blocks(v->F.u, const_cast<float *>(v->F.W), v->d_perm, L.n_local, true, s) < 0)
+            return bail(fail(VOL_ECUDA, "input permutation failed"));
+    }
 
     // K1: hash + CSR bucket table over all n_global blocks
     if (cudaMemsetAsync(v->d_count, 0, ((size_t)L.T + 1) * 4, s) != cudaSuccess ||

@@ -382,3 +382,22 @@ def test_skewed_schedule_resume_and_mixed_calls(V, tiny_scene):
     for other in outs[1:]:
         for a, b in zip(outs[0], other):
             assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("where", ["host", "cuda"])
+def test_create_w8_equals_float_weights(V, where):
+    """vol_create_w8 (W as 8-bit observation counts) builds the same volume as vol_create with W as fp32:
+    tables and the iterate after 25 iterations bit for bit (host and device inputs)."""
+    s = random_instance(500, seed=41, extent=6, w_density=0.7, w_max=9, lam=0.5, iters=25)
+    W8 = s.W.to(torch.uint8)
+    assert torch.equal(W8.float(), s.W)
+    dev = (lambda t: t.cuda()) if where == "cuda" else (lambda t: t)
+    a = V(dev(s.coords), dev(s.f), dev(s.W))
+    b = V(dev(s.coords), dev(s.f), dev(W8))
+    for x, y in zip(a.tables(), b.tables()):
+        assert np.array_equal(np.asarray(x), np.asarray(y))
+    a.regularise_scene(s)
+    b.regularise_scene(s)
+    for x, y in zip(a.state(), b.state()):
+        assert torch.equal(x, y)
+    assert a.energy(s.lam, s.eps) == b.energy(s.lam, s.eps)
