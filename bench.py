@@ -599,7 +599,7 @@ def main():
     achieved = ALG_BYTES_PER_VOXEL * n_local_vox / (it_ms / 1e3) / 1e9
     tr = load_traffic()
     traffic = None
-    kname = {0: "k_fused" if sharded else "k_skew", 1: "k_dual+k_primal", 2: "k_skew", 3: "k_fused"}[args.kernel]
+    kname = {0: "k_skew", 1: "k_dual+k_primal", 2: "k_skew", 3: "k_fused"}[args.kernel]
     if tr and tr.get("workload") == scene.name and tr.get("kernel") == kname \
             and bool(tr.get("freeze", True)) == bool(args.freeze):
         traffic = tr.get("dram_bytes_per_launch")

@@ -52,12 +52,12 @@ typedef struct {
                         1: W-weighted L2 prox, paper Eq. 8                               */
     int init;        /* 0 (d): warm start u = ū = f, p = 0; 1: u = ū = 0 on Ω, p = 0 */
     int resume;      /* 0 (d): initialise before iterating; 1: continue from the current state        */
-    int kernel;      /* 0 (d): the product path — on one GPU the skewed fused schedule (one HBM sweep
-                           per iteration: primal k + dual k+1 per launch, ū never stored inside the
-                           loop), on sharded volumes the one-pass fused kernel;
-                        1: two-kernel baseline (dual kernel, then primal+relax kernel);
-                        2: skewed fused schedule (single GPU only);
-                        3: one-pass fused kernel (dual k + primal k per launch).
+    int kernel;      /* 0 (d): the product path = 2;
+                        1: two-kernel baseline (dual kernel, then primal+relax kernel; single GPU only);
+                        2: skewed fused schedule (one HBM sweep per iteration: primal k + dual k+1 per
+                           launch, ū never stored inside the loop; sharded: a (u, p) halo before
+                           every launch);
+                        3: one-pass fused kernel (dual k + primal k per launch; sharded: (ū, p) halo).
                         All four give bit-identical results                        */
     int freeze;      /* 1 (d): with the L1 data term, voxels whose primal step is provably the identity
                         for the whole call (τλW >= τ(3+√3) plus rounding margin, and u = ū = f in both

@@ -84,6 +84,7 @@ struct vol_s {
     uint8_t *d_w8 = nullptr;           // [S][512] exact 8-bit weights (used when F.W8 != null)
     int32_t *d_perm = nullptr;         // [n_local] caller index of store row r
     float *d_tmp = nullptr;            // [n_local][512] scratch for caller-order I/O
+    float *d_u2 = nullptr;             // [S][512] second u buffer of the skewed schedule
     unsigned long long *d_misc = nullptr;  // [4]: dup, bad, n_omega, spare
     double *d_part = nullptr;          // [S][5]
     double *d_eout = nullptr;          // [8]

@@ -74,10 +74,10 @@ int launch_fused(const View &V, const int32_t *nbr, const int32_t *work, int64_t
 // k_dual reads ū_in, p_in, W and writes p_out; k_primal reads p_out (p^{k+1}), u, f, W and writes u, ū_out.
 int launch_dual_only(const View &V, const int32_t *nbr, int64_t n_work, const IterParams &P, cudaStream_t s);
 int launch_primal_only(const View &V, const int32_t *nbr, int64_t n_work, const IterParams &P, cudaStream_t s);
-// Skewed schedule (iterate.cu): one launch = primal step k + dual step k+1 of every block; reads u_in and
-// p[p_in] (p^{k+1}), writes u_out and p[p_in ^ 1] (p^{k+2}).
+// Skewed schedule (iterate.cu): one launch = primal step k + dual step k+1 of store rows
+// [first, first + n_blocks); reads u_in and p[p_in] (p^{k+1}), writes u_out and p[p_in ^ 1] (p^{k+2}).
 int launch_skew(const Fields &F, const float *u_in, float *u_out, int p_in, const uint32_t *frozen,
-                const int32_t *nbr, int64_t n_blocks, const IterParams &P, cudaStream_t s);
+                const int32_t *nbr, int64_t first, int64_t n_blocks, const IterParams &P, cudaStream_t s);
 int launch_two_kernel(const View &V, const int32_t *nbr, const int32_t *work, int64_t n_work, const IterParams &P,
                       cudaStream_t s);
 

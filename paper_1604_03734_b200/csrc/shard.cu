@@ -452,9 +452,91 @@ vol_status shard_timing(vol_s *v, float *interior_ms, float *exchange_ms, float 
     return VOL_OK;
 }
 
+// ---- skewed schedule on a sharded volume (opts.kernel = 2), NCCL transport.  The same sequence as the
+// single-GPU run_iterations_skew, with a halo exchange in front of every launch that reads ghosts:
+//   X(ū^0, p^0) · k_dual · { X(u^j, p^{j+1}) ∥ k_skew A ; k_skew B }_{j < iters−1} · X(p^iters) · k_primal
+// (A = local blocks without a remote neighbour, launched while the exchange runs; B the others).  The
+// exchange moves four fields per boundary block (a u field and p), like the one-pass schedule's (ū, p).
+static vol_status nccl_exchange_fields(vol_s *v, float *a, float *px, float *py, float *pz, bool timed = false) {
+    ShardRuntime *R = v->shard;
+    CK(cudaEventRecord(R->ev_pack, v->stream));
+    CK(cudaStreamWaitEvent(R->cs, R->ev_pack, 0));
+    if (timed) CK(cudaEventRecord(R->ev_t[2], R->cs));
+    if (v->pending_exchange) {   // opts.exchange = 0: no-op chain (timing only)
+        vol_status st = pack(v, a, px, py, pz, R->cs);
+        if (st != VOL_OK) return st;
+        if ((st = nccl_exchange(v, R->cs)) != VOL_OK) return st;
+        if ((st = unpack(v, a, px, py, pz, R->cs)) != VOL_OK) return st;
+    }
+    if (timed) CK(cudaEventRecord(R->ev_t[3], R->cs));
+    CK(cudaEventRecord(R->ev_halo, R->cs));
+    return VOL_OK;
+}
+
+static vol_status nccl_skew(vol_s *v, const IterParams &P, int32_t iters) {
+    ShardRuntime *R = v->shard;
+    const ShardPlan &SP = R->plan;
+    cudaStream_t s = v->stream;
+    const int c = v->cur;
+    const int64_t nl = SP.n_local(), nA = SP.nA;
+    int64_t launches = 0;
+    CK(cudaMemcpyAsync(v->d_u2, v->F.u, (size_t)v->L.S * kBlockVox * 4, cudaMemcpyDeviceToDevice, s));
+    float *B[2];
+    B[(iters - 1) & 1] = v->F.u;
+    B[iters & 1] = v->d_u2;
+    vol_status st = nccl_exchange_fields(v, v->F.ub[c], v->F.px[c], v->F.py[c], v->F.pz[c]);
+    if (st != VOL_OK) return st;
+    CK(cudaStreamWaitEvent(s, R->ev_halo, 0));
+    int r = launch_dual_only(view_of(v->F, c), v->d_nbr, nl, P, s);
+    CKL(r);
+    launches += r + 2;
+    for (int j = 0; j < iters - 1; j++) {
+        const int pin = c ^ ((j + 1) & 1);
+        const bool timed = j == iters - 2;   // vol_shard_timing: the last skewed launch
+        if ((st = nccl_exchange_fields(v, B[j & 1], v->F.px[pin], v->F.py[pin], v->F.pz[pin], timed)) != VOL_OK)
+            return st;
+        if (timed) CK(cudaEventRecord(R->ev_t[0], s));
+        int a = launch_skew(v->F, B[j & 1], B[(j + 1) & 1], pin, v->pending_frozen, v->d_nbr, 0, nA, P, s);
+        CKL(a);
+        if (timed) CK(cudaEventRecord(R->ev_t[1], s));
+        CK(cudaStreamWaitEvent(s, R->ev_halo, 0));
+        if (timed) CK(cudaEventRecord(R->ev_t[4], s));
+        int b = launch_skew(v->F, B[j & 1], B[(j + 1) & 1], pin, v->pending_frozen, v->d_nbr, nA, nl - nA, P, s);
+        CKL(b);
+        if (timed) {
+            CK(cudaEventRecord(R->ev_t[5], s));
+            R->timed = true;
+        }
+        launches += a + b + 2;
+    }
+    if (iters < 2) {   // no skewed launch: the timing events record an empty interval
+        for (int k = 0; k < 6; k++) CK(cudaEventRecord(R->ev_t[k], k == 2 || k == 3 ? R->cs : s));
+        R->timed = true;
+    }
+    const int c2 = c ^ (iters & 1);
+    if ((st = nccl_exchange_fields(v, v->F.ub[c2], v->F.px[c2], v->F.py[c2], v->F.pz[c2])) != VOL_OK) return st;
+    CK(cudaStreamWaitEvent(s, R->ev_halo, 0));
+    View V = view_of(v->F, c2 ^ 1);   // px_out = p[c2] (p^iters), ub_out = ub[c2]
+    V.u = B[(iters - 1) & 1];         // == F.u
+    r = launch_primal_only(V, v->d_nbr, nl, P, s);
+    CKL(r);
+    launches += r + 2;
+    v->cur = c2;
+    v->last_launches = launches;
+    return VOL_OK;
+}
+
 vol_status shard_iterate(vol_s *v, const IterParams &P, int32_t iters) {
     ShardRuntime *R = v->shard;
     if (!R->nccl) return fail(VOL_EINVAL, "loopback-sharded volume: use vol_regularise_group");
+    if (v->pending_kernel == 0 || v->pending_kernel == 2) {   // the product path: the skewed schedule
+        vol_status st = nccl_skew(v, P, iters);
+        if (st != VOL_OK) return st;
+        ncclResult_t async = ncclSuccess;
+        if (ncclCommGetAsyncError(R->comm, &async) == ncclSuccess && async != ncclSuccess && async != ncclInProgress)
+            return fail(VOL_ENCCL, "NCCL asynchronous error: %s", ncclGetErrorString(async));
+        return VOL_OK;
+    }
     int64_t launches = 0;
     for (int32_t k = 0; k < iters; k++) {
         vol_status st = nccl_iteration(v, P, launches, k == iters - 1);
@@ -578,6 +660,75 @@ extern "C" vol_status vol_regularise_group(vol_t *h, int world, float lambda, fl
     cudaStream_t s = h[0]->stream;
     for (int r = 1; r < world; r++) CK(cudaStreamSynchronize(h[r]->stream));
     int64_t launches = 0;
+    if ((h[0]->pending_kernel == 0 || h[0]->pending_kernel == 2) && iters > 0) {   // skewed, as nccl_skew
+        const int c = h[0]->cur;
+        float *Bu[64][2];
+        if (world > 64) return fail(VOL_EINVAL, "group: at most 64 loopback shards");
+        auto X = [&](auto field_of) -> vol_status {
+            vol_status st2;
+            for (int r = 0; r < world; r++) {
+                float *f4[4];
+                field_of(r, f4);
+                if ((st2 = pack(h[r], f4[0], f4[1], f4[2], f4[3], s)) != VOL_OK) return st2;
+            }
+            if ((st2 = loopback_exchange(h, world, s)) != VOL_OK) return st2;
+            for (int r = 0; r < world; r++) {
+                float *f4[4];
+                field_of(r, f4);
+                if ((st2 = unpack(h[r], f4[0], f4[1], f4[2], f4[3], s)) != VOL_OK) return st2;
+            }
+            launches += 2 * world;
+            return VOL_OK;
+        };
+        for (int r = 0; r < world; r++) {
+            CK(cudaMemcpyAsync(h[r]->d_u2, h[r]->F.u, (size_t)h[r]->L.S * kBlockVox * 4, cudaMemcpyDeviceToDevice, s));
+            Bu[r][(iters - 1) & 1] = h[r]->F.u;
+            Bu[r][iters & 1] = h[r]->d_u2;
+        }
+        if ((st = X([&](int r, float **f4) {
+                 f4[0] = h[r]->F.ub[c], f4[1] = h[r]->F.px[c], f4[2] = h[r]->F.py[c], f4[3] = h[r]->F.pz[c];
+             })) != VOL_OK)
+            return st;
+        for (int r = 0; r < world; r++) {
+            int a = launch_dual_only(view_of(h[r]->F, c), h[r]->d_nbr, h[r]->shard->plan.n_local(), P, s);
+            CKL(a);
+            launches += a;
+        }
+        for (int j = 0; j < iters - 1; j++) {
+            const int pin = c ^ ((j + 1) & 1);
+            if ((st = X([&](int r, float **f4) {
+                     f4[0] = Bu[r][j & 1], f4[1] = h[r]->F.px[pin], f4[2] = h[r]->F.py[pin], f4[3] = h[r]->F.pz[pin];
+                 })) != VOL_OK)
+                return st;
+            for (int r = 0; r < world; r++) {
+                const ShardPlan &SP = h[r]->shard->plan;
+                const int64_t nl = SP.n_local(), nA = SP.nA;
+                int a = launch_skew(h[r]->F, Bu[r][j & 1], Bu[r][(j + 1) & 1], pin, h[r]->pending_frozen, h[r]->d_nbr,
+                                    0, nA, P, s);
+                CKL(a);
+                int b = launch_skew(h[r]->F, Bu[r][j & 1], Bu[r][(j + 1) & 1], pin, h[r]->pending_frozen, h[r]->d_nbr,
+                                    nA, nl - nA, P, s);
+                CKL(b);
+                launches += a + b;
+            }
+        }
+        const int c2 = c ^ (iters & 1);
+        if ((st = X([&](int r, float **f4) {
+                 f4[0] = h[r]->F.ub[c2], f4[1] = h[r]->F.px[c2], f4[2] = h[r]->F.py[c2], f4[3] = h[r]->F.pz[c2];
+             })) != VOL_OK)
+            return st;
+        for (int r = 0; r < world; r++) {
+            View V = view_of(h[r]->F, c2 ^ 1);
+            V.u = Bu[r][(iters - 1) & 1];
+            int a = launch_primal_only(V, h[r]->d_nbr, h[r]->shard->plan.n_local(), P, s);
+            CKL(a);
+            launches += a;
+            h[r]->cur = c2;
+        }
+        CK(cudaStreamSynchronize(s));
+        for (int r = 0; r < world; r++) h[r]->last_launches = launches;
+        return VOL_OK;
+    }
     for (int32_t k = 0; k < iters; k++) {
         const int cur = h[0]->cur;
         for (int r = 0; r < world; r++)

@@ -94,6 +94,7 @@ static void carve_all(Carve &c, vol_s *v, const Layout &L) {
     auto frozen = c.take<uint32_t>((size_t)L.n_local * 16 + 16);
     auto perm = c.take<int32_t>((size_t)L.n_local + 1);
     auto tmp = c.take<float>((size_t)L.n_local * kBlockVox + 4);
+    auto u2 = c.take<float>((size_t)L.S * kBlockVox + 4);   // second u buffer of the skewed schedule
     auto misc = c.take<unsigned long long>(4);
     auto part = c.take<double>(5 * (size_t)L.S + 5);
     auto eout = c.take<double>(8);
@@ -109,6 +110,7 @@ static void carve_all(Carve &c, vol_s *v, const Layout &L) {
         v->d_frozen = frozen;
         v->d_perm = perm;
         v->d_tmp = tmp;
+        v->d_u2 = u2;
         v->d_misc = misc;
         v->d_part = part;
         v->d_eout = eout;
@@ -411,9 +413,8 @@ extern "C" void vol_destroy(vol_t v) {
 
 // ------------------------------------------------------------------------------- iterations
 
-// Skewed schedule (opts.kernel = 2, single GPU): k_dual (p^1 from ū^0), iters − 1 launches of k_skew
-// (primal k + dual k+1), k_primal (u^iters, ū^iters).  u is double-buffered through the caller-order
-// scratch field d_tmp (free during iterations); both buffers start equal to u^0 so voxels that are never
+// Skewed schedule (opts.kernel = 0/2, single GPU): k_dual (p^1 from ū^0), iters − 1 launches of k_skew
+// (primal k + dual k+1), k_primal (u^iters, ū^iters).  u is double-buffered with d_u2; both buffers start equal to u^0 so voxels that are never
 // written (Ω̄, frozen) hold the same value in both, and the buffer order is chosen so that the epilogue
 // updates F.u in place.
 static vol_status run_iterations_skew(vol_s *v, const IterParams &P, int32_t iters) {
@@ -422,10 +423,10 @@ static vol_status run_iterations_skew(vol_s *v, const IterParams &P, int32_t ite
     const int64_t n = v->L.n_local;
     const size_t ubytes = (size_t)n * kBlockVox * 4;
     int64_t launches = 0;
-    CK(cudaMemcpyAsync(v->d_tmp, v->F.u, ubytes, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(v->d_u2, v->F.u, ubytes, cudaMemcpyDeviceToDevice, s));
     float *B[2];
     B[(iters - 1) & 1] = v->F.u;
-    B[iters & 1] = v->d_tmp;
+    B[iters & 1] = v->d_u2;
     {
         View V = view_of(v->F, cur);   // ū^0 = ub[cur], p^0 = p[cur] → p^1 = p[cur ^ 1]
         int r = launch_dual_only(V, v->d_nbr, n, P, s);
@@ -433,7 +434,8 @@ static vol_status run_iterations_skew(vol_s *v, const IterParams &P, int32_t ite
         launches += r;
     }
     auto skew = [&](cudaStream_t st, int j) -> int {
-        return launch_skew(v->F, B[j & 1], B[(j + 1) & 1], cur ^ ((j + 1) & 1), v->pending_frozen, v->d_nbr, n, P, st);
+        return launch_skew(v->F, B[j & 1], B[(j + 1) & 1], cur ^ ((j + 1) & 1), v->pending_frozen, v->d_nbr, 0, n, P,
+                           st);
     };
     int j = 0;
     const int total = iters - 1;
@@ -562,8 +564,7 @@ vol_status vol_regularise_prepare(vol_s *v, float lambda, float eps, float tau, 
     if (o.init != 0 && o.init != 1) return fail(VOL_EINVAL, "init must be 0 (warm) or 1 (zero)");
     if (o.kernel < 0 || o.kernel > 3)
         return fail(VOL_EINVAL, "kernel must be 0 (product), 1 (two-kernel), 2 (skewed) or 3 (one-pass fused)");
-    if (v->shard && (o.kernel == 1 || o.kernel == 2))
-        return fail(VOL_ENOTSUP, "the two-kernel and skewed schedules are single-GPU only");
+    if (v->shard && o.kernel == 1) return fail(VOL_ENOTSUP, "the two-kernel baseline is single-GPU only");
     if (o.exchange != 0 && o.exchange != 1) return fail(VOL_EINVAL, "exchange must be 0 (no-op, timing only) or 1");
     if (v->shard) {
         vol_status st = shard_reset(v);

@@ -220,7 +220,7 @@ def test_gpu_invariants_tiny(V, tiny_scene):
 # ------------------------------------------------------------------ sharded path (loopback, 1 GPU)
 
 @pytest.mark.parametrize("world", [2, 3, 4])
-def test_loopback_shards_bitwise_equal_single(V, world):
+def test_loopback_shards_bitwise_equal_single(V, world, kernel=0):
     from paper_1604_03734_b200 import connect_group, group_energy, regularise_group
     s = random_instance(500, seed=10 + world, extent=6, w_density=0.7, lam=0.4, eps=0.01, iters=40)
     c = s.coords
@@ -236,7 +236,7 @@ def test_loopback_shards_bitwise_equal_single(V, world):
         vols.append(V(c, s.f[mine], s.W[mine], part=part, loopback=(r, world)))
     assert all(v.n_ghost > 0 for v in vols)
     connect_group(vols)
-    regularise_group(vols, s.lam, s.eps, s.tau, s.sigma, s.iters)
+    regularise_group(vols, s.lam, s.eps, s.tau, s.sigma, s.iters, kernel=kernel)
     u = torch.empty(len(c), 512)
     for r, v in enumerate(vols):
         mine = (part == r).nonzero().squeeze(1)
@@ -246,6 +246,46 @@ def test_loopback_shards_bitwise_equal_single(V, world):
     P1, D1 = single.energy(s.lam, s.eps, s.data_term)
     Pg, Dg = group_energy(vols, s.lam, s.eps, s.data_term)
     assert abs(P1 - Pg) <= 1e-9 * abs(P1) and abs(D1 - Dg) <= 1e-9 * abs(P1)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_loopback_shards_onepass_bitwise_equal_single(V, world):
+    """The one-pass fused kernel on shards (opts.kernel = 3: (ū, p) halo, k_fused A/B) equals the
+    single-GPU result bit for bit."""
+    test_loopback_shards_bitwise_equal_single(V, world, kernel=3)
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_loopback_shards_skewed_bitwise_equal_single(V, world):
+    """The skewed schedule on shards (opts.kernel = 2: an exchange of (u^j, p^{j+1}) before every launch,
+    interior launch A / boundary launch B, dual-only prologue and primal-only epilogue with their own
+    exchanges) equals the single-GPU result bit for bit."""
+    test_loopback_shards_bitwise_equal_single(V, world, kernel=2)
+
+
+def test_loopback_shards_skewed_resume_and_short_calls(V):
+    from paper_1604_03734_b200 import connect_group, regularise_group
+    s = random_instance(400, seed=44, extent=6, w_density=0.7, lam=0.5, eps=0.0, iters=9)
+    c = s.coords
+    key = c[:, 0].to(torch.int64) * 64 + c[:, 1].to(torch.int64)
+    order = torch.argsort(key, stable=True)
+    part = torch.empty(len(c), dtype=torch.int32)
+    for r in range(2):
+        part[order[r * len(c) // 2:(r + 1) * len(c) // 2]] = r
+    vols = []
+    for r in range(2):
+        mine = (part == r).nonzero().squeeze(1)
+        vols.append(V(c, s.f[mine], s.W[mine], part=part, loopback=(r, 2)))
+    connect_group(vols)
+    single = V(s.coords.cuda(), s.f.cuda(), s.W.cuda())
+    for k, (it, kern) in enumerate([(1, 2), (2, 2), (5, 3), (3, 0)]):
+        regularise_group(vols, s.lam, s.eps, s.tau, s.sigma, it, kernel=kern, resume=k > 0)
+        single.regularise(s.lam, s.eps, s.tau, s.sigma, it, resume=k > 0)
+    u = torch.empty(len(c), 512)
+    for r, v in enumerate(vols):
+        mine = (part == r).nonzero().squeeze(1)
+        u[mine] = v.u().cpu()
+    assert np.array_equal(u.numpy(), single.u().cpu().numpy())
 
 
 def test_paper_literal_variant(V):
@@ -306,11 +346,17 @@ def test_nccl_runtime_world1(V):
         assert vol.n_ghost == 0 and vol.n_local == len(s.coords)
         vol.regularise_scene(s)
         assert np.array_equal(vol.u().cpu().numpy(), u1)
+        vol.regularise_scene(s, kernel=3)                 # the one-pass kernel through the NCCL runtime
+        assert np.array_equal(vol.u().cpu().numpy(), u1)
         E = vol.energy(s.lam, s.eps, s.data_term)
         assert abs(E[0] - E1[0]) <= 1e-9 * abs(E1[0]) and abs(E[1] - E1[1]) <= 1e-9 * abs(E1[0])
-        # per-stream timing of the last iteration: interior A, halo chain, boundary B
+        # per-stream timing of the last iteration: interior A, halo chain, boundary B —
+        # after a call of the product (skewed) schedule and after a one-iteration call
         a, c, b = vol.shard_timing()
         assert a >= 0 and c >= 0 and b >= 0
+        vol.regularise(s.lam, s.eps, s.tau, s.sigma, 1, resume=True)
+        assert all(t >= 0 for t in vol.shard_timing())
+        vol.regularise_scene(s)
         # no-op exchange (timing only): with no peers nothing is exchanged, so the bits are unchanged
         vol.regularise_scene(s, exchange=False)
         assert np.array_equal(vol.u().cpu().numpy(), u1)
