@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <mutex>
 #include <numeric>
 #include <unordered_map>
 #include <unordered_set>
@@ -313,14 +314,21 @@ struct CommEntry {
     ncclComm_t comm;
 };
 std::vector<CommEntry> g_comms;
-}  // namespace
+std::mutex g_comms_mu;   // the cache is process-wide; ncclCommInitRank itself runs outside the lock
 
-static vol_status comm_acquire(const void *id_bytes, int world, int rank, int device, ncclComm_t *out) {
+bool comm_lookup(const void *id_bytes, int world, int rank, int device, ncclComm_t *out) {
+    std::lock_guard<std::mutex> lk(g_comms_mu);
     for (const CommEntry &e : g_comms)
         if (e.world == world && e.rank == rank && e.device == device && !memcmp(e.id, id_bytes, NCCL_UNIQUE_ID_BYTES)) {
             *out = e.comm;
-            return VOL_OK;
+            return true;
         }
+    return false;
+}
+}  // namespace
+
+static vol_status comm_acquire(const void *id_bytes, int world, int rank, int device, ncclComm_t *out) {
+    if (comm_lookup(id_bytes, world, rank, device, out)) return VOL_OK;
     ncclUniqueId id;
     memcpy(&id, id_bytes, sizeof id);
     ncclComm_t comm;
@@ -331,7 +339,10 @@ static vol_status comm_acquire(const void *id_bytes, int world, int rank, int de
     e.rank = rank;
     e.device = device;
     e.comm = comm;
-    g_comms.push_back(e);
+    {
+        std::lock_guard<std::mutex> lk(g_comms_mu);
+        g_comms.push_back(e);
+    }
     *out = comm;
     return VOL_OK;
 }
