@@ -41,7 +41,9 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="street")
+    ap.add_argument("--config", default=None,
+                    help="street (default at N = 1), city (1 km route, strong scaling; default at N > 1), "
+                         "city-weak (125 m of route per GPU), city-heavy, street-outlier, tiny")
     ap.add_argument("--iters", type=int, default=None, help="override the config's iteration count")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kernel", type=int, default=0, help="0 product (skewed on one GPU), 1 two-kernel baseline, 2 skewed, 3 one-pass fused")
@@ -143,17 +145,89 @@ def make_scene(cfg: str, world: int, seed: int, device):
     return scenes.by_name(cfg, seed=seed, device=device)
 
 
-def partition(coords, world):
-    """Owner rank per block: contiguous ranges of equal block count along the route (x for the
-    street; arc length for polyline routes is approximated by x + y on the staircase)."""
+def partition(scene, world):
+    """Owner rank per block: the product's route-axis partition (libvol vol_partition_route) —
+    blocks ordered by the arc length of the nearest point of the scene's camera path, cut into contiguous
+    ranges of equal block count."""
     import torch
-    key = coords[:, 0].to(torch.int64) * 4096 + coords[:, 1].to(torch.int64)
-    order = torch.argsort(key * 65536 + coords[:, 2].to(torch.int64), stable=True)
-    part = torch.empty(coords.shape[0], dtype=torch.int32)
-    n = coords.shape[0]
-    for r in range(world):
-        part[order[r * n // world:(r + 1) * n // world].cpu()] = r
-    return part
+
+    from paper_1604_03734_b200 import partition_route
+    return torch.from_numpy(partition_route(scene.coords.cpu(), scene.meta["route"], 8 * scene.meta["voxel"], world))
+
+
+# ---------------------------------------------------------------- per-shard generation (configs 4/5)
+
+def route_plan(cfg: str, seed: int, device):
+    """Geometry + candidate blocks of a city config (cheap; every rank builds the same plan)."""
+    from synth import scenes
+    if cfg == "city":
+        return scenes.city_plan(seed, length=1000.0, device=device)
+    if cfg == "city-heavy":
+        return scenes.city_plan(seed, length=1000.0, device=device, lanes=13)
+    if cfg.startswith("city-weak"):
+        g = int(cfg.split(":")[1])
+        return scenes.city_plan(seed, length=125.0 * g, device=device)
+    raise KeyError(cfg)
+
+
+def shard_generate(plan, world: int, rank: int, chunk_blocks: int = 4096):
+    """SURVEY §1 L0 `gen(config, seed, shard)`: the allocated blocks (coords, f, W) among this rank's
+    candidate blocks — the `world` equal-count arc-length ranges of the candidates (vol_partition_route).
+    The per-voxel values come from the counter-based generator, so they do not depend on the sharding."""
+    import torch
+
+    from paper_1604_03734_b200 import partition_route
+    from synth import scenes
+    cpart = torch.from_numpy(partition_route(plan.cand.cpu(), plan.route, plan.block_edge, world)).to(plan.cand.device)
+    return scenes.route_blocks(plan, plan.cand[cpart == rank], chunk_blocks)
+
+
+def shard_assemble(plan, world: int, rank: int, coords_all, coords_r, f_r, W_r, chunk_blocks: int = 4096):
+    """Global block list = the ranks' generated blocks in rank order; owner map = the exact equal-count route
+    partition of the allocated blocks (the one every sharded test uses); blocks whose owner differs from
+    the rank that generated them (a few near each cut) are regenerated by their new owner.  Returns
+    coords [n, 3] (all ranks identical), part [n] and this rank's f, W in global order."""
+    import numpy as np
+    import torch
+
+    from paper_1604_03734_b200 import partition_route
+    from synth import scenes
+    dev = coords_r.device
+    coords = torch.cat([c.to(dev) for c in coords_all], 0).contiguous()
+    origin = torch.cat([torch.full((c.shape[0],), q, dtype=torch.int32) for q, c in enumerate(coords_all)])
+    part = partition_route(coords.cpu(), plan.route, plan.block_edge, world)
+    mine = torch.from_numpy(part == rank)
+    have = origin == rank
+    f = torch.empty(int(mine.sum()), 512, dtype=torch.float32, device=dev)
+    W = torch.empty_like(f)
+    pos = torch.cumsum(mine.to(torch.int64), 0) - 1                       # row among my blocks
+    own_idx = torch.cumsum(have.to(torch.int64), 0) - 1                   # row in my generated piece
+    keep = mine & have
+    f[pos[keep].to(dev)] = f_r[own_idx[keep].to(dev)]
+    W[pos[keep].to(dev)] = W_r[own_idx[keep].to(dev)]
+    need = mine & ~have
+    n_moved = int(need.sum())
+    if n_moved:
+        c2, f2, W2 = scenes.route_blocks(plan, coords[need.to(dev)], chunk_blocks)
+        assert torch.equal(c2, coords[need.to(dev)]), "a moved block is no longer allocated"
+        f[pos[need].to(dev)] = f2
+        W[pos[need].to(dev)] = W2
+    return {"coords": coords, "part": np.ascontiguousarray(part), "f": f, "W": W, "moved": n_moved}
+
+
+def gather_coords(coords_r, world, dev):
+    """all_gather of every rank's generated block coordinates (variable counts, padded)."""
+    import torch
+    import torch.distributed as dist
+    n = torch.tensor([coords_r.shape[0]], device=dev)
+    ns = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(ns, n)
+    m = int(max(int(x) for x in ns))
+    pad = torch.zeros(m, 3, dtype=torch.int32, device=dev)
+    pad[:coords_r.shape[0]] = coords_r
+    bufs = [torch.zeros_like(pad) for _ in range(world)]
+    dist.all_gather(bufs, pad)
+    return [b[:int(k)] for b, k in zip(bufs, ns)]
 
 
 def alu_peak():
@@ -392,7 +466,17 @@ def reference_arm(args):
     if rank != 0:
         return 0
     dev = "cuda" if torch.cuda.is_available() else "cpu"
-    scene = make_scene(args.config, 1, args.seed, dev).to("cpu")
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    cfg = args.config or ("street" if world == 1 else "city")   # the same workload as our arm
+    if cfg == "city-weak":
+        cfg = f"city-weak:{world}"
+    if cfg.startswith("city"):
+        from synth.scenes import Scene
+        plan = route_plan(cfg, args.seed, dev)
+        c, f, W = shard_generate(plan, 1, 0)
+        scene = Scene(cfg, c.cpu(), f.cpu(), W.cpu(), lam=0.8, eps=0.01, iters=200, meta=plan.meta())
+    else:
+        scene = make_scene(cfg, 1, args.seed, dev).to("cpu")
     n_alloc = scene.n_alloc
     per_step_iters = 1
     for _ in range(args.warmup):
@@ -403,7 +487,8 @@ def reference_arm(args):
     sample = f"{per_step_iters} oracle iteration(s) over the whole {scene.name} volume ({n_alloc} voxels) per step"
     line = {"impl": "reference", "metric": "voxel-updates/s", "value": val, "unit": "voxel-updates/s",
             "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if cfg in ("city", "city-heavy") else "weak",
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": scene.name, "n_alloc": n_alloc, "blocks": scene.n_blocks,
                                             "iters_per_step": per_step_iters},
             "cpu_baseline": {"value": val, "unit": "voxel-updates/s", "cores": 1, "kind": "oracle", "sample": sample},
@@ -441,17 +526,42 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
         group = dist.group.WORLD
 
-    scene = make_scene(args.config, world, args.seed, dev)
-    iters = scene.iters if args.iters is None else args.iters
-    coords = scene.coords.contiguous()
-    if sharded:
-        part = partition(coords.cpu(), world)
-        mine = (part == rank).nonzero().squeeze(1).to(dev)
-        f_loc, W_loc = scene.f[mine].contiguous(), scene.W[mine].contiguous()
+    # workload: config 2 (street) on one GPU; BASELINE configs[4] (config 5) at N > 1 — the 1 km city route
+    # at a fixed size (strong scaling), or `--config city-weak` (125 m of route per GPU, weak scaling)
+    cfg = args.config or ("street" if world == 1 else "city")
+    if cfg == "city-weak":
+        cfg = f"city-weak:{world}"
+    gen_s = None
+    if cfg.startswith("city"):
+        # per-shard generation: each rank generates only the blocks of its arc range
+        from synth.scenes import Scene
+        t_gen = time.perf_counter()
+        plan = route_plan(cfg, args.seed, dev)
+        coords_r, f_r, W_r = shard_generate(plan, world, rank)
+        coords_all = gather_coords(coords_r, world, dev) if world > 1 else [coords_r]
+        sh = shard_assemble(plan, world, rank, coords_all, coords_r, f_r, W_r)
+        del coords_r, f_r, W_r, coords_all
+        gen_s = time.perf_counter() - t_gen
+        scene = Scene(cfg if not cfg.startswith("city-weak") else f"city-weak ({125 * world} m)", sh["coords"],
+                      sh["f"], sh["W"], lam=0.8, eps=0.01, iters=200, meta=plan.meta())
+        coords = sh["coords"]
+        f_loc, W_loc = sh["f"], sh["W"]
+        part = torch.from_numpy(sh["part"]) if sharded else None
+        n_moved = sh["moved"]
     else:
-        part = None
-        f_loc, W_loc = scene.f, scene.W
+        scene = make_scene(cfg, world, args.seed, dev)
+        coords = scene.coords.contiguous()
+        if sharded:
+            part = partition(scene, world)
+            mine = (part == rank).nonzero().squeeze(1).to(dev)
+            f_loc, W_loc = scene.f[mine].contiguous(), scene.W[mine].contiguous()
+        else:
+            part = None
+            f_loc, W_loc = scene.f, scene.W
+        n_moved = 0
+    iters = scene.iters if args.iters is None else args.iters
     n_local_vox = f_loc.shape[0] * 512
+    scaling = "strong" if cfg in ("city", "city-heavy") else "weak"
     stream = torch.cuda.current_stream(dev)
 
     def barrier():
@@ -512,6 +622,10 @@ def main():
     it_ms = float(it_t.item())
     n_alloc_total = scene.n_alloc
     value = n_alloc_total * iters / (ms / 1e3)
+    n_omega_t = torch.tensor([int((W_loc > 0).sum())], device=dev, dtype=torch.int64)
+    if sharded:
+        dist.all_reduce(n_omega_t)
+    n_omega_total = int(n_omega_t.item())
 
     # transparency: the same step with opts.freeze = 0 (every Ω voxel recomputed and rewritten)
     nf = None
@@ -651,13 +765,17 @@ def main():
     line = {
         "metric": "voxel-updates/s", "value": value, "unit": "voxel-updates/s", "n_gpus": world,
         "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": scene.name, "n_alloc": n_alloc_total, "n_omega": scene.n_omega(),
+        "scaling": scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": scene.name, "n_alloc": n_alloc_total, "n_omega": n_omega_total,
                    "blocks": scene.n_blocks, "iters": iters, "lambda": scene.lam, "eps": scene.eps,
                    "data_term": "L1" if scene.data_term == 0 else "L2",
                    "step": "vol_create + vol_regularise(init + iters) + vol_energy + vol_read_u",
                    "l2": f"inputs larger than L2 ({n_alloc_total * 48 / 1e9:.2f} GB of state vs 126 MB L2)",
                    "parallelism": f"route-axis shards x{world}" if sharded else "single GPU",
+                   "partition": ("vol_partition_route: arc length of the nearest camera-path point, equal "
+                                 "block counts" if sharded else None),
+                   "generation": ({"per_shard": True, "seconds": gen_s, "blocks_moved_at_rebalance": n_moved}
+                                  if gen_s is not None else None),
                    "energy": {"primal": E[0], "dual": E[1]}},
         "roofline": roofline, "cpu_baseline": cpu, "cpu_baseline_omp": cpu_omp, "e2e": e2e, "halo": halo, "gpu_launches": int(launches),
         "freeze": bool(args.freeze), "no_freeze": nf,

@@ -204,6 +204,26 @@ vol_status vol_plan_shard(const int32_t *block_xyz, int64_t n_global, const int3
                           int64_t *ghost_global, int64_t *send_global, int64_t *peer_send,
                           int64_t *peer_recv);
 
+/* Route-axis partition (the regulariser is block-local with boundary
+ * conditions from the neighbour blocks, so the cut surface between ranks is the halo).  Host only.
+ *   block_xyz   [n_global][3] int32 block coordinates (host memory);
+ *   route       [n_route][3] float64 polyline vertices in metres (the camera path), n_route >= 1;
+ *   block_edge  block edge length in metres (8 x voxel size); a block's centre is (b + 0.5)*block_edge;
+ *   world       number of ranks; part [n_global] (out): owner rank of every block;
+ *   arc         [n_global] (out, nullable): arc length (metres) of the route point nearest to each
+ *               block centre (the first segment wins a tie in distance).
+ * Blocks are ordered by (arc, x, y, z) and cut into `world` contiguous ranges of equal block count:
+ * rank r owns positions [r*n/world, (r+1)*n/world).  The result is a pure function of the arguments
+ * (every rank computes the same map).  Returns VOL_OK or VOL_EINVAL.                               */
+vol_status vol_partition_route(const int32_t *block_xyz, int64_t n_global, const double *route, int32_t n_route,
+                               double block_edge, int world, int32_t *part, double *arc);
+
+/* Destroy every cached NCCL communicator of this process (teardown; volumes still using one must be
+ * destroyed first).  Communicators are cached per (unique id, world, rank, device) so that volumes
+ * created over one process group share one; a communicator that reports an asynchronous error is
+ * aborted and evicted automatically.                                                              */
+vol_status vol_release_comms(void);
+
 /* Isosurface extraction ("extract the surface", P:132-133 zero-crossing
  * level set).  Readings X-1 … X-7: marching tetrahedra over the cells spanned by every
  * voxel g and g + {0,1}^3 (voxel centres (g + ½)·voxel metres) whose 8 corners are allocated with

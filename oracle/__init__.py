@@ -108,6 +108,9 @@ def _declare(L):
         r = getattr(L, f"orc_regularise_{sfx}")
         r.restype = cint
         r.argtypes = [i64, P, P, P, real, real, real, real, real, cint, cint, i64, P, P, P, cint]
+        ph = getattr(L, f"orc_phase_{sfx}")
+        ph.restype = cint
+        ph.argtypes = [i64, P, P, P, real, real, real, real, real, cint, cint, P, P, P]
     L.orc_energy.restype = None
     L.orc_energy.argtypes = [i64, P, P, P, P, P, dbl, dbl, cint, P, P]
     # fusion (fusion_oracle.c)
@@ -253,6 +256,28 @@ def regularise(coords, f, W, lam, eps, tau, sigma, iters, theta=1.0, data_term=0
     getattr(lib(omp), f"orc_regularise_{sfx}")(n, _ptr(nbr), _ptr(ff), _ptr(Wf), r32(lam), r32(eps), r32(tau),
                                             r32(sigma), r32(theta), int(data_term), int(init), int(iters),
                                             _ptr(u), _ptr(ub), _ptr(p), resume)
+    return u, ub, p
+
+
+def phase(coords, f, W, lam, eps, tau, sigma, which, state, theta=1.0, data_term=0, precision="f64", nbr=None):
+    """One phase of the iteration on `state` = (u, ubar, p), updated in place and returned:
+    which = "dual" (Eq. 3 + Eq. 7 with Huber) or "primal" (Eq. 4 + Eq. 8 + Eq. 9 relaxation).
+    `regularise` is dual then primal, `iters` times; tests use the split to replay other schedules."""
+    dt, sfx = _rt(precision)
+    if nbr is None:
+        nbr = neighbours(coords)
+    nbr = _np(nbr, np.int32)
+    n = nbr.shape[0]
+    ff = _np(f, np.float32).reshape(n, 512)
+    Wf = _np(W, np.float32).reshape(n, 512)
+    u, ub, p = state
+    for a in (u, ub, p):
+        assert a.dtype == dt and a.flags.c_contiguous
+    r32 = lambda x: float(np.float32(x))
+    rc = getattr(lib(), f"orc_phase_{sfx}")(n, _ptr(nbr), _ptr(ff), _ptr(Wf), r32(lam), r32(eps), r32(tau), r32(sigma),
+                                            r32(theta), int(data_term), {"dual": 0, "primal": 1}[which],
+                                            _ptr(u), _ptr(ub), _ptr(p))
+    assert rc == 0
     return u, ub, p
 
 

@@ -5,6 +5,8 @@ this package is its thin Python binding.  It never imports the CPU oracle and ha
 """
 from . import stereo  # noqa: F401
 from .stream import Reconstruction  # noqa: F401
-from .volume import Volume, block_hash, connect_group, fuse, group_energy, nccl_unique_id, plan_shard, regularise_group  # noqa: F401
+from .volume import (Volume, block_hash, connect_group, fuse, group_energy, nccl_unique_id,  # noqa: F401
+                     partition_route, plan_shard, regularise_group, release_comms)
 
-__all__ = ["Volume", "fuse", "Reconstruction", "block_hash", "plan_shard", "nccl_unique_id", "connect_group", "regularise_group", "group_energy"]
+__all__ = ["Volume", "fuse", "Reconstruction", "block_hash", "plan_shard", "partition_route", "nccl_unique_id",
+           "connect_group", "regularise_group", "group_energy", "release_comms"]

@@ -18,7 +18,12 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cmath>
 #include <climits>
+#include <cstring>
+#include <future>
+#include <memory>
 #include <mutex>
 #include <numeric>
 #include <unordered_map>
@@ -209,6 +214,69 @@ extern "C" vol_status vol_plan_shard(const int32_t *xyz, int64_t n, const int32_
     return VOL_OK;
 }
 
+// Route-axis partition: order the blocks by the arc length of the point of the route
+// polyline nearest to the block centre (ties by (x, y, z)) and cut the order into `world` contiguous
+// ranges of equal block count.  The paper's regulariser is block-local with boundary conditions taken
+// from the neighbours, so the cut surface is the halo: cutting across the route keeps it
+// to one canyon cross-section per rank boundary, and a route that never comes back to itself gives
+// every rank at most the two peers r - 1 and r + 1.
+extern "C" vol_status vol_partition_route(const int32_t *xyz, int64_t n, const double *route, int32_t n_route,
+                                          double block_edge, int world, int32_t *part, double *arc_out) {
+    if (!xyz || n < 1 || !route || n_route < 1 || !(block_edge > 0.0) || world < 1 || !part)
+        return fail(VOL_EINVAL, "vol_partition_route: bad arguments");
+    // cumulative arc length at every polyline vertex
+    std::vector<double> cum(n_route, 0.0);
+    for (int k = 1; k < n_route; k++) {
+        const double *a = route + 3 * (k - 1), *b = route + 3 * k;
+        cum[k] = cum[k - 1] + std::sqrt((b[0] - a[0]) * (b[0] - a[0]) + (b[1] - a[1]) * (b[1] - a[1]) +
+                                        (b[2] - a[2]) * (b[2] - a[2]));
+    }
+    std::vector<double> arc(n);
+    for (int64_t g = 0; g < n; g++) {
+        double c[3];
+        for (int a = 0; a < 3; a++) c[a] = ((double)xyz[3 * g + a] + 0.5) * block_edge;
+        double best_d2 = INFINITY, best_s = 0.0;
+        if (n_route == 1) {
+            best_s = 0.0;
+        } else {
+            for (int k = 0; k + 1 < n_route; k++) {   // first segment with the strictly smallest distance wins
+                const double *a = route + 3 * k, *b = route + 3 * (k + 1);
+                const double d[3] = {b[0] - a[0], b[1] - a[1], b[2] - a[2]};
+                const double len2 = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
+                double t = 0.0;
+                if (len2 > 0.0) {
+                    t = ((c[0] - a[0]) * d[0] + (c[1] - a[1]) * d[1] + (c[2] - a[2]) * d[2]) / len2;
+                    t = std::min(1.0, std::max(0.0, t));
+                }
+                double d2 = 0.0;
+                for (int q = 0; q < 3; q++) {
+                    const double e = c[q] - (a[q] + t * d[q]);
+                    d2 += e * e;
+                }
+                if (d2 < best_d2) {
+                    best_d2 = d2;
+                    best_s = cum[k] + t * (cum[k + 1] - cum[k]);
+                }
+            }
+        }
+        arc[g] = best_s;
+        if (arc_out) arc_out[g] = best_s;
+    }
+    std::vector<int64_t> order(n);
+    std::iota(order.begin(), order.end(), (int64_t)0);
+    std::sort(order.begin(), order.end(), [&](int64_t i, int64_t j) {
+        if (arc[i] != arc[j]) return arc[i] < arc[j];
+        for (int a = 0; a < 3; a++)
+            if (xyz[3 * i + a] != xyz[3 * j + a]) return xyz[3 * i + a] < xyz[3 * j + a];
+        return i < j;
+    });
+    for (int r = 0; r < world; r++) {
+        const int64_t lo = (int64_t)r * n / world, hi = (int64_t)(r + 1) * n / world;
+        for (int64_t k = lo; k < hi; k++) part[order[k]] = r;
+    }
+    return VOL_OK;
+}
+
 // ------------------------------------------------------------------------------ device runtime
 
 constexpr int64_t kMsgFloats = 4 * kBlockVox;  // ū (or W), p_x (or f), p_y, p_z per block
@@ -290,60 +358,134 @@ static vol_status nccl_exchange(vol_s *v, cudaStream_t s) {
     NvtxRange nvtx_range_("halo_exchange");
     ShardRuntime *R = v->shard;
     const ShardPlan &P = R->plan;
-    NCK(ncclGroupStart());
-    for (int q = 0; q < P.world; q++) {
+    // the group is always closed, even when a send/recv fails inside it: an open group would defer
+    // every later NCCL call of this thread
+    ncclResult_t first = ncclGroupStart();
+    if (first != ncclSuccess) return fail(VOL_ENCCL, "ncclGroupStart: %s", ncclGetErrorString(first));
+    const char *what = nullptr;
+    for (int q = 0; q < P.world && !what; q++) {
         if (q == P.rank) continue;
-        if (P.send_cnt[q] > 0)
-            NCK(ncclSend(R->sendbuf + P.send_off[q] * kMsgFloats, (size_t)(P.send_cnt[q] * kMsgFloats), ncclFloat, q,
-                         R->comm, s));
-        if (P.recv_cnt[q] > 0)
-            NCK(ncclRecv(R->recvbuf + P.recv_off[q] * kMsgFloats, (size_t)(P.recv_cnt[q] * kMsgFloats), ncclFloat, q,
-                         R->comm, s));
+        if (P.send_cnt[q] > 0) {
+            const ncclResult_t r = ncclSend(R->sendbuf + P.send_off[q] * kMsgFloats, (size_t)(P.send_cnt[q] * kMsgFloats),
+                                            ncclFloat, q, R->comm, s);
+            if (r != ncclSuccess) first = r, what = "ncclSend";
+        }
+        if (!what && P.recv_cnt[q] > 0) {
+            const ncclResult_t r = ncclRecv(R->recvbuf + P.recv_off[q] * kMsgFloats, (size_t)(P.recv_cnt[q] * kMsgFloats),
+                                            ncclFloat, q, R->comm, s);
+            if (r != ncclSuccess) first = r, what = "ncclRecv";
+        }
     }
-    NCK(ncclGroupEnd());
+    const ncclResult_t end = ncclGroupEnd();
+    if (what) return fail(VOL_ENCCL, "%s: %s", what, ncclGetErrorString(first));
+    if (end != ncclSuccess) return fail(VOL_ENCCL, "ncclGroupEnd: %s", ncclGetErrorString(end));
     return VOL_OK;
 }
 
 // NCCL communicators are cached by (unique id, world, rank, device): creating a communicator costs
 // hundreds of milliseconds, and a process typically builds many volumes over one process group (the
-// Python binding reuses one unique id per torch.distributed group).
+// Python binding reuses one unique id per torch.distributed group).  The first caller of a key inserts
+// a placeholder (a shared future) under the lock and runs ncclCommInitRank outside it — so threads of
+// one process driving different ranks of one id cannot deadlock each other — and later callers of the
+// same key wait on the placeholder instead of initialising the same rank twice.  A failed init removes
+// the placeholder (its waiters see the failure); a communicator that reports an asynchronous error is
+// aborted and evicted (comm_evict), so later volumes of the group build a fresh one.
 namespace {
 struct CommEntry {
     unsigned char id[NCCL_UNIQUE_ID_BYTES];
     int world, rank, device;
-    ncclComm_t comm;
+    std::shared_future<ncclComm_t> comm;   // nullptr once ready = init failed
 };
-std::vector<CommEntry> g_comms;
-std::mutex g_comms_mu;   // the cache is process-wide; ncclCommInitRank itself runs outside the lock
+std::vector<std::shared_ptr<CommEntry>> g_comms;
+std::mutex g_comms_mu;
 
-bool comm_lookup(const void *id_bytes, int world, int rank, int device, ncclComm_t *out) {
-    std::lock_guard<std::mutex> lk(g_comms_mu);
-    for (const CommEntry &e : g_comms)
-        if (e.world == world && e.rank == rank && e.device == device && !memcmp(e.id, id_bytes, NCCL_UNIQUE_ID_BYTES)) {
-            *out = e.comm;
-            return true;
-        }
-    return false;
+bool same_comm_key(const CommEntry &e, const void *id_bytes, int world, int rank, int device) {
+    return e.world == world && e.rank == rank && e.device == device && !memcmp(e.id, id_bytes, NCCL_UNIQUE_ID_BYTES);
 }
 }  // namespace
 
 static vol_status comm_acquire(const void *id_bytes, int world, int rank, int device, ncclComm_t *out) {
-    if (comm_lookup(id_bytes, world, rank, device, out)) return VOL_OK;
-    ncclUniqueId id;
-    memcpy(&id, id_bytes, sizeof id);
-    ncclComm_t comm;
-    NCK(ncclCommInitRank(&comm, world, id, rank));
-    CommEntry e;
-    memcpy(e.id, id_bytes, NCCL_UNIQUE_ID_BYTES);
-    e.world = world;
-    e.rank = rank;
-    e.device = device;
-    e.comm = comm;
+    std::promise<ncclComm_t> made;
+    std::shared_ptr<CommEntry> mine;
+    std::shared_future<ncclComm_t> wait;
     {
         std::lock_guard<std::mutex> lk(g_comms_mu);
-        g_comms.push_back(e);
+        for (const auto &e : g_comms)
+            if (same_comm_key(*e, id_bytes, world, rank, device)) wait = e->comm;
+        if (!wait.valid()) {
+            mine = std::make_shared<CommEntry>();
+            memcpy(mine->id, id_bytes, NCCL_UNIQUE_ID_BYTES);
+            mine->world = world;
+            mine->rank = rank;
+            mine->device = device;
+            mine->comm = made.get_future().share();
+            g_comms.push_back(mine);
+        }
     }
+    if (!mine) {   // another thread owns (or owned) the initialisation of this key
+        ncclComm_t c = wait.get();
+        if (!c) return fail(VOL_ENCCL, "ncclCommInitRank of this (id, rank) failed in another thread");
+        *out = c;
+        return VOL_OK;
+    }
+    ncclUniqueId id;
+    memcpy(&id, id_bytes, sizeof id);
+    ncclComm_t comm = nullptr;
+    const ncclResult_t r = ncclCommInitRank(&comm, world, id, rank);
+    if (r != ncclSuccess) {
+        {
+            std::lock_guard<std::mutex> lk(g_comms_mu);
+            g_comms.erase(std::remove(g_comms.begin(), g_comms.end(), mine), g_comms.end());
+        }
+        made.set_value(nullptr);
+        return fail(VOL_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+    }
+    made.set_value(comm);
     *out = comm;
+    return VOL_OK;
+}
+
+// A communicator with an asynchronous error is unusable: abort it and drop it from the cache.
+static void comm_evict(ncclComm_t comm) {
+    bool found = false;
+    {
+        std::lock_guard<std::mutex> lk(g_comms_mu);
+        for (auto it = g_comms.begin(); it != g_comms.end(); ++it) {
+            const std::shared_future<ncclComm_t> &f = (*it)->comm;
+            if (f.wait_for(std::chrono::seconds(0)) == std::future_status::ready && f.get() == comm) {
+                g_comms.erase(it);
+                found = true;
+                break;
+            }
+        }
+    }
+    if (found) ncclCommAbort(comm);
+}
+
+// Asynchronous NCCL failures of earlier work (SURVEY §5 failure detection): evict the communicator.
+static vol_status check_async(ncclComm_t comm) {
+    ncclResult_t async = ncclSuccess;
+    if (ncclCommGetAsyncError(comm, &async) == ncclSuccess && async != ncclSuccess && async != ncclInProgress) {
+        comm_evict(comm);
+        return fail(VOL_ENCCL, "NCCL asynchronous error: %s (communicator aborted)", ncclGetErrorString(async));
+    }
+    return VOL_OK;
+}
+
+extern "C" vol_status vol_release_comms(void) {
+    std::vector<std::shared_ptr<CommEntry>> all;
+    {
+        std::lock_guard<std::mutex> lk(g_comms_mu);
+        all.swap(g_comms);
+    }
+    ncclResult_t first = ncclSuccess;
+    for (auto &e : all) {
+        ncclComm_t c = e->comm.get();
+        if (!c) continue;
+        const ncclResult_t r = ncclCommDestroy(c);
+        if (first == ncclSuccess) first = r;
+    }
+    if (first != ncclSuccess) return fail(VOL_ENCCL, "ncclCommDestroy: %s", ncclGetErrorString(first));
     return VOL_OK;
 }
 
@@ -543,10 +685,7 @@ vol_status shard_iterate(vol_s *v, const IterParams &P, int32_t iters) {
     if (v->pending_kernel == 0 || v->pending_kernel == 2) {   // the product path: the skewed schedule
         vol_status st = nccl_skew(v, P, iters);
         if (st != VOL_OK) return st;
-        ncclResult_t async = ncclSuccess;
-        if (ncclCommGetAsyncError(R->comm, &async) == ncclSuccess && async != ncclSuccess && async != ncclInProgress)
-            return fail(VOL_ENCCL, "NCCL asynchronous error: %s", ncclGetErrorString(async));
-        return VOL_OK;
+        return check_async(R->comm);
     }
     int64_t launches = 0;
     for (int32_t k = 0; k < iters; k++) {
@@ -554,11 +693,7 @@ vol_status shard_iterate(vol_s *v, const IterParams &P, int32_t iters) {
         if (st != VOL_OK) return st;
     }
     v->last_launches = launches;
-    // asynchronous NCCL failures of earlier work (SURVEY §5 failure detection)
-    ncclResult_t async = ncclSuccess;
-    if (ncclCommGetAsyncError(R->comm, &async) == ncclSuccess && async != ncclSuccess && async != ncclInProgress)
-        return fail(VOL_ENCCL, "NCCL asynchronous error: %s", ncclGetErrorString(async));
-    return VOL_OK;
+    return check_async(R->comm);
 }
 
 // Refresh every ghost's u and p (energy needs u of +neighbours and p of −neighbours), then the

@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <vector>
 
@@ -737,9 +738,18 @@ struct GraphKey {
     vol_stereo_params p;
 };
 
+// The executable graph is reference-counted: a call holds its own reference from lookup to launch, so
+// evicting the entry (another thread inserting a 9th key) cannot destroy an exec about to be launched.
+using ExecRef = std::shared_ptr<CUgraphExec_st>;
+ExecRef exec_ref(cudaGraphExec_t e) {
+    return ExecRef(e, [](cudaGraphExec_t x) {
+        if (x) cudaGraphExecDestroy(x);
+    });
+}
+
 struct GraphEntry {
     GraphKey key;
-    cudaGraphExec_t exec;
+    ExecRef exec;
     long long launches;
 };
 
@@ -806,7 +816,7 @@ extern "C" vol_status vol_stereo(const float *left, const float *right, int32_t 
         int dev = 0;
         cudaGetDevice(&dev);
         GraphKey key{ws, n_frames, chunk, mode, dev, *prm};
-        cudaGraphExec_t exec = nullptr;
+        ExecRef exec;
         {
             std::lock_guard<std::mutex> lk(g_graph_mu);
             for (auto &e : g_graphs)
@@ -819,25 +829,24 @@ extern "C" vol_status vol_stereo(const float *left, const float *right, int32_t 
             cudaStream_t cs;
             CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
             cudaGraph_t graph;
+            cudaGraphExec_t ge = nullptr;
             cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
             if (e == cudaSuccess) {
                 enqueue_solve(L, prm, n_frames, chunk, mode, cs, launches);
                 e = cudaStreamEndCapture(cs, &graph);
             }
             if (e == cudaSuccess) {
-                e = cudaGraphInstantiate(&exec, graph, 0);
+                e = cudaGraphInstantiate(&ge, graph, 0);
                 cudaGraphDestroy(graph);
             }
             cudaStreamDestroy(cs);
             if (e != cudaSuccess) return fail(VOL_ECUDA, "vol_stereo: graph capture failed: %s", cudaGetErrorString(e));
+            exec = exec_ref(ge);
             std::lock_guard<std::mutex> lk(g_graph_mu);
-            if (g_graphs.size() >= 8) {
-                cudaGraphExecDestroy(g_graphs.front().exec);
-                g_graphs.erase(g_graphs.begin());
-            }
+            if (g_graphs.size() >= 8) g_graphs.erase(g_graphs.begin());   // freed once no call holds it
             g_graphs.push_back(GraphEntry{key, exec, launches});
         }
-        CK(cudaGraphLaunch(exec, s));
+        CK(cudaGraphLaunch(exec.get(), s));
     }
     counted((int)launches);
     const cudaMemcpyKind kind = dev_out ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;

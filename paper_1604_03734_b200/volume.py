@@ -9,6 +9,7 @@ host/device pointers.  Names follow the paper: λ (lam), ε (eps, Huber), τ (ta
 from __future__ import annotations
 
 import ctypes
+import weakref
 
 import numpy as np
 import torch
@@ -66,15 +67,39 @@ def plan_shard(coords, part, world: int, rank: int) -> dict:
                 peer_send=psend, peer_recv=precv)
 
 
-_GROUP_IDS = {}
+def partition_route(coords, route, block_edge: float, world: int, return_arc: bool = False):
+    """Route-axis partition (``vol_partition_route``; host only): owner rank per block —
+    blocks ordered by the arc length of the nearest route point (ties by x, y, z), cut into `world`
+    contiguous ranges of equal block count.  `route` is the polyline [m, 3] in metres, `block_edge`
+    the block edge in metres (8 × voxel).  Returns int32 part [n] (and float64 arc [n])."""
+    c = np.ascontiguousarray(coords.cpu().numpy() if isinstance(coords, torch.Tensor) else coords,
+                             dtype=np.int32).reshape(-1, 3)
+    r = np.ascontiguousarray(route, dtype=np.float64).reshape(-1, 3)
+    part = np.zeros(c.shape[0], np.int32)
+    arc = np.zeros(c.shape[0], np.float64)
+    N.check(N.lib().vol_partition_route(c.ctypes.data, c.shape[0], r.ctypes.data, r.shape[0], float(block_edge),
+                                        int(world), part.ctypes.data, arc.ctypes.data))
+    return (part, arc) if return_arc else part
+
+
+def release_comms():
+    """Destroy libvol's cached NCCL communicators (teardown, after every sharded volume is closed)."""
+    N.check(N.lib().vol_release_comms())
+
+
+# one NCCL unique id per live process group: weak keys, so a destroyed group's entry disappears with it
+# (an id() key could be reused by a later group and hand it a stale id); the group's name and ranks are
+# checked too
+_GROUP_IDS = weakref.WeakKeyDictionary()
 
 
 def _group_nccl_id(group, device) -> bytes:
     """One NCCL unique id per torch.distributed group (created by the group's rank 0, broadcast once);
     libvol caches the communicator built from it, so later volumes of the group reuse it."""
     import torch.distributed as dist_mod
-    key = id(group)
-    if key not in _GROUP_IDS:
+    sig = (getattr(group, "group_name", None), tuple(dist_mod.get_process_group_ranks(group)))
+    ent = _GROUP_IDS.get(group)
+    if ent is None or ent[0] != sig:
         idbuf = torch.zeros(128, dtype=torch.uint8)
         if dist_mod.get_rank(group) == 0:
             idbuf = torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8).clone()
@@ -85,8 +110,8 @@ def _group_nccl_id(group, device) -> bytes:
             idbuf = idd.cpu()
         else:
             dist_mod.broadcast(idbuf, src=src, group=group)
-        _GROUP_IDS[key] = bytes(idbuf.numpy().tobytes())
-    return _GROUP_IDS[key]
+        _GROUP_IDS[group] = (sig, bytes(idbuf.numpy().tobytes()))
+    return _GROUP_IDS[group][1]
 
 
 class Volume:

@@ -350,9 +350,9 @@ def _make_boxes(seed, cfg, segs, per_metre, device):
     return out
 
 
-def _route_scene(name, segs, boxes_per_seg, v, mu, H, seed, cfg, device, chunk_blocks, R=25.0,
-                 cam_step=1.0, near_pred=None, compact=False):
-    """Shared body of street and city: candidate blocks → sd, W per voxel → allocation → f."""
+def _route_candidates(segs, boxes_per_seg, v, mu, H, device, near_pred=None, compact=False):
+    """Candidate blocks of a route scene: every block whose centre lies within μ + half a block diagonal
+    of a surface (a superset of the allocated blocks), slab by slab in x; int32 [m, 3]."""
     allboxes = torch.cat(boxes_per_seg, 0) if boxes_per_seg else torch.zeros(0, 6, dtype=torch.float64, device=device)
     B = 8 * v
     # candidate block range = route bounding box ± (4 m + 1 block), z in [−μ−B, H+μ+B]
@@ -383,6 +383,14 @@ def _route_scene(name, segs, boxes_per_seg, v, mu, H, seed, cfg, device, chunk_b
         sc = (cand.to(torch.int64) >> 4) + (1 << 20)
         key = (sc[:, 0] << 42) | (sc[:, 1] << 21) | sc[:, 2]
         cand = cand[torch.argsort(key, stable=True)]
+    return cand
+
+
+def _route_alloc(cand, segs, boxes_per_seg, v, mu, H, device, chunk_blocks, R=25.0, cam_step=1.0):
+    """sd and W (observation count) of every voxel of the candidate blocks, chunk by chunk; keeps the
+    blocks with some voxel at |sd| ≤ μ and W > 0.  Every value depends only on the voxel and the scene,
+    so any subset of candidates gives the same per-block result (per-shard generation)."""
+    allboxes = torch.cat(boxes_per_seg, 0) if boxes_per_seg else torch.zeros(0, 6, dtype=torch.float64, device=device)
     # camera samples per segment
     seg_samples = []
     for seg in segs:
@@ -412,10 +420,28 @@ def _route_scene(name, segs, boxes_per_seg, v, mu, H, seed, cfg, device, chunk_b
         keep_coords.append(cb[alloc])
         keep_sd.append(sd[alloc])
         keep_W.append(W[alloc])
+    if not keep_coords:
+        return (torch.zeros(0, 3, dtype=torch.int32, device=device), torch.zeros(0, 512, dtype=torch.float64, device=device),
+                torch.zeros(0, 512, dtype=torch.float64, device=device))
     coords = torch.cat(keep_coords, 0).contiguous()
     sd = torch.cat(keep_sd, 0)
     W = torch.cat(keep_W, 0).to(torch.float64)
     return coords, sd, W
+
+
+def _route_scene(name, segs, boxes_per_seg, v, mu, H, seed, cfg, device, chunk_blocks, R=25.0,
+                 cam_step=1.0, near_pred=None, compact=False):
+    """Shared body of street and city: candidate blocks → sd, W per voxel → allocation → f."""
+    cand = _route_candidates(segs, boxes_per_seg, v, mu, H, device, near_pred, compact)
+    return _route_alloc(cand, segs, boxes_per_seg, v, mu, H, device, chunk_blocks, R, cam_step)
+
+
+def route_polyline(segs, z=CAM_Z):
+    """Vertices [m, 3] (metres) of the camera path through the segments (the route of SURVEY §8(e))."""
+    pts = [(segs[0].x0, segs[0].y0, z)]
+    for s in segs:
+        pts.append((s.x0 + s.L * s.dx, s.y0 + s.L * s.dy, z))
+    return np.asarray(pts, np.float64)
 
 
 def _street_noise(coords, sd, W, v, mu, seed, cfg, path_dist, want_ctr=True, chunk=65536):
@@ -452,7 +478,8 @@ def street(seed: int = 0, outlier: bool = False, length: float = 60.0, H: float 
                                  near_pred=lambda c: (c[:, 0] >= 0) & (c[:, 0] <= length))
     path_dist = lambda P: torch.sqrt(P[..., 1] ** 2 + (P[..., 2] - CAM_Z) ** 2)
     f, ctr = _street_noise(coords, sd, W, v, mu, seed, cfg, path_dist)
-    meta = dict(voxel=v, mu=mu, H=H, length=length, seed=seed, n_boxes=int(boxes[0].shape[0]))
+    meta = dict(voxel=v, mu=mu, H=H, length=length, seed=seed, n_boxes=int(boxes[0].shape[0]),
+                route=route_polyline([seg]))
     if not outlier:
         return Scene("street", coords, f.float().contiguous(), W.float().contiguous(), lam=0.8, eps=0.01,
                      iters=300, meta=meta)
@@ -506,11 +533,50 @@ def _outliers_and_clumps(coords, f, W, ctr, seed, cfg, frac=0.30, clump=20):
     return f, W
 
 
-def city(seed: int = 0, length: float = 1000.0, H: float = 20.0, device="cpu", chunk_blocks: int = 1024,
-         lanes: int = 1) -> Scene:
-    """Config 4 (city): staircase polyline from the origin heading +x, segments U[100,200] m, 90° turns
-    alternating left/right, truncated to `length` metres; each segment a config-2 canyon (20 boxes per 60 m),
-    v = 0.1 m, μ = 0.5 m.  `lanes` > 1 is the city-heavy density knob (parallel canyons offset by 40 m)."""
+@dataclass
+class RoutePlan:
+    """The cheap, global part of a route scene (city configs 4/5): geometry, solver-independent constants
+    and the candidate blocks.  Every rank of a sharded run computes the same plan; the expensive per-voxel
+    values are generated only for the blocks a rank owns (:func:`route_blocks`)."""
+    name: str
+    seed: int
+    cfg: int
+    segs: list          # all canyons (lanes × route segments)
+    route_segs: list    # the route itself (first lane)
+    boxes: list
+    v: float
+    mu: float
+    H: float
+    length: float
+    cand: torch.Tensor  # int32 [m, 3] candidate blocks (superset of the allocated blocks)
+
+    @property
+    def block_edge(self) -> float:
+        return 8.0 * self.v
+
+    @property
+    def route(self) -> np.ndarray:
+        return route_polyline(self.route_segs)
+
+    def path_dist(self, P):
+        best = None
+        for s in self.segs:
+            sP, lat = s.local(P[..., 0], P[..., 1])
+            ds = torch.clamp(torch.maximum(-sP, sP - s.L), min=0.0)
+            d = torch.sqrt(ds ** 2 + lat ** 2 + (P[..., 2] - CAM_Z) ** 2)
+            best = d if best is None else torch.minimum(best, d)
+        return best
+
+    def meta(self) -> dict:
+        return dict(voxel=self.v, mu=self.mu, H=self.H, length=self.length, seed=self.seed, route=self.route,
+                    segments=[(s.x0, s.y0, s.dx, s.dy, s.L) for s in self.segs])
+
+
+def city_plan(seed: int = 0, length: float = 1000.0, H: float = 20.0, device="cpu", lanes: int = 1) -> RoutePlan:
+    """Geometry and candidate blocks of config 4 (city): staircase polyline from the origin heading +x,
+    segments U[100,200] m, 90° turns alternating left/right, truncated to `length` metres; each segment a
+    config-2 canyon (20 boxes per 60 m), v = 0.1 m, μ = 0.5 m.  `lanes` > 1 is the city-heavy density
+    knob (parallel canyons offset by 40 m)."""
     v, mu = 0.1, 0.5
     cfg = CONFIG_IDS["city"]
     key = rng.stream_key(seed, cfg, rng.S_ROUTE)
@@ -529,22 +595,25 @@ def city(seed: int = 0, length: float = 1000.0, H: float = 20.0, device="cpu", c
                   for k in range(lanes) for s in segs]
     all_segs = lanes_segs if lanes > 1 else segs
     boxes = _make_boxes(seed, cfg, all_segs, 20.0 / 60.0, device)
-    coords, sd, W = _route_scene("city", all_segs, boxes, v, mu, H, seed, cfg, device, chunk_blocks,
-                                 compact=lanes > 1)
+    cand = _route_candidates(all_segs, boxes, v, mu, H, device, compact=lanes > 1)
+    return RoutePlan("city" if lanes == 1 else "city-heavy", seed, cfg, all_segs, segs, boxes, v, mu, H, length, cand)
 
-    def path_dist(P):
-        best = None
-        for s in all_segs:
-            sP, lat = s.local(P[..., 0], P[..., 1])
-            ds = torch.clamp(torch.maximum(-sP, sP - s.L), min=0.0)
-            d = torch.sqrt(ds ** 2 + lat ** 2 + (P[..., 2] - CAM_Z) ** 2)
-            best = d if best is None else torch.minimum(best, d)
-        return best
 
-    f, _ = _street_noise(coords, sd, W, v, mu, seed, cfg, path_dist, want_ctr=False)
-    meta = dict(voxel=v, mu=mu, H=H, length=length, seed=seed, segments=[(s.x0, s.y0, s.dx, s.dy, s.L) for s in all_segs])
-    return Scene("city" if lanes == 1 else "city-heavy", coords, f.float().contiguous(), W.float().contiguous(),
-                 lam=0.8, eps=0.01, iters=200, meta=meta)
+def route_blocks(plan: RoutePlan, cand: torch.Tensor, chunk_blocks: int = 1024):
+    """The allocated blocks among the candidate blocks `cand` of `plan`, with their f and W
+    (float32 [m, 512]), in the order of `cand`.  Per-block values do not depend on which other blocks
+    are generated, so shards generated separately and concatenated equal the whole scene."""
+    coords, sd, W = _route_alloc(cand, plan.segs, plan.boxes, plan.v, plan.mu, plan.H, cand.device, chunk_blocks)
+    f, _ = _street_noise(coords, sd, W, plan.v, plan.mu, plan.seed, plan.cfg, plan.path_dist, want_ctr=False)
+    return coords, f.float().contiguous(), W.float().contiguous()
+
+
+def city(seed: int = 0, length: float = 1000.0, H: float = 20.0, device="cpu", chunk_blocks: int = 1024,
+         lanes: int = 1) -> Scene:
+    """Config 4 (city) on one device: :func:`city_plan` + :func:`route_blocks` over every candidate."""
+    plan = city_plan(seed, length, H, device, lanes)
+    coords, f, W = route_blocks(plan, plan.cand, chunk_blocks)
+    return Scene(plan.name, coords, f, W, lam=0.8, eps=0.01, iters=200, meta=plan.meta())
 
 
 # ----------------------------------------------------------------------------------------------

@@ -174,6 +174,19 @@ def _city():
     return _cache["city"]
 
 
+def _city_oracle():
+    """fp32 and fp64 oracle u after the config's 200 iterations (OpenMP timing build, bitwise the plain
+    oracle), computed once for the tests below."""
+    if "city-oracle" not in _cache:
+        s = _city()
+        nbr = oracle.neighbours(s.coords)
+        kw = dict(theta=s.theta, data_term=s.data_term, init=s.init, nbr=nbr, omp=True)
+        u32, _, _ = oracle.regularise(s.coords, s.f, s.W, s.lam, s.eps, s.tau, s.sigma, s.iters, precision="f32", **kw)
+        u64, _, _ = oracle.regularise(s.coords, s.f, s.W, s.lam, s.eps, s.tau, s.sigma, s.iters, precision="f64", **kw)
+        _cache["city-oracle"] = (nbr, u32, u64)
+    return _cache["city-oracle"]
+
+
 def test_city_first_iterations_match_oracle(V):
     """configs[3] geometry (staircase route, v = 10 cm, μ = 0.5 m, Huber-TV): the whole volume after
     2 iterations, bitwise against the fp32 oracle and within 1e-5 of fp64; after all 200 iterations
@@ -183,41 +196,88 @@ def test_city_first_iterations_match_oracle(V):
     vol = V(s.coords.cuda(), s.f.cuda(), s.W.cuda())
     vol.regularise_scene(s, iters=2)
     u = vol.u().cpu().numpy()
-    nbr = oracle.neighbours(s.coords)
+    nbr, u32_full, _ = _city_oracle()
     u32, _, _ = oracle.regularise_scene(s, precision="f32", iters=2, nbr=nbr)
     assert np.array_equal(u, u32)
     u64, _, _ = oracle.regularise_scene(s, precision="f64", iters=2, nbr=nbr)
     assert float(np.abs(u - u64).max()) <= 1e-5
-    # and after the config's full 200 iterations, bit for bit (OpenMP timing build of the oracle)
+    # and after the config's full 200 iterations, bit for bit
     vol.regularise_scene(s)
     u = vol.u().cpu().numpy()
-    u32, _, _ = oracle.regularise(s.coords, s.f, s.W, s.lam, s.eps, s.tau, s.sigma, s.iters, theta=s.theta,
-                                  data_term=s.data_term, init=s.init, precision="f32", nbr=nbr, omp=True)
+    assert np.array_equal(u.view(np.uint32), u32_full.view(np.uint32))
+
+
+def _check_vs_oracle(u, u32, u64):
     assert np.array_equal(u.view(np.uint32), u32.view(np.uint32))
+    d = np.abs(u - u64)
+    mag = np.abs(u64)
+    assert float(d[mag < 4].max()) <= 1e-5                         # north_star tolerance (DESIGN §3 P-1)
+    assert float((d / np.maximum(mag, 1.0)).max()) <= 1e-5
 
 
-def test_city_route_shards_bitwise_equal_single(V):
-    """The sharded runtime on the city route prefix (8 route-axis shards, loopback transport on one GPU, the same
-    plan, pack/unpack and two-launch schedule as NCCL) equals the single-GPU result bit for bit after
-    the config's 200 iterations (SURVEY §8(e) correctness gate)."""
-    from paper_1604_03734_b200 import connect_group, group_energy, regularise_group
-    import bench
+def test_city_route_shards_match_oracle(V):
+    """SURVEY §8(e) gate and §8(c) pin (viii) on the city route prefix: 8 shards cut along the route by the
+    product partition (vol_partition_route: arc length of the nearest camera-path point), the product
+    (skewed) schedule with its (u^j, p^{j+1}) halo before every launch — loopback transport on one GPU:
+    the same plan, pack/unpack kernels and launch A/B sequence as NCCL — after the config's 200
+    iterations compared DIRECTLY with the oracle: every voxel bit-identical to the fp32 oracle and within
+    1e-5 of fp64; also bitwise the single-GPU run, energies within 1e-9.  Every rank has at most the
+    peers r - 1 and r + 1."""
+    from paper_1604_03734_b200 import connect_group, group_energy, partition_route, plan_shard, regularise_group
     s = _city()
     world = 8
-    part = bench.partition(s.coords, world)
+    part_np = partition_route(s.coords, s.meta["route"], 8 * s.meta["voxel"], world)
+    part = torch.from_numpy(part_np)
     vols = []
     for r in range(world):
         mine = (part == r).nonzero().squeeze(1)
         vols.append(V(s.coords.cuda(), s.f[mine].cuda(), s.W[mine].cuda(), part=part, loopback=(r, world)))
+        plan = plan_shard(s.coords.numpy(), part_np, world, r)
+        peers = {q for q in range(world) if plan["peer_send"][q] or plan["peer_recv"][q]}
+        assert peers and peers <= {r - 1, r + 1}
+        print(f"rank {r}: {vols[-1].n_local} blocks, {vols[-1].n_ghost} ghosts, launch B "
+              f"{len(np.unique(plan['send']))}")
     assert all(v.n_ghost > 0 for v in vols)
     connect_group(vols)
     regularise_group(vols, s.lam, s.eps, s.tau, s.sigma, s.iters, data_term=s.data_term)
+    u = np.empty((s.n_blocks, 512), np.float32)
+    for r, v in enumerate(vols):
+        u[(part == r).numpy()] = v.u().cpu().numpy()
+    _, u32, u64 = _city_oracle()
+    _check_vs_oracle(u, u32, u64)
     single = V(s.coords.cuda(), s.f.cuda(), s.W.cuda())
     single.regularise_scene(s)
-    u1 = single.u().cpu()
-    for r, v in enumerate(vols):
-        mine = (part == r).nonzero().squeeze(1)
-        assert torch.equal(v.u().cpu(), u1[mine])
+    assert np.array_equal(u, single.u().cpu().numpy())
     P1, D1 = single.energy(s.lam, s.eps, s.data_term)
     Pg, Dg = group_energy(vols, s.lam, s.eps, s.data_term)
     assert abs(P1 - Pg) <= 1e-9 * abs(P1) and abs(D1 - Dg) <= 1e-9 * abs(P1)
+
+
+def test_city_shard_generation_equals_whole_scene(V):
+    """Per-shard generation (bench.py at N > 1): every rank generates only the candidate blocks of its arc
+    range; after an all-gather of the allocated coordinates the exact equal-count route partition of the
+    allocated blocks is taken and the few blocks that change owner are regenerated by their new owner.
+    The union over ranks equals the single-device scene block for block, and the partition equals
+    vol_partition_route of the whole scene's blocks."""
+    import bench
+    from paper_1604_03734_b200 import partition_route
+    s = _city()
+    plan = bench.route_plan("city-weak:3", 0, torch.device("cuda"))
+    for world in (3, 8):
+        pieces = [bench.shard_generate(plan, world, r) for r in range(world)]
+        coords_all = [p[0] for p in pieces]
+        got = [bench.shard_assemble(plan, world, r, coords_all, *pieces[r]) for r in range(world)]
+        coords = got[0]["coords"].cpu()
+        for g in got[1:]:
+            assert torch.equal(g["coords"].cpu(), coords)
+        key = lambda c: (c[:, 0].long() * 65536 + c[:, 1].long()) * 65536 + c[:, 2].long()
+        i1, i2 = torch.argsort(key(coords)), torch.argsort(key(s.coords))
+        assert torch.equal(coords[i1], s.coords[i2])
+        f = torch.empty(coords.shape[0], 512)
+        W = torch.empty(coords.shape[0], 512)
+        for r, g in enumerate(got):
+            mine = torch.from_numpy(g["part"] == r)
+            f[mine], W[mine] = g["f"].cpu(), g["W"].cpu()
+        assert torch.equal(f[i1], s.f[i2]) and torch.equal(W[i1], s.W[i2])
+        part = partition_route(coords, s.meta["route"], 8 * s.meta["voxel"], world)
+        assert np.array_equal(got[0]["part"], part)

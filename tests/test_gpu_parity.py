@@ -219,17 +219,21 @@ def test_gpu_invariants_tiny(V, tiny_scene):
 
 # ------------------------------------------------------------------ sharded path (loopback, 1 GPU)
 
+def _x_route_part(c, world):
+    """The product partition (vol_partition_route) along a straight route in x through the block set:
+    contiguous x ranges, ties by (x, y, z).  On these random block clouds every cut is a full 12³-block
+    cross-section — far more halo than a street canyon's, which stresses the exchange."""
+    from paper_1604_03734_b200 import partition_route
+    lo, hi = float(c[:, 0].min()), float(c[:, 0].max()) + 1.0
+    return torch.from_numpy(partition_route(c, np.array([[lo, 0.0, 0.0], [hi, 0.0, 0.0]]), 1.0, world))
+
+
 @pytest.mark.parametrize("world", [2, 3, 4])
 def test_loopback_shards_bitwise_equal_single(V, world, kernel=0):
     from paper_1604_03734_b200 import connect_group, group_energy, regularise_group
     s = random_instance(500, seed=10 + world, extent=6, w_density=0.7, lam=0.4, eps=0.01, iters=40)
     c = s.coords
-    # contiguous ranges along x (the route axis), ties by y
-    key = c[:, 0].to(torch.int64) * 64 + c[:, 1].to(torch.int64)
-    order = torch.argsort(key, stable=True)
-    part = torch.empty(len(c), dtype=torch.int32)
-    for r in range(world):
-        part[order[r * len(c) // world:(r + 1) * len(c) // world]] = r
+    part = _x_route_part(c, world)
     vols = []
     for r in range(world):
         mine = (part == r).nonzero().squeeze(1)
@@ -267,11 +271,7 @@ def test_loopback_shards_skewed_resume_and_short_calls(V):
     from paper_1604_03734_b200 import connect_group, regularise_group
     s = random_instance(400, seed=44, extent=6, w_density=0.7, lam=0.5, eps=0.0, iters=9)
     c = s.coords
-    key = c[:, 0].to(torch.int64) * 64 + c[:, 1].to(torch.int64)
-    order = torch.argsort(key, stable=True)
-    part = torch.empty(len(c), dtype=torch.int32)
-    for r in range(2):
-        part[order[r * len(c) // 2:(r + 1) * len(c) // 2]] = r
+    part = _x_route_part(c, 2)
     vols = []
     for r in range(2):
         mine = (part == r).nonzero().squeeze(1)

@@ -305,3 +305,30 @@ def test_openmp_timing_build_is_bitwise_the_plain_oracle(tiny_scene, prec):
                           data_term=s.data_term, init=s.init, precision=prec, omp=True)
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
+
+
+def test_phase_split_composes_to_the_iteration():
+    """oracle.phase (dual = Eq. 3 + Eq. 7, primal = Eq. 4 + Eq. 8 + Eq. 9) applied alternately equals
+    oracle.regularise bit for bit, in both precisions; a primal phase alone on the initial state (p = 0)
+    leaves u = f, and a dual phase alone from u = ū = f gives the projected σ-scaled gradient of f."""
+    import oracle
+    from synth import random_instance
+    s = random_instance(60, seed=5, extent=3, w_density=0.8, lam=0.7, eps=0.02, iters=7)
+    nbr = oracle.neighbours(s.coords)
+    for prec in ("f32", "f64"):
+        ref = oracle.regularise_scene(s, precision=prec, nbr=nbr)
+        st = oracle.regularise_scene(s, precision=prec, iters=0, nbr=nbr)
+        for _ in range(s.iters):
+            oracle.phase(s.coords, s.f, s.W, s.lam, s.eps, s.tau, s.sigma, "dual", st, precision=prec, nbr=nbr)
+            oracle.phase(s.coords, s.f, s.W, s.lam, s.eps, s.tau, s.sigma, "primal", st, precision=prec, nbr=nbr)
+        for a, b in zip(st, ref):
+            assert np.array_equal(a, b)
+    st = oracle.regularise_scene(s, precision="f64", iters=0, nbr=nbr)
+    oracle.phase(s.coords, s.f, s.W, s.lam, s.eps, s.tau, s.sigma, "primal", st, nbr=nbr)
+    assert np.array_equal(st[0], s.f.numpy().astype(np.float64))
+    st = oracle.regularise_scene(s, precision="f64", iters=0, nbr=nbr)
+    oracle.phase(s.coords, s.f, s.W, s.lam, s.eps, s.tau, s.sigma, "dual", st, nbr=nbr)
+    g = oracle.gradient(nbr, s.W, s.f.numpy().astype(np.float64))
+    q = np.float64(np.float32(s.sigma)) * g * (1.0 / (1.0 + np.float64(np.float32(s.sigma)) * np.float64(np.float32(s.eps))))
+    nrm = np.sqrt((q ** 2).sum(0))
+    assert np.allclose(st[2], q / np.maximum(1.0, nrm)[None], rtol=1e-14, atol=1e-15)

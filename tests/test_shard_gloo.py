@@ -15,6 +15,14 @@ import torch.multiprocessing as mp
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
+def _route_part(c, world):
+    """The product partition (libvol vol_partition_route) with a straight route along x through the block
+    set: arc length = x of the block centre, ties by (x, y, z) — every rank gets one contiguous x range."""
+    from paper_1604_03734_b200 import partition_route
+    lo, hi = float(c[:, 0].min()), float(c[:, 0].max()) + 1.0
+    return partition_route(c, np.array([[lo, 0.0, 0.0], [hi, 0.0, 0.0]]), 1.0, world)
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -34,12 +42,7 @@ def _worker(rank, world, port, q):
         from synth import random_instance
         s = random_instance(600, seed=21, extent=6)
         c = s.coords.numpy()
-        # contiguous ranges along x (the route axis), ties by y then z
-        key = (c[:, 0].astype(np.int64) * 4096 + c[:, 1]) * 4096 + c[:, 2]
-        order = np.argsort(key, kind="stable")
-        part = np.empty(len(c), np.int32)
-        for r in range(world):
-            part[order[r * len(c) // world:(r + 1) * len(c) // world]] = r
+        part = _route_part(c, world)
         plan = plan_shard(c, part, world, rank)
         local = np.nonzero(part == rank)[0]
         assert plan["n_local"] == len(local)
@@ -120,11 +123,7 @@ def _oracle_worker(rank, world, port, q):
         s = random_instance(500, seed=23, extent=6, w_density=0.75, w_max=3, lam=0.6, eps=0.02, iters=12)
         c = s.coords.numpy()
         f, W = s.f.numpy(), s.W.numpy()
-        key = (c[:, 0].astype(np.int64) * 4096 + c[:, 1]) * 4096 + c[:, 2]
-        order = np.argsort(key, kind="stable")
-        part = np.empty(len(c), np.int32)
-        for r in range(world):
-            part[order[r * len(c) // world:(r + 1) * len(c) // world]] = r
+        part = _route_part(c, world)
         plan = plan_shard(c, part, world, rank)
         local = np.nonzero(part == rank)[0]
         ghost = plan["ghost"]
@@ -184,3 +183,129 @@ def test_gloo_sharded_oracle_equals_single_volume(world):
         p.join(60)
     assert all(r[1] == "ok" for r in res), res
     assert all(r[2] > 0 for r in res)
+
+
+def _exchange(plan, rank, world, local_n, row_of, fields):
+    """One halo exchange over gloo in the plan's order: every peer gets its send blocks' rows of each
+    field, and the ghost rows [local_n + recv_off, ...) receive the owners' rows (in place)."""
+    off_s = np.concatenate([[0], np.cumsum(plan["peer_send"])])
+    off_r = np.concatenate([[0], np.cumsum(plan["peer_recv"])])
+    k = len(fields)
+    reqs, keep = [], []
+    for peer in range(world):
+        if peer == rank:
+            continue
+        blk = [row_of[int(g)] for g in plan["send"][off_s[peer]:off_s[peer + 1]]]
+        if blk:
+            buf = torch.from_numpy(np.stack([np.asarray(fl[blk], np.float32) for fl in fields], 1).copy())
+            keep.append(buf)
+            reqs.append(dist.isend(buf, dst=peer))
+        n = int(plan["peer_recv"][peer])
+        if n:
+            rb = torch.empty(n, k, 512)
+            reqs.append((dist.irecv(rb, src=peer), rb, local_n + off_r[peer]))
+    for r in reqs:
+        if isinstance(r, tuple):
+            r[0].wait()
+            a, b = r[2], r[2] + len(r[1])
+            for j, fl in enumerate(fields):
+                fl[a:b] = r[1][:, j].numpy()
+        else:
+            r.wait()
+
+
+def _skew_worker(rank, world, port, q, exchange_p):
+    """The product (skewed) schedule of the sharded GPU path, replayed with the CPU oracle's phases on
+    each rank's blocks plus the plan's ghost rows (csrc/shard.cu nccl_skew):
+        X(ū^0, p^0) · dual · { X(u^j, p^{j+1}) · primal · dual }_{j < iters−1} · X(u, p^iters) · primal
+    ū is never exchanged inside the loop: each rank recomputes the primal step of the ghost voxels from
+    the exchanged u^j and p^{j+1} (the +face primal recompute of k_skew), and its own blocks must come
+    out bit-identical to the single-volume oracle.  exchange_p=False drops p^{j+1} from the loop's
+    messages (only u^j is sent): the ghosts' p is then the rank's own dual step of the ghost voxels,
+    which reads ū beyond the halo, and the result must differ (the check has teeth).  (Dropping u^j
+    instead would not: here every rank runs the primal phase on the ghost rows too, and a ghost
+    face voxel's u^{j+1} depends only on its own u^j and on p^{j+1} of the voxel and its −neighbours,
+    all exchanged or local; the kernels recompute that primal step without storing it and take u^j from
+    the message.)"""
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import oracle
+        from paper_1604_03734_b200 import plan_shard
+        from synth import random_instance
+        s = random_instance(500, seed=29, extent=6, w_density=0.75, w_max=3, lam=0.6, eps=0.02, iters=14)
+        c = s.coords.numpy()
+        f, W = s.f.numpy(), s.W.numpy()
+        part = _route_part(c, world)
+        plan = plan_shard(c, part, world, rank)
+        local = np.nonzero(part == rank)[0]
+        ghost = plan["ghost"]
+        # context rows: the remaining face neighbours of the ghost blocks, with their static W only.  The
+        # oracle masks p_a(v) by the validity of edge v → v + ê_a (Eq. 4 as written), which needs Ω one
+        # block beyond a ghost; the kernels read p as stored instead (p_a = +0 on invalid edges, the
+        # iteration's invariant), so the GPU path needs no such rows.  Their u and p are never exchanged
+        # and never reach a local block's result.
+        known = set(local.tolist()) | set(ghost.tolist())
+        key = {tuple(x): i for i, x in enumerate(c.tolist())}
+        ctx = sorted({key[t] for g in ghost for a in range(3) for d in (-1, 1)
+                      for t in [tuple(c[g] + d * np.eye(3, dtype=np.int32)[a])] if t in key} - known)
+        rows = np.concatenate([local, ghost, np.asarray(ctx, np.int64)]).astype(np.int64)
+        row_of = {int(g): i for i, g in enumerate(rows)}
+        cr, fr, Wr = c[rows], f[rows], W[rows]
+        nbr = oracle.neighbours(cr)
+        kw = dict(theta=s.theta, data_term=s.data_term, precision="f32", nbr=nbr)
+        # init (warm): u = ū = f, p = 0 — zero iterations of the oracle
+        u, ub, p = oracle.regularise(cr, fr, Wr, s.lam, s.eps, s.tau, s.sigma, 0, theta=s.theta,
+                                     data_term=s.data_term, init=s.init, precision="f32", nbr=nbr)
+        st = (u, ub, p)
+        ph = lambda which: oracle.phase(cr, fr, Wr, s.lam, s.eps, s.tau, s.sigma, which, st, **kw)
+        X = lambda ufield, loop=True: _exchange(plan, rank, world, len(local), row_of,
+                                                [ufield] + ([p[0], p[1], p[2]] if exchange_p or not loop else []))
+        X(ub, loop=False)
+        ph("dual")
+        for j in range(s.iters - 1):
+            X(u)                  # (u^j, p^{j+1})
+            ph("primal")          # u^{j+1}, ū^{j+1} (own rows and the ghost rows' recompute)
+            ph("dual")            # p^{j+2}
+        X(u)                      # (u^{iters-1}, p^{iters})
+        ph("primal")
+        u_single, _, _ = oracle.regularise_scene(s, precision="f32")
+        ok = np.array_equal(u[:len(local)].view(np.uint32), u_single[local].view(np.uint32))
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, ok, len(ghost)))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put((rank, f"error: {e!r}", 0))
+
+
+def _run(target, world, *extra):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=target, args=(r, world, port, q) + extra) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(60)
+    return res
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_skewed_schedule_oracle_equals_single_volume(world):
+    from paper_1604_03734_b200 import build
+    build.build()
+    res = _run(_skew_worker, world, True)
+    assert all(r[1] is True for r in res), res
+    assert all(r[2] > 0 for r in res)
+
+
+def test_gloo_skewed_schedule_needs_the_p_halo():
+    from paper_1604_03734_b200 import build
+    build.build()
+    res = _run(_skew_worker, 2, False)
+    assert all(not isinstance(r[1], str) for r in res), res
+    assert not all(r[1] for r in res)
