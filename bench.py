@@ -576,14 +576,17 @@ def main():
     iter_ms = []
 
     shard_t = []
+    host_us = []
 
     def step(c, f, W, out, record, freeze=bool(args.freeze), rec=None, exchange=True):
         vol = Volume(c, f, W, stream=stream, **kw)
         vol.regularise(scene.lam, scene.eps, scene.tau, scene.sigma, 0, theta=scene.theta,
                        data_term=scene.data_term, init=scene.init, kernel=args.kernel)
         ev_a.record(stream)
+        th = time.perf_counter()
         vol.regularise(scene.lam, scene.eps, scene.tau, scene.sigma, iters, theta=scene.theta,
                        data_term=scene.data_term, resume=True, kernel=args.kernel, freeze=freeze, exchange=exchange)
+        host_us.append(1e6 * (time.perf_counter() - th) / iters)   # host issue time (asynchronous call)
         ev_b.record(stream)
         if sharded and record and rec is None:
             shard_t.append(vol.shard_timing())   # last iteration: interior A, halo chain, boundary B
@@ -659,9 +662,12 @@ def main():
         tt = torch.tensor([statistics.median(off_ms)] + [statistics.median(x[i] for x in shard_t) for i in range(3)],
                           device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        hu = torch.tensor([statistics.median(host_us)], device=dev)
+        dist.all_reduce(hu, op=dist.ReduceOp.MAX)
         halo = {"exposed_us_per_iter": 1e3 * (it_ms - float(tt[0])), "iter_ms_exchange_off": float(tt[0]),
+                "host_issue_us_per_iter": float(hu.item()), "gpu_us_per_iter": 1e3 * it_ms,
                 "interior_ms": float(tt[1]), "exchange_chain_ms": float(tt[2]), "boundary_ms": float(tt[3]),
-                "transport": "NCCL send/recv per peer (comm stream), pack/unpack kernels",
+                "transport": "NCCL send/recv per peer on the comm stream (fork/join inside the CUDA graph of the skewed loop), pack/unpack kernels",
                 "note": "max over ranks; chain overlaps the interior launch"}
 
     # end to end from pinned host buffers through the same API

@@ -294,6 +294,7 @@ struct ShardRuntime {
     int32_t *send_rows = nullptr;
     unsigned long long *omega = nullptr;  // [2] device scratch for the Ω count all-reduce
     bool connected = false;
+    bool graphs = true;              // capture the skewed loop into a CUDA graph (HVG_SHARD_NO_GRAPH=1: eager)
 };
 
 size_t hvg::shard_extra_bytes(const ShardPlan &P) {
@@ -513,6 +514,7 @@ vol_status shard_setup(vol_s *v, const ShardPlan &plan, const vol_dist *dist) {
     CK(cudaMemcpyAsync(R->send_rows, send32.data(), send32.size() * 4, cudaMemcpyHostToDevice, s));
     CK(cudaStreamSynchronize(s));  // the host vector goes out of scope
     CK(cudaStreamCreateWithFlags(&R->cs, cudaStreamNonBlocking));
+    R->graphs = getenv("HVG_SHARD_NO_GRAPH") == nullptr;
     CK(cudaEventCreateWithFlags(&R->ev_pack, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&R->ev_halo, cudaEventDisableTiming));
     for (auto &e : R->ev_t) CK(cudaEventCreate(&e));
@@ -610,9 +612,13 @@ vol_status shard_timing(vol_s *v, float *interior_ms, float *exchange_ms, float 
 //   X(ū^0, p^0) · k_dual · { X(u^j, p^{j+1}) ∥ k_skew A ; k_skew B }_{j < iters−1} · X(p^iters) · k_primal
 // (A = local blocks without a remote neighbour, launched while the exchange runs; B the others).  The
 // exchange moves four fields per boundary block (a u field and p), like the one-pass schedule's (ū, p).
-static vol_status nccl_exchange_fields(vol_s *v, float *a, float *px, float *py, float *pz, bool timed = false) {
+// The halo chain of one exchange: fork from the compute stream `s` to the communication stream, pack →
+// ncclSend/ncclRecv → unpack there, and record ev_halo for launch B to wait on.  Returns the number of
+// kernels it launches (pack, unpack).
+static vol_status nccl_exchange_fields(vol_s *v, cudaStream_t s, float *a, float *px, float *py, float *pz,
+                                       int64_t &launches, bool timed = false) {
     ShardRuntime *R = v->shard;
-    CK(cudaEventRecord(R->ev_pack, v->stream));
+    CK(cudaEventRecord(R->ev_pack, s));
     CK(cudaStreamWaitEvent(R->cs, R->ev_pack, 0));
     if (timed) CK(cudaEventRecord(R->ev_t[2], R->cs));
     if (v->pending_exchange) {   // opts.exchange = 0: no-op chain (timing only)
@@ -620,12 +626,24 @@ static vol_status nccl_exchange_fields(vol_s *v, float *a, float *px, float *py,
         if (st != VOL_OK) return st;
         if ((st = nccl_exchange(v, R->cs)) != VOL_OK) return st;
         if ((st = unpack(v, a, px, py, pz, R->cs)) != VOL_OK) return st;
+        launches += (R->plan.send_rows.empty() ? 0 : 1) + (R->plan.ghost.empty() ? 0 : 1);
     }
     if (timed) CK(cudaEventRecord(R->ev_t[3], R->cs));
     CK(cudaEventRecord(R->ev_halo, R->cs));
     return VOL_OK;
 }
 
+// Skewed schedule on a sharded volume, NCCL transport — the single-GPU run_iterations_skew with a halo
+// exchange in front of every launch that reads ghosts:
+//   X(ū^0, p^0) · k_dual · { X(u^j, p^{j+1}) ∥ k_skew A ; k_skew B }_{j < iters−1} · X(p^iters) · k_primal
+// (A = local blocks without a remote neighbour, launched while the exchange runs; B the others).  The
+// exchange moves four fields per boundary block (a u field and p).  The loop body is captured once per
+// call into a CUDA graph of 2m iterations (the buffer parities repeat every 2) — the compute stream
+// forks to the communication stream and joins back through ev_pack / ev_halo inside the graph, NCCL's
+// send/recv are captured as graph nodes — and replayed, so the host issues one graph launch per 2m
+// iterations instead of ~10 API calls and an NCCL group per iteration ("careful synchronization
+// between subsequent primal and dual variable updates": here it is the graph's dependency edges).  The
+// last skewed iteration runs eagerly with the timing events (vol_shard_timing).
 static vol_status nccl_skew(vol_s *v, const IterParams &P, int32_t iters) {
     ShardRuntime *R = v->shard;
     const ShardPlan &SP = R->plan;
@@ -637,43 +655,82 @@ static vol_status nccl_skew(vol_s *v, const IterParams &P, int32_t iters) {
     float *B[2];
     B[(iters - 1) & 1] = v->F.u;
     B[iters & 1] = v->d_u2;
-    vol_status st = nccl_exchange_fields(v, v->F.ub[c], v->F.px[c], v->F.py[c], v->F.pz[c]);
+    vol_status st = nccl_exchange_fields(v, s, v->F.ub[c], v->F.px[c], v->F.py[c], v->F.pz[c], launches);
     if (st != VOL_OK) return st;
     CK(cudaStreamWaitEvent(s, R->ev_halo, 0));
     int r = launch_dual_only(view_of(v->F, c), v->d_nbr, nl, P, s);
     CKL(r);
-    launches += r + 2;
-    for (int j = 0; j < iters - 1; j++) {
+    launches += r;
+    // one skewed iteration j on compute stream `cs_` (the chain on R->cs)
+    auto skew_iter = [&](cudaStream_t cs_, int j, bool timed, int64_t &n) -> vol_status {
         const int pin = c ^ ((j + 1) & 1);
-        const bool timed = j == iters - 2;   // vol_shard_timing: the last skewed launch
-        if ((st = nccl_exchange_fields(v, B[j & 1], v->F.px[pin], v->F.py[pin], v->F.pz[pin], timed)) != VOL_OK)
-            return st;
-        if (timed) CK(cudaEventRecord(R->ev_t[0], s));
-        int a = launch_skew(v->F, B[j & 1], B[(j + 1) & 1], pin, v->pending_frozen, v->d_nbr, 0, nA, P, s);
+        vol_status st2 = nccl_exchange_fields(v, cs_, B[j & 1], v->F.px[pin], v->F.py[pin], v->F.pz[pin], n, timed);
+        if (st2 != VOL_OK) return st2;
+        if (timed) CK(cudaEventRecord(R->ev_t[0], cs_));
+        int a = launch_skew(v->F, B[j & 1], B[(j + 1) & 1], pin, v->pending_frozen, v->d_nbr, 0, nA, P, cs_);
         CKL(a);
-        if (timed) CK(cudaEventRecord(R->ev_t[1], s));
-        CK(cudaStreamWaitEvent(s, R->ev_halo, 0));
-        if (timed) CK(cudaEventRecord(R->ev_t[4], s));
-        int b = launch_skew(v->F, B[j & 1], B[(j + 1) & 1], pin, v->pending_frozen, v->d_nbr, nA, nl - nA, P, s);
+        if (timed) CK(cudaEventRecord(R->ev_t[1], cs_));
+        CK(cudaStreamWaitEvent(cs_, R->ev_halo, 0));
+        if (timed) CK(cudaEventRecord(R->ev_t[4], cs_));
+        int b = launch_skew(v->F, B[j & 1], B[(j + 1) & 1], pin, v->pending_frozen, v->d_nbr, nA, nl - nA, P, cs_);
         CKL(b);
         if (timed) {
-            CK(cudaEventRecord(R->ev_t[5], s));
+            CK(cudaEventRecord(R->ev_t[5], cs_));
             R->timed = true;
         }
-        launches += a + b + 2;
+        n += a + b;
+        return VOL_OK;
+    };
+    const int total = iters - 1;            // skewed launches
+    const int body = total - 1;             // all but the last (timed, eager)
+    const int m = std::min(16, body / 2);
+    int j = 0;
+    if (m >= 1 && R->graphs) {
+        cudaGraph_t g = nullptr;
+        cudaGraphExec_t ge = nullptr;
+        const long long before = g_launches.load();
+        int64_t per = 0;
+        CK(cudaStreamBeginCapture(v->cap, cudaStreamCaptureModeThreadLocal));
+        vol_status cst = VOL_OK;
+        for (int k = 0; k < 2 * m && cst == VOL_OK; k++) cst = skew_iter(v->cap, k, false, per);
+        cudaError_t e = cudaStreamEndCapture(v->cap, &g);
+        g_launches.fetch_sub(g_launches.load() - before);   // capture does not execute; replays count below
+        if (cst != VOL_OK || e != cudaSuccess) {
+            if (g) cudaGraphDestroy(g);
+            if (cst != VOL_OK) return cst;
+            return fail(VOL_ECUDA, "sharded graph capture failed: %s", cudaGetErrorString(e));
+        }
+        e = cudaGraphInstantiate(&ge, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) return fail(VOL_ECUDA, "sharded graph instantiate failed: %s", cudaGetErrorString(e));
+        const int reps = body / (2 * m);
+        for (int q = 0; q < reps; q++) {
+            e = cudaGraphLaunch(ge, s);
+            if (e != cudaSuccess) {
+                cudaGraphExecDestroy(ge);
+                return fail(VOL_ECUDA, "sharded graph launch failed: %s", cudaGetErrorString(e));
+            }
+            launches += per;
+            g_launches.fetch_add(per);
+        }
+        cudaGraphExecDestroy(ge);   // destruction is deferred until the launches complete
+        j = reps * 2 * m;
     }
+    for (; j < total; j++)
+        if ((st = skew_iter(s, j, j == total - 1, launches)) != VOL_OK) return st;
     if (iters < 2) {   // no skewed launch: the timing events record an empty interval
         for (int k = 0; k < 6; k++) CK(cudaEventRecord(R->ev_t[k], k == 2 || k == 3 ? R->cs : s));
         R->timed = true;
     }
     const int c2 = c ^ (iters & 1);
-    if ((st = nccl_exchange_fields(v, v->F.ub[c2], v->F.px[c2], v->F.py[c2], v->F.pz[c2])) != VOL_OK) return st;
+    if ((st = nccl_exchange_fields(v, s, v->F.ub[c2], v->F.px[c2], v->F.py[c2], v->F.pz[c2], launches)) != VOL_OK)
+        return st;
     CK(cudaStreamWaitEvent(s, R->ev_halo, 0));
     View V = view_of(v->F, c2 ^ 1);   // px_out = p[c2] (p^iters), ub_out = ub[c2]
     V.u = B[(iters - 1) & 1];         // == F.u
     r = launch_primal_only(V, v->d_nbr, nl, P, s);
     CKL(r);
-    launches += r + 2;
+    launches += r;
     v->cur = c2;
     v->last_launches = launches;
     return VOL_OK;
