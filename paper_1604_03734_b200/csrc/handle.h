@@ -4,7 +4,9 @@
 #include <cuda_runtime.h>
 #include <stdarg.h>
 
+#include <cstring>
 #include <string>
+#include <vector>
 
 #include <nvtx3/nvToolsExt.h>   // header-only NVTX 3: ranges show up in nsys / ncu timelines
 
@@ -60,7 +62,17 @@ struct Layout {
     uint32_t T;
 };
 
+// An instantiated CUDA graph of an iteration loop, kept by the volume and reused by later calls with
+// the same key (kernel parameters, buffer parity, schedule); destroyed in vol_destroy after the stream is
+// idle — destroying an executable graph right after launching it makes the host wait for it.
+struct GraphEntry {
+    std::string key;
+    cudaGraphExec_t exec = nullptr;
+    int64_t per = 0;   // kernel launches per replay
+};
+
 struct vol_s {
+    std::vector<GraphEntry> graphs;
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaStream_t cap = nullptr;  // private stream used only for graph capture
@@ -107,3 +119,51 @@ vol_status finalize_w8(vol_s *v);
 double energy_dual_value(const double *o, float eps, int data_term);
 
 bool is_device_ptr(const void *p);
+
+// Key bytes of a graph: any trivially copyable values, appended in order.
+struct GraphKey {
+    std::string bytes;
+    template <class T>
+    GraphKey &add(const T &x) {
+        bytes.append(reinterpret_cast<const char *>(&x), sizeof x);
+        return *this;
+    }
+};
+
+// The volume's graph for `key`: a cached executable, or `body(cap_stream, per)` captured on the volume's
+// private capture stream and instantiated (the kernels it launches during capture are not counted:
+// they run at replay, counted by the caller).
+template <class Body>
+vol_status cached_graph(vol_s *v, const GraphKey &key, Body body, cudaGraphExec_t *exec, int64_t *per) {
+    for (const GraphEntry &e : v->graphs)
+        if (e.key == key.bytes) {
+            *exec = e.exec;
+            *per = e.per;
+            return VOL_OK;
+        }
+    if (v->graphs.size() >= 8) {   // bounded: evict the oldest once the stream has drained it
+        CK(cudaStreamSynchronize(v->stream));
+        cudaGraphExecDestroy(v->graphs.front().exec);
+        v->graphs.erase(v->graphs.begin());
+    }
+    cudaGraph_t g = nullptr;
+    const long long before = hvg::g_launches.load();
+    int64_t n = 0;
+    CK(cudaStreamBeginCapture(v->cap, cudaStreamCaptureModeThreadLocal));
+    vol_status st = body(v->cap, n);
+    cudaError_t e = cudaStreamEndCapture(v->cap, &g);
+    hvg::g_launches.fetch_sub(hvg::g_launches.load() - before);
+    if (st != VOL_OK || e != cudaSuccess) {
+        if (g) cudaGraphDestroy(g);
+        if (st != VOL_OK) return st;
+        return fail(VOL_ECUDA, "graph capture failed: %s", cudaGetErrorString(e));
+    }
+    cudaGraphExec_t ge = nullptr;
+    e = cudaGraphInstantiate(&ge, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(VOL_ECUDA, "graph instantiate failed: %s", cudaGetErrorString(e));
+    v->graphs.push_back(GraphEntry{key.bytes, ge, n});
+    *exec = ge;
+    *per = n;
+    return VOL_OK;
+}

@@ -686,34 +686,27 @@ static vol_status nccl_skew(vol_s *v, const IterParams &P, int32_t iters) {
     const int m = std::min(16, body / 2);
     int j = 0;
     if (m >= 1 && R->graphs) {
-        cudaGraph_t g = nullptr;
+        GraphKey key;
+        key.add('N').add(c).add(m).add(iters & 1).add(v->pending_frozen).add(v->pending_exchange).add(P);
         cudaGraphExec_t ge = nullptr;
-        const long long before = g_launches.load();
         int64_t per = 0;
-        CK(cudaStreamBeginCapture(v->cap, cudaStreamCaptureModeThreadLocal));
-        vol_status cst = VOL_OK;
-        for (int k = 0; k < 2 * m && cst == VOL_OK; k++) cst = skew_iter(v->cap, k, false, per);
-        cudaError_t e = cudaStreamEndCapture(v->cap, &g);
-        g_launches.fetch_sub(g_launches.load() - before);   // capture does not execute; replays count below
-        if (cst != VOL_OK || e != cudaSuccess) {
-            if (g) cudaGraphDestroy(g);
-            if (cst != VOL_OK) return cst;
-            return fail(VOL_ECUDA, "sharded graph capture failed: %s", cudaGetErrorString(e));
-        }
-        e = cudaGraphInstantiate(&ge, g, 0);
-        cudaGraphDestroy(g);
-        if (e != cudaSuccess) return fail(VOL_ECUDA, "sharded graph instantiate failed: %s", cudaGetErrorString(e));
+        st = cached_graph(
+            v, key,
+            [&](cudaStream_t cap, int64_t &n) -> vol_status {
+                for (int k = 0; k < 2 * m; k++) {
+                    vol_status s2 = skew_iter(cap, k, false, n);
+                    if (s2 != VOL_OK) return s2;
+                }
+                return VOL_OK;
+            },
+            &ge, &per);
+        if (st != VOL_OK) return st;
         const int reps = body / (2 * m);
         for (int q = 0; q < reps; q++) {
-            e = cudaGraphLaunch(ge, s);
-            if (e != cudaSuccess) {
-                cudaGraphExecDestroy(ge);
-                return fail(VOL_ECUDA, "sharded graph launch failed: %s", cudaGetErrorString(e));
-            }
+            CK(cudaGraphLaunch(ge, s));
             launches += per;
             g_launches.fetch_add(per);
         }
-        cudaGraphExecDestroy(ge);   // destruction is deferred until the launches complete
         j = reps * 2 * m;
     }
     for (; j < total; j++)

@@ -729,7 +729,7 @@ void enqueue_solve(const StereoLayout &L, const vol_stereo_params *prm, int32_t 
     }
 }
 
-struct GraphKey {
+struct StereoGraphKey {
     void *ws;
     int32_t F;
     int chunk;
@@ -747,16 +747,16 @@ ExecRef exec_ref(cudaGraphExec_t e) {
     });
 }
 
-struct GraphEntry {
-    GraphKey key;
+struct StereoGraphEntry {
+    StereoGraphKey key;
     ExecRef exec;
     long long launches;
 };
 
 std::mutex g_graph_mu;
-std::vector<GraphEntry> g_graphs;   // most recent last; at most 8
+std::vector<StereoGraphEntry> g_graphs;   // most recent last; at most 8
 
-bool same_key(const GraphKey &a, const GraphKey &b) {
+bool same_key(const StereoGraphKey &a, const StereoGraphKey &b) {
     return a.ws == b.ws && a.F == b.F && a.chunk == b.chunk && a.mode == b.mode && a.device == b.device &&
            memcmp(&a.p, &b.p, sizeof a.p) == 0;
 }
@@ -815,7 +815,7 @@ extern "C" vol_status vol_stereo(const float *left, const float *right, int32_t 
     } else {
         int dev = 0;
         cudaGetDevice(&dev);
-        GraphKey key{ws, n_frames, chunk, mode, dev, *prm};
+        StereoGraphKey key{ws, n_frames, chunk, mode, dev, *prm};
         ExecRef exec;
         {
             std::lock_guard<std::mutex> lk(g_graph_mu);
@@ -844,7 +844,7 @@ extern "C" vol_status vol_stereo(const float *left, const float *right, int32_t 
             exec = exec_ref(ge);
             std::lock_guard<std::mutex> lk(g_graph_mu);
             if (g_graphs.size() >= 8) g_graphs.erase(g_graphs.begin());   // freed once no call holds it
-            g_graphs.push_back(GraphEntry{key, exec, launches});
+            g_graphs.push_back(StereoGraphEntry{key, exec, launches});
         }
         CK(cudaGraphLaunch(exec.get(), s));
     }

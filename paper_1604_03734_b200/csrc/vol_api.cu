@@ -406,6 +406,8 @@ extern "C" void vol_destroy(vol_t v) {
     if (!v) return;
     if (v->shard) shard_destroy(v);
     if (v->stream) cudaStreamSynchronize(v->stream);
+    for (GraphEntry &e : v->graphs) cudaGraphExecDestroy(e.exec);
+    v->graphs.clear();
     if (v->cap) cudaStreamDestroy(v->cap);
     if (v->owns_ws && v->ws) cudaFree(v->ws);
     delete v;
@@ -441,35 +443,28 @@ static vol_status run_iterations_skew(vol_s *v, const IterParams &P, int32_t ite
     const int total = iters - 1;
     const int m = std::min<int>(16, total / 2);
     if (m >= 1) {   // a graph of 2m launches (buffer parities repeat every 2), replayed
-        cudaGraph_t g = nullptr;
+        GraphKey key;
+        key.add('S').add(cur).add(m).add(iters & 1).add(v->pending_frozen).add(P);
         cudaGraphExec_t ge = nullptr;
-        CK(cudaStreamBeginCapture(v->cap, cudaStreamCaptureModeThreadLocal));
-        int per = 0, bad = 0;
-        for (int k = 0; k < 2 * m; k++) {
-            int r = skew(v->cap, k);
-            if (r < 0) bad = 1;
-            per += r;
-        }
-        cudaError_t e = cudaStreamEndCapture(v->cap, &g);
-        if (bad || e != cudaSuccess) {
-            if (g) cudaGraphDestroy(g);
-            return fail(VOL_ECUDA, "graph capture failed: %s", cudaGetErrorString(e != cudaSuccess ? e : cudaGetLastError()));
-        }
-        g_launches.fetch_sub(per);
-        e = cudaGraphInstantiate(&ge, g, 0);
-        cudaGraphDestroy(g);
-        if (e != cudaSuccess) return fail(VOL_ECUDA, "graph instantiate failed: %s", cudaGetErrorString(e));
+        int64_t per = 0;
+        vol_status st = cached_graph(
+            v, key,
+            [&](cudaStream_t cs, int64_t &n) -> vol_status {
+                for (int k = 0; k < 2 * m; k++) {
+                    int r = skew(cs, k);
+                    if (r < 0) return fail(VOL_ECUDA, "skew launch failed during capture");
+                    n += r;
+                }
+                return VOL_OK;
+            },
+            &ge, &per);
+        if (st != VOL_OK) return st;
         const int reps = total / (2 * m);
         for (int r = 0; r < reps; r++) {
-            e = cudaGraphLaunch(ge, s);
-            if (e != cudaSuccess) {
-                cudaGraphExecDestroy(ge);
-                return fail(VOL_ECUDA, "graph launch failed: %s", cudaGetErrorString(e));
-            }
+            CK(cudaGraphLaunch(ge, s));
             launches += per;
             g_launches.fetch_add(per);
         }
-        cudaGraphExecDestroy(ge);
         j = reps * 2 * m;
     }
     for (; j < total; j++) {
@@ -504,36 +499,31 @@ static vol_status run_iterations_single(vol_s *v, const IterParams &P, int32_t i
     // CUDA graph of 2·m iterations (ū parity returns to the start), replayed; remainder launched directly.
     const int m = std::min<int>(16, iters / 2);
     if (m >= 1) {
-        cudaGraph_t g = nullptr;
+        GraphKey key;
+        key.add('F').add(kernel).add(v->cur).add(m).add(v->pending_frozen).add(P);
         cudaGraphExec_t ge = nullptr;
-        CK(cudaStreamBeginCapture(v->cap, cudaStreamCaptureModeThreadLocal));
-        int per = 0, cur = v->cur, bad = 0;
-        for (int k = 0; k < 2 * m; k++) {
-            int r = one(v->cap, cur);
-            if (r < 0) bad = 1;
-            per += r;
-            cur ^= 1;
-        }
-        cudaError_t e = cudaStreamEndCapture(v->cap, &g);
-        if (bad || e != cudaSuccess) {
-            if (g) cudaGraphDestroy(g);
-            return fail(VOL_ECUDA, "graph capture failed: %s", cudaGetErrorString(e != cudaSuccess ? e : cudaGetLastError()));
-        }
-        g_launches.fetch_sub(per);  // capture does not execute; replays are counted below
-        e = cudaGraphInstantiate(&ge, g, 0);
-        cudaGraphDestroy(g);
-        if (e != cudaSuccess) return fail(VOL_ECUDA, "graph instantiate failed: %s", cudaGetErrorString(e));
+        int64_t per = 0;
+        const int cur0 = v->cur;
+        vol_status st = cached_graph(
+            v, key,
+            [&](cudaStream_t cs, int64_t &n) -> vol_status {
+                int cur = cur0;
+                for (int k = 0; k < 2 * m; k++) {
+                    int r = one(cs, cur);
+                    if (r < 0) return fail(VOL_ECUDA, "launch failed during capture");
+                    n += r;
+                    cur ^= 1;
+                }
+                return VOL_OK;
+            },
+            &ge, &per);
+        if (st != VOL_OK) return st;
         const int reps = iters / (2 * m);
         for (int r = 0; r < reps; r++) {
-            e = cudaGraphLaunch(ge, s);
-            if (e != cudaSuccess) {
-                cudaGraphExecDestroy(ge);
-                return fail(VOL_ECUDA, "graph launch failed: %s", cudaGetErrorString(e));
-            }
+            CK(cudaGraphLaunch(ge, s));
             launches += per;
             g_launches.fetch_add(per);
         }
-        cudaGraphExecDestroy(ge);  // safe: destruction is deferred until the launches complete
         iters -= reps * 2 * m;
     }
     for (int k = 0; k < iters; k++) {

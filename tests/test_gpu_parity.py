@@ -447,3 +447,21 @@ def test_create_w8_equals_float_weights(V, where):
     for x, y in zip(a.state(), b.state()):
         assert torch.equal(x, y)
     assert a.energy(s.lam, s.eps) == b.energy(s.lam, s.eps)
+
+
+def test_graph_cache_across_calls(V):
+    """The iteration graphs are cached per volume (keyed by parameters, buffer parity, iteration-count
+    parity, schedule): a sequence of resumed calls on ONE volume — odd and even iteration counts, the
+    skewed and the one-pass schedule, freeze on and off, a λ change — equals the fp32 oracle run through
+    the same sequence of (λ, iters) bit for bit after every call."""
+    s = random_instance(300, seed=61, extent=5, w_density=0.7, lam=0.5, eps=0.01, iters=0)
+    vol = V(s.coords.cuda(), s.f.cuda(), s.W.cuda())
+    nbr = oracle.neighbours(s.coords)
+    st = None
+    seq = [(37, 0, True, 0.5), (36, 0, True, 0.5), (37, 0, False, 0.5), (40, 3, True, 0.5), (37, 0, True, 0.5),
+           (37, 0, True, 0.7), (36, 3, False, 0.7), (37, 0, True, 0.5)]
+    for k, (it, kern, frz, lam) in enumerate(seq):
+        vol.regularise(lam, s.eps, s.tau, s.sigma, it, kernel=kern, freeze=frz, resume=k > 0)
+        st = oracle.regularise(s.coords, s.f, s.W, lam, s.eps, s.tau, s.sigma, it, precision="f32", nbr=nbr,
+                               state=st)
+        assert np.array_equal(vol.u().cpu().numpy(), st[0]), (k, it, kern, frz, lam)
