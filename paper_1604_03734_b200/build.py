@@ -41,7 +41,7 @@ def sources():
 
 
 def deps():
-    return sources() + sorted(glob.glob(os.path.join(CSRC, "*.h"))) + [os.path.join(ROOT, "include", "vol.h"), __file__]
+    return sources() + sorted(glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(ROOT, "include", "vol.h"), __file__]
 
 
 def build(force: bool = False, verbose: bool = False, out: str = SO, defines=()) -> str:
