@@ -1,18 +1,16 @@
-// skew_tma.cu — the skewed Chambolle–Pock launch with every halo read by the tensor memory accelerator
+// skew_tma.cu — the skewed Chambolle–Pock launch with the halo planes read by the tensor memory accelerator
 // (SURVEY §8(a) rows a-3 … a-5; arXiv 1604.03734 §III-C; the schedule of iterate.cu's k_skew).
 //
 // Launch k computes, for one 8³ block per 128-thread CTA, the primal step k + relaxation of its own voxels,
 // the primal step of the 3×64 voxels of its +x/+y/+z neighbour faces (recomputed: same function, same
 // inputs ⇒ bit-identical to the owner), then the dual step k+1 of its own voxels.  What
-// differs from k_skew is only how the data arrives: k_skew gathers the +face and −face halo with per-thread
-// loads (≈1.3 k scattered 4-byte loads per block, 64 of the +x face's 32-byte sectors per field, ~20 live
-// registers per thread); here warp 0 issues, per neighbour, tensor TMA copies (cp.async.bulk.tensor.4d) of
-// exactly the face planes and edge lines the recompute reads, into shared memory, completing on the same
-// mbarrier as the block's own bulk copies:
-//   +x / +y / +z neighbour   u^k, f, W, p^{k+1} (x, y, z) of its x=0 / y=0 / z=0 plane (box {4,8,8} /
-//                            {8,1,8} / {8,8,1}: the x box is 4 wide because a TMA row is >= 16 bytes)
-//   −x / −y / −z neighbour   p^{k+1} normal component of its x=7 / y=7 / z=7 plane
-//   6 edge neighbours        the in-face −neighbour p of the +face planes' first row / column
+// differs from k_skew is how the halo arrives.  k_skew gathers all of it with per-thread loads through the
+// L1 load pipe, which ncu shows ~72 % busy (the limiter next to DRAM).  Here warp 0 issues tensor TMA
+// copies (cp.async.bulk.tensor.4d) of the +y / +z face planes (u^k, f, W, p^{k+1}), the −y / −z normal
+// p components and the four edge lines the y / z recomputes need, into shared memory, completing on the
+// block's own mbarrier; only the +x plane (and the −x p_x) keep per-thread register loads.  The x=0
+// plane of a block is 64 rows of one float, every 32-byte row a separate TMA request — measured 1.55x
+// slower when fetched by TMA (probe and A/B in DESIGN.md §10), the TMA unit being row-rate bound.
 // An absent neighbour is block coordinate −1: the box is out of bounds, TMA fills zeros (W = 0 ⇒ Ω̄, p = 0)
 // and still completes the full byte count (probed on B200: scripts/probes/tma_probe.cu), so the barrier's
 // transaction count is a per-launch constant and no thread tests neighbour existence.
@@ -23,6 +21,10 @@
 #include "device_common.cuh"
 #include "internal.h"
 
+#ifndef HVG_TMA_MINB
+#define HVG_TMA_MINB 8   // CTAs per SM k_skew_tma is compiled for (register budget)
+#endif
+
 namespace hvg {
 
 // map table: index = box * kMapFields + field
@@ -31,7 +33,7 @@ enum { kBoxX = 0, kBoxY = 1, kBoxZ = 2, kBoxD = 3, kBoxE = 4, kBoxF = 5, kBoxSha
 // box dims {x, y, z, block} per shape: the +x/−x planes, +y/−y planes, +z/−z planes, and edge lines
 static const uint32_t kBoxDim[kBoxShapes][4] = {{4, 8, 8, 1}, {8, 1, 8, 1}, {8, 8, 1, 1},
                                                 {4, 1, 8, 1}, {4, 8, 1, 1}, {8, 1, 1, 1}};
-constexpr uint32_t kNbrTx = 6 * 1024 + 6 * 256 + 6 * 256 + 1024 + 256 + 256 + 2 * 128 + 2 * 128 + 2 * 32;
+constexpr uint32_t kNbrTx = 6 * 256 + 6 * 256 + 256 + 256 + 128 + 128 + 32 + 32;   // +y, +z planes; −y, −z; 4 edge lines
 
 size_t skew_tma_map_bytes() { return (size_t)kBoxShapes * kMapFields * sizeof(CUtensorMap); }
 
@@ -89,24 +91,51 @@ struct __align__(128) TStage {
     float u[kBlockVox + 192];    // u^k own → ū^{k+1} own (in place); [512 + 64a + entry): ū^{k+1} of +face a
     float Wf[kBlockVox + 192];   // W own (fp32); [512 + 64a + entry): W of +face a
     float px[kBlockVox], py[kBlockVox], pz[kBlockVox];   // p^{k+1} own
-    float xf[6][256];            // +x face plane, fields (u, f, W, px, py, pz): [(z·8 + y)·4 + x], x = 0 used
     float yf[6][64];             // +y face plane: [z·8 + x]
     float zf[6][64];             // +z face plane: [y·8 + x]
-    float mx[256];               // −x neighbour p_x at x = 4..7: (7, y, z) → [(z·8 + y)·4 + 3]
+    float mx[64];                // −x neighbour p_x at x = 7: [z·8 + y] (per-thread loads)
     float my[64];                // −y neighbour p_y at y = 7: [z·8 + x]
     float mz[64];                // −z neighbour p_z at z = 7: [y·8 + x]
-    float e8[32];                // (+1,−1,0) p_y at (x<4, 7, z): [z·4 + x]
-    float e10[32];               // (+1,0,−1) p_z at (x<4, y, 7): [y·4 + x]
     float e6[32];                // (−1,+1,0) p_x at (4+x, 0, z): [z·4 + x]
     float e7[32];                // (−1,0,+1) p_x at (4+x, y, 0): [y·4 + x]
     __align__(128) float e11[8];  // (0,+1,−1) p_z at (x, 0, 7)
     __align__(128) float e9[8];   // (0,−1,+1) p_y at (x, 7, 0)
     __align__(128) uint8_t W8b[W8 ? kBlockVox : 16];
     uint32_t fz[16];
+    int32_t snb[kNbr];
 };
 
+// +x face entry k = y + 8z (voxel (0, y, z) of the +x neighbour): its u^k, f, W, p^{k+1} and the p_y, p_z of
+// its in-face −neighbours (same block, or the edge neighbours (+1,−1,0) / (+1,0,−1) for y = 0 / z = 0),
+// loaded into registers before the own primal step and consumed after it
+struct XReg {
+    float u, f, w, px, py, pz, m1, m2;
+};
 template <bool W8>
-__global__ void __launch_bounds__(128, 8) k_skew_tma(SkewTmaView V, const int32_t *__restrict__ nbr, int64_t first,
+__device__ __forceinline__ XReg xface_load(const SkewTmaView &V, const int32_t *nb, int k) {
+    const int y = k & 7, z = k >> 3;
+    const int32_t b = nb[1];
+    const uint32_t idx = b >= 0 ? (uint32_t)b * (uint32_t)kBlockVox + (uint32_t)(8 * k) : 0u;
+    XReg r;
+    r.u = V.u_in[idx];
+    r.f = V.f[idx];
+    r.w = W8 ? (float)V.W8[idx] : V.W[idx];
+    r.px = V.px_in[idx];
+    r.py = V.py_in[idx];
+    r.pz = V.pz_in[idx];
+    const int32_t b1 = y > 0 ? b : nb[8], b2 = z > 0 ? b : nb[10];
+    const uint32_t i1 = b1 >= 0 ? (uint32_t)b1 * (uint32_t)kBlockVox + (uint32_t)(y > 0 ? 8 * k - 8 : 56 + 64 * z) : 0u;
+    const uint32_t i2 = b2 >= 0 ? (uint32_t)b2 * (uint32_t)kBlockVox + (uint32_t)(z > 0 ? 8 * k - 64 : 8 * y + 448) : 0u;
+    r.m1 = V.py_in[i1];
+    r.m2 = V.pz_in[i2];
+    if (b < 0) r.w = 0.0f;
+    if (b1 < 0) r.m1 = 0.0f;
+    if (b2 < 0) r.m2 = 0.0f;
+    return r;
+}
+
+template <bool W8>
+__global__ void __launch_bounds__(128, HVG_TMA_MINB) k_skew_tma(SkewTmaView V, const int32_t *__restrict__ nbr, int64_t first,
                                                      IterParams P) {
     __shared__ TStage<W8> S;
     __shared__ uint64_t bar;
@@ -120,10 +149,10 @@ __global__ void __launch_bounds__(128, 8) k_skew_tma(SkewTmaView V, const int32_
                                         kNbrTx);
     }
     if (!V.frozen && tid >= 32 && tid < 48) S.fz[tid - 32] = 0u;
-    __syncthreads();
+    __syncwarp();
     if (tid < 32) {
-        // warp 0: lanes 12-18 the block's own fields (no dependency), lanes 0-11 the neighbour row entry
-        // then that neighbour's planes / lines
+        // warp 0: lanes 12-18 the block's own fields (no dependency), lanes 0-11 the neighbour row entry,
+        // then lanes 2-11 that neighbour's planes / lines
         int32_t nb = -1;
         if (tid < kNbr) nb = ld_hint(nbr + kNbr * row + tid, policy_evict_last());
         switch (tid) {
@@ -144,34 +173,44 @@ __global__ void __launch_bounds__(128, 8) k_skew_tma(SkewTmaView V, const int32_
             default: break;
         }
         if (tid < kNbr) {
+            S.snb[tid] = nb;
             const CUtensorMap *M = V.maps;
             const int fu = kFieldU + V.ui, fx = kFieldPX + V.pi, fy = kFieldPY + V.pi, fz = kFieldPZ + V.pi;
-            if (tid == 1 || tid == 3 || tid == 5) {   // +face planes: u, f, W, p_x, p_y, p_z
+            if (tid == 3 || tid == 5) {   // +y / +z face planes: u, f, W, p_x, p_y, p_z
                 const int box = tid >> 1;
-                float *dst = tid == 1 ? S.xf[0] : (tid == 3 ? S.yf[0] : S.zf[0]);
-                const int step = tid == 1 ? 256 : 64;
+                float *dst = tid == 3 ? S.yf[0] : S.zf[0];
                 const int fl[6] = {fu, kFieldF, kFieldW, fx, fy, fz};
 #pragma unroll
-                for (int q = 0; q < 6; q++) tma_load_4d(dst + q * step, M + box * kMapFields + fl[q], 0, 0, 0, nb, &bar);
-            } else {
+                for (int q = 0; q < 6; q++) tma_load_4d(dst + q * 64, M + box * kMapFields + fl[q], 0, 0, 0, nb, &bar);
+            } else if (tid != 0 && tid != 1 && tid != 8 && tid != 10) {   // x-face data: per-thread loads
                 float *dst;
                 int map, c0 = 0, c1 = 0, c2 = 0;
                 switch (tid) {
-                    case 0: dst = S.mx; map = kBoxX * kMapFields + fx; c0 = 4; break;
                     case 2: dst = S.my; map = kBoxY * kMapFields + fy; c1 = 7; break;
                     case 4: dst = S.mz; map = kBoxZ * kMapFields + fz; c2 = 7; break;
                     case 6: dst = S.e6; map = kBoxD * kMapFields + fx; c0 = 4; break;
                     case 7: dst = S.e7; map = kBoxE * kMapFields + fx; c0 = 4; break;
-                    case 8: dst = S.e8; map = kBoxD * kMapFields + fy; c1 = 7; break;
                     case 9: dst = S.e9; map = kBoxF * kMapFields + fy; c1 = 7; break;
-                    case 10: dst = S.e10; map = kBoxE * kMapFields + fz; c2 = 7; break;
                     default: dst = S.e11; map = kBoxF * kMapFields + fz; c2 = 7; break;
                 }
                 tma_load_4d(dst, M + map, c0, c1, c2, nb, &bar);
             }
         }
     }
+    __syncthreads();   // snb
+    XReg xr;
+    if (tid < 64) {
+        xr = xface_load<W8>(V, S.snb, tid);
+    } else {
+        // −x neighbour p_x at (7, y, z), entry y + 8z
+        const int k = tid - 64;
+        const int32_t b = S.snb[0];
+        const uint32_t idx = b >= 0 ? (uint32_t)b * (uint32_t)kBlockVox + (uint32_t)(7 + 8 * k) : 0u;
+        const float v = V.px_in[idx];
+        S.mx[k] = b >= 0 ? v : 0.0f;
+    }
     mbar_wait(&bar, 0);
+    __syncthreads();   // mx
     constexpr int NV = 4;
     const int x = tid & 7, y = (tid >> 3) & 7, z0 = (tid >> 6) * NV;
     const int c = tid & 63;
@@ -203,8 +242,7 @@ __global__ void __launch_bounds__(128, 8) k_skew_tma(SkewTmaView V, const int32_
         const float2 u = f2(S.u[i0], S.u[i1]);
         if (__any_sync(0xffffffffu, upd0 || upd1)) {
             const int z = z0 + k;
-            const float2 pxm = f2(x > 0 ? S.px[i0 - 1] : S.mx[4 * (y + 8 * z) + 3],
-                                  x > 0 ? S.px[i1 - 1] : S.mx[4 * (y + 8 * (z + 1)) + 3]);
+            const float2 pxm = f2(x > 0 ? S.px[i0 - 1] : S.mx[y + 8 * z], x > 0 ? S.px[i1 - 1] : S.mx[y + 8 * (z + 1)]);
             const float2 pym = f2(y > 0 ? S.py[i0 - 8] : S.my[x + 8 * z], y > 0 ? S.py[i1 - 8] : S.my[x + 8 * (z + 1)]);
             const float2 d = A2.add(A2.add(A2.sub(f2(px[k], px[k + 1]), pxm), A2.sub(f2(py[k], py[k + 1]), pym)),
                                     A2.sub(f2(pz[k], pz[k + 1]), f2(pzm, pz[k])));
@@ -223,12 +261,11 @@ __global__ void __launch_bounds__(128, 8) k_skew_tma(SkewTmaView V, const int32_
         auto face = [&](int A, int k) {
             const int c0 = k & 7, c1 = k >> 3;
             float u, f, w, qx, qy, qz, pxm, pym, pzm2;
-            if (A == 0) {        // v = (0, y, z) of the +x neighbour, y = c0, z = c1
-                const int j = 4 * k;
-                u = S.xf[0][j], f = S.xf[1][j], w = S.xf[2][j], qx = S.xf[3][j], qy = S.xf[4][j], qz = S.xf[5][j];
+            if (A == 0) {        // v = (0, y, z) of the +x neighbour, y = c0, z = c1 (registers)
+                u = xr.u, f = xr.f, w = xr.w, qx = xr.px, qy = xr.py, qz = xr.pz;
                 pxm = S.px[7 + 8 * c0 + 64 * c1];
-                pym = c0 > 0 ? S.xf[4][j - 4] : S.e8[4 * c1];
-                pzm2 = c1 > 0 ? S.xf[5][j - 32] : S.e10[4 * c0];
+                pym = xr.m1;
+                pzm2 = xr.m2;
             } else if (A == 1) { // v = (x, 0, z) of the +y neighbour, x = c0, z = c1
                 u = S.yf[0][k], f = S.yf[1][k], w = S.yf[2][k], qx = S.yf[3][k], qy = S.yf[4][k], qz = S.yf[5][k];
                 pxm = c0 > 0 ? S.yf[3][k - 1] : S.e6[4 * c1 + 3];
