@@ -97,7 +97,6 @@ struct vol_s {
     int32_t *d_perm = nullptr;         // [n_local] caller index of store row r
     float *d_tmp = nullptr;            // [n_local][512] scratch for caller-order I/O
     float *d_u2 = nullptr;             // [S][512] second u buffer of the skewed schedule
-    char *d_tmaps = nullptr;           // TMA tensor maps of the fields (skew_tma.cu)
     unsigned long long *d_misc = nullptr;  // [4]: dup, bad, n_omega, spare
     double *d_part = nullptr;          // [S][5]
     double *d_eout = nullptr;          // [8]

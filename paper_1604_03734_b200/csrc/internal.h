@@ -36,7 +36,6 @@ struct Fields {
     float *ub[2];          // relaxed primal ū, double-buffered
     float *px[2], *py[2], *pz[2];  // dual p, double-buffered
     float *u2 = nullptr;           // second u buffer of the skewed schedule
-    const void *tmaps = nullptr;   // device table of the TMA tensor maps of these fields (skew_tma.cu), or null
 };
 
 // The buffers of one iteration, selected on the host (no dynamic indexing in kernels).
@@ -80,12 +79,6 @@ int launch_primal_only(const View &V, const int32_t *nbr, int64_t n_work, const 
 // [first, first + n_blocks); reads u_in and p[p_in] (p^{k+1}), writes u_out and p[p_in ^ 1] (p^{k+2}).
 int launch_skew(const Fields &F, const float *u_in, float *u_out, int p_in, const uint32_t *frozen,
                 const int32_t *nbr, int64_t first, int64_t n_blocks, const IterParams &P, cudaStream_t s);
-// The same launch with the halo read by tensor TMA (skew_tma.cu); u_in = ui ? F.u2 : F.u, u_out the other.
-int launch_skew_tma(const Fields &F, int ui, int p_in, const uint32_t *frozen, const int32_t *nbr, int64_t first,
-                    int64_t n_blocks, const IterParams &P, cudaStream_t s);
-size_t skew_tma_map_bytes();
-// Encodes the tensor maps of F's fields (S store rows) into d_maps (device, 64-byte aligned); 0 or -1.
-int skew_tma_build_maps(const Fields &F, int64_t S, void *d_maps, cudaStream_t s);
 int launch_two_kernel(const View &V, const int32_t *nbr, const int32_t *work, int64_t n_work, const IterParams &P,
                       cudaStream_t s);
 

@@ -98,7 +98,6 @@ static void carve_all(Carve &c, vol_s *v, const Layout &L) {
     auto misc = c.take<unsigned long long>(4);
     auto part = c.take<double>(5 * (size_t)L.S + 5);
     auto eout = c.take<double>(8);
-    auto tmaps = c.take<char>(skew_tma_map_bytes());
     if (v) {
         v->d_xyz = xyz;
         v->d_hash = hash;
@@ -116,7 +115,6 @@ static void carve_all(Carve &c, vol_s *v, const Layout &L) {
         v->d_part = part;
         v->d_eout = eout;
         v->F.u2 = u2;
-        v->d_tmaps = tmaps;
     }
 }
 
@@ -291,8 +289,6 @@ static vol_status create_impl(const int32_t *block_xyz, int64_t n_global, const 
     carve_all(c, v, L);
     v->extra = c.base + ((c.off + 255) & ~(size_t)255);
     cudaStream_t s = v->stream;
-    // tensor maps of the halo TMA (skew_tma.cu); without them launch_skew takes the per-thread gather
-    if (skew_tma_build_maps(v->F, L.S, v->d_tmaps, s) == 0) v->F.tmaps = v->d_tmaps;
 
     // store order: Morton order of the blocks (single GPU) or the shard plan's [launch A | launch B]
     // rows + ghosts; row_caller[r] is the block's index in the caller's f / W / u arrays
