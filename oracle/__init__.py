@@ -69,12 +69,49 @@ def build_omp(force: bool = False) -> str:
     return _SO_OMP
 
 
+def _cpu_tag() -> str:
+    """A short digest of this host's CPU model and ISA flags (the -march=native build is host-specific)."""
+    import hashlib
+    info = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith(("model name", "flags")):
+                info += line
+                if line.startswith("flags"):
+                    break
+    except OSError:
+        pass
+    return hashlib.sha1(info.encode()).hexdigest()[:10]
+
+
+def build_native(omp: bool = False, force: bool = False) -> str:
+    """TIMING build for bench.py's CPU baselines ("O1 is built -O3 -march=native
+    -ffp-contract=off"): the same sources, -O3 -march=native, optionally -fopenmp.  Built on the host that
+    runs it (the file name carries a digest of the CPU model and flags, so a library built for another
+    CPU is never loaded).  No contraction and no fast-math, and every loop is over independent voxels,
+    so the arithmetic is the plain build's bit for bit (checked in tests/test_oracle_iteration.py)."""
+    so = os.path.join(_HERE, f"liboracle_native{'_omp' if omp else ''}_{_cpu_tag()}.so")
+    newest = max(os.path.getmtime(s) for s in _SRC)
+    if force or not os.path.exists(so) or os.path.getmtime(so) < newest:
+        tmp = so + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O3", "-march=native", "-std=c99", "-ffp-contract=off", "-fno-fast-math",
+                               "-fPIC", "-shared", "-Wall"] + (["-fopenmp"] if omp else []) +
+                              ["-o", tmp, _SRC[0], _SRC[1], _SRC[2], _SRC[3], "-lm"])
+        os.replace(tmp, so)
+    return so
+
+
 _lib = None
 _lib_omp = None
+_lib_native = {}
 
 
-def lib(omp: bool = False):
+def lib(omp: bool = False, native: bool = False):
     global _lib, _lib_omp
+    if native:
+        if omp not in _lib_native:
+            _lib_native[omp] = _declare(ctypes.CDLL(build_native(omp)))
+        return _lib_native[omp]
     if omp:
         if _lib_omp is None:
             _lib_omp = _declare(ctypes.CDLL(build_omp()))
@@ -231,7 +268,7 @@ def divergence(nbr, W, p, precision="f64") -> np.ndarray:
 
 
 def regularise(coords, f, W, lam, eps, tau, sigma, iters, theta=1.0, data_term=0, init=0, precision="f64",
-               state=None, nbr=None, omp=False):
+               state=None, nbr=None, omp=False, native=False):
     """Run `iters` CP iterations; returns (u, ubar, p) with u, ubar [n, 512] and p [3, n, 512].
 
     `state` = (u, ubar, p) resumes from a previous call.  Parameters are rounded to fp32 first
@@ -253,7 +290,7 @@ def regularise(coords, f, W, lam, eps, tau, sigma, iters, theta=1.0, data_term=0
         u, ub, p = (np.array(a, dtype=dt, copy=True) for a in state)
         resume = 1
     r32 = lambda x: float(np.float32(x))
-    getattr(lib(omp), f"orc_regularise_{sfx}")(n, _ptr(nbr), _ptr(ff), _ptr(Wf), r32(lam), r32(eps), r32(tau),
+    getattr(lib(omp, native), f"orc_regularise_{sfx}")(n, _ptr(nbr), _ptr(ff), _ptr(Wf), r32(lam), r32(eps), r32(tau),
                                             r32(sigma), r32(theta), int(data_term), int(init), int(iters),
                                             _ptr(u), _ptr(ub), _ptr(p), resume)
     return u, ub, p

@@ -332,3 +332,19 @@ def test_phase_split_composes_to_the_iteration():
     q = np.float64(np.float32(s.sigma)) * g * (1.0 / (1.0 + np.float64(np.float32(s.sigma)) * np.float64(np.float32(s.eps))))
     nrm = np.sqrt((q ** 2).sum(0))
     assert np.allclose(st[2], q / np.maximum(1.0, nrm)[None], rtol=1e-14, atol=1e-15)
+
+
+def test_native_timing_build_is_bitwise_the_oracle():
+    """bench.py's CPU baselines run the -O3 -march=native build; it must compute the same
+    bits as the parity oracle (no contraction, no fast-math, independent per-voxel loops)."""
+    import oracle
+    from synth import random_instance
+    s = random_instance(150, seed=8, extent=4, w_density=0.8, lam=0.6, eps=0.02, iters=15)
+    nbr = oracle.neighbours(s.coords)
+    for prec in ("f32", "f64"):
+        kw = dict(theta=s.theta, data_term=s.data_term, init=s.init, precision=prec, nbr=nbr)
+        a = oracle.regularise(s.coords, s.f, s.W, s.lam, s.eps, s.tau, s.sigma, s.iters, **kw)
+        b = oracle.regularise(s.coords, s.f, s.W, s.lam, s.eps, s.tau, s.sigma, s.iters, native=True, **kw)
+        c = oracle.regularise(s.coords, s.f, s.W, s.lam, s.eps, s.tau, s.sigma, s.iters, native=True, omp=True, **kw)
+        for x, y, z in zip(a, b, c):
+            assert np.array_equal(x, y) and np.array_equal(x, z)
