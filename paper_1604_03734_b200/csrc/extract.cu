@@ -105,9 +105,9 @@ __device__ __forceinline__ float sel4f(int i, float a0, float a1, float a2, floa
 // (v0 … v3).  X-5: the lone corner (nin = 1: the inside one, nin = 3: the outside one) or the inside pair
 // goes first, the remaining corners follow in tetrahedron order, and the last two are swapped when that
 // permutation is odd, so (a, b, c, d) stays positively oriented.
-template <bool EMIT, class VertexOf>
+template <bool EMIT>
 __device__ __forceinline__ void tet(int k0, int k1, int k2, int k3, float v0, float v1, float v2, float v3,
-                                    const VertexOf &vertex, float *out, unsigned &m) {
+                                    const CellGeom &G, float *out, unsigned &m) {
     const int mask = (v0 < 0.0f) | ((v1 < 0.0f) << 1) | ((v2 < 0.0f) << 2) | ((v3 < 0.0f) << 3);   // X-3
     if (mask == 0 || mask == 15) return;
     const int nin = __popc(mask);
@@ -138,18 +138,18 @@ __device__ __forceinline__ void tet(int k0, int k1, int k2, int k3, float v0, fl
     const float uc = sel4f(pc, v0, v1, v2, v3), ud = sel4f(pd, v0, v1, v2, v3);
     float e1[3], e2[3], e3[3];
     if (nin != 2) {
-        vertex(ca, ua, cb, ub, e1);
-        vertex(ca, ua, cc, uc, e2);
-        vertex(ca, ua, cd, ud, e3);
+        edge_vertex(G, ca, ua, cb, ub, e1);
+        edge_vertex(G, ca, ua, cc, uc, e2);
+        edge_vertex(G, ca, ua, cd, ud, e3);
         // 1 inside: never degenerate; 1 outside (a): all three vertices sit on a iff u_a = 0
         if (nin == 1) put<EMIT>(out, m, e1, e2, e3, false);
         else put<EMIT>(out, m, e1, e3, e2, ua == 0.0f);
     } else {
         float e4[3];
-        vertex(ca, ua, cc, uc, e1);   // E_ac
-        vertex(ca, ua, cd, ud, e2);   // E_ad
-        vertex(cb, ub, cd, ud, e3);   // E_bd
-        vertex(cb, ub, cc, uc, e4);   // E_bc
+        edge_vertex(G, ca, ua, cc, uc, e1);   // E_ac
+        edge_vertex(G, ca, ua, cd, ud, e2);   // E_ad
+        edge_vertex(G, cb, ub, cd, ud, e3);   // E_bd
+        edge_vertex(G, cb, ub, cc, uc, e4);   // E_bc
         put<EMIT>(out, m, e1, e2, e3, ud == 0.0f);   // E_ad = E_bd iff u_d = 0
         put<EMIT>(out, m, e1, e3, e4, uc == 0.0f);   // E_ac = E_bc iff u_c = 0
     }
@@ -168,44 +168,6 @@ __device__ __forceinline__ int tet_code(int q, int r) {   // r = 1, 2, 3
 
 __device__ __forceinline__ int tile_index(int cx, int cy, int cz, int code) {
     return (cx + (code & 1)) + kT * (cy + ((code >> 1) & 1)) + kT * kT * (cz + (code >> 2));
-}
-
-// Emit-pass vertex cache.  Every edge of the Freudenthal split joins corners a ⊂ b (componentwise ≤), so
-// it is identified by its lower end (anchor, a tile point in [0, 8]^3) and its direction d = b − a, one of
-// the 7 nonzero 0/1 vectors: slot = (x + 9y + 81z)·7 + (d − 1).  The lower end is also the lexicographically
-// smaller one, so the X-4 vertex of a slot is a function of the anchor's global coordinates, d and the two
-// values only — the same bits in every tetrahedron, cell and block that uses the edge.  The emit pass marks
-// the slots of the crossing edges of its crossing tetrahedra, computes each marked vertex once, and the
-// triangles copy them (a block with more than kVCap crossing edges computes its vertices per
-// tetrahedron as before).
-constexpr int kSlots = kTile * 7;                 // 5103
-constexpr int kSlotWords = (kSlots + 31) / 32;    // 160
-constexpr int kVCap = 2048;                       // cached vertices per block
-
-__device__ __forceinline__ int slot_of(int cx, int cy, int cz, int ca, int cb) {
-    const int lo = ca & cb, d = ca ^ cb;   // corners of a Kuhn tetrahedron are nested: lo ⊂ hi
-    return tile_index(cx, cy, cz, lo) * 7 + (d - 1);
-}
-
-// X-4 vertex of edge slot `slot` (anchor tile point + direction) with the block's global voxel origin g
-__device__ __forceinline__ void slot_vertex(int slot, const float *su, int gx, int gy, int gz, float voxel,
-                                            float *p) {
-    const int a = slot / 7, d = slot - 7 * a + 1;
-    const int ax = a % kT, ay = (a / kT) % kT, az = a / (kT * kT);
-    const int hi = (ax + (d & 1)) + kT * (ay + ((d >> 1) & 1)) + kT * kT * (az + (d >> 2));
-    const float ulo = su[a], uhi = su[hi];
-    const float t = __fdiv_rn(ulo, __fsub_rn(ulo, uhi));
-    const int o[3] = {gx + ax, gy + ay, gz + az};
-#pragma unroll
-    for (int k = 0; k < 3; k++) {
-        const float x0 = __fmul_rn(__fadd_rn((float)o[k], 0.5f), voxel);
-        if ((d >> k) & 1) {
-            const float x1 = __fmul_rn(__fadd_rn((float)(o[k] + 1), 0.5f), voxel);
-            p[k] = __fadd_rn(x0, __fmul_rn(t, __fsub_rn(x1, x0)));
-        } else {
-            p[k] = x0;
-        }
-    }
 }
 
 constexpr int kMaxItems = 512 * 6;   // (cell, tetrahedron) pairs of one block
@@ -230,9 +192,6 @@ __global__ void __launch_bounds__(128) k_extract(ExArgs A, int64_t n_rows, uint3
     // with consecutive lanes on consecutive floats (coalesced) instead of 9 scattered 4-byte stores
     // per triangle 36 B apart
     __shared__ float sout[EMIT ? 2 * 128 * 9 : 1];
-    __shared__ uint32_t emask[EMIT ? kSlotWords : 1];
-    __shared__ uint32_t eoff[EMIT ? kSlotWords + 1 : 1];
-    __shared__ float vc[EMIT ? 3 * kVCap : 1];   // cached vertices, [rank][3]
     const int64_t r = blockIdx.x;
     if (r >= n_rows) return;
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
@@ -315,65 +274,6 @@ __global__ void __launch_bounds__(128) k_extract(ExArgs A, int64_t n_rows, uint3
         sitem[pos++] = (uint16_t)(((4 * t + q) << 3) | k);
     }
     __syncthreads();
-    bool cached = false;
-    if (EMIT) {
-        // vertex cache: mark the crossing edges of the crossing tetrahedra, rank them, compute each once
-        for (int w = t; w < kSlotWords; w += 128) emask[w] = 0u;
-        __syncthreads();
-        for (uint32_t i = t; i < n_items; i += 128) {
-            const int cell = sitem[i] >> 3, k = sitem[i] & 7;
-            const int cx = cell & 7, cyy = (cell >> 3) & 7, czz = cell >> 6;
-            const int cc[4] = {0, tet_code(k, 1), tet_code(k, 2), tet_code(k, 3)};
-            bool in[4];
-#pragma unroll
-            for (int q = 0; q < 4; q++) in[q] = su[tile_index(cx, cyy, czz, cc[q])] < 0.0f;   // X-3
-#pragma unroll
-            for (int a = 0; a < 4; a++)
-#pragma unroll
-                for (int b = a + 1; b < 4; b++)
-                    if (in[a] != in[b]) {
-                        const int sl = slot_of(cx, cyy, czz, cc[a], cc[b]);
-                        atomicOr(&emask[sl >> 5], 1u << (sl & 31));
-                    }
-        }
-        __syncthreads();
-        if (wid == 0) {   // exclusive prefix of the per-word popcounts (5 words per lane)
-            uint32_t c5[5], sum = 0;
-#pragma unroll
-            for (int j = 0; j < 5; j++) {
-                c5[j] = __popc(emask[5 * lane + j]);
-                sum += c5[j];
-            }
-            uint32_t inc = sum;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-                if (lane >= o) inc += y;
-            }
-            uint32_t run0 = inc - sum;
-#pragma unroll
-            for (int j = 0; j < 5; j++) {
-                eoff[5 * lane + j] = run0;
-                run0 += c5[j];
-            }
-            if (lane == 31) eoff[kSlotWords] = inc;
-        }
-        __syncthreads();
-        cached = eoff[kSlotWords] <= (uint32_t)kVCap;
-        if (cached) {
-            for (int w = t; w < kSlotWords; w += 128) {
-                uint32_t bits = emask[w];
-                uint32_t rank = eoff[w];
-                while (bits) {
-                    const int b = __ffs(bits) - 1;
-                    bits &= bits - 1;
-                    slot_vertex(32 * w + b, su, gx, gy, gz, A.voxel, vc + 3 * rank);
-                    rank++;
-                }
-            }
-        }
-        __syncthreads();
-    }
     // (B) items round-robin: item i = t + 128·round, in list order
     uint32_t run = 0;            // EMIT: triangles written by the earlier rounds
     uint32_t block_total = 0;    // count pass: triangles of this thread's items
@@ -405,23 +305,9 @@ __global__ void __launch_bounds__(128) k_extract(ExArgs A, int64_t n_rows, uint3
             const uint32_t round_total = swarp[0] + swarp[1] + swarp[2] + swarp[3];
             if (cnt) {
                 unsigned m = 0;
-                const float v0 = su[tile_index(cx, cyy, czz, 0)], v1 = su[tile_index(cx, cyy, czz, k1)];
-                const float v2 = su[tile_index(cx, cyy, czz, k2)], v3 = su[tile_index(cx, cyy, czz, k3)];
-                if (cached) {
-                    auto vertex = [&](int ca, float, int cb, float, float *p) {
-                        const int sl = slot_of(cx, cyy, czz, ca, cb);
-                        const uint32_t w = (uint32_t)sl >> 5, bit = (uint32_t)sl & 31u;
-                        const float *q = vc + 3 * (eoff[w] + __popc(emask[w] & ((1u << bit) - 1u)));
-                        p[0] = q[0];
-                        p[1] = q[1];
-                        p[2] = q[2];
-                    };
-                    tet<true>(0, k1, k2, k3, v0, v1, v2, v3, vertex, sout + 9 * before, m);
-                } else {
-                    const CellGeom G = cell_geom(gx + cx, gy + cyy, gz + czz, A.voxel);
-                    auto vertex = [&](int ca, float ua, int cb, float ub, float *p) { edge_vertex(G, ca, ua, cb, ub, p); };
-                    tet<true>(0, k1, k2, k3, v0, v1, v2, v3, vertex, sout + 9 * before, m);
-                }
+                const CellGeom G = cell_geom(gx + cx, gy + cyy, gz + czz, A.voxel);
+                tet<true>(0, k1, k2, k3, su[tile_index(cx, cyy, czz, 0)], su[tile_index(cx, cyy, czz, k1)],
+                          su[tile_index(cx, cyy, czz, k2)], su[tile_index(cx, cyy, czz, k3)], G, sout + 9 * before, m);
             }
             __syncthreads();
             float *dst = base_out + 9ull * run;
@@ -431,8 +317,7 @@ __global__ void __launch_bounds__(128) k_extract(ExArgs A, int64_t n_rows, uint3
             unsigned m = 0;
             if (i < n_items)
                 tet<false>(0, k1, k2, k3, su[tile_index(cx, cyy, czz, 0)], su[tile_index(cx, cyy, czz, k1)],
-                           su[tile_index(cx, cyy, czz, k2)], su[tile_index(cx, cyy, czz, k3)],
-                           [](int, float, int, float, float *) {}, nullptr, m);
+                           su[tile_index(cx, cyy, czz, k2)], su[tile_index(cx, cyy, czz, k3)], CellGeom{}, nullptr, m);
             const uint32_t b0 = __ballot_sync(0xffffffffu, m & 1u), b1 = __ballot_sync(0xffffffffu, (m >> 1) & 1u);
             if (lane == 0 && i0 + 32 * wid < n_items) {
                 uint32_t *wb = item_bits + (size_t)r * kItemWords + 2 * ((i0 >> 5) + wid);
