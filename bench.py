@@ -121,15 +121,36 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def load_traffic():
-    """DRAM bytes per fused-kernel launch from the committed ncu --set full capture, if any."""
-    p = os.path.join(ROOT, "profiles", "fused_traffic.json")
+def ncu_inputs():
+    """Per-kernel figures of the committed ncu captures (profiles/ncu_inputs.json, scripts/ncu_inputs.py)."""
     try:
-        with open(p) as fh:
-            d = json.load(fh)
-        return d
+        with open(os.path.join(ROOT, "profiles", "ncu_inputs.json")) as fh:
+            return json.load(fh)
     except Exception:
-        return None
+        return {}
+
+
+def issue_peak():
+    """Warp-instruction issue peak: 148 SMs x 4 schedulers x 1 warp instruction per clock x the max SM clock."""
+    mhz = 1965.0
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            mhz = float(json.load(fh).get("sm_max_mhz", mhz))
+    except Exception:
+        pass
+    return 148 * 4 * mhz * 1e6, f"148 SMs x 4 schedulers x 1 warp-instruction/clk x {mhz:.0f} MHz"
+
+
+def l2_peak():
+    """L2 (LTS) throughput cap: ~6300 B per SM clock full-chip (B300_MICROARCH.md, measured on B300; not
+    re-measured on B200) x the max SM clock."""
+    mhz = 1965.0
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            mhz = float(json.load(fh).get("sm_max_mhz", mhz))
+    except Exception:
+        pass
+    return 6300.0 * mhz * 1e6 / 1e9, f"6300 B/clk LTS cap (B300_MICROARCH.md, a B300 measurement) x {mhz:.0f} MHz"
 
 
 def make_scene(cfg: str, world: int, seed: int, device):
@@ -284,8 +305,19 @@ def fusion_leg(args, dev):
            "step": "vol_fuse (alloc + compact + radix sort + integrate), depth maps and poses resident in HBM",
            "roofline": {"bound": "alu", "kernel": "k_fuse_integrate", "achieved": ach / 1e12, "peak": peak / 1e12,
                         "unit": "Tops/s", "frac": ach / peak, "peak_source": peak_src,
+                        "basis": "algorithmic: 36 fp32 operations per evaluated voxel-frame (DESIGN.md §11) / "
+                                 "issue-limited lane-op peak",
                         "alg_ops_per_launch": FUSE_OPS_PER_EVAL * evals, "avg_launch_ms": t_int,
                         "traffic": None}}
+    ni = ncu_inputs().get("k_fuse_integrate/fusion-street")
+    if ni:
+        ip, ip_src = issue_peak()
+        iss = ni["warp_instructions"] / (t_int / 1e3)
+        res["roofline"].update({"issue": {"achieved": iss / 1e12, "peak": ip / 1e12, "unit": "T warp-instructions/s",
+                                          "frac": iss / ip, "peak_source": ip_src,
+                                          "warp_instructions_per_launch": ni["warp_instructions"],
+                                          "source": ni["source"]},
+                                "traffic": ni["dram_bytes"]})
     if not args.no_cpu_baseline:
         import oracle
         k = 4
@@ -329,9 +361,24 @@ def extraction_leg(args, dev, scene, iters, stream):
            "triangles": ntri, "cells": nvox, "ms_per_call": ms, "cells_per_s": nvox / (ms / 1e3),
            "triangles_per_s": ntri / (ms / 1e3),
            "step": "vol_extract: count kernel + exclusive scan + ordered emit kernel, output in HBM",
-           "roofline": {"bound": "hbm", "kernel": "k_extract (count + emit)", "achieved": alg / (ms / 1e3) / 1e9,
-                        "peak": peak, "unit": "GB/s", "frac": alg / (ms / 1e3) / 1e9 / peak, "peak_source": peak_src,
-                        "alg_bytes_per_call": alg, "traffic": None}}
+           "hbm": {"achieved": alg / (ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                   "frac": alg / (ms / 1e3) / 1e9 / peak, "alg_bytes_per_call": alg,
+                   "note": "algorithmic bytes (read u and W once, write 36 B per triangle); not the bound"}}
+    nc, ne = (ncu_inputs().get(k) for k in ("k_extract_count/street", "k_extract_emit/street"))
+    ip, ip_src = issue_peak()
+    if nc and ne and scene.name == "street":
+        inst = nc["warp_instructions"] + ne["warp_instructions"]
+        iss = inst / (ms / 1e3)
+        res["roofline"] = {"bound": "issue", "kernel": "k_extract (count + emit)", "achieved": iss / 1e12,
+                           "peak": ip / 1e12, "unit": "T warp-instructions/s", "frac": iss / ip, "peak_source": ip_src,
+                           "basis": "physical: ncu warp instructions of both passes / CUDA-event call time",
+                           "warp_instructions_per_call": inst,
+                           "thread_instructions_per_triangle": 32 * inst / max(ntri, 1),
+                           "traffic": nc["dram_bytes"] + ne["dram_bytes"], "sources": [nc["source"], ne["source"]]}
+    else:
+        res["roofline"] = {"bound": "issue", "kernel": "k_extract (count + emit)", "achieved": None, "peak": ip / 1e12,
+                           "unit": "T warp-instructions/s", "frac": None, "peak_source": ip_src, "traffic": None,
+                           "basis": "no ncu capture of this workload"}
     vol.close()
     return res
 
@@ -376,12 +423,26 @@ def stereo_leg(args, dev):
            "median_abs_disparity_error_px": err,
            "step": "vol_stereo: census x2, tensor, WTA init, 200 TGV iterations (k_dual4 + k_primal4 on L2-sized "
                    "chunks of 2 frames), 10 data steps, one CUDA graph",
-           "roofline": {"bound": "hbm", "kernel": "k_dual4 + k_primal4 (one TGV iteration)", "achieved": ach,
-                        "note": "the chunked iteration state is L2-resident, so the algorithmic rate is quoted "
-                                "against HBM but served mostly from L2 (frac can exceed 1)",
-                        "peak": peak, "unit": "GB/s",
-                        "frac": ach / peak, "peak_source": peak_src, "avg_launch_ms": it_ms,
-                        "alg_bytes_per_launch": STEREO_BYTES_PER_PIXEL_ITER * npx, "traffic": None}}
+           "hbm_alg": {"achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "peak_source": peak_src,
+                       "alg_bytes_per_iteration": STEREO_BYTES_PER_PIXEL_ITER * npx,
+                       "note": "112 algorithmic B per pixel-iteration; the chunked state is L2-resident, so this is "
+                               "not a DRAM figure (see roofline)"}}
+    nd, npr = (ncu_inputs().get(k) for k in ("k_dual4/stereo-street", "k_primal4/stereo-street"))
+    lp, lp_src = l2_peak()
+    if nd and npr:
+        px_launch = 2 * 1240 * 376   # one chunk of 2 frames per launch
+        l2b = (nd["lts_bytes"] + npr["lts_bytes"]) / px_launch
+        drb = (nd["dram_bytes"] + npr["dram_bytes"]) / px_launch
+        l2a = l2b * npx / (it_ms / 1e3) / 1e9
+        res["roofline"] = {"bound": "l2", "kernel": "k_dual4 + k_primal4 (one TGV iteration)", "achieved": l2a,
+                           "peak": lp, "unit": "GB/s", "frac": l2a / lp, "peak_source": lp_src,
+                           "basis": "physical: ncu lts__t_sectors x 32 B per pixel-iteration x pixels / event time",
+                           "avg_launch_ms": it_ms, "l2_bytes_per_pixel_iter": l2b, "dram_bytes_per_pixel_iter": drb,
+                           "dram_achieved": drb * npx / (it_ms / 1e3) / 1e9,
+                           "traffic": drb * npx, "sources": [nd["source"], npr["source"]]}
+    else:
+        res["roofline"] = {"bound": "l2", "kernel": "k_dual4 + k_primal4", "achieved": None, "peak": lp, "unit": "GB/s",
+                           "frac": None, "peak_source": lp_src, "traffic": None, "basis": "no ncu capture"}
     if not args.no_cpu_baseline:
         import time as _t
 
@@ -446,18 +507,42 @@ def platform_cpu() -> str:
     return "unknown CPU"
 
 
-def time_oracle(scene, iters: int, omp: bool = False):
-    import numpy as np
-
+def time_oracle(scene, iters: int, omp: bool = False, precision: str = "f64", nbr=None):
+    """Wall time of `iters` oracle iterations over the whole scene — the -O3 -march=native timing build of
+    the oracle (bitwise the parity build), one thread or OpenMP over all host threads."""
     import oracle
     coords, f, W = scene.numpy()
-    nbr = oracle.neighbours(coords)
+    if nbr is None:
+        nbr = oracle.neighbours(coords)
     t0 = time.perf_counter()
     oracle.regularise(coords, f, W, scene.lam, scene.eps, scene.tau, scene.sigma, iters, theta=scene.theta,
-                      data_term=scene.data_term, init=scene.init, precision="f64", nbr=nbr, omp=omp)
-    dt = time.perf_counter() - t0
-    del np
-    return dt
+                      data_term=scene.data_term, init=scene.init, precision=precision, nbr=nbr, omp=omp, native=True)
+    return time.perf_counter() - t0
+
+
+def cpu_baselines(scene):
+    """SURVEY §8(d) CPU baselines on the box's host cores, each a bounded sample (~10 s) of the same volume:
+    the fp64 oracle on one thread (`cpu_baseline`), on all host threads (`cpu_baseline_omp`), and the fp32
+    oracle on one thread (`cpu_baseline_f32`)."""
+    import oracle
+    sc = scene.to("cpu")
+    nbr = oracle.neighbours(sc.coords)
+    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    host = {"cpu_model": platform_cpu(), "nproc": os.cpu_count(), "build": "gcc -O3 -march=native -ffp-contract=off"}
+    out = {}
+    for key, omp, prec in (("cpu_baseline", False, "f64"), ("cpu_baseline_omp", True, "f64"),
+                           ("cpu_baseline_f32", False, "f32")):
+        k = 1
+        t = time_oracle(sc, k, omp=omp, precision=prec, nbr=nbr)
+        while t < 5.0:   # grow the sample to ~10 s (the first short runs include thread start-up)
+            k = max(2 * k, int(k * 10.0 / max(t, 1e-3)))
+            t = time_oracle(sc, k, omp=omp, precision=prec, nbr=nbr)
+        cores = threads if omp else 1
+        out[key] = dict({"value": sc.n_alloc * k / t, "unit": "voxel-updates/s", "cores": cores,
+                         "kind": "oracle" + (" (OpenMP)" if omp else ""), "precision": prec,
+                         "sample": f"{k} {prec} oracle iteration(s) over the whole {scene.name} volume "
+                                   f"({sc.n_alloc} voxels), {t:.1f} s on {cores} host thread(s)"}, **host)
+    return out
 
 
 def reference_arm(args):
@@ -716,58 +801,38 @@ def main():
         return 0
 
     peak, peak_src = load_peaks()
-    achieved = ALG_BYTES_PER_VOXEL * n_local_vox / (it_ms / 1e3) / 1e9
-    tr = load_traffic()
-    traffic = None
     kname = {0: "k_skew", 1: "k_dual+k_primal", 2: "k_skew", 3: "k_fused"}[args.kernel]
-    if tr and tr.get("workload") == scene.name and tr.get("kernel") == kname \
-            and bool(tr.get("freeze", True)) == bool(args.freeze):
-        traffic = tr.get("dram_bytes_per_launch")
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "peak_source": peak_src,
-                "kernel": kname,
-                "alg_bytes_per_launch": ALG_BYTES_PER_VOXEL * n_local_vox,
-                "avg_launch_ms": it_ms, "frac_of_8TBps": achieved / 8000.0}
-    if traffic:
-        roofline["dram_gbs_actual"] = traffic / (it_ms / 1e3) / 1e9
-        roofline["dram_frac_actual"] = roofline["dram_gbs_actual"] / peak
-    if args.freeze:
-        roofline["note"] = ("achieved counts SURVEY 8(d)'s 48 B per allocated voxel-iteration; with opts.freeze the kernel "
-                            "does not rewrite u/u-bar of frozen voxels (bit-identical result), so frac can exceed 1 - "
-                            "dram_frac_actual is the physical DRAM throughput, no_freeze the full-traffic run")
+    n_omega_local = int((W_loc > 0).sum())
+    ncu = ncu_inputs()
+
+    def hbm_roofline(ms_launch, freeze):
+        """Roofline position of the iteration kernel: physical DRAM bytes per launch (the committed ncu capture
+        of this kernel on this workload) over the CUDA-event launch time; SURVEY §8(d)'s algorithmic 48 B per
+        allocated voxel-iteration beside it (alg_*).  Without a capture of this workload the algorithmic
+        figure is the position (basis says which)."""
+        alg_bytes = ALG_BYTES_PER_VOXEL * n_local_vox
+        alg = alg_bytes / (ms_launch / 1e3) / 1e9
+        ni = ncu.get(f"{kname}/{scene.name}/{'freeze' if freeze else 'nofreeze'}") if not sharded else None
+        r = {"bound": "hbm", "kernel": kname, "peak": peak, "unit": "GB/s", "peak_source": peak_src,
+             "avg_launch_ms": ms_launch, "alg_bytes_per_launch": alg_bytes, "alg_achieved": alg,
+             "alg_frac": alg / peak, "alg_frac_of_8TBps": alg / 8000.0}
+        if ni:
+            tr = ni["dram_bytes"]
+            ach = tr / (ms_launch / 1e3) / 1e9
+            r.update({"basis": "physical: ncu dram__bytes_read + dram__bytes_write per launch / CUDA-event launch time",
+                      "achieved": ach, "frac": ach / peak, "frac_of_8TBps": ach / 8000.0, "traffic": tr,
+                      "traffic_source": ni["source"], "bytes_per_alloc_voxel": tr / n_local_vox,
+                      "bytes_per_omega_voxel": tr / max(n_omega_local, 1),
+                      "l2_bytes_per_launch": ni.get("lts_bytes"), "warp_instructions_per_launch": ni.get("warp_instructions")})
+        else:
+            r.update({"basis": "algorithmic: 48 B per allocated voxel-iteration (no ncu capture of this workload)",
+                      "achieved": alg, "frac": alg / peak, "frac_of_8TBps": alg / 8000.0, "traffic": None})
+        return r
+
+    roofline = hbm_roofline(it_ms, bool(args.freeze))
     if nf:
-        nf_ach = ALG_BYTES_PER_VOXEL * n_local_vox / (nf["avg_launch_ms"] / 1e3) / 1e9
-        nf.update({"achieved": nf_ach, "frac": nf_ach / peak})
-        nft = (tr or {}).get("no_freeze") if tr and tr.get("workload") == scene.name and tr.get("kernel") == kname else None
-        if nft:
-            nf["traffic"] = nft["dram_bytes_per_launch"]
-            nf["dram_gbs_actual"] = nft["dram_bytes_per_launch"] / (nf["avg_launch_ms"] / 1e3) / 1e9
-            nf["dram_frac_actual"] = nf["dram_gbs_actual"] / peak
-    cpu = None
-    if not args.no_cpu_baseline and world == 1:
-        sc = scene.to("cpu")
-        k = 1
-        t = time_oracle(sc, k)
-        if t < 5.0:
-            k = max(1, int(10.0 / max(t, 1e-3)))
-            t = time_oracle(sc, k)
-        cpu = {"value": sc.n_alloc * k / t, "unit": "voxel-updates/s", "cores": 1, "kind": "oracle",
-               "sample": f"{k} fp64 oracle iteration(s) over the whole {scene.name} volume ({sc.n_alloc} voxels), "
-                         f"{t:.1f} s on one host core"}
-    cpu_omp = None
-    if not args.no_cpu_baseline and world == 1:
-        # the same oracle with its phase loops over all host cores (OpenMP timing build,
-        # bitwise the plain oracle); a bounded sample like the single-core figure
-        sc = scene.to("cpu")
-        threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
-        k = 1
-        t = time_oracle(sc, k, omp=True)
-        if t < 5.0:
-            k = max(1, int(10.0 / max(t, 1e-3)))
-            t = time_oracle(sc, k, omp=True)
-        cpu_omp = {"value": sc.n_alloc * k / t, "unit": "voxel-updates/s", "cores": threads, "kind": "oracle (OpenMP)",
-                   "sample": f"{k} fp64 oracle iteration(s) over the whole {scene.name} volume, {t:.1f} s on "
-                             f"{threads} host threads ({platform_cpu()})"}
+        nf["roofline"] = hbm_roofline(nf["avg_launch_ms"], False)
+    cpus = cpu_baselines(scene) if (not args.no_cpu_baseline and world == 1) else {}
     line = {
         "metric": "voxel-updates/s", "value": value, "unit": "voxel-updates/s", "n_gpus": world,
         "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
@@ -783,7 +848,9 @@ def main():
                    "generation": ({"per_shard": True, "seconds": gen_s, "blocks_moved_at_rebalance": n_moved}
                                   if gen_s is not None else None),
                    "energy": {"primal": E[0], "dual": E[1]}},
-        "roofline": roofline, "cpu_baseline": cpu, "cpu_baseline_omp": cpu_omp, "e2e": e2e, "halo": halo, "gpu_launches": int(launches),
+        "omega_updates_per_s": n_omega_total * iters / (ms / 1e3),
+        "roofline": roofline, "cpu_baseline": cpus.get("cpu_baseline"), "cpu_baseline_omp": cpus.get("cpu_baseline_omp"),
+        "cpu_baseline_f32": cpus.get("cpu_baseline_f32"), "e2e": e2e, "halo": halo, "gpu_launches": int(launches),
         "freeze": bool(args.freeze), "no_freeze": nf,
         "clocks": clk, "fusion": fusion, "extraction": extraction, "stereo": stereo_res, "pipeline": pipeline,
     }
