@@ -14,7 +14,8 @@ run skew_nofreeze "-k regex:k_skew -s 150 -c 1" python scripts/skew_ab.py --iter
 run extract "-k regex:k_extract -s 6 -c 2" python scripts/extract_timing.py
 run fuse "-k regex:k_fuse_integrate -s 2 -c 1" python scripts/fuse_timing.py
 run stereo "-k regex:k_dual4|k_primal4 -s 200 -c 2" python scripts/stereo_timing.py
-B="python bench.py --steps 2 --warmup 3 --no-fusion --no-e2e --no-cpu-baseline"
-$B > gpurun_out/plain_bench.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-  --log-file gpurun_out/r02_launches.csv $B > gpurun_out/ncu_launches.log 2>&1
+B="python bench.py --steps 1 --warmup 3 --no-fusion --no-e2e --no-cpu-baseline"
+# launch list of one timed step (each step issues ~310 launches; skip the 3 warm-up steps)
+$B > gpurun_out/plain_bench.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -k regex:^k_ \
+  -s 940 -c 320 --csv --log-file gpurun_out/r02_launches.csv $B > gpurun_out/ncu_launches.log 2>&1
 echo "launches rc=$?" >> gpurun_out/r02_status.txt
