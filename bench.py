@@ -142,15 +142,14 @@ def issue_peak():
 
 
 def l2_peak():
-    """L2 (LTS) throughput cap: ~6300 B per SM clock full-chip (B300_MICROARCH.md, measured on B300; not
-    re-measured on B200) x the max SM clock."""
-    mhz = 1965.0
+    """L2 read bandwidth measured on this pool's B200 (profiles/l2_peak.json, scripts/probes/l2_bw.cu: a 64 MB
+    L2-resident buffer streamed by every SM); fallback: the ~6300 B/clk LTS cap of B300_MICROARCH.md."""
     try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
-            mhz = float(json.load(fh).get("sm_max_mhz", mhz))
+        with open(os.path.join(ROOT, "profiles", "l2_peak.json")) as fh:
+            d = json.load(fh)
+        return float(d["l2_read_gbs"]), "measured L2 read bandwidth (profiles/l2_peak.json)"
     except Exception:
-        pass
-    return 6300.0 * mhz * 1e6 / 1e9, f"6300 B/clk LTS cap (B300_MICROARCH.md, a B300 measurement) x {mhz:.0f} MHz"
+        return 6300.0 * 1965e6 / 1e9, "fallback: 6300 B/clk LTS cap (B300_MICROARCH.md) x 1965 MHz"
 
 
 def make_scene(cfg: str, world: int, seed: int, device):
@@ -431,12 +430,14 @@ def stereo_leg(args, dev):
     lp, lp_src = l2_peak()
     if nd and npr:
         px_launch = 2 * 1240 * 376   # one chunk of 2 frames per launch
-        l2b = (nd["lts_bytes"] + npr["lts_bytes"]) / px_launch
+        l2b = (nd["lts_tex_bytes"] + npr["lts_tex_bytes"]) / px_launch
         drb = (nd["dram_bytes"] + npr["dram_bytes"]) / px_launch
         l2a = l2b * npx / (it_ms / 1e3) / 1e9
         res["roofline"] = {"bound": "l2", "kernel": "k_dual4 + k_primal4 (one TGV iteration)", "achieved": l2a,
                            "peak": lp, "unit": "GB/s", "frac": l2a / lp, "peak_source": lp_src,
-                           "basis": "physical: ncu lts__t_sectors x 32 B per pixel-iteration x pixels / event time",
+                           "basis": "physical: ncu lts__t_sectors_srcunit_tex x 32 B (the SMs' L2 traffic) per "
+                                    "pixel-iteration x pixels / event time; ncu's DRAM bytes are cold-cache (flushed "
+                                    "before each replay), an upper bound for the L2-resident chunks",
                            "avg_launch_ms": it_ms, "l2_bytes_per_pixel_iter": l2b, "dram_bytes_per_pixel_iter": drb,
                            "dram_achieved": drb * npx / (it_ms / 1e3) / 1e9,
                            "traffic": drb * npx, "sources": [nd["source"], npr["source"]]}

@@ -16,7 +16,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "profiles", "ncu_inputs.json")
 METRICS = {"dram__bytes_read.sum": "dram_read_bytes", "dram__bytes_write.sum": "dram_write_bytes",
-           "lts__t_sectors.sum": "lts_sectors", "smsp__inst_executed.sum": "warp_instructions",
+           "lts__t_sectors.sum": "lts_sectors", "lts__t_sectors_srcunit_tex.sum": "lts_tex_sectors", "smsp__inst_executed.sum": "warp_instructions",
            "gpu__time_duration.sum": "duration_us", "launch__grid_size": "grid"}
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0,
          "msecond": 1e3, "ms": 1e3, "second": 1e6, "sector": 1, "inst": 1, "": 1}
@@ -41,7 +41,8 @@ def read(report, kernel_re):
         raise SystemExit(f"{report}: no launch of {kernel_re}")
     r = {k: v / n for k, v in acc.items()}
     r["dram_bytes"] = r.get("dram_read_bytes", 0) + r.get("dram_write_bytes", 0)
-    r["lts_bytes"] = 32 * r.pop("lts_sectors", 0)
+    r["lts_bytes"] = 32 * r.pop("lts_sectors", 0)               # all L2 tag traffic (incl. cross-die fabric)
+    r["lts_tex_bytes"] = 32 * r.pop("lts_tex_sectors", 0)       # requests from the SMs (L1 / TMA)
     r["launches_captured"] = n
     r["source"] = os.path.relpath(report, ROOT)
     return r
