@@ -24,7 +24,6 @@ inline int counted(int r) {
 
 constexpr int kBlockVox = 512;     // 8^3 voxels per block
 constexpr int kThreads = 128;      // CTA size of the per-block kernels: 4 voxels per thread
-constexpr int kFrozenStride = 20;  // words per row of the frozen mask: 16 bit words, the static flag, pad (80 B)
 constexpr int kNbr = 12;           // 6 face neighbours (−x,+x,−y,+y,−z,+z) + 6 edge (diagonal) neighbours
 // Edge neighbours read by the −face halo recompute, as block-coordinate offsets (iterate.cu):
 //   6: (−1,+1,0)  7: (−1,0,+1)  8: (+1,−1,0)  9: (0,−1,+1)  10: (+1,0,−1)  11: (0,+1,−1)
@@ -97,9 +96,7 @@ int launch_neighbours(const int32_t *xyz, int64_t n, const uint32_t *start, cons
 int launch_validate(const float *f, const float *W, int64_t nvox, unsigned long long *bad,
                     unsigned long long *n_omega, cudaStream_t s);
 int launch_init_state(const Fields &F, int64_t nvox, int init, cudaStream_t s);
-// frozen[row * kFrozenStride + w] bit b (w < 16): voxel 32w + b of the row has an identity primal step for
-// this call (L1 only); frozen[row * kFrozenStride + 16] != 0: no voxel of the row can change (every voxel
-// frozen or Ω̄), so u = f on the whole block (a "static" block)
+// frozen[row][w] bit b: voxel 32w + b of the row has an identity primal step for this call (L1 only)
 int launch_freeze_mask(const Fields &F, int cur, const IterParams &P, int64_t n_blocks, uint32_t *frozen,
                        cudaStream_t s);
 // W8[i] = W[i] for W integer in [0, 255]; *bad = 1 if some W is not (W8 then unusable)

@@ -385,7 +385,6 @@ __global__ void k_freeze_mask(Fields F, int cur, IterParams P, uint32_t *__restr
     const int64_t b = blockIdx.x;
     const float *ubc = cur ? F.ub[1] : F.ub[0];
     const float *ubo = cur ? F.ub[0] : F.ub[1];
-    bool all_static = true;
 #pragma unroll
     for (int j = 0; j < 4; j++) {
         const int i = threadIdx.x + 128 * j;
@@ -397,16 +396,9 @@ __global__ void k_freeze_mask(Fields F, int cur, IterParams P, uint32_t *__restr
         const uint32_t fb = __float_as_uint(fv);
         const bool fz = P.data_term == 0 && w > 0.0f && t >= bound && fb != 0x80000000u &&
                         __float_as_uint(F.u[v]) == fb && __float_as_uint(ubc[v]) == fb && __float_as_uint(ubo[v]) == fb;
-        // Ω̄ voxels are never written: u = f in every u buffer (both skewed-schedule buffers start as u)
-        all_static &= fz || !(w > 0.0f);
         const unsigned m = __ballot_sync(0xffffffffu, fz);
-        if ((threadIdx.x & 31) == 0) frozen[b * kFrozenStride + (i >> 5)] = m;
+        if ((threadIdx.x & 31) == 0) frozen[b * 16 + (i >> 5)] = m;
     }
-    // the block is static iff every voxel is frozen or Ω̄ *and* holds u = f (Ω̄ voxels under the zero init
-    // keep u = f too: init only zeroes Ω voxels); k_skew then reads its u^k from f (an L2 hit: the same
-    // 2 KiB the block's f copy just fetched) instead of from the u buffer
-    const int st = __syncthreads_and(all_static);
-    if (threadIdx.x == 0) frozen[b * kFrozenStride + 16] = st ? 1u : 0u;
 }
 
 int launch_freeze_mask(const Fields &F, int cur, const IterParams &P, int64_t n_blocks, uint32_t *frozen,

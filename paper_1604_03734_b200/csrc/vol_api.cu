@@ -91,7 +91,7 @@ static void carve_all(Carve &c, vol_s *v, const Layout &L) {
     auto scan = c.take<uint32_t>((size_t)L.T / 4096 + 4);
     auto nbr = c.take<int32_t>(kNbr * (size_t)L.S);
     auto w8 = c.take<uint8_t>((size_t)L.S * kBlockVox + 16);
-    auto frozen = c.take<uint32_t>((size_t)L.n_local * kFrozenStride + 16);
+    auto frozen = c.take<uint32_t>((size_t)L.n_local * 16 + 16);
     auto perm = c.take<int32_t>((size_t)L.n_local + 1);
     auto tmp = c.take<float>((size_t)L.n_local * kBlockVox + 4);
     auto u2 = c.take<float>((size_t)L.S * kBlockVox + 4);   // second u buffer of the skewed schedule
