@@ -58,22 +58,18 @@ __device__ __forceinline__ CellGeom cell_geom(int ox, int oy, int oz, float voxe
 }
 
 // X-4: vertex on the edge between cell corners ca and cb (values ua, ub).  The ends are ordered by global
-// voxel coordinate, lexicographically in (x, y, z); inside one cell that is the order of the offsets.
-// t = u_lo/(u_lo − u_hi), p = P_lo + t·(P_hi − P_lo) per coordinate, in fp32 (the oracle's written order).
+// voxel coordinate, lexicographically in (x, y, z).  The corners of a Freudenthal tetrahedron are nested
+// (000 ⊂ e_a ⊂ e_a + e_b ⊂ 111), so of any two corners one is a bitwise subset of the other — the lower end,
+// lexicographically first as well: lo = ca & cb, and the axes where the ends differ are d = ca ^ cb.
+// t = u_lo/(u_lo − u_hi), p = P_lo + t·(P_hi − P_lo) per coordinate, in fp32 (the oracle's written order):
+// on an axis in d, P_lo = X[0] and P_hi − P_lo = dX; elsewhere p = P_lo exactly.
 __device__ __forceinline__ void edge_vertex(const CellGeom &G, int ca, float ua, int cb, float ub, float *p) {
-    const int ax = ca & 1, ay = (ca >> 1) & 1, az = ca >> 2;
-    const int bx = cb & 1, by = (cb >> 1) & 1, bz = cb >> 2;
-    const bool swap = ax != bx ? bx < ax : (ay != by ? by < ay : bz < az);
-    const int cl = swap ? cb : ca, ch = swap ? ca : cb;
-    const float ulo = swap ? ub : ua, uhi = swap ? ua : ub;
+    const int lo = ca & cb, d = ca ^ cb;
+    const float ulo = lo == ca ? ua : ub, uhi = lo == ca ? ub : ua;
     const float t = __fdiv_rn(ulo, __fsub_rn(ulo, uhi));
 #pragma unroll
-    for (int k = 0; k < 3; k++) {
-        const int al = (cl >> k) & 1, ah = (ch >> k) & 1;
-        const float plo = al ? G.X[1][k] : G.X[0][k];
-        const float d = ah ? G.dX[k] : -G.dX[k];
-        p[k] = al == ah ? plo : __fadd_rn(plo, __fmul_rn(t, d));
-    }
+    for (int k = 0; k < 3; k++)
+        p[k] = ((d >> k) & 1) ? __fadd_rn(G.X[0][k], __fmul_rn(t, G.dX[k])) : G.X[(lo >> k) & 1][k];
 }
 
 // X-6: a triangle is dropped iff its area is zero in exact arithmetic, decided on the corner values (an
@@ -94,9 +90,6 @@ __device__ __forceinline__ void put(float *out, unsigned &m, const float *p0, co
     m++;
 }
 
-__device__ __forceinline__ int sel4(int i, int a0, int a1, int a2, int a3) {
-    return i == 0 ? a0 : (i == 1 ? a1 : (i == 2 ? a2 : a3));
-}
 __device__ __forceinline__ float sel4f(int i, float a0, float a1, float a2, float a3) {
     return i == 0 ? a0 : (i == 1 ? a1 : (i == 2 ? a2 : a3));
 }
@@ -132,8 +125,9 @@ __device__ __forceinline__ void tet(int k0, int k1, int k2, int k3, float v0, fl
         pc = (a & 1) ? r2 : r1;
         pd = (a & 1) ? r1 : r2;
     }
-    const int ca = sel4(pa, k0, k1, k2, k3), cb = sel4(pb, k0, k1, k2, k3);
-    const int cc = sel4(pc, k0, k1, k2, k3), cd = sel4(pd, k0, k1, k2, k3);
+    const int packed = k0 | (k1 << 4) | (k2 << 8) | (k3 << 12);   // corner code of position i at bits 4i
+    const int ca = (packed >> (4 * pa)) & 15, cb = (packed >> (4 * pb)) & 15;
+    const int cc = (packed >> (4 * pc)) & 15, cd = (packed >> (4 * pd)) & 15;
     const float ua = sel4f(pa, v0, v1, v2, v3), ub = sel4f(pb, v0, v1, v2, v3);
     const float uc = sel4f(pc, v0, v1, v2, v3), ud = sel4f(pd, v0, v1, v2, v3);
     float e1[3], e2[3], e3[3];
@@ -191,7 +185,8 @@ __global__ void __launch_bounds__(128) k_extract(ExArgs A, int64_t n_rows, uint3
     // emit pass: one round's triangles (≤ 2 per item) staged here, then written out by the whole CTA
     // with consecutive lanes on consecutive floats (coalesced) instead of 9 scattered 4-byte stores
     // per triangle 36 B apart
-    __shared__ float sout[EMIT ? 2 * 128 * 9 : 1];
+    __shared__ float sout[EMIT ? 2 * 128 * 9 : 1];   // 4 warp slices of 2 triangles x 32 lanes
+    __shared__ uint32_t goff[EMIT ? kMaxItems / 32 : 1];   // triangle offset of each 32-item group
     const int64_t r = blockIdx.x;
     if (r >= n_rows) return;
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
@@ -274,46 +269,75 @@ __global__ void __launch_bounds__(128) k_extract(ExArgs A, int64_t n_rows, uint3
         sitem[pos++] = (uint16_t)(((4 * t + q) << 3) | k);
     }
     __syncthreads();
-    // (B) items round-robin: item i = t + 128·round, in list order
-    uint32_t run = 0;            // EMIT: triangles written by the earlier rounds
+    // (B) items in list order.  Count pass: round-robin, item i = t + 128·round, 2 count bits per item
+    // stored per 32-item group (ballots).  Emit pass: the group totals (popcounts of those bits) are scanned
+    // once per block; then each warp takes whole groups (w, w + 4, …), places its lanes' triangles with a
+    // warp scan at the group's offset, stages them in its own slice of shared memory and writes them out
+    // with consecutive lanes on consecutive floats — no block-wide barrier inside the loop.
     uint32_t block_total = 0;    // count pass: triangles of this thread's items
-    float *base_out = EMIT ? out + 9ull * offsets[ci] : nullptr;
-    for (uint32_t i0 = 0; i0 < n_items; i0 += 128) {
-        const uint32_t i = i0 + t;
-        int cell = 0, k = 0;
-        if (i < n_items) {
-            cell = sitem[i] >> 3;
-            k = sitem[i] & 7;
+    if (EMIT) {
+        const uint32_t ng = (n_items + 31) / 32;   // <= kMaxItems / 32 = 96
+        const uint32_t *wbb = item_bits + (size_t)r * kItemWords;
+        if (wid == 0) {
+            uint32_t c3[3], sum = 0;
+#pragma unroll
+            for (int j = 0; j < 3; j++) {
+                const uint32_t g = 3 * lane + j;
+                c3[j] = g < ng ? __popc(wbb[2 * g]) + 2 * __popc(wbb[2 * g + 1]) : 0u;
+                sum += c3[j];
+            }
+            uint32_t inc = sum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+            uint32_t ex = inc - sum;
+#pragma unroll
+            for (int j = 0; j < 3; j++) {
+                goff[3 * lane + j] = ex;
+                ex += c3[j];
+            }
         }
-        const int cx = cell & 7, cyy = (cell >> 3) & 7, czz = cell >> 6;
-        const int k1 = tet_code(k, 1), k2 = tet_code(k, 2), k3 = tet_code(k, 3);
-        if (EMIT) {
-            const uint32_t *wb = item_bits + (size_t)r * kItemWords + 2 * ((i0 >> 5) + wid);
-            const uint32_t cnt = i < n_items ? (((wb[0] >> lane) & 1u) | (((wb[1] >> lane) & 1u) << 1)) : 0u;
-            // block-exclusive scan of this round's counts (list order = thread order)
+        __syncthreads();
+        float *wsout = sout + wid * (2 * 32 * 9);
+        float *base_out = out + 9ull * offsets[ci];
+        for (uint32_t g = wid; g < ng; g += 4) {
+            const uint32_t i = 32 * g + lane;
+            const uint32_t w0 = wbb[2 * g], w1 = wbb[2 * g + 1];
+            const uint32_t cnt = i < n_items ? (((w0 >> lane) & 1u) | (((w1 >> lane) & 1u) << 1)) : 0u;
             uint32_t y = cnt;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t z = __shfl_up_sync(0xffffffffu, y, o);
                 if (lane >= o) y += z;
             }
-            __syncthreads();
-            if (lane == 31) swarp[wid] = y;
-            __syncthreads();
-            uint32_t before = y - cnt;
-            for (int w = 0; w < wid; w++) before += swarp[w];
-            const uint32_t round_total = swarp[0] + swarp[1] + swarp[2] + swarp[3];
+            const uint32_t gtot = __shfl_sync(0xffffffffu, y, 31);
             if (cnt) {
+                const int cell = sitem[i] >> 3, k = sitem[i] & 7;
+                const int cx = cell & 7, cyy = (cell >> 3) & 7, czz = cell >> 6;
+                const int k1 = tet_code(k, 1), k2 = tet_code(k, 2), k3 = tet_code(k, 3);
                 unsigned m = 0;
                 const CellGeom G = cell_geom(gx + cx, gy + cyy, gz + czz, A.voxel);
                 tet<true>(0, k1, k2, k3, su[tile_index(cx, cyy, czz, 0)], su[tile_index(cx, cyy, czz, k1)],
-                          su[tile_index(cx, cyy, czz, k2)], su[tile_index(cx, cyy, czz, k3)], G, sout + 9 * before, m);
+                          su[tile_index(cx, cyy, czz, k2)], su[tile_index(cx, cyy, czz, k3)], G,
+                          wsout + 9 * (y - cnt), m);
             }
-            __syncthreads();
-            float *dst = base_out + 9ull * run;
-            for (uint32_t j = t; j < 9 * round_total; j += 128) dst[j] = sout[j];
-            run += round_total;
-        } else {
+            __syncwarp();
+            float *dst = base_out + 9ull * goff[g];
+            for (uint32_t j = lane; j < 9 * gtot; j += 32) dst[j] = wsout[j];
+            __syncwarp();
+        }
+    } else {
+        for (uint32_t i0 = 0; i0 < n_items; i0 += 128) {
+            const uint32_t i = i0 + t;
+            int cell = 0, k = 0;
+            if (i < n_items) {
+                cell = sitem[i] >> 3;
+                k = sitem[i] & 7;
+            }
+            const int cx = cell & 7, cyy = (cell >> 3) & 7, czz = cell >> 6;
+            const int k1 = tet_code(k, 1), k2 = tet_code(k, 2), k3 = tet_code(k, 3);
             unsigned m = 0;
             if (i < n_items)
                 tet<false>(0, k1, k2, k3, su[tile_index(cx, cyy, czz, 0)], su[tile_index(cx, cyy, czz, k1)],
