@@ -309,3 +309,87 @@ def test_gloo_skewed_schedule_needs_the_p_halo():
     res = _run(_skew_worker, 2, False)
     assert all(not isinstance(r[1], str) for r in res), res
     assert not all(r[1] for r in res)
+
+
+def _gid_worker(rank, world, port, q):
+    """The binding's per-group NCCL unique id (volume._group_nccl_id): one id per live group, shared by all
+    its ranks, a different id for a new group — even one created after the first is destroyed (weak keys
+    plus the group's name and ranks; an id() key could hand the new group the old id)."""
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_1604_03734_b200 import volume
+        g1 = dist.new_group(list(range(world)))
+        a = volume._group_nccl_id(g1, "cpu")
+        a2 = volume._group_nccl_id(g1, "cpu")
+        dist.destroy_process_group(g1)
+        del g1
+        g2 = dist.new_group(list(range(world)))
+        b = volume._group_nccl_id(g2, "cpu")
+        ids = [None] * world
+        dist.all_gather_object(ids, (a, b))
+        ok = a == a2 and a != b and all(x == (a, b) for x in ids)
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, ok, 0))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put((rank, f"error: {e!r}", 0))
+
+
+def test_group_unique_id_per_live_group():
+    from paper_1604_03734_b200 import build
+    build.build()
+    res = _run(_gid_worker, 2)
+    assert all(r[1] is True for r in res), res
+
+
+def _gen_worker(rank, world, port, q):
+    """bench.py's per-shard generation under torch.distributed (here gloo on the CPU): each rank generates
+    the candidates of its arc range, all-gathers the allocated coordinates, takes the exact route partition
+    and regenerates the blocks that changed owner.  The union over ranks must equal the single-process
+    scene, block for block, and the owner map must be vol_partition_route of the whole block set."""
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import bench
+        from paper_1604_03734_b200 import partition_route
+        from synth import scenes
+        plan = scenes.city_plan(0, length=6.0, device="cpu")
+        c_r, f_r, W_r = bench.shard_generate(plan, world, rank, chunk_blocks=512)
+        allc = bench.gather_coords(c_r, world, torch.device("cpu"))
+        sh = bench.shard_assemble(plan, world, rank, allc, c_r, f_r, W_r, chunk_blocks=512)
+        mine = torch.from_numpy(sh["part"] == rank)
+        ok = np.array_equal(sh["part"], partition_route(sh["coords"], plan.route, plan.block_edge, world))
+        fs = [None] * world
+        dist.all_gather_object(fs, (sh["f"].numpy(), sh["W"].numpy()))
+        if rank == 0:
+            whole = scenes.city(0, length=6.0, chunk_blocks=512)
+            coords = sh["coords"]
+            f = torch.empty(coords.shape[0], 512)
+            W = torch.empty(coords.shape[0], 512)
+            for r, (fr, Wr) in enumerate(fs):
+                m = torch.from_numpy(sh["part"] == r)
+                f[m], W[m] = torch.from_numpy(fr), torch.from_numpy(Wr)
+            key = lambda c: (c[:, 0].long() * 65536 + c[:, 1].long()) * 65536 + c[:, 2].long()
+            i1, i2 = torch.argsort(key(coords)), torch.argsort(key(whole.coords))
+            ok = ok and torch.equal(coords[i1], whole.coords[i2]) and torch.equal(f[i1], whole.f[i2]) \
+                and torch.equal(W[i1], whole.W[i2])
+        ok = ok and bool(mine.any())
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, ok, int(sh["moved"])))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put((rank, f"error: {e!r}", 0))
+
+
+def test_bench_per_shard_generation_gloo():
+    from paper_1604_03734_b200 import build
+    build.build()
+    res = _run(_gen_worker, 2)
+    assert all(r[1] is True for r in res), res
