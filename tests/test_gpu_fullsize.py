@@ -281,3 +281,27 @@ def test_city_shard_generation_equals_whole_scene(V):
         assert torch.equal(f[i1], s.f[i2]) and torch.equal(W[i1], s.W[i2])
         part = partition_route(coords, s.meta["route"], 8 * s.meta["voxel"], world)
         assert np.array_equal(got[0]["part"], part)
+
+
+def test_street_outlier_route_shards_match_oracle(V):
+    """Config 3 (street-outlier: ≥ 30 % of the voxels unobserved in 1 m³ clumps, impulse outliers, TV-L1,
+    500 iterations) on 4 route shards (vol_partition_route along the street's camera path), the product
+    schedule with freeze, loopback transport: every voxel bit-identical to the fp32 oracle after all 500
+    iterations — the sharded path with frozen voxels, Ω̄ clumps cut by the shard boundaries and the L1
+    prox (SURVEY §8(c) pin (viii), §8(e))."""
+    from paper_1604_03734_b200 import connect_group, partition_route, regularise_group
+    s = _scene("street-outlier")
+    world = 4
+    part = torch.from_numpy(partition_route(s.coords, s.meta["route"], 8 * s.meta["voxel"], world))
+    vols = []
+    for r in range(world):
+        mine = (part == r).nonzero().squeeze(1)
+        vols.append(V(s.coords.cuda(), s.f[mine].cuda(), s.W[mine].cuda(), part=part, loopback=(r, world)))
+    connect_group(vols)
+    regularise_group(vols, s.lam, s.eps, s.tau, s.sigma, s.iters, data_term=s.data_term)
+    u = np.empty((s.n_blocks, 512), np.float32)
+    for r, v in enumerate(vols):
+        u[(part == r).numpy()] = v.u().cpu().numpy()
+    u32, _, _ = oracle.regularise(s.coords, s.f, s.W, s.lam, s.eps, s.tau, s.sigma, s.iters, theta=s.theta,
+                                  data_term=s.data_term, init=s.init, precision="f32", omp=True)
+    assert np.array_equal(u.view(np.uint32), u32.view(np.uint32))
