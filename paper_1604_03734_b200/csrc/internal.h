@@ -96,7 +96,8 @@ int launch_neighbours(const int32_t *xyz, int64_t n, const uint32_t *start, cons
 int launch_validate(const float *f, const float *W, int64_t nvox, unsigned long long *bad,
                     unsigned long long *n_omega, cudaStream_t s);
 int launch_init_state(const Fields &F, int64_t nvox, int init, cudaStream_t s);
-// frozen[row][w] bit b: voxel 32w + b of the row has an identity primal step for this call (L1 only)
+// frozen: 64 bytes per row, byte c (column c = x + 8y) bit z set iff voxel c + 64z has an identity primal step
+// for this call (L1 only)
 int launch_freeze_mask(const Fields &F, int cur, const IterParams &P, int64_t n_blocks, uint32_t *frozen,
                        cudaStream_t s);
 // W8[i] = W[i] for W integer in [0, 255]; *bad = 1 if some W is not (W8 then unusable)

@@ -381,24 +381,31 @@ int launch_pack_w8(const float *W, uint8_t *W8, int64_t nvox, unsigned *bad, cud
 // t >= τ(3+√3)(1 + 2^-19) + |f|·2^-22 guarantees u' = f and then ū' = f + θ·(f − f) = f, at every
 // iteration of the call.  A voxel that satisfies it with u = ū = f in both ū buffers at the start of the
 // call therefore never changes during the call; the fused kernel skips its primal step and stores.
+// Layout of a row's 64 bytes: byte c (column c = x + 8y) holds bit z for voxel c + 64z — the layout the
+// iteration kernels read, where a thread owns one column and a run of z (one byte load per thread).
 __global__ void k_freeze_mask(Fields F, int cur, IterParams P, uint32_t *__restrict__ frozen) {
+    __shared__ uint32_t part[128];
     const int64_t b = blockIdx.x;
+    const int t = threadIdx.x;
     const float *ubc = cur ? F.ub[1] : F.ub[0];
     const float *ubo = cur ? F.ub[0] : F.ub[1];
+    uint32_t bits = 0;
 #pragma unroll
     for (int j = 0; j < 4; j++) {
-        const int i = threadIdx.x + 128 * j;
+        const int i = t + 128 * j;   // column t & 63, z = (t >> 6) + 2j
         const int64_t v = b * 512 + i;
         const float fv = F.f[v], w = F.W[v];
-        const float t = P.tl * w;
+        const float tt = P.tl * w;
         const float bound = P.tau * (4.7320508f * 1.0000019f) + fabsf(fv) * 2.3841858e-7f;
         // bitwise equality, and f ≠ −0 (ū' = f + (+0) would turn −0 into +0)
         const uint32_t fb = __float_as_uint(fv);
-        const bool fz = P.data_term == 0 && w > 0.0f && t >= bound && fb != 0x80000000u &&
+        const bool fz = P.data_term == 0 && w > 0.0f && tt >= bound && fb != 0x80000000u &&
                         __float_as_uint(F.u[v]) == fb && __float_as_uint(ubc[v]) == fb && __float_as_uint(ubo[v]) == fb;
-        const unsigned m = __ballot_sync(0xffffffffu, fz);
-        if ((threadIdx.x & 31) == 0) frozen[b * 16 + (i >> 5)] = m;
+        bits |= (fz ? 1u : 0u) << (i >> 6);
     }
+    part[t] = bits;
+    __syncthreads();
+    if (t < 64) reinterpret_cast<uint8_t *>(frozen + b * 16)[t] = (uint8_t)(part[t] | part[t + 64]);
 }
 
 int launch_freeze_mask(const Fields &F, int cur, const IterParams &P, int64_t n_blocks, uint32_t *frozen,
