@@ -36,7 +36,6 @@ struct Fields {
     float *ub[2];          // relaxed primal ū, double-buffered
     float *px[2], *py[2], *pz[2];  // dual p, double-buffered
     float *u2 = nullptr;           // second u buffer of the skewed schedule
-    int32_t zero_row = -1;         // the all-zero row after the S store rows of every field (vol_api.cu carve_all)
 };
 
 // The buffers of one iteration, selected on the host (no dynamic indexing in kernels).

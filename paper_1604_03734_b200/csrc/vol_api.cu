@@ -68,10 +68,8 @@ bool is_device_ptr(const void *p) {
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
-// Every field has one extra row after the S store rows: the all-zero row (zeroed at create, never written),
-// which k_skew reads in place of an absent neighbour block (W = 0 ⇒ Ω̄, p = 0) instead of masking its loads.
 static void carve_all(Carve &c, vol_s *v, const Layout &L) {
-    const int64_t nv = (L.S + 1) * kBlockVox;
+    const int64_t nv = L.S * kBlockVox;
     float *fields[11];
     for (int k = 0; k < 11; k++) fields[k] = c.take<float>(nv);
     if (v) {
@@ -92,11 +90,11 @@ static void carve_all(Carve &c, vol_s *v, const Layout &L) {
     auto entry = c.take<int32_t>((size_t)L.n_global + 1);
     auto scan = c.take<uint32_t>((size_t)L.T / 4096 + 4);
     auto nbr = c.take<int32_t>(kNbr * (size_t)L.S);
-    auto w8 = c.take<uint8_t>((size_t)(L.S + 1) * kBlockVox + 16);
+    auto w8 = c.take<uint8_t>((size_t)L.S * kBlockVox + 16);
     auto frozen = c.take<uint32_t>((size_t)L.n_local * 16 + 16);
     auto perm = c.take<int32_t>((size_t)L.n_local + 1);
     auto tmp = c.take<float>((size_t)L.n_local * kBlockVox + 4);
-    auto u2 = c.take<float>((size_t)(L.S + 1) * kBlockVox + 4);   // second u buffer of the skewed schedule
+    auto u2 = c.take<float>((size_t)L.S * kBlockVox + 4);   // second u buffer of the skewed schedule
     auto misc = c.take<unsigned long long>(4);
     auto part = c.take<double>(5 * (size_t)L.S + 5);
     auto eout = c.take<double>(8);
@@ -117,7 +115,6 @@ static void carve_all(Carve &c, vol_s *v, const Layout &L) {
         v->d_part = part;
         v->d_eout = eout;
         v->F.u2 = u2;
-        v->F.zero_row = (int32_t)L.S;
     }
 }
 
@@ -292,16 +289,6 @@ static vol_status create_impl(const int32_t *block_xyz, int64_t n_global, const 
     carve_all(c, v, L);
     v->extra = c.base + ((c.off + 255) & ~(size_t)255);
     cudaStream_t s = v->stream;
-    {   // the zero row of every field (see carve_all)
-        const size_t zoff = (size_t)L.S * kBlockVox;
-        float *zf[] = {const_cast<float *>(v->F.f), const_cast<float *>(v->F.W), v->F.u, v->F.ub[0], v->F.ub[1],
-                       v->F.px[0], v->F.px[1], v->F.py[0], v->F.py[1], v->F.pz[0], v->F.pz[1], v->d_u2};
-        for (float *p : zf)
-            if (cudaMemsetAsync(p + zoff, 0, kBlockVox * 4, s) != cudaSuccess)
-                return bail(fail(VOL_ECUDA, "zero-row memset failed"));
-        if (cudaMemsetAsync(v->d_w8 + zoff, 0, kBlockVox, s) != cudaSuccess)
-            return bail(fail(VOL_ECUDA, "zero-row memset failed"));
-    }
 
     // store order: Morton order of the blocks (single GPU) or the shard plan's [launch A | launch B]
     // rows + ghosts; row_caller[r] is the block's index in the caller's f / W / u arrays
