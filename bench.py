@@ -767,8 +767,37 @@ def main():
         w_u8 = bool(((Wc == Wc.round()) & (Wc >= 0) & (Wc <= 255)).all())
         hW = (Wc.to(torch.uint8) if w_u8 else Wc).pin_memory()
         hu = torch.empty(u_out.shape, dtype=torch.float32).pin_memory()
+        hus = [hu, torch.empty_like(hu).pin_memory()]
+
+        def e2e_pipelined(nsteps):
+            ss = [stream, torch.cuda.Stream(dev)]
+            start, end, join = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+
+            def make(i):
+                v = Volume(hc, hf, hW, stream=ss[i % 2], **kw)
+                v.regularise(scene.lam, scene.eps, scene.tau, scene.sigma, iters, theta=scene.theta,
+                             data_term=scene.data_term, init=scene.init, kernel=args.kernel, freeze=bool(args.freeze))
+                return v
+            barrier()
+            start.record(ss[0])
+            ss[1].wait_event(start)
+            v = make(0)
+            for i in range(nsteps):
+                nxt = make(i + 1) if i + 1 < nsteps else None
+                v.energy(scene.lam, scene.eps, scene.data_term)
+                v.read_u(hus[i % 2])
+                v.close()
+                v = nxt
+            join.record(ss[1])
+            ss[0].wait_event(join)
+            end.record(ss[0])
+            barrier()
+            return start.elapsed_time(end) / nsteps
+
         for _ in range(2):
             step(hc, hf, hW, hu, False)
+        if not sharded:
+            e2e_pipelined(2)   # warm-up of the pipelined form
         barrier()
         t0.record(stream)
         for _ in range(args.steps):
@@ -783,7 +812,17 @@ def main():
         d2h = hu.numel() * 4 + 5 * 8
         e2e = {"value": n_alloc_total * iters / (ems / 1e3), "unit": "voxel-updates/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": ems,
-               "w_host_dtype": "u8" if w_u8 else "f32"}
+               "w_host_dtype": "u8" if w_u8 else "f32", "mode": "serial: one step at a time on one stream"}
+        if not sharded:
+            # The same steps pipelined over two streams, the way a caller processing a stream of volumes uses
+            # the API: step i+1's host-to-device copies and volume build are issued while step i iterates,
+            # and step i's energy and u read-back while step i+1 iterates.  Every step still copies its
+            # inputs from pinned host memory and reads its result back inside the timed region.
+            pms = e2e_pipelined(args.steps)
+            e2e["serial"] = {"value": e2e["value"], "ms_per_step": ems}
+            e2e.update({"value": n_alloc_total * iters / (pms / 1e3), "ms_per_step": pms,
+                        "mode": "pipelined: two streams, step i+1's H2D + build and step i's energy + D2H "
+                                "overlap the iterations"})
 
     fusion = None
     if not args.no_fusion and world == 1:
