@@ -189,6 +189,32 @@ vol_status vol_regularise_group(vol_t *handles, int world, float lambda, float e
 vol_status vol_group_energy(vol_t *handles, int world, float lambda, float eps, int data_term, double *primal,
                             double *dual);
 
+/* Direct-store halo transport (the paper's "boundary conditions" of a block taken from its
+ * neighbours, fetched across GPUs).  A sharded volume whose peers are all connected writes,
+ * in its boundary launch, the (u, p) of every block a peer reads straight into that peer's ghost rows
+ * (peer memory over NVLink; in one process, another volume's workspace) and signals a per-source counter
+ * in the peer's memory; the peer waits for it before its own boundary launch.  No pack, no NCCL, no
+ * unpack inside the loop; results are bit-identical to the other transports.  Collective: every rank
+ * connects every peer it exchanges with, and all ranks use the transport for the same calls.
+ *   vol_peer_info(v, info, cap, &n)  this rank's descriptor for its peers (n int64: ranks, sizes,
+ *                                    receive offsets, byte offsets of the field buffers and counters
+ *                                    inside the workspace); info = NULL queries n.
+ *   vol_connect_peer(v, q, ws, info, n)   register peer q whose workspace is mapped at device address
+ *                                    `ws` in this process (its vol_peer_info in `info`); peers this rank
+ *                                    has no halo with are ignored.  After the last needed peer the
+ *                                    volume switches to direct stores (vol_transport = 3).
+ *   vol_ipc_handle(v, handle64, &off) the CUDA IPC handle (64 bytes) of the allocation holding this
+ *                                    volume's workspace and the workspace's offset inside it;
+ *   vol_connect_peer_ipc(v, q, handle64, off, info, n)  opens it (cudaIpcOpenMemHandle, NVLink peer
+ *                                    access) and connects peer q; the mapping is closed by vol_destroy.
+ *   vol_transport(v)                 0 unsharded, 1 NCCL, 2 loopback copies, 3 direct stores.        */
+vol_status vol_peer_info(vol_t v, int64_t *info, int64_t cap, int64_t *n);
+vol_status vol_connect_peer(vol_t v, int peer, void *peer_workspace, const int64_t *info, int64_t n);
+vol_status vol_ipc_handle(vol_t v, void *handle64, int64_t *offset);
+vol_status vol_connect_peer_ipc(vol_t v, int peer, const void *handle64, int64_t offset, const int64_t *info,
+                                int64_t n);
+int vol_transport(vol_t v);
+
 /* Host-only helpers (no GPU needed), used by the sharding planner tests -------------------------- */
 
 /* The block hash of vol_create (no device work). */

@@ -60,7 +60,8 @@ EXPORTS = [
     "vol_group_energy", "vol_block_hash", "vol_plan_shard", "vol_total_launches", "vol_fuse_workspace_bytes",
     "vol_fuse", "vol_fuse_incremental", "vol_extract", "vol_stereo_default_params", "vol_stereo_workspace_bytes", "vol_stereo",
     "vol_stereo_census", "vol_stereo_tensor", "vol_disparity_to_depth", "vol_shard_timing", "vol_create_w8",
-    "vol_partition_route", "vol_release_comms",
+    "vol_partition_route", "vol_release_comms", "vol_peer_info", "vol_connect_peer", "vol_ipc_handle",
+    "vol_connect_peer_ipc", "vol_transport",
 ]
 
 _lib = None
@@ -101,6 +102,11 @@ def lib() -> ctypes.CDLL:
         "vol_total_launches": (i64, []),
         "vol_partition_route": (st, [P, i64, P, i32, ctypes.c_double, c_int, P, P]),
         "vol_release_comms": (st, []),
+        "vol_peer_info": (st, [P, P, i64, P]),
+        "vol_connect_peer": (st, [P, c_int, P, P, i64]),
+        "vol_ipc_handle": (st, [P, P, P]),
+        "vol_connect_peer_ipc": (st, [P, c_int, P, i64, P, i64]),
+        "vol_transport": (c_int, [P]),
         "vol_shard_timing": (st, [P, P, P, P]),
         "vol_extract": (st, [P, c_int, f32, f32, P, i64, P]),
         "vol_fuse_incremental": (st, [P, P, P, i64, P, i32, ctypes.POINTER(vol_camera), P,

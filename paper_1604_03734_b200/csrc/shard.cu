@@ -15,6 +15,8 @@
 // result (no reduction crosses GPUs inside the iteration).
 // Transports: NCCL point-to-point, or for tests on one GPU a loopback of device-to-device copies
 // between handles of one process (vol_group_connect / vol_regularise_group / vol_group_energy).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -31,6 +33,7 @@
 #include <vector>
 
 #include "handle.h"
+#include "peer.cuh"
 #include "shard.h"
 
 using namespace hvg;
@@ -295,6 +298,20 @@ struct ShardRuntime {
     unsigned long long *omega = nullptr;  // [2] device scratch for the Ω count all-reduce
     bool connected = false;
     bool graphs = true;              // capture the skewed loop into a CUDA graph (HVG_SHARD_NO_GRAPH=1: eager)
+    // direct-store transport (peer.cuh): connected peers, their mapped buffers, destinations, counters
+    bool p2p = false;
+    std::vector<int> peers;                          // ranks this rank exchanges with (send_cnt > 0)
+    std::vector<int64_t> peer_slot;                  // [world] slot of a connected peer, −1
+    std::vector<PeerOut> peer_out;                   // [slot]
+    std::vector<std::vector<int64_t>> peer_info;     // [slot] the peer's vol_peer_info
+    std::vector<void *> peer_ipc;                    // IPC mappings to close at destroy
+    PeerOut *d_peers = nullptr;                      // [world]
+    PeerDst *d_dst = nullptr;                        // [n_local − nA] destinations of each launch-B row
+    int2 *d_push = nullptr;                          // [n_send] (slot, peer row) of each send entry
+    unsigned long long *flags = nullptr;             // [world] arrivals from each rank (written by peers)
+    unsigned long long *expect = nullptr;            // [world] arrivals consumed so far (local)
+    int *d_peer_ranks = nullptr;                     // [n_peers]
+    int *d_peer_slots = nullptr;                     // [n_peers]
 };
 
 size_t hvg::shard_extra_bytes(const ShardPlan &P) {
@@ -303,6 +320,11 @@ size_t hvg::shard_extra_bytes(const ShardPlan &P) {
     c.take<float>((size_t)P.ghost.size() * kMsgFloats + 4);
     c.take<int32_t>(P.send_rows.size() + 1);
     c.take<unsigned long long>(4);
+    c.take<unsigned long long>(2 * (size_t)P.world + 2);          // flags, expect
+    c.take<PeerOut>((size_t)P.world + 1);
+    c.take<PeerDst>((size_t)(P.n_local() - P.nA) + 1);
+    c.take<int2>(P.send_rows.size() + 1);
+    c.take<int>(2 * (size_t)P.world + 2);
     return c.off + 512;
 }
 
@@ -510,6 +532,17 @@ vol_status shard_setup(vol_s *v, const ShardPlan &plan, const vol_dist *dist) {
     R->recvbuf = c.take<float>((size_t)P.ghost.size() * kMsgFloats + 4);
     R->send_rows = c.take<int32_t>(P.send_rows.size() + 1);
     R->omega = c.take<unsigned long long>(4);
+    R->flags = c.take<unsigned long long>(2 * (size_t)P.world + 2);
+    R->expect = R->flags + P.world;
+    R->d_peers = c.take<PeerOut>((size_t)P.world + 1);
+    R->d_dst = c.take<PeerDst>((size_t)(P.n_local() - P.nA) + 1);
+    R->d_push = c.take<int2>(P.send_rows.size() + 1);
+    R->d_peer_ranks = c.take<int>(2 * (size_t)P.world + 2);
+    R->d_peer_slots = R->d_peer_ranks + P.world;
+    CK(cudaMemsetAsync(R->flags, 0, (2 * (size_t)P.world + 2) * sizeof(unsigned long long), s));
+    R->peer_slot.assign(P.world, -1);
+    for (int q = 0; q < P.world; q++)
+        if (q != P.rank && P.send_cnt[q] > 0) R->peers.push_back(q);
     std::vector<int32_t> send32(P.send_rows.begin(), P.send_rows.end());
     CK(cudaMemcpyAsync(R->send_rows, send32.data(), send32.size() * 4, cudaMemcpyHostToDevice, s));
     CK(cudaStreamSynchronize(s));  // the host vector goes out of scope
@@ -729,11 +762,114 @@ static vol_status nccl_skew(vol_s *v, const IterParams &P, int32_t iters) {
     return VOL_OK;
 }
 
+static int p2p_signal(vol_s *v, cudaStream_t s);
+static int p2p_wait(vol_s *v, cudaStream_t s);
+static int p2p_push(vol_s *v, const float *a, int which_a, int pidx, cudaStream_t s);
+
+// The skewed schedule with the direct-store transport (one rank; its peers run the same sequence):
+//   ready · push(ū⁰, p⁰) · k_dual · push(u⁰, p¹) · { A_j · wait · B_j (+ stores into the peers) · signal } · wait · k_primal
+// with a signal after every push and a wait before every consumer of ghost data (see above).
+static vol_status p2p_skew(vol_s *v, const IterParams &P, int32_t iters) {
+    ShardRuntime *R = v->shard;
+    const ShardPlan &SP = R->plan;
+    cudaStream_t s = v->stream;
+    const int c = v->cur;
+    const int64_t nl = SP.n_local(), nA = SP.nA;
+    int64_t launches = 0;
+    CK(cudaMemcpyAsync(v->d_u2, v->F.u, (size_t)v->L.S * kBlockVox * 4, cudaMemcpyDeviceToDevice, s));
+    float *B[2];
+    B[(iters - 1) & 1] = v->F.u;
+    B[iters & 1] = v->d_u2;
+    auto uidx = [&](const float *p) { return p == v->F.u ? 0 : 1; };
+    auto step = [&](int r) -> vol_status {
+        CKL(r);
+        launches += r;
+        return VOL_OK;
+    };
+    vol_status st;
+    if ((st = step(p2p_signal(v, s))) != VOL_OK || (st = step(p2p_wait(v, s))) != VOL_OK) return st;   // ready
+    if ((st = step(p2p_push(v, v->F.ub[c], 2 + c, c, s))) != VOL_OK || (st = step(p2p_signal(v, s))) != VOL_OK ||
+        (st = step(p2p_wait(v, s))) != VOL_OK)
+        return st;
+    if ((st = step(launch_dual_only(view_of(v->F, c), v->d_nbr, nl, P, s))) != VOL_OK) return st;
+    if ((st = step(p2p_push(v, B[0], uidx(B[0]), c ^ 1, s))) != VOL_OK || (st = step(p2p_signal(v, s))) != VOL_OK)
+        return st;
+    auto skew_iter = [&](cudaStream_t cs_, int j, bool timed, int64_t &n) -> vol_status {
+        const int pin = c ^ ((j + 1) & 1);
+        if (timed) CK(cudaEventRecord(R->ev_t[0], cs_));
+        int a = launch_skew(v->F, B[j & 1], B[(j + 1) & 1], pin, v->pending_frozen, v->d_nbr, 0, nA, P, cs_);
+        CKL(a);
+        if (timed) {
+            CK(cudaEventRecord(R->ev_t[1], cs_));
+            CK(cudaEventRecord(R->ev_t[2], cs_));
+        }
+        int w = p2p_wait(v, cs_);
+        CKL(w);
+        if (timed) {
+            CK(cudaEventRecord(R->ev_t[3], cs_));
+            CK(cudaEventRecord(R->ev_t[4], cs_));
+        }
+        int b = launch_skew_peers(v->F, B[j & 1], B[(j + 1) & 1], pin, v->pending_frozen, v->d_nbr, nA, nl - nA, P,
+                                  R->d_peers, R->d_dst, cs_);
+        CKL(b);
+        if (timed) {
+            CK(cudaEventRecord(R->ev_t[5], cs_));
+            R->timed = true;
+        }
+        int g = p2p_signal(v, cs_);
+        CKL(g);
+        n += a + w + b + g;
+        return VOL_OK;
+    };
+    const int total = iters - 1;
+    const int body = total - 1;
+    const int m = std::min(16, body / 2);
+    int j = 0;
+    if (m >= 1 && R->graphs) {
+        GraphKey key;
+        key.add('Q').add(c).add(m).add(iters & 1).add(v->pending_frozen).add(P);
+        cudaGraphExec_t ge = nullptr;
+        int64_t per = 0;
+        st = cached_graph(
+            v, key,
+            [&](cudaStream_t cap, int64_t &n) -> vol_status {
+                for (int k = 0; k < 2 * m; k++) {
+                    vol_status s2 = skew_iter(cap, k, false, n);
+                    if (s2 != VOL_OK) return s2;
+                }
+                return VOL_OK;
+            },
+            &ge, &per);
+        if (st != VOL_OK) return st;
+        const int reps = body / (2 * m);
+        for (int q = 0; q < reps; q++) {
+            CK(cudaGraphLaunch(ge, s));
+            launches += per;
+            g_launches.fetch_add(per);
+        }
+        j = reps * 2 * m;
+    }
+    for (; j < total; j++)
+        if ((st = skew_iter(s, j, j == total - 1, launches)) != VOL_OK) return st;
+    if (iters < 2) {
+        for (int k = 0; k < 6; k++) CK(cudaEventRecord(R->ev_t[k], s));
+        R->timed = true;
+    }
+    if ((st = step(p2p_wait(v, s))) != VOL_OK) return st;
+    const int c2 = c ^ (iters & 1);
+    View V = view_of(v->F, c2 ^ 1);   // px_out = p[c2] (p^iters), ub_out = ub[c2]
+    V.u = B[(iters - 1) & 1];         // == F.u
+    if ((st = step(launch_primal_only(V, v->d_nbr, nl, P, s))) != VOL_OK) return st;
+    v->cur = c2;
+    v->last_launches = launches;
+    return VOL_OK;
+}
+
 vol_status shard_iterate(vol_s *v, const IterParams &P, int32_t iters) {
     ShardRuntime *R = v->shard;
     if (!R->nccl) return fail(VOL_EINVAL, "loopback-sharded volume: use vol_regularise_group");
     if (v->pending_kernel == 0 || v->pending_kernel == 2) {   // the product path: the skewed schedule
-        vol_status st = nccl_skew(v, P, iters);
+        vol_status st = (R->p2p && v->pending_exchange) ? p2p_skew(v, P, iters) : nccl_skew(v, P, iters);
         if (st != VOL_OK) return st;
         return check_async(R->comm);
     }
@@ -780,8 +916,221 @@ void shard_destroy(vol_s *v) {
     for (auto &e : R->ev_t)
         if (e) cudaEventDestroy(e);
     // the communicator stays cached for later volumes of the same process group (comm_acquire)
+    for (void *p : R->peer_ipc) cudaIpcCloseMemHandle(p);
     delete R;
     v->shard = nullptr;
+}
+
+// ---------------------------------------------------------------- direct-store transport (peers)
+// The boundary launch writes each block a peer reads straight into the peer's ghost rows (k_skew<…, true>,
+// peer.cuh); the prologue / post-dual exchanges copy with k_push.  Completion is a per-source arrival
+// counter in the receiver's memory (k_signal: system-scope fence, then an atomic add into every peer's
+// counter for this rank) and a device-side expected count (k_wait spins until every peer's counter
+// reaches it), so the same graph can be replayed.  Waits before every consumer of ghost data also order
+// the writes against the peer's previous reads of the same buffers (the rank only writes buffer parity
+// j + 1 after every peer has signalled the end of its launch j − 1), and a "ready" handshake at the start
+// of a call orders the first pushes after the peer's previous call.
+
+__global__ void k_push(const int32_t *__restrict__ rows, const int2 *__restrict__ push, const PeerOut *__restrict__ peers,
+                       const float *a, const float *px, const float *py, const float *pz, int which_a, int pidx) {
+    const int64_t e = blockIdx.x;
+    const int64_t r = rows[e];
+    const int2 d = push[e];
+    const PeerOut &Q = peers[d.x];
+    float *dst[4] = {which_a == 0 ? Q.u[0] : (which_a == 1 ? Q.u[1] : (which_a == 2 ? Q.ub[0] : Q.ub[1])),
+                     Q.px[pidx], Q.py[pidx], Q.pz[pidx]};
+    const float *src[4] = {a, px, py, pz};
+#pragma unroll
+    for (int f = 0; f < 4; f++)
+        reinterpret_cast<float4 *>(dst[f] + (int64_t)d.y * kBlockVox)[threadIdx.x] =
+            reinterpret_cast<const float4 *>(src[f] + r * kBlockVox)[threadIdx.x];
+    __threadfence_system();
+}
+
+__global__ void k_signal(const PeerOut *__restrict__ peers, const int *__restrict__ slots, int n, int me) {
+    __threadfence_system();
+    const int i = threadIdx.x;
+    if (i < n) atomicAdd_system(peers[slots[i]].flags + me, 1ull);
+}
+
+__global__ void k_wait(unsigned long long *flags, unsigned long long *expect, const int *__restrict__ ranks, int n) {
+    const int i = threadIdx.x;
+    if (i < n) {
+        const int q = ranks[i];
+        const unsigned long long target = expect[q] + 1;
+        unsigned long long v;
+        do {
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + q) : "memory");
+        } while (v < target);
+        expect[q] = target;
+    }
+    __syncwarp();
+}
+
+static int p2p_signal(vol_s *v, cudaStream_t s) {
+    ShardRuntime *R = v->shard;
+    const int n = (int)R->peers.size();
+    if (n == 0) return 0;
+    k_signal<<<1, 32, 0, s>>>(R->d_peers, R->d_peer_slots, n, R->plan.rank);
+    return cudaPeekAtLastError() == cudaSuccess ? counted(1) : -1;
+}
+
+static int p2p_wait(vol_s *v, cudaStream_t s) {
+    ShardRuntime *R = v->shard;
+    const int n = (int)R->peers.size();
+    if (n == 0) return 0;
+    k_wait<<<1, 32, 0, s>>>(R->flags, R->expect, R->d_peer_ranks, n);
+    return cudaPeekAtLastError() == cudaSuccess ? counted(1) : -1;
+}
+
+// which_a: 0/1 = the peer's u / u2 buffer, 2/3 = its ū[0] / ū[1]; pidx: the peer's p parity
+static int p2p_push(vol_s *v, const float *a, int which_a, int pidx, cudaStream_t s) {
+    ShardRuntime *R = v->shard;
+    const int64_t n = (int64_t)R->plan.send_rows.size();
+    if (n == 0) return 0;
+    k_push<<<(unsigned)n, 128, 0, s>>>(R->send_rows, R->d_push, R->d_peers, a, v->F.px[pidx], v->F.py[pidx],
+                                       v->F.pz[pidx], which_a, pidx);
+    return cudaPeekAtLastError() == cudaSuccess ? counted(1) : -1;
+}
+
+static constexpr int kPeerInfoFixed = 6, kPeerInfoOffsets = 11;
+
+extern "C" vol_status vol_peer_info(vol_t v, int64_t *info, int64_t cap, int64_t *n) {
+    if (!v || !v->shard || !n) return fail(VOL_EINVAL, "vol_peer_info: not a sharded volume");
+    const ShardPlan &P = v->shard->plan;
+    const int64_t need = kPeerInfoFixed + P.world + kPeerInfoOffsets;
+    *n = need;
+    if (!info) return VOL_OK;
+    if (cap < need) return fail(VOL_EINVAL, "vol_peer_info: %lld entries needed", (long long)need);
+    const char *base = (const char *)v->ws;
+    int64_t k = 0;
+    info[k++] = 1;   // version
+    info[k++] = P.rank;
+    info[k++] = P.world;
+    info[k++] = P.n_local();
+    info[k++] = v->L.S;
+    info[k++] = need;
+    for (int q = 0; q < P.world; q++) info[k++] = P.recv_off[q];
+    const void *ptrs[kPeerInfoOffsets] = {v->F.u,     v->d_u2,    v->F.ub[0], v->F.ub[1], v->F.px[0], v->F.px[1],
+                                          v->F.py[0], v->F.py[1], v->F.pz[0], v->F.pz[1], v->shard->flags};
+    for (const void *p : ptrs) info[k++] = (int64_t)((const char *)p - base);
+    return VOL_OK;
+}
+
+// All peers connected: build the destination tables and switch the volume to direct stores.
+static vol_status p2p_finalize(vol_s *v) {
+    ShardRuntime *R = v->shard;
+    const ShardPlan &P = R->plan;
+    const int64_t nB = P.n_local() - P.nA;
+    std::vector<PeerDst> dst((size_t)std::max<int64_t>(nB, 1));
+    for (auto &d : dst)
+        for (int k = 0; k < kMaxDst; k++) d.slot[k] = -1, d.row[k] = 0;
+    std::vector<int2> push(P.send_rows.size());
+    for (int q : R->peers) {
+        const int64_t slot = R->peer_slot[q];
+        const std::vector<int64_t> &I = R->peer_info[slot];
+        const int64_t q_nlocal = I[3], q_recv_off_me = I[kPeerInfoFixed + P.rank];
+        for (int64_t i = 0; i < P.send_cnt[q]; i++) {
+            const int64_t e = P.send_off[q] + i;
+            const int64_t row = P.send_rows[e];
+            const int64_t prow = q_nlocal + q_recv_off_me + i;
+            push[e] = make_int2((int)slot, (int)prow);
+            if (row < P.nA || row >= P.n_local()) return fail(VOL_EINVAL, "peer transport: send row outside launch B");
+            PeerDst &d = dst[row - P.nA];
+            int k = 0;
+            while (k < kMaxDst && d.slot[k] >= 0) k++;
+            if (k == kMaxDst) return fail(VOL_ENOTSUP, "peer transport: a block is read by more than %d peers", kMaxDst);
+            d.slot[k] = (int)slot;
+            d.row[k] = (int)prow;
+        }
+    }
+    std::vector<int> ranks(R->peers.begin(), R->peers.end()), slots;
+    for (int q : R->peers) slots.push_back((int)R->peer_slot[q]);
+    cudaStream_t s = v->stream;
+    CK(cudaMemcpyAsync(R->d_peers, R->peer_out.data(), R->peer_out.size() * sizeof(PeerOut), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(R->d_dst, dst.data(), dst.size() * sizeof(PeerDst), cudaMemcpyHostToDevice, s));
+    if (!push.empty()) CK(cudaMemcpyAsync(R->d_push, push.data(), push.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
+    if (!ranks.empty()) {
+        CK(cudaMemcpyAsync(R->d_peer_ranks, ranks.data(), ranks.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(R->d_peer_slots, slots.data(), slots.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+    }
+    CK(cudaStreamSynchronize(s));
+    R->p2p = true;
+    return VOL_OK;
+}
+
+static vol_status connect_peer_impl(vol_s *v, int peer, char *peer_ws, const int64_t *info, int64_t n) {
+    if (!v || !v->shard) return fail(VOL_EINVAL, "vol_connect_peer: not a sharded volume");
+    ShardRuntime *R = v->shard;
+    const ShardPlan &P = R->plan;
+    if (peer < 0 || peer >= P.world || peer == P.rank || !peer_ws || !info)
+        return fail(VOL_EINVAL, "vol_connect_peer: bad peer %d", peer);
+    if (n != kPeerInfoFixed + P.world + kPeerInfoOffsets || info[0] != 1 || info[1] != peer || info[2] != P.world ||
+        info[5] != n)
+        return fail(VOL_EINVAL, "vol_connect_peer: peer info does not match (rank %d of %d)", peer, P.world);
+    if (std::find(R->peers.begin(), R->peers.end(), peer) == R->peers.end()) return VOL_OK;   // no halo with it
+    if (R->peer_slot[peer] < 0) {
+        R->peer_slot[peer] = (int64_t)R->peer_out.size();
+        R->peer_out.push_back(PeerOut{});
+        R->peer_info.emplace_back();
+    }
+    const int64_t slot = R->peer_slot[peer];
+    R->peer_info[slot].assign(info, info + n);
+    const int64_t *off = info + kPeerInfoFixed + P.world;
+    PeerOut &Q = R->peer_out[slot];
+    Q.u[0] = (float *)(peer_ws + off[0]);
+    Q.u[1] = (float *)(peer_ws + off[1]);
+    Q.ub[0] = (float *)(peer_ws + off[2]);
+    Q.ub[1] = (float *)(peer_ws + off[3]);
+    Q.px[0] = (float *)(peer_ws + off[4]);
+    Q.px[1] = (float *)(peer_ws + off[5]);
+    Q.py[0] = (float *)(peer_ws + off[6]);
+    Q.py[1] = (float *)(peer_ws + off[7]);
+    Q.pz[0] = (float *)(peer_ws + off[8]);
+    Q.pz[1] = (float *)(peer_ws + off[9]);
+    Q.flags = (unsigned long long *)(peer_ws + off[10]);
+    for (int q : R->peers)
+        if (R->peer_slot[q] < 0) return VOL_OK;   // more peers to come
+    return p2p_finalize(v);
+}
+
+extern "C" vol_status vol_connect_peer(vol_t v, int peer, void *peer_workspace, const int64_t *info, int64_t n) {
+    return connect_peer_impl(v, peer, (char *)peer_workspace, info, n);
+}
+
+extern "C" vol_status vol_ipc_handle(vol_t v, void *handle64, int64_t *offset) {
+    if (!v || !handle64 || !offset) return fail(VOL_EINVAL, "vol_ipc_handle: NULL argument");
+    static PFN_cuMemGetAddressRange_v3020 range = nullptr;
+    if (!range) {
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", (void **)&range, cudaEnableDefault, &q) != cudaSuccess || !range)
+            return fail(VOL_ENOTSUP, "vol_ipc_handle: cuMemGetAddressRange unavailable");
+    }
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range(&base, &size, (CUdeviceptr)v->ws) != CUDA_SUCCESS) return fail(VOL_ECUDA, "vol_ipc_handle: address range");
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, (void *)base));
+    memcpy(handle64, &h, sizeof h);
+    *offset = (int64_t)((char *)v->ws - (char *)base);
+    return VOL_OK;
+}
+
+extern "C" vol_status vol_connect_peer_ipc(vol_t v, int peer, const void *handle64, int64_t offset, const int64_t *info,
+                                          int64_t n) {
+    if (!v || !v->shard || !handle64) return fail(VOL_EINVAL, "vol_connect_peer_ipc: NULL argument");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle64, sizeof h);
+    void *base = nullptr;
+    CK(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    v->shard->peer_ipc.push_back(base);
+    return connect_peer_impl(v, peer, (char *)base + offset, info, n);
+}
+
+extern "C" int vol_transport(vol_t v) {
+    if (!v || !v->shard) return 0;
+    if (v->shard->p2p) return 3;
+    return v->shard->nccl ? 1 : 2;
 }
 
 // ------------------------------------------------------------------------- loopback transport
@@ -856,6 +1205,72 @@ extern "C" vol_status vol_regularise_group(vol_t *h, int world, float lambda, fl
     cudaStream_t s = h[0]->stream;
     for (int r = 1; r < world; r++) CK(cudaStreamSynchronize(h[r]->stream));
     int64_t launches = 0;
+    bool all_p2p = true;
+    for (int r = 0; r < world; r++) all_p2p = all_p2p && h[r]->shard->p2p;
+    if ((h[0]->pending_kernel == 0 || h[0]->pending_kernel == 2) && iters > 0 && all_p2p && h[0]->pending_exchange) {
+        // the direct-store transport, as p2p_skew, every stage issued for all shards before the next stage
+        // (one stream: every wait finds its peers' signals already counted)
+        const int c = h[0]->cur;
+        float *Bu[64][2];
+        if (world > 64) return fail(VOL_EINVAL, "group: at most 64 loopback shards");
+        for (int r = 0; r < world; r++) {
+            CK(cudaMemcpyAsync(h[r]->d_u2, h[r]->F.u, (size_t)h[r]->L.S * kBlockVox * 4, cudaMemcpyDeviceToDevice, s));
+            Bu[r][(iters - 1) & 1] = h[r]->F.u;
+            Bu[r][iters & 1] = h[r]->d_u2;
+        }
+        auto all = [&](auto fn) -> vol_status {
+            for (int r = 0; r < world; r++) {
+                const int n = fn(r);
+                CKL(n);
+                launches += n;
+            }
+            return VOL_OK;
+        };
+        auto sig = [&](int r) { return p2p_signal(h[r], s); };
+        auto wt = [&](int r) { return p2p_wait(h[r], s); };
+        if ((st = all(sig)) != VOL_OK || (st = all(wt)) != VOL_OK) return st;   // ready
+        if ((st = all([&](int r) { return p2p_push(h[r], h[r]->F.ub[c], 2 + c, c, s); })) != VOL_OK ||
+            (st = all(sig)) != VOL_OK || (st = all(wt)) != VOL_OK)
+            return st;
+        if ((st = all([&](int r) {
+                 return launch_dual_only(view_of(h[r]->F, c), h[r]->d_nbr, h[r]->shard->plan.n_local(), P, s);
+             })) != VOL_OK)
+            return st;
+        if ((st = all([&](int r) {
+                 return p2p_push(h[r], Bu[r][0], Bu[r][0] == h[r]->F.u ? 0 : 1, c ^ 1, s);
+             })) != VOL_OK ||
+            (st = all(sig)) != VOL_OK)
+            return st;
+        for (int j = 0; j < iters - 1; j++) {
+            const int pin = c ^ ((j + 1) & 1);
+            if ((st = all([&](int r) {
+                     return launch_skew(h[r]->F, Bu[r][j & 1], Bu[r][(j + 1) & 1], pin, h[r]->pending_frozen,
+                                        h[r]->d_nbr, 0, h[r]->shard->plan.nA, P, s);
+                 })) != VOL_OK ||
+                (st = all(wt)) != VOL_OK)
+                return st;
+            if ((st = all([&](int r) {
+                     const ShardPlan &SP = h[r]->shard->plan;
+                     return launch_skew_peers(h[r]->F, Bu[r][j & 1], Bu[r][(j + 1) & 1], pin, h[r]->pending_frozen,
+                                              h[r]->d_nbr, SP.nA, SP.n_local() - SP.nA, P, h[r]->shard->d_peers,
+                                              h[r]->shard->d_dst, s);
+                 })) != VOL_OK ||
+                (st = all(sig)) != VOL_OK)
+                return st;
+        }
+        if ((st = all(wt)) != VOL_OK) return st;
+        const int c2 = c ^ (iters & 1);
+        if ((st = all([&](int r) {
+                 View V = view_of(h[r]->F, c2 ^ 1);
+                 V.u = Bu[r][(iters - 1) & 1];
+                 return launch_primal_only(V, h[r]->d_nbr, h[r]->shard->plan.n_local(), P, s);
+             })) != VOL_OK)
+            return st;
+        for (int r = 0; r < world; r++) h[r]->cur = c2;
+        CK(cudaStreamSynchronize(s));
+        for (int r = 0; r < world; r++) h[r]->last_launches = launches;
+        return VOL_OK;
+    }
     if ((h[0]->pending_kernel == 0 || h[0]->pending_kernel == 2) && iters > 0) {   // skewed, as nccl_skew
         const int c = h[0]->cur;
         float *Bu[64][2];

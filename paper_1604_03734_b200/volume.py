@@ -279,6 +279,46 @@ class Volume:
                                       n.value, ctypes.byref(m)))
         return out[:m.value]
 
+    # -- direct-store halo transport (vol.h "Direct-store halo transport") --------------------------
+    def peer_info(self) -> np.ndarray:
+        n = ctypes.c_int64()
+        N.check(self._lib.vol_peer_info(self._h, None, 0, ctypes.byref(n)))
+        info = np.zeros(n.value, np.int64)
+        N.check(self._lib.vol_peer_info(self._h, info.ctypes.data, n.value, ctypes.byref(n)))
+        return info
+
+    def connect_peer(self, peer: int, workspace_ptr: int, info: np.ndarray):
+        info = np.ascontiguousarray(info, np.int64)
+        N.check(self._lib.vol_connect_peer(self._h, int(peer), ctypes.c_void_p(int(workspace_ptr)), info.ctypes.data,
+                                           info.shape[0]))
+
+    def ipc_handle(self):
+        buf = ctypes.create_string_buffer(64)
+        off = ctypes.c_int64()
+        N.check(self._lib.vol_ipc_handle(self._h, buf, ctypes.byref(off)))
+        return buf.raw, off.value
+
+    def connect_peer_ipc(self, peer: int, handle: bytes, offset: int, info: np.ndarray):
+        info = np.ascontiguousarray(info, np.int64)
+        hb = ctypes.create_string_buffer(bytes(handle), 64)
+        N.check(self._lib.vol_connect_peer_ipc(self._h, int(peer), hb, int(offset), info.ctypes.data, info.shape[0]))
+
+    @property
+    def transport(self) -> str:
+        return {0: "none", 1: "nccl", 2: "loopback", 3: "peer"}[int(self._lib.vol_transport(self._h))]
+
+    def connect_peers(self, group):
+        """Direct-store transport over a torch.distributed group (collective): every rank publishes its
+        workspace's CUDA IPC handle and peer descriptor, and opens its peers' (NVLink peer access)."""
+        import torch.distributed as dist_mod
+        handle, off = self.ipc_handle()
+        mine = (self.rank, handle, off, self.peer_info().tolist())
+        allv = [None] * dist_mod.get_world_size(group)
+        dist_mod.all_gather_object(allv, mine, group=group)
+        for q, h, o, info in allv:
+            if q != self.rank:
+                self.connect_peer_ipc(q, h, o, np.asarray(info, np.int64))
+
     def close(self):
         if getattr(self, "_h", None):
             self._lib.vol_destroy(self._h)
@@ -377,8 +417,19 @@ def _handles(vols):
     return arr
 
 
-def connect_group(vols):
+def connect_group(vols, transport: str = "copy"):
+    """Connect loopback shards (one process).  transport "copy": pack → device copies → unpack per exchange;
+    "peer": the direct-store transport, each volume writing its boundary blocks into the others'
+    workspaces (the in-process form of the NVLink peer path)."""
     N.check(N.lib().vol_group_connect(_handles(vols), len(vols)))
+    if transport == "peer":
+        infos = [v.peer_info() for v in vols]
+        for r, v in enumerate(vols):
+            for q, w in enumerate(vols):
+                if q != r:
+                    v.connect_peer(q, w.workspace.data_ptr(), infos[q])
+    elif transport != "copy":
+        raise ValueError(transport)
 
 
 def regularise_group(vols, lam, eps, tau, sigma, iters, **kw):

@@ -215,14 +215,16 @@ def _check_vs_oracle(u, u32, u64):
     assert float((d / np.maximum(mag, 1.0)).max()) <= 1e-5
 
 
-def test_city_route_shards_match_oracle(V):
+@pytest.mark.parametrize("transport", ["copy", "peer"])
+def test_city_route_shards_match_oracle(V, transport):
     """SURVEY §8(e) gate and §8(c) pin (viii) on the city route prefix: 8 shards cut along the route by the
     product partition (vol_partition_route: arc length of the nearest camera-path point), the product
     (skewed) schedule with its (u^j, p^{j+1}) halo before every launch — loopback transport on one GPU:
     the same plan, pack/unpack kernels and launch A/B sequence as NCCL — after the config's 200
     iterations compared DIRECTLY with the oracle: every voxel bit-identical to the fp32 oracle and within
     1e-5 of fp64; also bitwise the single-GPU run, energies within 1e-9.  Every rank has at most the
-    peers r - 1 and r + 1."""
+    peers r - 1 and r + 1.  Both transports: "copy" (pack → copies → unpack, the NCCL data path) and
+    "peer" (the boundary launch writes straight into the peers' ghost rows, counters for completion)."""
     from paper_1604_03734_b200 import connect_group, group_energy, partition_route, plan_shard, regularise_group
     s = _city()
     world = 8
@@ -238,7 +240,7 @@ def test_city_route_shards_match_oracle(V):
         print(f"rank {r}: {vols[-1].n_local} blocks, {vols[-1].n_ghost} ghosts, launch B "
               f"{len(np.unique(plan['send']))}")
     assert all(v.n_ghost > 0 for v in vols)
-    connect_group(vols)
+    connect_group(vols, transport=transport)
     regularise_group(vols, s.lam, s.eps, s.tau, s.sigma, s.iters, data_term=s.data_term)
     u = np.empty((s.n_blocks, 512), np.float32)
     for r, v in enumerate(vols):

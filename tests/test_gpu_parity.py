@@ -465,3 +465,30 @@ def test_graph_cache_across_calls(V):
         st = oracle.regularise(s.coords, s.f, s.W, lam, s.eps, s.tau, s.sigma, it, precision="f32", nbr=nbr,
                                state=st)
         assert np.array_equal(vol.u().cpu().numpy(), st[0]), (k, it, kern, frz, lam)
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_loopback_peer_transport_bitwise_equal_single(V, world):
+    """The direct-store transport (each shard's boundary launch writes its blocks into the peers' ghost
+    rows — here other volumes' workspaces in this process — with per-source arrival counters; no pack, copy
+    or unpack in the loop) equals the single-GPU result bit for bit, and the counters stay consistent over
+    a sequence of calls: resumed, odd and even lengths, iters = 1 and 2, and a one-pass call in between
+    (which uses the copy transport)."""
+    from paper_1604_03734_b200 import connect_group, regularise_group
+    s = random_instance(500, seed=50 + world, extent=6, w_density=0.7, lam=0.4, eps=0.01, iters=0)
+    c = s.coords
+    part = _x_route_part(c, world)
+    vols = []
+    for r in range(world):
+        mine = (part == r).nonzero().squeeze(1)
+        vols.append(V(c, s.f[mine], s.W[mine], part=part, loopback=(r, world)))
+    connect_group(vols, transport="peer")
+    assert all(v.transport == "peer" for v in vols)
+    single = V(s.coords.cuda(), s.f.cuda(), s.W.cuda())
+    for k, (it, kern) in enumerate([(37, 0), (1, 0), (2, 0), (36, 0), (5, 3), (40, 2)]):
+        regularise_group(vols, s.lam, s.eps, s.tau, s.sigma, it, kernel=kern, resume=k > 0)
+        single.regularise(s.lam, s.eps, s.tau, s.sigma, it, kernel=kern, resume=k > 0)
+        u = torch.empty(len(c), 512)
+        for r, v in enumerate(vols):
+            u[(part == r).nonzero().squeeze(1)] = v.u().cpu()
+        assert np.array_equal(u.numpy(), single.u().cpu().numpy()), (k, it, kern)
