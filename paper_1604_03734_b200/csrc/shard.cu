@@ -953,14 +953,22 @@ __global__ void k_signal(const PeerOut *__restrict__ peers, const int *__restric
     if (i < n) atomicAdd_system(peers[slots[i]].flags + me, 1ull);
 }
 
-__global__ void k_wait(unsigned long long *flags, unsigned long long *expect, const int *__restrict__ ranks, int n) {
+// Spins at most ~10 s (a peer that never signals is a broken peer, not a slow one): then it records the
+// failure in expect[world] (read back by the host after loopback calls) and gives up.
+__global__ void k_wait(unsigned long long *flags, unsigned long long *expect, const int *__restrict__ ranks, int n,
+                       int world) {
     const int i = threadIdx.x;
     if (i < n) {
         const int q = ranks[i];
         const unsigned long long target = expect[q] + 1;
+        const long long t0 = clock64();
         unsigned long long v;
         do {
             asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + q) : "memory");
+            if (v < target && clock64() - t0 > 20000000000ll) {
+                atomicExch(expect + world, 1ull);
+                break;
+            }
         } while (v < target);
         expect[q] = target;
     }
@@ -979,7 +987,7 @@ static int p2p_wait(vol_s *v, cudaStream_t s) {
     ShardRuntime *R = v->shard;
     const int n = (int)R->peers.size();
     if (n == 0) return 0;
-    k_wait<<<1, 32, 0, s>>>(R->flags, R->expect, R->d_peer_ranks, n);
+    k_wait<<<1, 32, 0, s>>>(R->flags, R->expect, R->d_peer_ranks, n, R->plan.world);
     return cudaPeekAtLastError() == cudaSuccess ? counted(1) : -1;
 }
 
@@ -1268,7 +1276,12 @@ extern "C" vol_status vol_regularise_group(vol_t *h, int world, float lambda, fl
             return st;
         for (int r = 0; r < world; r++) h[r]->cur = c2;
         CK(cudaStreamSynchronize(s));
-        for (int r = 0; r < world; r++) h[r]->last_launches = launches;
+        for (int r = 0; r < world; r++) {
+            h[r]->last_launches = launches;
+            unsigned long long err = 0;
+            CK(cudaMemcpy(&err, h[r]->shard->expect + world, 8, cudaMemcpyDeviceToHost));
+            if (err) return fail(VOL_ECUDA, "peer transport: shard %d waited for a peer that never signalled", r);
+        }
         return VOL_OK;
     }
     if ((h[0]->pending_kernel == 0 || h[0]->pending_kernel == 2) && iters > 0) {   // skewed, as nccl_skew
