@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--freeze", type=int, default=1, help="opts.freeze (bit-identical skip of identity updates)")
     ap.add_argument("--sharded", action="store_true",
                     help="use the NCCL sharded runtime even at one rank (tests the N > 1 code path on one GPU)")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "peer"],
+                    help="halo transport at N > 1: NCCL send/recv (default) or direct stores into the peers' "
+                         "ghost rows over NVLink (CUDA IPC; vol_connect_peer_ipc)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fusion", action="store_true",
@@ -666,6 +669,8 @@ def main():
 
     def step(c, f, W, out, record, freeze=bool(args.freeze), rec=None, exchange=True):
         vol = Volume(c, f, W, stream=stream, **kw)
+        if sharded and args.transport == "peer" and world > 1:
+            vol.connect_peers(group)
         vol.regularise(scene.lam, scene.eps, scene.tau, scene.sigma, 0, theta=scene.theta,
                        data_term=scene.data_term, init=scene.init, kernel=args.kernel)
         ev_a.record(stream)
@@ -753,7 +758,11 @@ def main():
         halo = {"exposed_us_per_iter": 1e3 * (it_ms - float(tt[0])), "iter_ms_exchange_off": float(tt[0]),
                 "host_issue_us_per_iter": float(hu.item()), "gpu_us_per_iter": 1e3 * it_ms,
                 "interior_ms": float(tt[1]), "exchange_chain_ms": float(tt[2]), "boundary_ms": float(tt[3]),
-                "transport": "NCCL send/recv per peer on the comm stream (fork/join inside the CUDA graph of the skewed loop), pack/unpack kernels",
+                "transport": ("direct stores into the peers' ghost rows by the boundary launch (CUDA IPC over NVLink), "
+                              "per-source arrival counters, inside the CUDA graph of the skewed loop"
+                              if args.transport == "peer" and world > 1 else
+                              "NCCL send/recv per peer on the comm stream (fork/join inside the CUDA graph of the "
+                              "skewed loop), pack/unpack kernels"),
                 "note": "max over ranks; chain overlaps the interior launch"}
 
     # end to end from pinned host buffers through the same API
