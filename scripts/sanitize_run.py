@@ -30,6 +30,15 @@ def main():
     connect_group(vols)
     regularise_group(vols, 0.5, 0.01, r.tau, r.sigma, 3)
     print("group energy", group_energy(vols, 0.5, 0.01))
+    # the direct-store transport on 3 loopback shards (peer stores, signal / wait kernels)
+    part3 = ((c[:, 0] + 4) * 3 // 8).clamp(0, 2).to(torch.int32)
+    vp = []
+    for k in range(3):
+        mine = (part3 == k).nonzero().squeeze(1)
+        vp.append(Volume(c, r.f[mine], r.W[mine], part=part3, loopback=(k, 3)))
+    connect_group(vp, transport="peer")
+    regularise_group(vp, 0.5, 0.01, r.tau, r.sigma, 6)
+    print("peer transport", [x.transport for x in vp])
     # widened rows: fusion, extraction, stereo
     from paper_1604_03734_b200 import fuse, stereo
     from synth.depth import sphere_depth
