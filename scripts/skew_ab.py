@@ -29,7 +29,10 @@ def main():
         d = torch.load(cache)
     else:
         from synth import scenes
-        s = scenes.by_name(a.config, device="cuda", chunk_blocks=4096)
+        if a.config.startswith("street-len:"):   # a shorter street (L2-residency experiments)
+            s = scenes.street(0, length=float(a.config.split(":")[1]), device="cuda", chunk_blocks=4096)
+        else:
+            s = scenes.by_name(a.config, device="cuda", chunk_blocks=4096)
         d = dict(coords=s.coords.cpu(), f=s.f.cpu(), W=s.W.cpu(), p=s.params())
         torch.save(d, cache)
     from paper_1604_03734_b200 import Volume
