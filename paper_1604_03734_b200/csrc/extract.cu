@@ -2,16 +2,15 @@
 // P:102 "regularise the model in 3D space, extract the surface", P:132-133 zero-crossing level set).
 // Readings X-1 … X-7: marching tetrahedra over the cells of fully observed voxels.
 //
-//   k_extract<false>  one 128-thread CTA per store row: stage the 9×9×9 tile of values and
-//                     "usable" flags (allocated ∧ W > 0 ∧ W >= w_min) of the block and its +x/+y/+z
-//                     neighbours (face, edge and corner blocks reached by neighbour-table chains: if an
-//                     intermediate block is missing, every cell needing the chained block has a corner
-//                     in the missing one, so it is skipped anyway); each thread counts the triangles of
-//                     its 4 cells; per-thread counts go to scratch, the block total to counts[caller].
-//   exclusive scan of the per-block totals in caller order → triangle offsets (deterministic output
-//   order X-7: caller block order, cell order, tetrahedron order, triangle order).
-//   k_extract<true>   same CTA layout: block scan of the per-thread counts, then each thread writes
-//                     its triangles at offset[caller] + prefix.
+//   k_extract<true>   the ordered single pass: CTAs take caller blocks in ticket order; each stages the
+//                     9×9×9 tile of values and "usable" flags (allocated ∧ W > 0 ∧ W >= w_min) of its block
+//                     and the +x/+y/+z neighbours (face, edge and corner blocks reached by neighbour-table
+//                     chains: if an intermediate block is missing, every cell needing the chained block has
+//                     a corner in the missing one, so it is skipped anyway), counts the triangles of every
+//                     (cell, tetrahedron) from corner signs and zeros alone, finds the triangle offset of its
+//                     block by decoupled look-back over its predecessors in caller order (deterministic
+//                     output order X-7: caller block, cell, tetrahedron, triangle) and writes its triangles.
+//   k_extract<false>  the counting half alone (count-only calls; sizing a host buffer's staging copy).
 // Vertex arithmetic is fp32 in the written order of X-4 (bit-identical to the oracle).
 #include <cuda_runtime.h>
 
@@ -72,37 +71,45 @@ __device__ __forceinline__ void edge_vertex(const CellGeom &G, int ca, float ua,
         p[k] = ((d >> k) & 1) ? __fadd_rn(G.X[0][k], __fmul_rn(t, G.dX[k])) : G.X[(lo >> k) & 1][k];
 }
 
-// X-6: a triangle is dropped iff its area is zero in exact arithmetic, decided on the corner values (an
-// edge vertex sits on its outside corner iff that corner's value is exactly 0), never on rounded vertices.
-template <bool EMIT>
-__device__ __forceinline__ void put(float *out, unsigned &m, const float *p0, const float *p1, const float *p2,
-                                    bool degenerate) {
-    if (degenerate) return;   // X-6
-    if (EMIT) {
-        float *o = out + 9ull * m;
-#pragma unroll
-        for (int k = 0; k < 3; k++) {
-            o[k] = p0[k];
-            o[3 + k] = p1[k];
-            o[6 + k] = p2[k];
-        }
-    }
-    m++;
+// X-2: the 6 Freudenthal tetrahedra 000 → e_a → e_a + e_b → 111 for the axis permutations (a, b, c) in
+// lexicographic order; odd permutations list their last two corners swapped (positive orientation):
+//   (0,1,2): 0 1 3 7   (0,2,1): 0 1 7 5   (1,0,2): 0 2 7 3   (1,2,0): 0 2 6 7   (2,0,1): 0 4 5 7   (2,1,0): 0 4 7 6
+// corner codes k1 k2 k3 of tetrahedron q, 4 bits each (k1 lowest), 12 bits per tetrahedron
+constexpr unsigned long long kTetLo = 0x731ull | (0x571ull << 12) | (0x372ull << 24);
+constexpr unsigned long long kTetHi = 0x762ull | (0x754ull << 12) | (0x674ull << 24);
+__device__ __forceinline__ int tet_code(int q, int r) {   // r = 1, 2, 3
+    const unsigned long long w = q < 3 ? kTetLo : kTetHi;
+    return (int)((w >> (12 * (q < 3 ? q : q - 3) + 4 * (r - 1))) & 0xF);
+}
+
+__device__ __forceinline__ int tile_index(int cx, int cy, int cz, int code) {
+    return (cx + (code & 1)) + kT * (cy + ((code >> 1) & 1)) + kT * kT * (cz + (code >> 2));
 }
 
 __device__ __forceinline__ float sel4f(int i, float a0, float a1, float a2, float a3) {
     return i == 0 ? a0 : (i == 1 ? a1 : (i == 2 ? a2 : a3));
 }
 
-// One tetrahedron with corner codes (k0, k1, k2, k3) in positively oriented order (X-2) and values
+// Triangles of one tetrahedron (X-5, X-6), from its 4-bit inside mask (bit i: corner i has value < 0, X-3)
+// and its 4-bit mask of corners with value ≠ 0: one for a lone inside corner; otherwise one per outside
+// corner whose value is not exactly 0 (X-6: with 3 inside, the triangle degenerates iff the outside corner is
+// 0; with 2 inside, the quad's (E_ac, E_ad, E_bd) iff u_d = 0 and (E_ac, E_bd, E_bc) iff u_c = 0).
+__device__ __forceinline__ uint32_t tet_triangles(int m4, int nz4) {
+    if (m4 == 0 || m4 == 15) return 0u;
+    return __popc(m4) == 1 ? 1u : (uint32_t)__popc(nz4 & ~m4 & 15);
+}
+
+// One tetrahedron with corner codes (0, k1, k2, k3) in positively oriented order (X-2) and values
 // (v0 … v3).  X-5: the lone corner (nin = 1: the inside one, nin = 3: the outside one) or the inside pair
 // goes first, the remaining corners follow in tetrahedron order, and the last two are swapped when that
-// permutation is odd, so (a, b, c, d) stays positively oriented.
-template <bool EMIT>
-__device__ __forceinline__ void tet(int k0, int k1, int k2, int k3, float v0, float v1, float v2, float v3,
-                                    const CellGeom &G, float *out, unsigned &m) {
+// permutation is odd, so (a, b, c, d) stays positively oriented.  Triangles: 1 inside (E_ab, E_ac, E_ad),
+// 3 inside (E_ab, E_ad, E_ac), 2 inside (E_ac, E_ad, E_bd) + (E_ac, E_bd, E_bc); with the edges
+//   E0 = (a, quad ? c : b), E1 = (a, quad ? d : c), E2 = (quad ? b : a, d), E3 = (b, c)
+// these are (E0, E1, E2) [(E0, E2, E1) for 3 inside] and (E0, E2, E3): one code path for every case (the
+// lanes of a warp hold mixed cases).  The surviving triangles (X-6) are written to o[0 …], 9 floats each.
+__device__ __forceinline__ void tet_emit(int k1, int k2, int k3, float v0, float v1, float v2, float v3,
+                                         const CellGeom &G, float *o) {
     const int mask = (v0 < 0.0f) | ((v1 < 0.0f) << 1) | ((v2 < 0.0f) << 2) | ((v3 < 0.0f) << 3);   // X-3
-    if (mask == 0 || mask == 15) return;
     const int nin = __popc(mask);
     int pa, pb, pc, pd;
     if (nin == 2) {
@@ -125,71 +132,91 @@ __device__ __forceinline__ void tet(int k0, int k1, int k2, int k3, float v0, fl
         pc = (a & 1) ? r2 : r1;
         pd = (a & 1) ? r1 : r2;
     }
-    const int packed = k0 | (k1 << 4) | (k2 << 8) | (k3 << 12);   // corner code of position i at bits 4i
+    const int packed = (k1 << 4) | (k2 << 8) | (k3 << 12);   // corner code of position i at bits 4i
     const int ca = (packed >> (4 * pa)) & 15, cb = (packed >> (4 * pb)) & 15;
     const int cc = (packed >> (4 * pc)) & 15, cd = (packed >> (4 * pd)) & 15;
     const float ua = sel4f(pa, v0, v1, v2, v3), ub = sel4f(pb, v0, v1, v2, v3);
     const float uc = sel4f(pc, v0, v1, v2, v3), ud = sel4f(pd, v0, v1, v2, v3);
-    float e1[3], e2[3], e3[3];
-    if (nin != 2) {
-        edge_vertex(G, ca, ua, cb, ub, e1);
-        edge_vertex(G, ca, ua, cc, uc, e2);
-        edge_vertex(G, ca, ua, cd, ud, e3);
-        // 1 inside: never degenerate; 1 outside (a): all three vertices sit on a iff u_a = 0
-        if (nin == 1) put<EMIT>(out, m, e1, e2, e3, false);
-        else put<EMIT>(out, m, e1, e3, e2, ua == 0.0f);
-    } else {
-        float e4[3];
-        edge_vertex(G, ca, ua, cc, uc, e1);   // E_ac
-        edge_vertex(G, ca, ua, cd, ud, e2);   // E_ad
-        edge_vertex(G, cb, ub, cd, ud, e3);   // E_bd
-        edge_vertex(G, cb, ub, cc, uc, e4);   // E_bc
-        put<EMIT>(out, m, e1, e2, e3, ud == 0.0f);   // E_ad = E_bd iff u_d = 0
-        put<EMIT>(out, m, e1, e3, e4, uc == 0.0f);   // E_ac = E_bc iff u_c = 0
+    const bool quad = nin == 2;
+    float e0[3], e1[3], e2[3];
+    edge_vertex(G, ca, ua, quad ? cc : cb, quad ? uc : ub, e0);
+    edge_vertex(G, ca, ua, quad ? cd : cc, quad ? ud : uc, e1);
+    edge_vertex(G, quad ? cb : ca, quad ? ub : ua, cd, ud, e2);
+    const bool drop1 = quad ? ud == 0.0f : (nin == 3 && ua == 0.0f);   // X-6
+    const bool sw = nin == 3;
+    if (!drop1) {
+#pragma unroll
+        for (int k = 0; k < 3; k++) {
+            o[k] = e0[k];
+            o[3 + k] = sw ? e2[k] : e1[k];
+            o[6 + k] = sw ? e1[k] : e2[k];
+        }
+        o += 9;
+    }
+    if (quad && uc != 0.0f) {   // X-6
+        float e3[3];
+        edge_vertex(G, cb, ub, cc, uc, e3);
+#pragma unroll
+        for (int k = 0; k < 3; k++) {
+            o[k] = e0[k];
+            o[3 + k] = e2[k];
+            o[6 + k] = e3[k];
+        }
     }
 }
 
-// X-2: the 6 Freudenthal tetrahedra 000 → e_a → e_a + e_b → 111 for the axis permutations (a, b, c) in
-// lexicographic order; odd permutations list their last two corners swapped (positive orientation):
-//   (0,1,2): 0 1 3 7   (0,2,1): 0 1 7 5   (1,0,2): 0 2 7 3   (1,2,0): 0 2 6 7   (2,0,1): 0 4 5 7   (2,1,0): 0 4 7 6
-// corner codes k1 k2 k3 of tetrahedron q, 4 bits each (k1 lowest), 12 bits per tetrahedron
-constexpr unsigned long long kTetLo = 0x731ull | (0x571ull << 12) | (0x372ull << 24);
-constexpr unsigned long long kTetHi = 0x762ull | (0x754ull << 12) | (0x674ull << 24);
-__device__ __forceinline__ int tet_code(int q, int r) {   // r = 1, 2, 3
-    const unsigned long long w = q < 3 ? kTetLo : kTetHi;
-    return (int)((w >> (12 * (q < 3 ? q : q - 3) + 4 * (r - 1))) & 0xF);
-}
-
-__device__ __forceinline__ int tile_index(int cx, int cy, int cz, int code) {
-    return (cx + (code & 1)) + kT * (cy + ((code >> 1) & 1)) + kT * kT * (cz + (code >> 2));
-}
-
 constexpr int kMaxItems = 512 * 6;   // (cell, tetrahedron) pairs of one block
-constexpr int kItemWords = 2 * kMaxItems / 32;   // 2 count bits per item
 
-// Two phases per CTA: (A) every thread tests its 4 cells (all corners usable, mixed signs) and their
-// 6 tetrahedra (mixed signs) and appends the crossing (cell, tetrahedron) items to a shared list in
-// cell, tetrahedron order; (B) the 128 threads process the items round-robin — the same code path for
-// every lane, instead of each lane walking its own cells' varying tetrahedra.  The count pass stores
-// the triangles of every item (0, 1 or 2 after the X-6 drop) for the emit pass as 2 bits per item:
-// item_bits[row][2·(4·round + warp) + b] = bit b of the counts of the warp's 32 items (ballots).
+// Output of one call.  Count pass (EMIT = false): only *total (atomic sum of the block totals).  Emit pass:
+// CTAs take caller blocks in ticket order and find their triangle offset by decoupled look-back over the
+// per-block words state[i] = flag << 62 | value (flag 1: the block's own total, 2: inclusive prefix), so one
+// pass both counts and writes in the deterministic order of X-7; triangles at index >= max_tris are not
+// written.
+struct ExOut {
+    const int32_t *inv;                  // [n] store row of caller block i
+    unsigned long long *state;           // [n] look-back words (zeroed)
+    unsigned *ticket;                    // CTA ticket (zeroed)
+    unsigned long long *total;           // triangles of the call (zeroed)
+    float *out;
+    long long max_tris;
+};
+
+constexpr unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62, kVal = (1ull << 62) - 1;
+
+__device__ __forceinline__ unsigned long long ld_volatile(const unsigned long long *p) {
+    return *reinterpret_cast<const volatile unsigned long long *>(p);
+}
+__device__ __forceinline__ void st_volatile(unsigned long long *p, unsigned long long v) {
+    *reinterpret_cast<volatile unsigned long long *>(p) = v;
+}
+
+// One 128-thread CTA per block: stage the 9³ tile; (A) every thread tests its 4 cells (all corners usable,
+// mixed signs) and their 6 tetrahedra and counts each one's triangles (tet_triangles: a function of the
+// corner signs and zeros alone); a block scan places the (cell, tetrahedron) items with triangles in a shared
+// list in cell, tetrahedron order, each with its triangle offset inside the block; (B, emit pass) after the
+// look-back, each warp takes whole 32-item groups (w, w + 4, …), computes their triangles into its own
+// slice of shared memory and writes them out with consecutive lanes on consecutive floats.
 template <bool EMIT>
-__global__ void __launch_bounds__(128) k_extract(ExArgs A, int64_t n_rows, uint32_t *__restrict__ block_counts,
-                                                 uint32_t *__restrict__ item_bits,
-                                                 const uint32_t *__restrict__ offsets, float *__restrict__ out) {
+__global__ void __launch_bounds__(128) k_extract(ExArgs A, int64_t n_rows, ExOut O) {
     __shared__ float su[kTile];
     __shared__ uint8_t sok[kTile];
-    __shared__ uint16_t sitem[kMaxItems];   // cell (9 bits) << 3 | tetrahedron (3 bits)
+    __shared__ uint16_t sitem[EMIT ? kMaxItems : 1];       // cell (9 bits) << 3 | tetrahedron (3 bits)
+    __shared__ uint16_t soff[EMIT ? kMaxItems + 1 : 1];    // triangle offset of each item in the block
     __shared__ int32_t srow[8];
     __shared__ uint32_t swarp[4];
-    // emit pass: one round's triangles (≤ 2 per item) staged here, then written out by the whole CTA
-    // with consecutive lanes on consecutive floats (coalesced) instead of 9 scattered 4-byte stores
-    // per triangle 36 B apart
-    __shared__ float sout[EMIT ? 2 * 128 * 9 : 1];   // 4 warp slices of 2 triangles x 32 lanes
-    __shared__ uint32_t goff[EMIT ? kMaxItems / 32 : 1];   // triangle offset of each 32-item group
-    const int64_t r = blockIdx.x;
-    if (r >= n_rows) return;
+    __shared__ float sout[EMIT ? 4 * 64 * 9 : 1];          // 4 warp slices of 64 triangles
+    __shared__ unsigned long long s_base;
+    __shared__ int64_t s_ci;
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    int64_t r, ci = 0;
+    if (EMIT) {
+        if (t == 0) s_ci = (int64_t)atomicAdd(O.ticket, 1u);
+        __syncthreads();
+        ci = s_ci;
+        r = O.inv[ci];
+    } else {
+        r = blockIdx.x;
+    }
     if (t == 0) {
         // blocks of the tile: index dx + 2dy + 4dz; chains +x → +y → +z (a missing intermediate block
         // holds a corner of every cell that needs the chained block, so such cells are skipped anyway)
@@ -224,33 +251,44 @@ __global__ void __launch_bounds__(128) k_extract(ExArgs A, int64_t n_rows, uint3
         sok[i] = ok;
     }
     __syncthreads();
-    const int32_t ci = A.perm[r];
-    const int gx = 8 * A.xyz[3 * ci], gy = 8 * A.xyz[3 * ci + 1], gz = 8 * A.xyz[3 * ci + 2];
     // (A) cells 4t … 4t+3 (voxel order): x = 4(t&1) + q, y = (t>>1)&7, z = t>>4
     const int cy = (t >> 1) & 7, cz = t >> 4;
-    uint32_t tets = 0;   // bit 6q + k: tetrahedron k of cell q crosses the level set
+    uint32_t tets = 0;             // bit 6q + k: tetrahedron k of cell q has triangles
+    unsigned long long tc = 0;     // its triangle count (1 or 2) at bits 2(6q + k)
+    uint32_t ntri = 0;
 #pragma unroll
     for (int q = 0; q < 4; q++) {
         const int cx = 4 * (t & 1) + q;
         bool ok = true;
-        int neg = 0;
+        int neg = 0, nz = 0;
 #pragma unroll
         for (int c8 = 0; c8 < 8; c8++) {
             const int idx = tile_index(cx, cy, cz, c8);
             ok = ok && sok[idx];
-            neg |= (su[idx] < 0.0f) << c8;   // X-3
+            const float v = su[idx];
+            neg |= (v < 0.0f) << c8;    // X-3
+            nz |= (v != 0.0f) << c8;
         }
         if (!ok || neg == 0 || neg == 255) continue;
-        uint32_t tm = 0;
 #pragma unroll
         for (int k = 0; k < 6; k++) {
-            const int m4 = (neg & 1) | (((neg >> tet_code(k, 1)) & 1) << 1) | (((neg >> tet_code(k, 2)) & 1) << 2) |
-                           (((neg >> tet_code(k, 3)) & 1) << 3);
-            tm |= (uint32_t)(m4 != 0 && m4 != 15) << k;
+            const int k1 = tet_code(k, 1), k2 = tet_code(k, 2), k3 = tet_code(k, 3);
+            const int m4 = (neg & 1) | (((neg >> k1) & 1) << 1) | (((neg >> k2) & 1) << 2) | (((neg >> k3) & 1) << 3);
+            const int z4 = (nz & 1) | (((nz >> k1) & 1) << 1) | (((nz >> k2) & 1) << 2) | (((nz >> k3) & 1) << 3);
+            const uint32_t c = tet_triangles(m4, z4);
+            tets |= (uint32_t)(c != 0) << (6 * q + k);
+            tc |= (unsigned long long)c << (2 * (6 * q + k));
+            ntri += c;
         }
-        tets |= tm << (6 * q);
     }
-    const uint32_t mine = __popc(tets);
+    if (!EMIT) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ntri += __shfl_xor_sync(0xffffffffu, ntri, o);
+        if (lane == 0 && ntri) atomicAdd(O.total, (unsigned long long)ntri);
+        return;
+    }
+    // block scan of (items, triangles), packed as items | triangles << 16 (≤ 3072 items, ≤ 6144 triangles)
+    const uint32_t mine = __popc(tets) | (ntri << 16);
     uint32_t x = mine;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -261,104 +299,80 @@ __global__ void __launch_bounds__(128) k_extract(ExArgs A, int64_t n_rows, uint3
     __syncthreads();
     uint32_t pos = x - mine;
     for (int w = 0; w < wid; w++) pos += swarp[w];
-    const uint32_t n_items = swarp[0] + swarp[1] + swarp[2] + swarp[3];
+    const uint32_t all = swarp[0] + swarp[1] + swarp[2] + swarp[3];
+    const uint32_t n_items = all & 0xFFFFu, block_total = all >> 16;
+    uint32_t ip = pos & 0xFFFFu, tp = pos >> 16;
     while (tets) {
         const int bit = __ffs(tets) - 1;
         tets &= tets - 1;
         const int q = bit / 6, k = bit - 6 * q;
-        sitem[pos++] = (uint16_t)(((4 * t + q) << 3) | k);
+        sitem[ip] = (uint16_t)(((4 * t + q) << 3) | k);
+        soff[ip++] = (uint16_t)tp;
+        tp += (uint32_t)(tc >> (2 * bit)) & 3u;
+    }
+    if (t == 0) soff[n_items] = (uint16_t)block_total;
+    // look-back (warp 0): publish this block's total, then sum the predecessors' words until an inclusive one
+    if (wid == 0) {
+        unsigned long long excl = 0;
+        if (ci == 0) {
+            if (lane == 0) st_volatile(&O.state[0], kInc | block_total);
+        } else {
+            if (lane == 0) st_volatile(&O.state[ci], kAgg | block_total);
+            int64_t end = ci - 1;   // predecessor read by lane 0
+            while (true) {
+                const int64_t j = end - lane;
+                unsigned long long w = j >= 0 ? ld_volatile(&O.state[j]) : kInc;
+                while (__any_sync(0xffffffffu, (w >> 62) == 0))
+                    if ((w >> 62) == 0) w = ld_volatile(&O.state[j]);
+                const uint32_t inc = __ballot_sync(0xffffffffu, (w >> 62) == 2);
+                // lanes up to (and including) the nearest inclusive word contribute
+                const int stop = inc ? __ffs(inc) - 1 : 31;
+                unsigned long long v = lane <= stop ? (w & kVal) : 0ull;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                excl += v;
+                if (inc) break;
+                end -= 32;
+            }
+            if (lane == 0) st_volatile(&O.state[ci], kInc | (excl + block_total));
+        }
+        if (lane == 0) {
+            s_base = excl;
+            if (ci == n_rows - 1) *O.total = excl + block_total;
+        }
     }
     __syncthreads();
-    // (B) items in list order.  Count pass: round-robin, item i = t + 128·round, 2 count bits per item
-    // stored per 32-item group (ballots).  Emit pass: the group totals (popcounts of those bits) are scanned
-    // once per block; then each warp takes whole groups (w, w + 4, …), places its lanes' triangles with a
-    // warp scan at the group's offset, stages them in its own slice of shared memory and writes them out
-    // with consecutive lanes on consecutive floats — no block-wide barrier inside the loop.
-    uint32_t block_total = 0;    // count pass: triangles of this thread's items
-    if (EMIT) {
-        const uint32_t ng = (n_items + 31) / 32;   // <= kMaxItems / 32 = 96
-        const uint32_t *wbb = item_bits + (size_t)r * kItemWords;
-        if (wid == 0) {
-            uint32_t c3[3], sum = 0;
-#pragma unroll
-            for (int j = 0; j < 3; j++) {
-                const uint32_t g = 3 * lane + j;
-                c3[j] = g < ng ? __popc(wbb[2 * g]) + 2 * __popc(wbb[2 * g + 1]) : 0u;
-                sum += c3[j];
-            }
-            uint32_t inc = sum;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-                if (lane >= o) inc += y;
-            }
-            uint32_t ex = inc - sum;
-#pragma unroll
-            for (int j = 0; j < 3; j++) {
-                goff[3 * lane + j] = ex;
-                ex += c3[j];
-            }
-        }
-        __syncthreads();
-        float *wsout = sout + wid * (2 * 32 * 9);
-        float *base_out = out + 9ull * offsets[ci];
-        for (uint32_t g = wid; g < ng; g += 4) {
-            const uint32_t i = 32 * g + lane;
-            const uint32_t w0 = wbb[2 * g], w1 = wbb[2 * g + 1];
-            const uint32_t cnt = i < n_items ? (((w0 >> lane) & 1u) | (((w1 >> lane) & 1u) << 1)) : 0u;
-            uint32_t y = cnt;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t z = __shfl_up_sync(0xffffffffu, y, o);
-                if (lane >= o) y += z;
-            }
-            const uint32_t gtot = __shfl_sync(0xffffffffu, y, 31);
-            if (cnt) {
-                const int cell = sitem[i] >> 3, k = sitem[i] & 7;
-                const int cx = cell & 7, cyy = (cell >> 3) & 7, czz = cell >> 6;
-                const int k1 = tet_code(k, 1), k2 = tet_code(k, 2), k3 = tet_code(k, 3);
-                unsigned m = 0;
-                const CellGeom G = cell_geom(gx + cx, gy + cyy, gz + czz, A.voxel);
-                tet<true>(0, k1, k2, k3, su[tile_index(cx, cyy, czz, 0)], su[tile_index(cx, cyy, czz, k1)],
-                          su[tile_index(cx, cyy, czz, k2)], su[tile_index(cx, cyy, czz, k3)], G,
-                          wsout + 9 * (y - cnt), m);
-            }
-            __syncwarp();
-            float *dst = base_out + 9ull * goff[g];
-            for (uint32_t j = lane; j < 9 * gtot; j += 32) dst[j] = wsout[j];
-            __syncwarp();
-        }
-    } else {
-        for (uint32_t i0 = 0; i0 < n_items; i0 += 128) {
-            const uint32_t i = i0 + t;
-            int cell = 0, k = 0;
-            if (i < n_items) {
-                cell = sitem[i] >> 3;
-                k = sitem[i] & 7;
-            }
+    const unsigned long long base = s_base;
+    const int32_t cidx = A.perm[r];
+    const int gx = 8 * A.xyz[3 * cidx], gy = 8 * A.xyz[3 * cidx + 1], gz = 8 * A.xyz[3 * cidx + 2];
+    const uint32_t ng = (n_items + 31) / 32;
+    float *wsout = sout + wid * (64 * 9);
+    const long long cap = O.max_tris;
+    for (uint32_t g = wid; g < ng; g += 4) {
+        const uint32_t i = 32 * g + lane;
+        const uint32_t g0 = soff[32 * g], g1 = soff[min(32 * g + 32, n_items)];
+        if (i < n_items) {
+            const int cell = sitem[i] >> 3, k = sitem[i] & 7;
             const int cx = cell & 7, cyy = (cell >> 3) & 7, czz = cell >> 6;
             const int k1 = tet_code(k, 1), k2 = tet_code(k, 2), k3 = tet_code(k, 3);
-            unsigned m = 0;
-            if (i < n_items)
-                tet<false>(0, k1, k2, k3, su[tile_index(cx, cyy, czz, 0)], su[tile_index(cx, cyy, czz, k1)],
-                           su[tile_index(cx, cyy, czz, k2)], su[tile_index(cx, cyy, czz, k3)], CellGeom{}, nullptr, m);
-            const uint32_t b0 = __ballot_sync(0xffffffffu, m & 1u), b1 = __ballot_sync(0xffffffffu, (m >> 1) & 1u);
-            if (lane == 0 && i0 + 32 * wid < n_items) {
-                uint32_t *wb = item_bits + (size_t)r * kItemWords + 2 * ((i0 >> 5) + wid);
-                wb[0] = b0;
-                wb[1] = b1;
-            }
-            block_total += m;
+            const CellGeom G = cell_geom(gx + cx, gy + cyy, gz + czz, A.voxel);
+            tet_emit(k1, k2, k3, su[tile_index(cx, cyy, czz, 0)], su[tile_index(cx, cyy, czz, k1)],
+                     su[tile_index(cx, cyy, czz, k2)], su[tile_index(cx, cyy, czz, k3)], G,
+                     wsout + 9 * (soff[i] - g0));
         }
+        __syncwarp();
+        const long long first = (long long)(base + g0);
+        const long long room = cap - first;
+        const uint32_t nt = room <= 0 ? 0u : (room < (long long)(g1 - g0) ? (uint32_t)room : g1 - g0);
+        float *dst = O.out + 9ull * (unsigned long long)first;
+        for (uint32_t j = lane; j < 9 * nt; j += 32) dst[j] = wsout[j];
+        __syncwarp();
     }
-    if (!EMIT) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) block_total += __shfl_xor_sync(0xffffffffu, block_total, o);
-        __syncthreads();
-        if (lane == 0) swarp[wid] = block_total;
-        __syncthreads();
-        if (t == 0) block_counts[ci] = swarp[0] + swarp[1] + swarp[2] + swarp[3];
-    }
+}
+
+__global__ void k_invert_perm(const int32_t *__restrict__ perm, int32_t *__restrict__ inv, int64_t n) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < n) inv[perm[r]] = (int32_t)r;
 }
 
 }  // namespace
@@ -379,34 +393,50 @@ extern "C" vol_status vol_extract(vol_t v, int field, float voxel, float w_min, 
     if (tris && max_tris < 0) return fail(VOL_EINVAL, "vol_extract: max_tris < 0");
     const int64_t n = v->L.n_local;
     cudaStream_t s = v->stream;
-    uint32_t *counts = v->d_count;                                   // [n] (build scratch, T >= 2n)
-    uint32_t *offs = v->d_hash;                                      // [n + 1] (build scratch)
-    // [n][192] words: 2 bits per (cell, tetrahedron) item (768 B per block <= the 2 KiB per block of d_tmp)
-    uint32_t *tcounts = reinterpret_cast<uint32_t *>(v->d_tmp);
+    if (n == 0) return VOL_OK;
+    // scratch in d_tmp (n × 2 KiB): look-back words [n] u64, ticket, total, inverse permutation [n] i32
+    unsigned long long *state = reinterpret_cast<unsigned long long *>(v->d_tmp);
+    unsigned *ticket = reinterpret_cast<unsigned *>(state + n);
+    unsigned long long *total = state + n + 1;
+    int32_t *inv = reinterpret_cast<int32_t *>(state + n + 2);
     ExArgs A{field == 0 ? v->F.u : v->F.f, v->F.W, v->d_nbr, v->d_perm, v->d_xyz, voxel, w_min};
-    k_extract<false><<<(unsigned)n, 128, 0, s>>>(A, n, counts, tcounts, nullptr, nullptr);
-    CK(cudaPeekAtLastError());
-    counted(1);
-    CKL(launch_exclusive_scan_u32(counts, offs, n, v->d_scan, s));
-    uint32_t total = 0;
-    CK(cudaMemcpyAsync(&total, offs + n, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    *n_tris = (int64_t)total;
-    if (!tris) return VOL_OK;
-    if ((int64_t)total > max_tris)
-        return fail(VOL_ENOMEM, "vol_extract: %lld triangles > max_tris = %lld", (long long)total, (long long)max_tris);
-    if (total == 0) return VOL_OK;
-    const bool dev = is_device_ptr(tris);
+    const bool dev = tris && is_device_ptr(tris);
+    unsigned long long m = 0;
     float *out = tris;
-    if (!dev) CK(cudaMallocAsync((void **)&out, (size_t)total * 36, s));
-    k_extract<true><<<(unsigned)n, 128, 0, s>>>(A, n, nullptr, tcounts, offs, out);
-    cudaError_t e = cudaPeekAtLastError();
-    if (e == cudaSuccess) counted(1);
     if (!dev) {
-        if (e == cudaSuccess) e = cudaMemcpyAsync(tris, out, (size_t)total * 36, cudaMemcpyDeviceToHost, s);
-        cudaFreeAsync(out, s);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        // count pass (count only, or a host buffer: the device staging buffer is sized by it)
+        CK(cudaMemsetAsync(total, 0, 8, s));
+        k_extract<false><<<(unsigned)n, 128, 0, s>>>(A, n, ExOut{nullptr, nullptr, nullptr, total, nullptr, 0});
+        CK(cudaPeekAtLastError());
+        counted(1);
+        CK(cudaMemcpyAsync(&m, total, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        *n_tris = (int64_t)m;
+        if (!tris) return VOL_OK;
+        if ((int64_t)m > max_tris)
+            return fail(VOL_ENOMEM, "vol_extract: %lld triangles > max_tris = %lld", (long long)m, (long long)max_tris);
+        if (m == 0) return VOL_OK;
+        CK(cudaMallocAsync((void **)&out, (size_t)m * 36, s));
+        max_tris = (int64_t)m;
     }
+    // single ordered pass: count, look-back, emit
+    cudaError_t e = cudaMemsetAsync(state, 0, ((size_t)n + 2) * 8, s);
+    if (e == cudaSuccess) {
+        k_invert_perm<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(v->d_perm, inv, n);
+        k_extract<true><<<(unsigned)n, 128, 0, s>>>(A, n, ExOut{inv, state, ticket, total, out, max_tris});
+        e = cudaPeekAtLastError();
+        if (e == cudaSuccess) counted(2);
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&m, total, 8, cudaMemcpyDeviceToHost, s);
+    if (!dev) {
+        if (e == cudaSuccess) e = cudaMemcpyAsync(tris, out, (size_t)max_tris * 36, cudaMemcpyDeviceToHost, s);
+        cudaFreeAsync(out, s);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return fail(VOL_ECUDA, "vol_extract: %s", cudaGetErrorString(e));
+    *n_tris = (int64_t)m;
+    if ((int64_t)m > max_tris)
+        return fail(VOL_ENOMEM, "vol_extract: %lld triangles > max_tris = %lld (the first max_tris written)",
+                    (long long)m, (long long)max_tris);
     return VOL_OK;
 }
