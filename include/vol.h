@@ -260,8 +260,10 @@ vol_status vol_release_comms(void);
  * of 3 vertices), ordered by caller block, cell (voxel order), tetrahedron, triangle.
  *   field   0: the current u (u = f from vol_create until the first vol_regularise), 1: the fused f;
  *   tris    host or device buffer of max_tris triangles, or NULL to count only; *n_tris receives m.
- * Synchronous.  Errors: VOL_EINVAL, VOL_ENOMEM (m > max_tris; *n_tris = m), VOL_ENOTSUP (sharded
- * volume), VOL_ECUDA.                                                                               */
+ * A device buffer is filled in one ordered pass (count, look-back, emit); a host buffer is sized by a
+ * counting pass first.  Synchronous.  Errors: VOL_EINVAL, VOL_ENOMEM (m > max_tris; *n_tris = m; a
+ * device buffer then holds the first max_tris triangles, a host buffer is untouched), VOL_ENOTSUP
+ * (sharded volume), VOL_ECUDA.                                                                      */
 vol_status vol_extract(vol_t v, int field, float voxel, float w_min, float *tris, int64_t max_tris, int64_t *n_tris);
 
 /* Depth-map estimation from rectified stereo (paper §IV) ----------

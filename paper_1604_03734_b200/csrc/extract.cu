@@ -68,7 +68,7 @@ __device__ __forceinline__ void edge_vertex(const CellGeom &G, int ca, float ua,
     const float t = __fdiv_rn(ulo, __fsub_rn(ulo, uhi));
 #pragma unroll
     for (int k = 0; k < 3; k++)
-        p[k] = ((d >> k) & 1) ? __fadd_rn(G.X[0][k], __fmul_rn(t, G.dX[k])) : G.X[(lo >> k) & 1][k];
+        p[k] = ((d >> k) & 1) ? __fadd_rn(G.X[0][k], __fmul_rn(t, G.dX[k])) : (((lo >> k) & 1) ? G.X[1][k] : G.X[0][k]);
 }
 
 // X-2: the 6 Freudenthal tetrahedra 000 → e_a → e_a + e_b → 111 for the axis permutations (a, b, c) in
@@ -166,6 +166,7 @@ __device__ __forceinline__ void tet_emit(int k1, int k2, int k3, float v0, float
 }
 
 constexpr int kMaxItems = 512 * 6;   // (cell, tetrahedron) pairs of one block
+constexpr int kSlice = 64 * 9 + 4;   // floats of one warp's staging slice: 64 triangles + alignment shift
 
 // Output of one call.  Count pass (EMIT = false): only *total (atomic sum of the block totals).  Emit pass:
 // CTAs take caller blocks in ticket order and find their triangle offset by decoupled look-back over the
@@ -177,8 +178,9 @@ struct ExOut {
     unsigned long long *state;           // [n] look-back words (zeroed)
     unsigned *ticket;                    // CTA ticket (zeroed)
     unsigned long long *total;           // triangles of the call (zeroed)
-    float *out;
+    float *out;                          // 16-byte aligned when vec
     long long max_tris;
+    int vec;
 };
 
 constexpr unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62, kVal = (1ull << 62) - 1;
@@ -204,7 +206,7 @@ __global__ void __launch_bounds__(128) k_extract(ExArgs A, int64_t n_rows, ExOut
     __shared__ uint16_t soff[EMIT ? kMaxItems + 1 : 1];    // triangle offset of each item in the block
     __shared__ int32_t srow[8];
     __shared__ uint32_t swarp[4];
-    __shared__ float sout[EMIT ? 4 * 64 * 9 : 1];          // 4 warp slices of 64 triangles
+    __shared__ __align__(16) float sout[EMIT ? 4 * kSlice : 1];   // 4 warp slices of 64 triangles (+ align)
     __shared__ unsigned long long s_base;
     __shared__ int64_t s_ci;
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
@@ -236,19 +238,40 @@ __global__ void __launch_bounds__(128) k_extract(ExArgs A, int64_t n_rows, ExOut
         srow[7] = bxyz;
     }
     __syncthreads();
-    for (int i = t; i < kTile; i += 128) {
-        const int x = i % kT, y = (i / kT) % kT, z = i / (kT * kT);
-        const int blk = srow[(x >> 3) + 2 * (y >> 3) + 4 * (z >> 3)];
-        float uv = 0.0f;
-        uint8_t ok = 0;
-        if (blk >= 0) {
-            const int64_t o = (int64_t)blk * kBlockVox + (x & 7) + 8 * (y & 7) + 64 * (z & 7);
-            const float w = A.W[o];
-            uv = A.val[o];
-            ok = (w > 0.0f && w >= A.w_min) ? 1 : 0;   // X-1
+    // the caller block's origin (emit pass), loaded before the tile so its latency overlaps the staging
+    int gx = 0, gy = 0, gz = 0;
+    if (EMIT) {
+        const int32_t cidx = A.perm[r];
+        gx = 8 * A.xyz[3 * cidx];
+        gy = 8 * A.xyz[3 * cidx + 1];
+        gz = 8 * A.xyz[3 * cidx + 2];
+    }
+    {
+        constexpr int kIt = (kTile + 127) / 128;   // 6 loads of u and W per thread, all issued before use
+        float uv[kIt], wv[kIt];
+#pragma unroll
+        for (int it = 0; it < kIt; it++) {
+            const int i = t + 128 * it;
+            uv[it] = 0.0f;
+            wv[it] = 0.0f;
+            if (i < kTile) {
+                const int x = i % kT, y = (i / kT) % kT, z = i / (kT * kT);
+                const int blk = srow[(x >> 3) + 2 * (y >> 3) + 4 * (z >> 3)];
+                if (blk >= 0) {
+                    const int64_t o = (int64_t)blk * kBlockVox + (x & 7) + 8 * (y & 7) + 64 * (z & 7);
+                    wv[it] = A.W[o];
+                    uv[it] = A.val[o];
+                }
+            }
         }
-        su[i] = uv;
-        sok[i] = ok;
+#pragma unroll
+        for (int it = 0; it < kIt; it++) {
+            const int i = t + 128 * it;
+            if (i < kTile) {
+                su[i] = uv[it];
+                sok[i] = (wv[it] > 0.0f && wv[it] >= A.w_min) ? 1 : 0;   // X-1 (unallocated: W = 0)
+            }
+        }
     }
     __syncthreads();
     // (A) cells 4t … 4t+3 (voxel order): x = 4(t&1) + q, y = (t>>1)&7, z = t>>4
@@ -343,14 +366,15 @@ __global__ void __launch_bounds__(128) k_extract(ExArgs A, int64_t n_rows, ExOut
     }
     __syncthreads();
     const unsigned long long base = s_base;
-    const int32_t cidx = A.perm[r];
-    const int gx = 8 * A.xyz[3 * cidx], gy = 8 * A.xyz[3 * cidx + 1], gz = 8 * A.xyz[3 * cidx + 2];
     const uint32_t ng = (n_items + 31) / 32;
-    float *wsout = sout + wid * (64 * 9);
+    float *wsout = sout + wid * kSlice;
     const long long cap = O.max_tris;
     for (uint32_t g = wid; g < ng; g += 4) {
         const uint32_t i = 32 * g + lane;
         const uint32_t g0 = soff[32 * g], g1 = soff[min(32 * g + 32, n_items)];
+        const long long first = (long long)(base + g0);
+        // stage at the global address's offset within 16 bytes, so that whole float4s copy out
+        const uint32_t shift = O.vec ? (uint32_t)(9ull * (unsigned long long)first) & 3u : 0u;
         if (i < n_items) {
             const int cell = sitem[i] >> 3, k = sitem[i] & 7;
             const int cx = cell & 7, cyy = (cell >> 3) & 7, czz = cell >> 6;
@@ -358,14 +382,23 @@ __global__ void __launch_bounds__(128) k_extract(ExArgs A, int64_t n_rows, ExOut
             const CellGeom G = cell_geom(gx + cx, gy + cyy, gz + czz, A.voxel);
             tet_emit(k1, k2, k3, su[tile_index(cx, cyy, czz, 0)], su[tile_index(cx, cyy, czz, k1)],
                      su[tile_index(cx, cyy, czz, k2)], su[tile_index(cx, cyy, czz, k3)], G,
-                     wsout + 9 * (soff[i] - g0));
+                     wsout + shift + 9 * (soff[i] - g0));
         }
         __syncwarp();
-        const long long first = (long long)(base + g0);
         const long long room = cap - first;
         const uint32_t nt = room <= 0 ? 0u : (room < (long long)(g1 - g0) ? (uint32_t)room : g1 - g0);
-        float *dst = O.out + 9ull * (unsigned long long)first;
-        for (uint32_t j = lane; j < 9 * nt; j += 32) dst[j] = wsout[j];
+        float *dst = O.out + 9ull * (unsigned long long)first - shift;   // element e ↔ wsout[e], e ∈ [shift, end)
+        const uint32_t end = shift + 9 * nt;
+        if (O.vec) {
+            const uint32_t q_lo = (shift + 3) / 4, q_hi = end / 4;
+            for (uint32_t q = q_lo + lane; q < q_hi; q += 32)
+                reinterpret_cast<float4 *>(dst)[q] = reinterpret_cast<const float4 *>(wsout)[q];
+            const uint32_t head_end = min(4 * q_lo, end), tail = max(4 * q_hi, head_end);
+            const uint32_t e = lane < 4 ? shift + lane : tail + (lane - 4);
+            if (lane < 8 && e < (lane < 4 ? head_end : end)) dst[e] = wsout[e];
+        } else {
+            for (uint32_t j = lane; j < end; j += 32) dst[j] = wsout[j];
+        }
         __syncwarp();
     }
 }
@@ -406,7 +439,7 @@ extern "C" vol_status vol_extract(vol_t v, int field, float voxel, float w_min, 
     if (!dev) {
         // count pass (count only, or a host buffer: the device staging buffer is sized by it)
         CK(cudaMemsetAsync(total, 0, 8, s));
-        k_extract<false><<<(unsigned)n, 128, 0, s>>>(A, n, ExOut{nullptr, nullptr, nullptr, total, nullptr, 0});
+        k_extract<false><<<(unsigned)n, 128, 0, s>>>(A, n, ExOut{nullptr, nullptr, nullptr, total, nullptr, 0, 0});
         CK(cudaPeekAtLastError());
         counted(1);
         CK(cudaMemcpyAsync(&m, total, 8, cudaMemcpyDeviceToHost, s));
@@ -423,7 +456,7 @@ extern "C" vol_status vol_extract(vol_t v, int field, float voxel, float w_min, 
     cudaError_t e = cudaMemsetAsync(state, 0, ((size_t)n + 2) * 8, s);
     if (e == cudaSuccess) {
         k_invert_perm<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(v->d_perm, inv, n);
-        k_extract<true><<<(unsigned)n, 128, 0, s>>>(A, n, ExOut{inv, state, ticket, total, out, max_tris});
+        k_extract<true><<<(unsigned)n, 128, 0, s>>>(A, n, ExOut{inv, state, ticket, total, out, max_tris, ((uintptr_t)out & 15) == 0});
         e = cudaPeekAtLastError();
         if (e == cudaSuccess) counted(2);
     }

@@ -14,10 +14,11 @@ def bench(path):
           f"clocks={d['clocks']} launches={d['gpu_launches']}")
 
 
-def raw(rep):
+def raw(rep, idx=0):
     out = subprocess.check_output(["ncu", "-i", rep, "--page", "raw", "--csv"], stderr=subprocess.DEVNULL).decode()
     rows = list(csv.reader(out.splitlines()))
-    H, U, D = rows[0], rows[1], rows[2]
+    H, U, D = rows[0], rows[1], rows[2 + idx]
+    print(f"  [{idx}] {D[H.index('Kernel Name')][:80]}")
     want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
             "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
             "launch__registers_per_thread", "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem",
@@ -41,9 +42,9 @@ def raw(rep):
     return vals
 
 
-def sass(rep, top=20):
-    out = subprocess.check_output(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass"],
-                                  stderr=subprocess.DEVNULL).decode()
+def sass(rep, top=20, idx=0):
+    out = subprocess.check_output(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass",
+                                   "--launch-skip", str(idx), "--launch-count", "1"], stderr=subprocess.DEVNULL).decode()
     rows = list(csv.reader(out.splitlines()))
     H = rows[1]
     data = []
@@ -88,8 +89,9 @@ if __name__ == "__main__":
     for a in sys.argv[1:]:
         if a.endswith(".log"):
             bench(a)
-        elif a.endswith(".ncu-rep"):
-            raw(a)
-            sass(a)
+        elif ".ncu-rep" in a:   # report[@launch index]
+            rep, _, i = a.partition("@")
+            raw(rep, int(i or 0))
+            sass(rep, idx=int(i or 0))
         elif a.endswith(".csv"):
             launches(a)

@@ -146,3 +146,36 @@ def test_degenerate_and_tiny_t_bit_exact(Vol):
     To = oracle.extract(c, u, W, V)
     assert To.shape[0] > 0
     _same(T, To)
+
+
+def test_device_output_offsets_and_overflow(Vol):
+    """The ordered single pass into a device buffer: every 4-byte offset of the output pointer (the copy-out
+    stages whole float4s at the buffer's alignment), and a buffer that is too small: VOL_ENOMEM with the
+    exact count, the first max_tris triangles written in order and nothing past the buffer."""
+    import ctypes
+    from paper_1604_03734_b200 import _native as N
+    c, u = _sphere(blocks=3, r_vox=10.5, c_vox=12.3)
+    W = np.ones_like(u)
+    rng = np.random.default_rng(5)
+    perm = rng.permutation(c.shape[0])
+    c, u = c[perm], u[perm]
+    vol = Vol(torch.from_numpy(c).cuda(), torch.from_numpy(u).cuda(), torch.from_numpy(W).cuda())
+    ref = oracle.extract(c, u, W, V)
+    n = ref.shape[0]
+    assert n > 1000
+    L = N.lib()
+    m = ctypes.c_int64()
+    for off in range(4):
+        buf = torch.full((n * 9 + 64,), 7.0, device="cuda")
+        st = L.vol_extract(vol._h, 1, V, 0.0, ctypes.c_void_p(buf.data_ptr() + 4 * off), n, ctypes.byref(m))
+        assert st == N.VOL_OK and m.value == n
+        h = buf.cpu().numpy()
+        _same(h[off:off + 9 * n].reshape(n, 3, 3), ref)
+        assert (h[:off] == 7.0).all() and (h[off + 9 * n:] == 7.0).all()
+    for cap in (0, 1, 333, n - 1):
+        buf = torch.full((n * 9 + 64,), 7.0, device="cuda")
+        st = L.vol_extract(vol._h, 1, V, 0.0, ctypes.c_void_p(buf.data_ptr() + 4), cap, ctypes.byref(m))
+        assert st == N.VOL_ENOMEM and m.value == n
+        h = buf.cpu().numpy()
+        _same(h[1:1 + 9 * cap].reshape(cap, 3, 3), ref[:cap])
+        assert (h[:1] == 7.0).all() and (h[1 + 9 * cap:] == 7.0).all()
