@@ -86,10 +86,6 @@ __device__ __forceinline__ int tile_index(int cx, int cy, int cz, int code) {
     return (cx + (code & 1)) + kT * (cy + ((code >> 1) & 1)) + kT * kT * (cz + (code >> 2));
 }
 
-__device__ __forceinline__ float sel4f(int i, float a0, float a1, float a2, float a3) {
-    return i == 0 ? a0 : (i == 1 ? a1 : (i == 2 ? a2 : a3));
-}
-
 // Triangles of one tetrahedron (X-5, X-6), from its 4-bit inside mask (bit i: corner i has value < 0, X-3)
 // and its 4-bit mask of corners with value ≠ 0: one for a lone inside corner; otherwise one per outside
 // corner whose value is not exactly 0 (X-6: with 3 inside, the triangle degenerates iff the outside corner is
@@ -99,15 +95,26 @@ __device__ __forceinline__ uint32_t tet_triangles(int m4, int nz4) {
     return __popc(m4) == 1 ? 1u : (uint32_t)__popc(nz4 & ~m4 & 15);
 }
 
-// One tetrahedron with corner codes (0, k1, k2, k3) in positively oriented order (X-2) and values
-// (v0 … v3).  X-5: the lone corner (nin = 1: the inside one, nin = 3: the outside one) or the inside pair
-// goes first, the remaining corners follow in tetrahedron order, and the last two are swapped when that
-// permutation is odd, so (a, b, c, d) stays positively oriented.  Triangles: 1 inside (E_ab, E_ac, E_ad),
-// 3 inside (E_ab, E_ad, E_ac), 2 inside (E_ac, E_ad, E_bd) + (E_ac, E_bd, E_bc); with the edges
+// Corner codes and tile offsets of the 4 corners of tetrahedron q, one byte per corner (corner 0 first):
+// code c ↔ tile offset (c & 1) + 9·((c >> 1) & 1) + 81·(c >> 2) from the cell's origin in the 9³ tile.
+__host__ __device__ constexpr int tile_off(int c) { return (c & 1) + kT * ((c >> 1) & 1) + kT * kT * (c >> 2); }
+__device__ __forceinline__ uint2 tet_words(int q) {
+    const int k1 = tet_code(q, 1), k2 = tet_code(q, 2), k3 = tet_code(q, 3);
+    return make_uint2((uint32_t)((k1 << 8) | (k2 << 16) | (k3 << 24)),
+                      (uint32_t)((tile_off(k1) << 8) | (tile_off(k2) << 16) | (tile_off(k3) << 24)));
+}
+__device__ __forceinline__ uint32_t byte_of(uint32_t w, int i) { return __byte_perm(w, 0u, 0x4440u | (uint32_t)i); }
+
+// One tetrahedron (corner codes and tile offsets TW = tet_words, positively oriented order, X-2) of the
+// cell whose origin is sb[0] in the staged tile, values v0 … v3.  X-5: the lone corner (nin = 1: the inside
+// one, nin = 3: the outside one) or the inside pair goes first, the remaining corners follow in tetrahedron
+// order, and the last two are swapped when that permutation is odd, so (a, b, c, d) stays positively
+// oriented.  Triangles: 1 inside (E_ab, E_ac, E_ad), 3 inside (E_ab, E_ad, E_ac), 2 inside (E_ac, E_ad, E_bd)
+// + (E_ac, E_bd, E_bc); with the edges
 //   E0 = (a, quad ? c : b), E1 = (a, quad ? d : c), E2 = (quad ? b : a, d), E3 = (b, c)
 // these are (E0, E1, E2) [(E0, E2, E1) for 3 inside] and (E0, E2, E3): one code path for every case (the
 // lanes of a warp hold mixed cases).  The surviving triangles (X-6) are written to o[0 …], 9 floats each.
-__device__ __forceinline__ void tet_emit(int k1, int k2, int k3, float v0, float v1, float v2, float v3,
+__device__ __forceinline__ void tet_emit(uint2 TW, const float *sb, float v0, float v1, float v2, float v3,
                                          const CellGeom &G, float *o) {
     const int mask = (v0 < 0.0f) | ((v1 < 0.0f) << 1) | ((v2 < 0.0f) << 2) | ((v3 < 0.0f) << 3);   // X-3
     const int nin = __popc(mask);
@@ -132,11 +139,10 @@ __device__ __forceinline__ void tet_emit(int k1, int k2, int k3, float v0, float
         pc = (a & 1) ? r2 : r1;
         pd = (a & 1) ? r1 : r2;
     }
-    const int packed = (k1 << 4) | (k2 << 8) | (k3 << 12);   // corner code of position i at bits 4i
-    const int ca = (packed >> (4 * pa)) & 15, cb = (packed >> (4 * pb)) & 15;
-    const int cc = (packed >> (4 * pc)) & 15, cd = (packed >> (4 * pd)) & 15;
-    const float ua = sel4f(pa, v0, v1, v2, v3), ub = sel4f(pb, v0, v1, v2, v3);
-    const float uc = sel4f(pc, v0, v1, v2, v3), ud = sel4f(pd, v0, v1, v2, v3);
+    const int ca = (int)byte_of(TW.x, pa), cb = (int)byte_of(TW.x, pb);
+    const int cc = (int)byte_of(TW.x, pc), cd = (int)byte_of(TW.x, pd);
+    const float ua = sb[byte_of(TW.y, pa)], ub = sb[byte_of(TW.y, pb)];
+    const float uc = sb[byte_of(TW.y, pc)], ud = sb[byte_of(TW.y, pd)];
     const bool quad = nin == 2;
     float e0[3], e1[3], e2[3];
     edge_vertex(G, ca, ua, quad ? cc : cb, quad ? uc : ub, e0);
@@ -207,6 +213,7 @@ __global__ void __launch_bounds__(128) k_extract(ExArgs A, int64_t n_rows, ExOut
     __shared__ int32_t srow[8];
     __shared__ uint32_t swarp[4];
     __shared__ __align__(16) float sout[EMIT ? 4 * kSlice : 1];   // 4 warp slices of 64 triangles (+ align)
+    __shared__ uint2 stw[6];                                 // tet_words of the 6 tetrahedra
     __shared__ unsigned long long s_base;
     __shared__ int64_t s_ci;
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
@@ -219,6 +226,7 @@ __global__ void __launch_bounds__(128) k_extract(ExArgs A, int64_t n_rows, ExOut
     } else {
         r = blockIdx.x;
     }
+    if (EMIT && t < 6) stw[t] = tet_words(t);
     if (t == 0) {
         // blocks of the tile: index dx + 2dy + 4dz; chains +x → +y → +z (a missing intermediate block
         // holds a corner of every cell that needs the chained block, so such cells are skipped anyway)
@@ -325,6 +333,8 @@ __global__ void __launch_bounds__(128) k_extract(ExArgs A, int64_t n_rows, ExOut
     const uint32_t all = swarp[0] + swarp[1] + swarp[2] + swarp[3];
     const uint32_t n_items = all & 0xFFFFu, block_total = all >> 16;
     uint32_t ip = pos & 0xFFFFu, tp = pos >> 16;
+    // publish this block's total for its successors' look-back before writing the item list
+    if (t == 0) st_volatile(&O.state[ci], (ci == 0 ? kInc : kAgg) | block_total);
     while (tets) {
         const int bit = __ffs(tets) - 1;
         tets &= tets - 1;
@@ -334,13 +344,10 @@ __global__ void __launch_bounds__(128) k_extract(ExArgs A, int64_t n_rows, ExOut
         tp += (uint32_t)(tc >> (2 * bit)) & 3u;
     }
     if (t == 0) soff[n_items] = (uint16_t)block_total;
-    // look-back (warp 0): publish this block's total, then sum the predecessors' words until an inclusive one
+    // look-back (warp 0): sum the predecessors' words back to the nearest inclusive one
     if (wid == 0) {
         unsigned long long excl = 0;
-        if (ci == 0) {
-            if (lane == 0) st_volatile(&O.state[0], kInc | block_total);
-        } else {
-            if (lane == 0) st_volatile(&O.state[ci], kAgg | block_total);
+        if (ci > 0) {
             int64_t end = ci - 1;   // predecessor read by lane 0
             while (true) {
                 const int64_t j = end - lane;
@@ -378,10 +385,10 @@ __global__ void __launch_bounds__(128) k_extract(ExArgs A, int64_t n_rows, ExOut
         if (i < n_items) {
             const int cell = sitem[i] >> 3, k = sitem[i] & 7;
             const int cx = cell & 7, cyy = (cell >> 3) & 7, czz = cell >> 6;
-            const int k1 = tet_code(k, 1), k2 = tet_code(k, 2), k3 = tet_code(k, 3);
+            const uint2 TW = stw[k];
+            const float *sb = su + tile_index(cx, cyy, czz, 0);
             const CellGeom G = cell_geom(gx + cx, gy + cyy, gz + czz, A.voxel);
-            tet_emit(k1, k2, k3, su[tile_index(cx, cyy, czz, 0)], su[tile_index(cx, cyy, czz, k1)],
-                     su[tile_index(cx, cyy, czz, k2)], su[tile_index(cx, cyy, czz, k3)], G,
+            tet_emit(TW, sb, sb[0], sb[byte_of(TW.y, 1)], sb[byte_of(TW.y, 2)], sb[byte_of(TW.y, 3)], G,
                      wsout + shift + 9 * (soff[i] - g0));
         }
         __syncwarp();
