@@ -334,7 +334,8 @@ def fusion_leg(args, dev):
 
 
 def extraction_leg(args, dev, scene, iters, stream):
-    """vol_extract of the regularised street u (count pass + scan + ordered emit pass), inputs in HBM."""
+    """vol_extract of the regularised street u into a device buffer (one ordered pass: count, decoupled
+    look-back, emit), inputs in HBM."""
     import torch
 
     from paper_1604_03734_b200 import Volume
@@ -362,25 +363,25 @@ def extraction_leg(args, dev, scene, iters, stream):
     res = {"workload": scene.name + " (regularised u, " + str(iters) + " iterations)", "field": "u", "w_min": 0.0,
            "triangles": ntri, "cells": nvox, "ms_per_call": ms, "cells_per_s": nvox / (ms / 1e3),
            "triangles_per_s": ntri / (ms / 1e3),
-           "step": "vol_extract: count kernel + exclusive scan + ordered emit kernel, output in HBM",
+           "step": "vol_extract: inverse permutation + one ordered count/look-back/emit kernel, output in HBM",
            "hbm": {"achieved": alg / (ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
                    "frac": alg / (ms / 1e3) / 1e9 / peak, "alg_bytes_per_call": alg,
                    "note": "algorithmic bytes (read u and W once, write 36 B per triangle); not the bound"}}
-    nc, ne = (ncu_inputs().get(k) for k in ("k_extract_count/street", "k_extract_emit/street"))
+    ne = ncu_inputs().get("k_extract/street")
     ip, ip_src = issue_peak()
-    if nc and ne and scene.name == "street":
-        inst = nc["warp_instructions"] + ne["warp_instructions"]
+    if ne and scene.name == "street":
+        inst = ne["warp_instructions"]
         iss = inst / (ms / 1e3)
-        res["roofline"] = {"bound": "issue", "kernel": "k_extract (count + emit)", "achieved": iss / 1e12,
+        res["roofline"] = {"bound": "issue", "kernel": "k_extract (single ordered pass)", "achieved": iss / 1e12,
                            "peak": ip / 1e12, "unit": "T warp-instructions/s", "frac": iss / ip, "peak_source": ip_src,
-                           "basis": "physical: ncu warp instructions of both passes / CUDA-event call time",
+                           "basis": "physical: ncu warp instructions of the pass / CUDA-event call time",
                            "warp_instructions_per_call": inst,
                            "thread_instructions_per_triangle": 32 * inst / max(ntri, 1),
-                           "traffic": nc["dram_bytes"] + ne["dram_bytes"], "sources": [nc["source"], ne["source"]]}
+                           "traffic": ne["dram_bytes"], "sources": [ne["source"]]}
     else:
-        res["roofline"] = {"bound": "issue", "kernel": "k_extract (count + emit)", "achieved": None, "peak": ip / 1e12,
-                           "unit": "T warp-instructions/s", "frac": None, "peak_source": ip_src, "traffic": None,
-                           "basis": "no ncu capture of this workload"}
+        res["roofline"] = {"bound": "issue", "kernel": "k_extract (single ordered pass)", "achieved": None,
+                           "peak": ip / 1e12, "unit": "T warp-instructions/s", "frac": None, "peak_source": ip_src,
+                           "traffic": None, "basis": "no ncu capture of this workload"}
     vol.close()
     return res
 
