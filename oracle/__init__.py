@@ -22,10 +22,16 @@ Parity status per function:
                           intersection, dense numpy brute force O2-fusion) — ``fusion_oracle.c``
   stereo (§IV) .......... pinned (census worked example, strict-order invariance, shifted-pair WTA, tensor
                           closed forms and eigen-structure, K/Kᵀ adjointness, dual feasibility,
-                          constant and slanted-plane disparities, λ → ∞ gives WTA) — ``stereo_oracle.c``
+                          constant and slanted-plane disparities, λ → ∞ gives WTA) — ``stereo_oracle.c``;
+                          ``oracle.stereo64``: a float64 numpy solve (textbook division forms), pinned by
+                          operator adjointness, tensor closed forms and agreement with the C oracle
+  fusion, float64 ....... ``oracle.dense_fusion`` precision "f64" (plain x/z projection), pinned by the
+                          fronto-parallel closed form and agreement with the fp32 dense fusion
   extraction ............ pinned (planar fields: vertices on the plane, exact area, orientation; analytic
                           sphere: closed 2-manifold, Euler characteristic 2, area/volume; Ω
-                          restriction) — ``extract_oracle.c``
+                          restriction) — ``extract_oracle.c``; ``oracle.extract64``: a float64 numpy
+                          version with geometric (determinant) orientation, pinned to the C oracle and
+                          to planar fields (vertices on the plane to 1e-12)
 """
 from __future__ import annotations
 

@@ -14,11 +14,16 @@ import numpy as np
 F = np.float32
 
 
-def fuse_dense(depth, intr, poses, voxel, mu, max_range, w_max, lo, hi):
+def fuse_dense(depth, intr, poses, voxel, mu, max_range, w_max, lo, hi, precision="f32"):
     """Fuse K depth maps into the dense voxel box lo <= g <= hi (global voxel coords, inclusive).
 
-    Returns (f, W) float32 arrays of shape [nz, ny, nx] (index [gz−lo_z, gy−lo_y, gx−lo_x]).
+    Returns (f, W) arrays of shape [nz, ny, nx] (index [gz−lo_z, gy−lo_y, gx−lo_x]).
+    precision "f32": the written fp32 order of the hashed-grid oracle and the kernel (reading F-12: one
+    reciprocal of z_c); "f64": every step in float64 with the paper's plain x/z, y/z — the
+    independent-precision reference (inputs are the same fp32 numbers, widened).
     """
+    if precision == "f64":
+        return _fuse_dense_f64(depth, intr, poses, voxel, mu, max_range, w_max, lo, hi)
     D = np.asarray(depth, F)
     if D.ndim == 2:
         D = D[None]
@@ -64,4 +69,40 @@ def fuse_dense(depth, intr, poses, voxel, mu, max_range, w_max, lo, hi):
         wn = np.minimum(w + F(1), wmax)
         f = np.where(upd, fn, f).astype(F)
         w = np.where(upd, wn, w).astype(F)
+    return f, w
+
+
+def _fuse_dense_f64(depth, intr, poses, voxel, mu, max_range, w_max, lo, hi):
+    """Steps 1-4 of P:152-176 in float64 (no reciprocal reading)."""
+    G = np.float64
+    D = np.asarray(depth, F).astype(G)
+    if D.ndim == 2:
+        D = D[None]
+    K, H, Wd = D.shape
+    fx, fy, cx, cy = (G(v) for v in np.asarray(intr, F).reshape(4))
+    P = np.asarray(poses, F).reshape(K, 12).astype(G)
+    v, mu, rmax, wmax = G(F(voxel)), G(F(mu)), G(F(max_range)), G(F(w_max))
+    gz, gy, gx = np.meshgrid(np.arange(lo[2], hi[2] + 1), np.arange(lo[1], hi[1] + 1), np.arange(lo[0], hi[0] + 1),
+                             indexing="ij")
+    px, py, pz = (gx + 0.5) * v, (gy + 0.5) * v, (gz + 0.5) * v
+    f = np.zeros(px.shape, G)
+    w = np.zeros(px.shape, G)
+    for k in range(K):
+        T = P[k]
+        d0, d1, d2 = px - T[3], py - T[7], pz - T[11]
+        xc = T[0] * d0 + T[4] * d1 + T[8] * d2     # p_c = R^T (p_g − t)
+        yc = T[1] * d0 + T[5] * d1 + T[9] * d2
+        zc = T[2] * d0 + T[6] * d1 + T[10] * d2
+        front = zc > 0
+        zs = np.where(front, zc, 1.0)
+        fi = np.floor(fx * xc / zs + cx + 0.5)     # nearest pixel (P:156)
+        fj = np.floor(fy * yc / zs + cy + 0.5)
+        inside = front & (fi >= 0) & (fi < Wd) & (fj >= 0) & (fj < H)
+        d = D[k][np.where(inside, fj, 0).astype(np.int64), np.where(inside, fi, 0).astype(np.int64)]
+        valid = inside & np.isfinite(d) & (d > 0) & (d <= rmax)
+        sdf = np.where(valid, d, 0.0) - zc
+        upd = valid & (sdf >= -mu)
+        tsdf = np.clip(sdf, -mu, mu) / mu
+        f = np.where(upd, (tsdf + w * f) / (w + 1), f)
+        w = np.where(upd, np.minimum(w + 1, wmax), w)
     return f, w

@@ -179,3 +179,29 @@ def test_device_output_offsets_and_overflow(Vol):
         h = buf.cpu().numpy()
         _same(h[1:1 + 9 * cap].reshape(cap, 3, 3), ref[:cap])
         assert (h[:1] == 7.0).all() and (h[1 + 9 * cap:] == 7.0).all()
+
+
+@pytest.mark.parametrize("case", ["sphere", "random"])
+def test_within_fp64_extraction(Vol, case):
+    """Independent-precision check: the kernel's triangles against the float64 numpy extraction
+    (oracle/extract64.py — written separately from the C oracle, orientation by determinant): same
+    triangles in the same order (topology is decided on exact signs and zeros), each equal up to a cyclic
+    rotation of its vertices (which keeps the orientation), vertices within 1e-6 (fp32 rounding of
+    coordinates below 3 m is ~2.4e-7)."""
+    from oracle.extract64 import extract_f64, match_up_to_rotation
+    if case == "sphere":
+        c, u = _sphere()
+        W = np.ones_like(u)
+    else:
+        rng = np.random.default_rng(9)
+        c = dense_box(2, 2, 2).coords.numpy()
+        u = rng.normal(size=(c.shape[0], 512)).astype(np.float32)
+        u[rng.random(u.shape) < 0.05] = 0.0
+        W = (rng.random(u.shape) < 0.97).astype(np.float32)
+        perm = rng.permutation(c.shape[0])
+        c, u, W = c[perm], u[perm], W[perm]
+    vol = Vol(torch.from_numpy(c).cuda(), torch.from_numpy(u).cuda(), torch.from_numpy(W).cuda())
+    T = vol.extract(V, field="f").cpu().numpy()
+    R = extract_f64(c, u, W, V)
+    assert T.shape == R.shape and T.shape[0] > 1000
+    assert match_up_to_rotation(T, R) <= 1e-6

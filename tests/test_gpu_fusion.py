@@ -243,3 +243,33 @@ def test_incremental_equals_batch_bit_exact(fuse, k):
     with pytest.raises(VolError) as e:
         fuse(D[k:], P[k:], I, *prm, prev=(torch.cat([x1, x1[:1]]), torch.cat([f1, f1[:1]]), torch.cat([W1, W1[:1]])))
     assert e.value.status == VOL_EDATA
+
+
+@pytest.mark.parametrize("seed", [11, 12, 13])
+def test_fusion_within_fp64_dense(fuse, seed):
+    """Independent-precision check (the bit-exact tests above compare with an fp32 oracle whose rounding
+    order follows reading F-12): the kernel's f and W against a float64 dense fusion with the paper's plain
+    x/z projection (oracle/dense_fusion.py, precision "f64"), on the blocks allocated by the first frame,
+    for 4 noisy depth maps from random poses.  Bar: W equal and |f − f64| <= 1e-4 on all but 1e-4 of the
+    voxels (a voxel projecting within fp32 rounding of a pixel boundary may pick the neighbouring pixel in
+    one precision; the axis-aligned sphere cameras put voxel centres exactly on pixel boundaries, so they
+    are not used here)."""
+    from oracle.dense_fusion import fuse_dense
+    P = np.stack([_rand_pose(seed + 100 * k, 1.0) for k in range(4)])
+    D = np.stack([np.full((HH, WW), d, np.float32) for d in (4.8, 5.1, 5.3, 4.9)])
+    D = D + np.random.default_rng(seed).uniform(-0.3, 0.3, D.shape).astype(np.float32)
+    args = (D, INTR, P, 0.1, 1.0, 100.0, 3.0)
+    xyz, first, f, W = _gpu(fuse, *args)
+    keep = first == 0
+    assert keep.sum() > 0
+    lo = xyz[keep].min(0) * 8
+    hi = xyz[keep].max(0) * 8 + 7
+    fd, Wd_ = fuse_dense(*args, lo, hi, precision="f64")
+    i = np.arange(512)
+    loc = np.stack([i % 8, (i // 8) % 8, i // 64], 1)
+    g = xyz[keep].astype(np.int64)[:, None, :] * 8 + loc[None] - lo
+    f64 = fd[g[..., 2], g[..., 1], g[..., 0]]
+    W64 = Wd_[g[..., 2], g[..., 1], g[..., 0]]
+    ok = (W[keep] == W64) & (np.abs(f[keep].astype(np.float64) - f64) <= 1e-4)
+    assert (W64 > 0).sum() > 10000
+    assert (~ok).mean() <= 1e-4, f"{int((~ok).sum())} of {ok.size} voxels off the fp64 fusion"

@@ -179,3 +179,39 @@ def test_degenerate_triangles_dropped():
     E = _edges(T2)
     assert len(set(E)) == len(E)
     assert (0.5 * np.linalg.norm(_normals(T2), axis=1)).min() >= V * V / 1000
+
+
+def test_extract64_planar_field_vertices_on_plane():
+    """Pin of the float64 extraction (oracle/extract64.py): on a planar field u = n·p − c the linear
+    interpolation of X-4 is exact, so in float64 every vertex lies on the plane to ~1e-12, and every
+    normal points toward u > 0 (X-5, decided there by a determinant, not a parity)."""
+    from oracle.extract64 import extract_f64
+    c = dense_box(2, 2, 2).coords.numpy()
+    P = _centres(c)
+    n = np.array([0.3, -0.5, 0.81])
+    n /= np.linalg.norm(n)
+    u = (P @ n - 0.77).astype(np.float32)
+    T = extract_f64(c, u, np.ones_like(u), V)
+    assert T.shape[0] > 100
+    # the field values are fp32 roundings of n·p − c: vertices sit on the plane of the rounded values to
+    # within the rounding (1e-7 of |u|), far below any formula error
+    assert np.abs(T.reshape(-1, 3) @ n - 0.77).max() <= 1e-6
+    N = np.cross(T[:, 1] - T[:, 0], T[:, 2] - T[:, 0])
+    assert (N @ n > 0).all()
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_extract64_matches_c_oracle(seed):
+    """The float64 numpy extraction and the fp32 C oracle, written separately (orientation by determinant
+    vs permutation parity), give the same triangles in the same order, vertices within fp32 rounding."""
+    from oracle.extract64 import extract_f64, match_up_to_rotation
+    rng = np.random.default_rng(seed)
+    c = dense_box(2, 2, 2).coords.numpy()
+    u = rng.normal(size=(c.shape[0], 512)).astype(np.float32)
+    u[rng.random(u.shape) < 0.05] = 0.0                  # exact zeros: the X-6 drops
+    W = (rng.random(u.shape) < 0.97).astype(np.float32)  # unobserved voxels: X-1
+    perm = rng.permutation(c.shape[0])
+    T = oracle.extract(c[perm], u[perm], W[perm], V)
+    R = extract_f64(c[perm], u[perm], W[perm], V)
+    assert T.shape == R.shape and T.shape[0] > 1000
+    assert match_up_to_rotation(T, R) <= 1e-6

@@ -347,3 +347,43 @@ def test_incremental_equals_batch():
     with pytest.raises(ValueError):
         oracle.fuse_incremental((np.concatenate([x1, x1[:1]]), np.concatenate([f1, f1[:1]]),
                                  np.concatenate([W1, W1[:1]])), D, I, P, *prm)
+
+
+def test_dense_f64_closed_form_fronto_parallel_plane():
+    """Pin of the float64 dense fusion (the independent-precision reference of the GPU fusion test): a plane
+    at depth d seen by an identity-pose camera gives, at every voxel centre in view with z − d <= mu,
+    f = clamp((d − z)/mu, −1, 1) after one frame and the running mean of those values after several."""
+    voxel, mu = 0.1, 0.3
+    intr = np.array([60.0, 60.0, 31.5, 23.5], np.float32)
+    pose = _pose(np.eye(3), [0.0, 0.0, 0.0])
+    depths = [2.0, 2.2, 1.9]
+    D = np.stack([np.full((48, 64), d, np.float32) for d in depths])
+    lo, hi = np.array([-3, -3, 10]), np.array([3, 3, 30])
+    f, W = fuse_dense(D, intr, np.repeat(pose[None], 3, 0), voxel, mu, 100.0, 1e30, lo, hi, precision="f64")
+    z = (np.arange(lo[2], hi[2] + 1) + 0.5) * np.float64(np.float32(voxel))
+    d64 = np.array(depths, np.float32).astype(np.float64)[:, None]   # the depth maps hold fp32 numbers
+    s = np.clip((d64 - z[None]) / np.float64(np.float32(mu)), -1, 1)
+    upd = (d64 - z[None]) >= -np.float64(np.float32(mu))
+    # centre column (x = y = 0 voxel: centre (0.05, 0.05) projects inside the image)
+    fz, wz = f[:, 3, 3], W[:, 3, 3]
+    exp_w = upd.sum(0)
+    exp_f = np.where(exp_w > 0, (s * upd).sum(0) / np.maximum(exp_w, 1), 0.0)
+    assert np.array_equal(wz, exp_w.astype(np.float64))
+    assert np.abs(fz - exp_f).max() <= 1e-12
+
+
+def test_dense_f64_agrees_with_f32_on_random_poses():
+    """The two precisions of the dense fusion agree to 1e-4 on all but 1e-4 of the voxels (random poses,
+    noisy depth): a dropped term or wrong sign in either fails."""
+    rng = np.random.default_rng(4)
+    P = np.stack([_pose(_rand_rot(rng), rng.uniform(-1, 1, size=3)) for _ in range(3)])
+    D = np.stack([np.full((HH, WW), d, np.float32) for d in (4.8, 5.1, 5.3)])
+    D = D + rng.uniform(-0.3, 0.3, D.shape).astype(np.float32)
+    xyz, first, f, W = oracle.fuse(D, INTR, P, 0.1, 1.0, 100.0, 3.0)
+    keep = first == 0
+    lo, hi = xyz[keep].min(0) * 8, xyz[keep].max(0) * 8 + 7
+    a = fuse_dense(D, INTR, P, 0.1, 1.0, 100.0, 3.0, lo, hi)
+    b = fuse_dense(D, INTR, P, 0.1, 1.0, 100.0, 3.0, lo, hi, precision="f64")
+    ok = (a[1] == b[1]) & (np.abs(a[0] - b[0]) <= 1e-4)
+    assert (b[1] > 0).sum() > 10000
+    assert (~ok).mean() <= 1e-4
