@@ -344,6 +344,28 @@ __global__ void __launch_bounds__(128) k_extract(ExArgs A, int64_t n_rows, ExOut
         tp += (uint32_t)(tc >> (2 * bit)) & 3u;
     }
     if (t == 0) soff[n_items] = (uint16_t)block_total;
+    __syncthreads();   // the item list is complete
+    const uint32_t ng = (n_items + 31) / 32;
+    float *wsout = sout + wid * kSlice;
+    // triangles of 32-item group g into this warp's slice at float offset `shift`
+    auto compute_group = [&](uint32_t g, uint32_t shift) {
+        const uint32_t i = 32 * g + lane;
+        if (i < n_items) {
+            const uint32_t g0 = soff[32 * g];
+            const int cell = sitem[i] >> 3, k = sitem[i] & 7;
+            const int cx = cell & 7, cyy = (cell >> 3) & 7, czz = cell >> 6;
+            const uint2 TW = stw[k];
+            const float *sb = su + tile_index(cx, cyy, czz, 0);
+            const CellGeom G = cell_geom(gx + cx, gy + cyy, gz + czz, A.voxel);
+            tet_emit(TW, sb, sb[0], sb[byte_of(TW.y, 1)], sb[byte_of(TW.y, 2)], sb[byte_of(TW.y, 3)], G,
+                     wsout + shift + 9 * (soff[i] - g0));
+        }
+        __syncwarp();
+    };
+    // warps 1-3 compute their first group (staged unshifted: its offset is not known yet) while warp 0
+    // runs the look-back
+    const bool pre = wid > 0 && wid < ng;
+    if (pre) compute_group(wid, 0u);
     // look-back (warp 0): sum the predecessors' words back to the nearest inclusive one
     if (wid == 0) {
         unsigned long long excl = 0;
@@ -373,27 +395,21 @@ __global__ void __launch_bounds__(128) k_extract(ExArgs A, int64_t n_rows, ExOut
     }
     __syncthreads();
     const unsigned long long base = s_base;
-    const uint32_t ng = (n_items + 31) / 32;
-    float *wsout = sout + wid * kSlice;
     const long long cap = O.max_tris;
     for (uint32_t g = wid; g < ng; g += 4) {
-        const uint32_t i = 32 * g + lane;
         const uint32_t g0 = soff[32 * g], g1 = soff[min(32 * g + 32, n_items)];
         const long long first = (long long)(base + g0);
-        // stage at the global address's offset within 16 bytes, so that whole float4s copy out
-        const uint32_t shift = O.vec ? (uint32_t)(9ull * (unsigned long long)first) & 3u : 0u;
-        if (i < n_items) {
-            const int cell = sitem[i] >> 3, k = sitem[i] & 7;
-            const int cx = cell & 7, cyy = (cell >> 3) & 7, czz = cell >> 6;
-            const uint2 TW = stw[k];
-            const float *sb = su + tile_index(cx, cyy, czz, 0);
-            const CellGeom G = cell_geom(gx + cx, gy + cyy, gz + czz, A.voxel);
-            tet_emit(TW, sb, sb[0], sb[byte_of(TW.y, 1)], sb[byte_of(TW.y, 2)], sb[byte_of(TW.y, 3)], G,
-                     wsout + shift + 9 * (soff[i] - g0));
-        }
-        __syncwarp();
         const long long room = cap - first;
         const uint32_t nt = room <= 0 ? 0u : (room < (long long)(g1 - g0) ? (uint32_t)room : g1 - g0);
+        if (pre && g == (uint32_t)wid) {   // staged unshifted: scalar copy-out
+            float *dst = O.out + 9ull * (unsigned long long)first;
+            for (uint32_t j = lane; j < 9 * nt; j += 32) dst[j] = wsout[j];
+            __syncwarp();
+            continue;
+        }
+        // stage at the global address's offset within 16 bytes, so that whole float4s copy out
+        const uint32_t shift = O.vec ? (uint32_t)(9ull * (unsigned long long)first) & 3u : 0u;
+        compute_group(g, shift);
         float *dst = O.out + 9ull * (unsigned long long)first - shift;   // element e ↔ wsout[e], e ∈ [shift, end)
         const uint32_t end = shift + 9 * nt;
         if (O.vec) {
