@@ -119,6 +119,15 @@ int launch_sanitize_state(const Fields &F, int cur, const int32_t *nbr, int64_t 
 int launch_energy(const View &V, const int32_t *nbr, const int32_t *blocks, int64_t n_blocks, float lam,
                   float eps, int data_term, double *partials, double *out, cudaStream_t s);
 
+// single-GPU store order on the device (order.cu): perm[r] = caller index of store row r (Morton order of the
+// coordinates relative to their bounding box, ties in caller order); *bad = lowest block index with a
+// coordinate outside (−2^30, 2^30) (*bad must be preset to ~0).  scratch: morton_order_scratch_bytes(n).
+size_t morton_order_scratch_bytes(int64_t n);
+int launch_morton_order(const int32_t *xyz, int64_t n, void *scratch, int32_t *perm, unsigned long long *bad,
+                        cudaStream_t s);
+// store_of_global[perm[r]] = r, rows[r] = perm[r]
+int launch_row_maps(const int32_t *perm, int64_t n, int32_t *sog, int64_t *rows, cudaStream_t s);
+
 uint32_t host_hash(int32_t x, int32_t y, int32_t z, uint32_t T);
 
 }  // namespace hvg

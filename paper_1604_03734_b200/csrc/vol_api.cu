@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -95,7 +97,7 @@ static void carve_all(Carve &c, vol_s *v, const Layout &L) {
     auto perm = c.take<int32_t>((size_t)L.n_local + 1);
     auto tmp = c.take<float>((size_t)L.n_local * kBlockVox + 4);
     auto u2 = c.take<float>((size_t)L.S * kBlockVox + 4);   // second u buffer of the skewed schedule
-    auto misc = c.take<unsigned long long>(4);
+    auto misc = c.take<unsigned long long>(6);
     auto part = c.take<double>(5 * (size_t)L.S + 5);
     auto eout = c.take<double>(8);
     if (v) {
@@ -214,9 +216,24 @@ extern "C" vol_status vol_create_w8(const int32_t *block_xyz, int64_t n_global, 
     return create_impl(block_xyz, n_global, f, nullptr, W8, dist, workspace, workspace_bytes, stream, out);
 }
 
+// HVG_TRACE_CREATE=1: host time of each phase of vol_create on stderr (development aid)
+namespace {
+struct PhaseTrace {
+    bool on = std::getenv("HVG_TRACE_CREATE") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void operator()(const char *what) {
+        if (!on) return;
+        const auto n = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[create] %-24s %8.1f us\n", what, std::chrono::duration<double, std::micro>(n - t).count());
+        t = n;
+    }
+};
+}  // namespace
+
 static vol_status create_impl(const int32_t *block_xyz, int64_t n_global, const float *f, const float *W,
                               const uint8_t *W8in, const vol_dist *dist, void *workspace, size_t workspace_bytes,
                               void *stream, vol_t *out) {
+    PhaseTrace trace;
     if (!out) return fail(VOL_EINVAL, "vol_create: out is NULL");
     *out = nullptr;
     if (n_global < 1) return fail(VOL_EINVAL, "vol_create: n_global must be >= 1 (got %lld)", (long long)n_global);
@@ -239,18 +256,24 @@ static vol_status create_impl(const int32_t *block_xyz, int64_t n_global, const 
     if (cudaStreamCreateWithFlags(&v->cap, cudaStreamNonBlocking) != cudaSuccess)
         return bail(fail(VOL_ECUDA, "cudaStreamCreate failed"));
 
-    // host copy of the coordinates (the work order and the shard plan are host-side schedules)
-    std::vector<int32_t> hxyz(3 * (size_t)n_global);
-    if (is_device_ptr(block_xyz)) {
-        if (cudaMemcpy(hxyz.data(), block_xyz, hxyz.size() * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
-            return bail(fail(VOL_ECUDA, "copy of block_xyz failed"));
-    } else {
-        memcpy(hxyz.data(), block_xyz, hxyz.size() * 4);
+    // host copy of the coordinates: the shard plan is a host-side schedule (sharded volumes only — one GPU
+    // orders and checks the blocks on the device, order.cu)
+    std::vector<int32_t> hxyz;
+    if (sharded) {
+        hxyz.resize(3 * (size_t)n_global);
+        if (is_device_ptr(block_xyz)) {
+            if (cudaMemcpy(hxyz.data(), block_xyz, hxyz.size() * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
+                return bail(fail(VOL_ECUDA, "copy of block_xyz failed"));
+        } else {
+            memcpy(hxyz.data(), block_xyz, hxyz.size() * 4);
+        }
+        // block coordinates must leave room for the ±1 neighbour offsets in int32 arithmetic
+        for (size_t k = 0; k < hxyz.size(); k++)
+            if (hxyz[k] <= -(1 << 30) || hxyz[k] >= (1 << 30))
+                return bail(fail(VOL_EDATA, "block %lld: coordinate %d outside (-2^30, 2^30)", (long long)(k / 3),
+                                 hxyz[k]));
     }
-    // block coordinates must leave room for the ±1 neighbour offsets in int32 arithmetic
-    for (size_t k = 0; k < hxyz.size(); k++)
-        if (hxyz[k] <= -(1 << 30) || hxyz[k] >= (1 << 30))
-            return bail(fail(VOL_EDATA, "block %lld: coordinate %d outside (-2^30, 2^30)", (long long)(k / 3), hxyz[k]));
+    trace("stream (+ coords D2H)");
 
     ShardPlan plan;
     Layout L{};
@@ -289,30 +312,40 @@ static vol_status create_impl(const int32_t *block_xyz, int64_t n_global, const 
     carve_all(c, v, L);
     v->extra = c.base + ((c.off + 255) & ~(size_t)255);
     cudaStream_t s = v->stream;
+    // status words: [0] duplicate pair, [1] first invalid voxel, [2] |Ω|, [3] W8 unusable, [4] first block
+    // with an out-of-range coordinate
+    if (cudaMemsetAsync(v->d_misc, 0, 6 * 8, s) != cudaSuccess || cudaMemsetAsync(v->d_misc, 0xFF, 2 * 8, s) != cudaSuccess ||
+        cudaMemsetAsync(&v->d_misc[4], 0xFF, 8, s) != cudaSuccess)
+        return bail(fail(VOL_ECUDA, "memset failed"));
 
-    // store order: Morton order of the blocks (single GPU) or the shard plan's [launch A | launch B]
-    // rows + ghosts; row_caller[r] is the block's index in the caller's f / W / u arrays
+    // store order: Morton order of the blocks (single GPU, on the device) or the shard plan's
+    // [launch A | launch B] rows + ghosts; d_perm[r] is the block's index in the caller's f / W / u arrays
+    vol_status st;
+    if ((st = copy_in(v->d_xyz, block_xyz, 3 * (size_t)n_global * 4, s)) != VOL_OK) return bail(st);
     std::vector<int64_t> row_global;
-    std::vector<int32_t> row_caller;
+    std::vector<int32_t> row_caller, store_of_global;
     if (!sharded) {
-        std::vector<int64_t> all(n_global);
-        std::iota(all.begin(), all.end(), 0);
-        morton_sort_rows(hxyz.data(), all, row_caller);
-        row_global.assign(row_caller.begin(), row_caller.end());
+        const size_t ms = morton_order_scratch_bytes(n_global);
+        void *scr = v->d_tmp;
+        const bool own = ms > (size_t)L.n_local * kBlockVox * 4;
+        if (own && cudaMallocAsync(&scr, ms, s) != cudaSuccess) return bail(fail(VOL_ENOMEM, "order scratch"));
+        const int r = launch_morton_order(v->d_xyz, n_global, scr, v->d_perm, &v->d_misc[4], s);
+        if (own) cudaFreeAsync(scr, s);
+        if (r < 0) return bail(fail(VOL_ECUDA, "store order launch failed: %s", cudaGetErrorString(cudaGetLastError())));
     } else {
         row_global = plan.local;
         row_global.insert(row_global.end(), plan.ghost.begin(), plan.ghost.end());
         row_caller = plan.local_caller;
+        store_of_global.assign(n_global, -1);
+        for (int64_t r = 0; r < L.S; r++) store_of_global[row_global[r]] = (int32_t)r;
+        if (cudaMemcpyAsync(v->d_perm, row_caller.data(), (size_t)L.n_local * 4, cudaMemcpyHostToDevice, s) !=
+            cudaSuccess)
+            return bail(fail(VOL_ECUDA, "permutation upload failed"));
     }
-    std::vector<int32_t> store_of_global(n_global, -1);
-    for (int64_t r = 0; r < L.S; r++) store_of_global[row_global[r]] = (int32_t)r;
+    trace("store order queued");
 
-    // inputs: coordinates as given; f and W through a staging copy, then permuted into store order
-    vol_status st;
-    if ((st = copy_in(v->d_xyz, block_xyz, 3 * (size_t)n_global * 4, s)) != VOL_OK) return bail(st);
+    // inputs: f and W through a staging copy, then permuted into store order
     const size_t fbytes = (size_t)L.n_local * kBlockVox * 4;
-    if (cudaMemcpyAsync(v->d_perm, row_caller.data(), (size_t)L.n_local * 4, cudaMemcpyHostToDevice, s) != cudaSuccess)
-        return bail(fail(VOL_ECUDA, "permutation upload failed"));
     if ((st = copy_in(v->d_tmp, f, fbytes, s)) != VOL_OK) return bail(st);
     if (W8in) {   // 8-bit counts: a quarter of the bytes to copy, widened on the device (exact)
         if ((st = copy_in(v->F.u, W8in, (size_t)L.n_local * kBlockVox, s)) != VOL_OK) return bail(st);
@@ -328,9 +361,7 @@ static vol_status create_impl(const int32_t *block_xyz, int64_t n_global, const 
     }
 
     // K1: hash + CSR bucket table over all n_global blocks
-    if (cudaMemsetAsync(v->d_count, 0, ((size_t)L.T + 1) * 4, s) != cudaSuccess ||
-        cudaMemsetAsync(v->d_misc, 0, 4 * 8, s) != cudaSuccess ||
-        cudaMemsetAsync(v->d_misc, 0xFF, 2 * 8, s) != cudaSuccess)
+    if (cudaMemsetAsync(v->d_count, 0, ((size_t)L.T + 1) * 4, s) != cudaSuccess)
         return bail(fail(VOL_ECUDA, "memset failed"));
     if (launch_hash_count(v->d_xyz, n_global, L.T, v->d_hash, v->d_count, s) < 0 ||
         launch_exclusive_scan_u32(v->d_count, v->d_start, L.T, v->d_scan, s) < 0)
@@ -341,48 +372,88 @@ static vol_status create_impl(const int32_t *block_xyz, int64_t n_global, const 
         launch_bucket_sort_and_dups(v->d_xyz, v->d_start, v->d_entry, L.T, n_global, &v->d_misc[0], s) < 0 ||
         launch_validate(v->F.f, v->F.W, (int64_t)L.n_local * kBlockVox, &v->d_misc[1], &v->d_misc[2], s) < 0)
         return bail(fail(VOL_ECUDA, "store build launch failed: %s", cudaGetErrorString(cudaGetLastError())));
-    unsigned long long misc[3];
-    if (cudaMemcpyAsync(misc, v->d_misc, 3 * 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-        cudaStreamSynchronize(s) != cudaSuccess)
-        return bail(fail(VOL_ECUDA, "store build failed: %s", cudaGetErrorString(cudaGetLastError())));
-    if (misc[0] != ~0ULL) {
-        long long i = (long long)(misc[0] >> 32), j = (long long)(misc[0] & 0xFFFFFFFFu);
-        return bail(fail(VOL_EDATA, "duplicate block coordinates: blocks %lld and %lld are both (%d, %d, %d)", j, i,
-                         hxyz[3 * i], hxyz[3 * i + 1], hxyz[3 * i + 2]));
-    }
-    if (misc[1] != ~0ULL) {
-        long long i = (long long)misc[1];
-        return bail(fail(VOL_EDATA, "invalid input in block %lld, voxel %lld: f must be finite, W finite and >= 0",
-                         (long long)row_caller[i / kBlockVox], i % kBlockVox));
-    }
-    v->n_omega_local = (int64_t)misc[2];
-    v->n_omega_global = v->n_omega_local;
-
-    // K2: neighbour table in store rows (faces + edges); the row maps reuse build scratch
+    // the row maps reuse build scratch (d_hash is free once the buckets are filled)
     int32_t *d_sog = reinterpret_cast<int32_t *>(v->d_hash);
     int64_t *d_rows = reinterpret_cast<int64_t *>(v->d_part);
-    if (cudaMemcpyAsync(d_sog, store_of_global.data(), (size_t)n_global * 4, cudaMemcpyHostToDevice, s) != cudaSuccess ||
-        cudaMemcpyAsync(d_rows, row_global.data(), (size_t)L.S * 8, cudaMemcpyHostToDevice, s) != cudaSuccess)
-        return bail(fail(VOL_ECUDA, "row map upload failed"));
-    if (launch_neighbours(v->d_xyz, n_global, v->d_start, v->d_entry, L.T, d_sog, d_rows, L.S, v->d_nbr, s) < 0)
-        return bail(fail(VOL_ECUDA, "neighbour launch failed"));
-    if (cudaStreamSynchronize(s) != cudaSuccess)  // the host row maps go out of scope
-        return bail(fail(VOL_ECUDA, "vol_create: %s", cudaGetErrorString(cudaGetLastError())));
-    if (sharded) {
+
+    // reports the first input error the status words hold (caller block indices and coordinates fetched on
+    // demand), else records |Ω|
+    auto check_inputs = [&](const unsigned long long *misc) -> vol_status {
+        auto coord = [&](long long i, int32_t *xyz3) {
+            if (!hxyz.empty()) {
+                for (int a = 0; a < 3; a++) xyz3[a] = hxyz[3 * i + a];
+            } else if (cudaMemcpy(xyz3, v->d_xyz + 3 * i, 12, cudaMemcpyDeviceToHost) != cudaSuccess) {
+                xyz3[0] = xyz3[1] = xyz3[2] = 0;
+            }
+        };
+        int32_t q[3];
+        if (misc[4] != ~0ULL) {
+            coord((long long)misc[4], q);
+            return fail(VOL_EDATA, "block %lld: coordinate (%d, %d, %d) outside (-2^30, 2^30)", (long long)misc[4],
+                        q[0], q[1], q[2]);
+        }
+        if (misc[0] != ~0ULL) {
+            long long i = (long long)(misc[0] >> 32), j = (long long)(misc[0] & 0xFFFFFFFFu);
+            coord(i, q);
+            return fail(VOL_EDATA, "duplicate block coordinates: blocks %lld and %lld are both (%d, %d, %d)", j, i,
+                        q[0], q[1], q[2]);
+        }
+        if (misc[1] != ~0ULL) {
+            long long i = (long long)misc[1];
+            int32_t blk = 0;
+            if (cudaMemcpy(&blk, v->d_perm + i / kBlockVox, 4, cudaMemcpyDeviceToHost) != cudaSuccess) blk = -1;
+            return fail(VOL_EDATA, "invalid input in block %lld, voxel %lld: f must be finite, W finite and >= 0",
+                        (long long)blk, i % kBlockVox);
+        }
+        v->n_omega_local = (int64_t)misc[2];
+        v->n_omega_global = v->n_omega_local;
+        return VOL_OK;
+    };
+
+    if (!sharded) {
+        // K2: neighbour table; K3: initial state (warm start) so read_u / energy are defined before the first
+        // iteration; 8-bit weights — all queued, then one synchronisation reads every status word
+        if (launch_row_maps(v->d_perm, n_global, d_sog, d_rows, s) < 0 ||
+            launch_neighbours(v->d_xyz, n_global, v->d_start, v->d_entry, L.T, d_sog, d_rows, L.S, v->d_nbr, s) < 0 ||
+            launch_init_state(v->F, L.S * kBlockVox, 0, s) < 0 ||
+            launch_pack_w8(v->F.W, v->d_w8, L.S * kBlockVox, reinterpret_cast<unsigned *>(&v->d_misc[3]), s) < 0)
+            return bail(fail(VOL_ECUDA, "store build launch failed: %s", cudaGetErrorString(cudaGetLastError())));
+        unsigned long long misc[5];
+        if (cudaMemcpyAsync(misc, v->d_misc, 5 * 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess)
+            return bail(fail(VOL_ECUDA, "store build failed: %s", cudaGetErrorString(cudaGetLastError())));
+        trace("build + init + sync");
+        if ((st = check_inputs(misc)) != VOL_OK) return bail(st);
+        v->F.W8 = (misc[3] & 0xFFFFFFFFull) ? nullptr : v->d_w8;
+    } else {
+        unsigned long long misc[5];
+        if (cudaMemcpyAsync(misc, v->d_misc, 5 * 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess)
+            return bail(fail(VOL_ECUDA, "store build failed: %s", cudaGetErrorString(cudaGetLastError())));
+        trace("store build + sync");
+        if ((st = check_inputs(misc)) != VOL_OK) return bail(st);
+        // K2: neighbour table in store rows (faces + edges)
+        if (cudaMemcpyAsync(d_sog, store_of_global.data(), (size_t)n_global * 4, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+            cudaMemcpyAsync(d_rows, row_global.data(), (size_t)L.S * 8, cudaMemcpyHostToDevice, s) != cudaSuccess)
+            return bail(fail(VOL_ECUDA, "row map upload failed"));
+        if (launch_neighbours(v->d_xyz, n_global, v->d_start, v->d_entry, L.T, d_sog, d_rows, L.S, v->d_nbr, s) < 0)
+            return bail(fail(VOL_ECUDA, "neighbour launch failed"));
+        if (cudaStreamSynchronize(s) != cudaSuccess)  // the host row maps go out of scope
+            return bail(fail(VOL_ECUDA, "vol_create: %s", cudaGetErrorString(cudaGetLastError())));
+        trace("neighbours + sync");
         st = shard_setup(v, plan, dist);
         if (st != VOL_OK) return bail(st);
-    }
-    // K3: initial state (warm start) so read_u / energy are defined before the first iteration
-    if (launch_init_state(v->F, L.S * kBlockVox, 0, s) < 0) return bail(fail(VOL_ECUDA, "init launch failed"));
-    if (cudaStreamSynchronize(s) != cudaSuccess)
-        return bail(fail(VOL_ECUDA, "vol_create: %s", cudaGetErrorString(cudaGetLastError())));
-    if (sharded) {
+        // K3: initial state (warm start) so read_u / energy are defined before the first iteration
+        if (launch_init_state(v->F, L.S * kBlockVox, 0, s) < 0) return bail(fail(VOL_ECUDA, "init launch failed"));
+        if (cudaStreamSynchronize(s) != cudaSuccess)
+            return bail(fail(VOL_ECUDA, "vol_create: %s", cudaGetErrorString(cudaGetLastError())));
         st = shard_after_create(v);
         if (st != VOL_OK) return bail(st);
-    }
-    if (!sharded || v->shard_nccl()) {   // loopback shards finish in vol_group_connect
-        st = finalize_w8(v);
-        if (st != VOL_OK) return bail(st);
+        trace("shard setup + init");
+        if (v->shard_nccl()) {   // loopback shards finish in vol_group_connect
+            st = finalize_w8(v);
+            if (st != VOL_OK) return bail(st);
+        }
     }
     v->cur = 0;
     v->initialised = true;

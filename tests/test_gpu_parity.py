@@ -78,11 +78,19 @@ def test_input_errors(V):
     with pytest.raises(VolError) as e:
         V(c, s.f, s.W)
     assert e.value.status == VOL_EDATA and "3 and 7" in str(e.value)
+    assert "(%d, %d, %d)" % tuple(int(x) for x in c[3]) in str(e.value)
     f = s.f.clone()
     f[2, 5] = float("nan")
     with pytest.raises(VolError) as e:
         V(s.coords, f, s.W)
-    assert e.value.status == VOL_EDATA
+    assert e.value.status == VOL_EDATA and "block 2, voxel 5" in str(e.value)
+    # coordinates must leave room for the ±1 neighbour offsets in int32 (checked on the device)
+    for big in (1 << 30, -(1 << 30)):
+        c = s.coords.clone()
+        c[11, 1] = big
+        with pytest.raises(VolError) as e:
+            V(c, s.f, s.W)
+        assert e.value.status == VOL_EDATA and "block 11" in str(e.value) and "outside" in str(e.value)
     W = s.W.clone()
     W[0, 0] = -1
     with pytest.raises(VolError) as e:
