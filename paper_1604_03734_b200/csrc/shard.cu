@@ -468,6 +468,90 @@ static vol_status comm_acquire(const void *id_bytes, int world, int rank, int de
     return VOL_OK;
 }
 
+// Process-wide cache of the sharded loop's graphs.  A graph with NCCL nodes is expensive to instantiate and
+// to destroy (~1.6 ms: NCCL's resources for captured work), and bench.py / an application creating one
+// volume per step would pay both every step.  The graph only holds device addresses inside the volume's
+// workspace and the communicator, so it is reused by any later volume whose key — workspace address and
+// size, layout, shard-plan digest, communicator, rank, device and the loop's parameters — is identical:
+// that volume's buffers sit at the same addresses with the same sizes and counts.  Entries of a
+// communicator are destroyed when it is evicted or released; at most kSharedGraphs are kept.
+namespace {
+struct SharedGraph {
+    std::string key;
+    cudaGraphExec_t exec;
+    int64_t per;
+    ncclComm_t comm;
+};
+std::mutex g_sg_mu;
+std::vector<SharedGraph> g_sg;
+constexpr size_t kSharedGraphs = 8;
+
+void shared_graphs_drop(ncclComm_t comm) {   // comm == nullptr: all
+    std::vector<SharedGraph> dead;
+    {
+        std::lock_guard<std::mutex> lk(g_sg_mu);
+        for (auto it = g_sg.begin(); it != g_sg.end();) {
+            if (!comm || it->comm == comm) {
+                dead.push_back(*it);
+                it = g_sg.erase(it);
+            } else {
+                ++it;
+            }
+        }
+    }
+    if (!dead.empty()) cudaDeviceSynchronize();
+    for (auto &e : dead) cudaGraphExecDestroy(e.exec);
+}
+}  // namespace
+
+template <class Body>
+static vol_status cached_graph_shared(vol_s *v, const GraphKey &key, ncclComm_t comm, Body body, cudaGraphExec_t *exec,
+                                      int64_t *per) {
+    {
+        std::lock_guard<std::mutex> lk(g_sg_mu);
+        for (const SharedGraph &e : g_sg)
+            if (e.key == key.bytes) {
+                *exec = e.exec;
+                *per = e.per;
+                return VOL_OK;
+            }
+    }
+    cudaGraph_t g = nullptr;
+    const long long before = hvg::g_launches.load();
+    int64_t n = 0;
+    CK(cudaStreamBeginCapture(v->cap, cudaStreamCaptureModeThreadLocal));
+    vol_status st = body(v->cap, n);
+    cudaError_t e = cudaStreamEndCapture(v->cap, &g);
+    hvg::g_launches.fetch_sub(hvg::g_launches.load() - before);
+    if (st != VOL_OK || e != cudaSuccess) {
+        if (g) cudaGraphDestroy(g);
+        if (st != VOL_OK) return st;
+        return fail(VOL_ECUDA, "graph capture failed: %s", cudaGetErrorString(e));
+    }
+    cudaGraphExec_t ge = nullptr;
+    e = cudaGraphInstantiate(&ge, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(VOL_ECUDA, "graph instantiate failed: %s", cudaGetErrorString(e));
+    SharedGraph old{};
+    bool evict = false;
+    {
+        std::lock_guard<std::mutex> lk(g_sg_mu);
+        if (g_sg.size() >= kSharedGraphs) {
+            old = g_sg.front();
+            g_sg.erase(g_sg.begin());
+            evict = true;
+        }
+        g_sg.push_back(SharedGraph{key.bytes, ge, n, comm});
+    }
+    if (evict) {   // the oldest entry may still run on some volume's stream
+        cudaDeviceSynchronize();
+        cudaGraphExecDestroy(old.exec);
+    }
+    *exec = ge;
+    *per = n;
+    return VOL_OK;
+}
+
 // A communicator with an asynchronous error is unusable: abort it and drop it from the cache.
 static void comm_evict(ncclComm_t comm) {
     bool found = false;
@@ -482,7 +566,10 @@ static void comm_evict(ncclComm_t comm) {
             }
         }
     }
-    if (found) ncclCommAbort(comm);
+    if (found) {
+        shared_graphs_drop(comm);
+        ncclCommAbort(comm);
+    }
 }
 
 // Asynchronous NCCL failures of earlier work (SURVEY §5 failure detection): evict the communicator.
@@ -496,6 +583,7 @@ static vol_status check_async(ncclComm_t comm) {
 }
 
 extern "C" vol_status vol_release_comms(void) {
+    shared_graphs_drop(nullptr);
     std::vector<std::shared_ptr<CommEntry>> all;
     {
         std::lock_guard<std::mutex> lk(g_comms_mu);
@@ -723,16 +811,20 @@ static vol_status nccl_skew(vol_s *v, const IterParams &P, int32_t iters) {
         key.add('N').add(c).add(m).add(iters & 1).add(v->pending_frozen).add(v->pending_exchange).add(P);
         cudaGraphExec_t ge = nullptr;
         int64_t per = 0;
-        st = cached_graph(
-            v, key,
-            [&](cudaStream_t cap, int64_t &n) -> vol_status {
-                for (int k = 0; k < 2 * m; k++) {
-                    vol_status s2 = skew_iter(cap, k, false, n);
-                    if (s2 != VOL_OK) return s2;
-                }
-                return VOL_OK;
-            },
-            &ge, &per);
+        auto capture = [&](cudaStream_t cap, int64_t &n) -> vol_status {
+            for (int k = 0; k < 2 * m; k++) {
+                vol_status s2 = skew_iter(cap, k, false, n);
+                if (s2 != VOL_OK) return s2;
+            }
+            return VOL_OK;
+        };
+        if (SP.digest != 0 && R->comm) {   // reusable by later volumes with the same workspace and plan
+            key.add(v->ws).add(v->ws_bytes).add(v->L.n_global).add(v->L.n_local).add(v->L.S).add(v->L.T)
+                .add(SP.digest).add(SP.rank).add(SP.world).add(R->comm).add(v->device);
+            st = cached_graph_shared(v, key, R->comm, capture, &ge, &per);
+        } else {
+            st = cached_graph(v, key, capture, &ge, &per);
+        }
         if (st != VOL_OK) return st;
         const int reps = body / (2 * m);
         for (int q = 0; q < reps; q++) {

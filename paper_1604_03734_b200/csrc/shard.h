@@ -27,6 +27,7 @@ struct ShardPlan {
     std::vector<int64_t> send_rows;    // local store rows sent, grouped by peer (rank order), peer's recv order
     std::vector<int64_t> send_off, send_cnt;  // [world] slice of send_rows per peer
     std::string error;
+    uint64_t digest = 0;               // digest of the plan's inputs (coordinates, owner map) when known, else 0
     int64_t n_local() const { return (int64_t)local.size(); }
     int64_t n_ghost() const { return (int64_t)ghost.size(); }
 };

@@ -158,6 +158,7 @@ static bool get_shard_plan(const int32_t *xyz, int64_t n, const vol_dist *d, Sha
         return true;
     }
     if (!make_shard_plan(xyz, n, d->part, d->world, d->rank, out)) return false;
+    out.digest = dg ? dg : 1;
     c.valid = true;
     c.n = n;
     c.world = d->world;
@@ -476,11 +477,16 @@ vol_status finalize_w8(vol_s *v) {
 
 extern "C" void vol_destroy(vol_t v) {
     if (!v) return;
+    PhaseTrace trace;
     if (v->shard) shard_destroy(v);
+    trace("destroy: shard");
     if (v->stream) cudaStreamSynchronize(v->stream);
+    trace("destroy: sync");
     for (GraphEntry &e : v->graphs) cudaGraphExecDestroy(e.exec);
     v->graphs.clear();
+    trace("destroy: graphs");
     if (v->cap) cudaStreamDestroy(v->cap);
+    trace("destroy: stream");
     if (v->owns_ws && v->ws) cudaFree(v->ws);
     delete v;
 }
