@@ -101,6 +101,10 @@ struct vol_s {
     double *d_part = nullptr;          // [S][5]
     double *d_eout = nullptr;          // [8]
     int64_t last_launches = 0;
+    // the state is the warm initial state (u = ū = f in both ū buffers, p = 0, cur = 0) — set by vol_create,
+    // cleared by any iteration, a zero initialisation or vol_load_state; a restart with the warm
+    // initialisation then has nothing to rewrite
+    bool pristine = false;
     // sharded state (world > 1)
     ShardRuntime *shard = nullptr;
     char *extra = nullptr;             // workspace tail for the sharded runtime

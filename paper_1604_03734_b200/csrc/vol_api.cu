@@ -458,6 +458,7 @@ static vol_status create_impl(const int32_t *block_xyz, int64_t n_global, const 
     }
     v->cur = 0;
     v->initialised = true;
+    v->pristine = true;
     *out = v;
     return VOL_OK;
 }
@@ -656,10 +657,14 @@ vol_status vol_regularise_prepare(vol_s *v, float lambda, float eps, float tau, 
     v->pending_exchange = o.exchange;
     v->last_launches = 0;
     if (!o.resume) {
-        CKL(launch_init_state(v->F, v->L.S * kBlockVox, o.init, v->stream));
+        if (!(v->pristine && o.init == 0)) {   // (the warm initial state needs no rewrite)
+            CKL(launch_init_state(v->F, v->L.S * kBlockVox, o.init, v->stream));
+            v->last_launches = 1;
+        }
         v->cur = 0;
-        v->last_launches = 1;
+        v->pristine = o.init == 0;
     }
+    if (iters > 0) v->pristine = false;
     v->pending_frozen = nullptr;
     if (o.freeze && o.data_term == 0 && o.kernel != 1 && iters > 0) {
         CKL(launch_freeze_mask(v->F, v->cur, P, v->L.n_local, v->d_frozen, v->stream));
@@ -742,6 +747,7 @@ extern "C" vol_status vol_load_state(vol_t v, const float *u, const float *ubar,
     NvtxRange nvtx_range_("vol_load_state");
     if (!v) return fail(VOL_EINVAL, "vol_load_state: NULL handle");
     if (v->shard) return fail(VOL_ENOTSUP, "vol_load_state: single-GPU volumes only");
+    v->pristine = false;
     const size_t nv = (size_t)v->L.n_local * kBlockVox;
     const int c = v->cur;
     vol_status st;
