@@ -66,16 +66,21 @@ k_energy_blocks(View F, const int32_t *__restrict__ nbr, const int32_t *__restri
         const double dv = (pxv - (double)sp[0][x > 0 ? 64 + i - 1 : y + 8 * z]) +
                           (pyv - (double)sp[1][y > 0 ? 64 + i - 8 : x + 8 * z]) +
                           (pzv - (double)sp[2][z > 0 ? i : x + 8 * y]);
-        const double s = sqrt(gx * gx + gy * gy + gz * gz);
-        const double h = (eps > 0.0 && s <= eps) ? s * s / (2.0 * eps) : s - eps / 2.0;
+        // H_ε(s), s = ‖∇u‖: the quadratic branch from s² directly (no square root; H is continuous at s = ε,
+        // so deciding s ≤ ε on s² ≤ ε² moves the value by rounding only)
+        const double s2 = gx * gx + gy * gy + gz * gz;
+        const double h = (eps > 0.0 && s2 <= eps * eps) ? s2 / (2.0 * eps) : sqrt(s2) - eps / 2.0;
         const double r = uv - fv;
         const double dt = data_term == 0 ? lam * Wd * fabs(r) : 0.5 * lam * Wd * r * r;
         acc[0] += h + dt;
         acc[1] += pxv * pxv + pyv * pyv + pzv * pzv;
         acc[2] += fv * dv;
-        acc[3] += dv * dv / (2.0 * lam * Wd);
-        const double lim = lam * Wd;
-        if (fabs(dv) > lim) acc[4] = fmin(acc[4], lim / fabs(dv));
+        if (data_term == 1) {   // Σ (div p)²/(2λW) enters only the L2 dual value
+            acc[3] += dv * dv / (2.0 * lam * Wd);
+        } else {                // the L1 dual's feasibility scale s = min λW/|div p| (1 for L2)
+            const double lim = lam * Wd;
+            if (fabs(dv) > lim) acc[4] = fmin(acc[4], lim / fabs(dv));
+        }
     }
     for (int k = 0; k < kNPart; k++) red[k][tid] = acc[k];
     __syncthreads();
