@@ -632,8 +632,8 @@ vol_status shard_setup(vol_s *v, const ShardPlan &plan, const vol_dist *dist) {
     for (int q = 0; q < P.world; q++)
         if (q != P.rank && P.send_cnt[q] > 0) R->peers.push_back(q);
     std::vector<int32_t> send32(P.send_rows.begin(), P.send_rows.end());
+    // (a copy from pageable host memory returns once the data is staged: the host vector may go)
     CK(cudaMemcpyAsync(R->send_rows, send32.data(), send32.size() * 4, cudaMemcpyHostToDevice, s));
-    CK(cudaStreamSynchronize(s));  // the host vector goes out of scope
     CK(cudaStreamCreateWithFlags(&R->cs, cudaStreamNonBlocking));
     R->graphs = getenv("HVG_SHARD_NO_GRAPH") == nullptr;
     CK(cudaEventCreateWithFlags(&R->ev_pack, cudaEventDisableTiming));

@@ -437,17 +437,16 @@ static vol_status create_impl(const int32_t *block_xyz, int64_t n_global, const 
         if (cudaMemcpyAsync(d_sog, store_of_global.data(), (size_t)n_global * 4, cudaMemcpyHostToDevice, s) != cudaSuccess ||
             cudaMemcpyAsync(d_rows, row_global.data(), (size_t)L.S * 8, cudaMemcpyHostToDevice, s) != cudaSuccess)
             return bail(fail(VOL_ECUDA, "row map upload failed"));
+        // (copies from pageable host memory return once the data is staged: the host row maps may go)
         if (launch_neighbours(v->d_xyz, n_global, v->d_start, v->d_entry, L.T, d_sog, d_rows, L.S, v->d_nbr, s) < 0)
             return bail(fail(VOL_ECUDA, "neighbour launch failed"));
-        if (cudaStreamSynchronize(s) != cudaSuccess)  // the host row maps go out of scope
-            return bail(fail(VOL_ECUDA, "vol_create: %s", cudaGetErrorString(cudaGetLastError())));
-        trace("neighbours + sync");
+        trace("neighbours");
         st = shard_setup(v, plan, dist);
         if (st != VOL_OK) return bail(st);
-        // K3: initial state (warm start) so read_u / energy are defined before the first iteration
-        if (launch_init_state(v->F, L.S * kBlockVox, 0, s) < 0) return bail(fail(VOL_ECUDA, "init launch failed"));
-        if (cudaStreamSynchronize(s) != cudaSuccess)
-            return bail(fail(VOL_ECUDA, "vol_create: %s", cudaGetErrorString(cudaGetLastError())));
+        // K3: initial state (warm start) so read_u / energy are defined before the first iteration (NCCL
+        // shards initialise in shard_after_create, once the ghosts' f and W have arrived)
+        if (!v->shard_nccl() && launch_init_state(v->F, L.S * kBlockVox, 0, s) < 0)
+            return bail(fail(VOL_ECUDA, "init launch failed"));
         st = shard_after_create(v);
         if (st != VOL_OK) return bail(st);
         trace("shard setup + init");
