@@ -568,9 +568,12 @@ def reference_arm(args):
     else:
         scene = make_scene(cfg, 1, args.seed, dev).to("cpu")
     n_alloc = scene.n_alloc
-    per_step_iters = 1
+    # 8 iterations per step: the oracle call's fixed cost (array conversion, its own table build, ~1 s on the
+    # street) would otherwise dominate a 1-iteration sample and understate its throughput ~4x; the untimed
+    # warm-up steps run one iteration each (they only page in the library and the arrays)
+    per_step_iters = 8 if n_alloc < 50_000_000 else 2   # city: 2 (the whole run stays within a few minutes)
     for _ in range(args.warmup):
-        time_oracle(scene, per_step_iters)
+        time_oracle(scene, 1)
     times = [time_oracle(scene, per_step_iters) for _ in range(args.steps)]
     t = sum(times) / len(times)
     val = n_alloc * per_step_iters / t
