@@ -369,6 +369,19 @@ def test_nccl_runtime_world1(V):
         vol.regularise_scene(s, exchange=False)
         assert np.array_equal(vol.u().cpu().numpy(), u1)
         vol.close()
+        # a later volume over the same blocks (same plan, same-size workspace — torch's allocator hands back
+        # the freed block, so the process-wide graph of the sharded loop is replayed) with different data:
+        # its result is its own, bit for bit the single-GPU one
+        import dataclasses
+        g = torch.Generator().manual_seed(5)
+        s2 = dataclasses.replace(s, f=s.f * 0.5 + 0.1 * torch.randn(s.f.shape, generator=g),
+                                 W=torch.where(torch.rand(s.W.shape, generator=g) < 0.1, torch.zeros_like(s.W), s.W))
+        _, u2 = run_gpu(V, s2)
+        for _ in range(2):
+            vol2 = Volume(s2.coords.cuda(), s2.f.cuda(), s2.W.cuda(), part=part, group=dist.group.WORLD)
+            vol2.regularise_scene(s2)
+            assert np.array_equal(vol2.u().cpu().numpy(), u2)
+            vol2.close()
     finally:
         dist.destroy_process_group()
 
