@@ -205,3 +205,23 @@ def test_within_fp64_extraction(Vol, case):
     R = extract_f64(c, u, W, V)
     assert T.shape == R.shape and T.shape[0] > 1000
     assert match_up_to_rotation(T, R) <= 1e-6
+
+
+def test_single_block_and_single_cell_row(Vol):
+    """The ordered single pass at its smallest: one block (one CTA, no predecessor in the look-back), and two
+    blocks far apart (no cell spans both), into a device buffer and through the count-only call."""
+    import ctypes
+    from paper_1604_03734_b200 import _native as N
+    rng = np.random.default_rng(3)
+    for coords in (np.array([[2, -1, 5]], np.int32), np.array([[0, 0, 0], [9, 9, 9]], np.int32)):
+        u = rng.normal(size=(coords.shape[0], 512)).astype(np.float32)
+        W = np.ones_like(u)
+        vol = Vol(torch.from_numpy(coords).cuda(), torch.from_numpy(u).cuda(), torch.from_numpy(W).cuda())
+        ref = oracle.extract(coords, u, W, V)
+        assert ref.shape[0] > 0
+        _same(vol.extract(V, field="f").cpu().numpy(), ref)
+        out = torch.empty(ref.shape[0] + 3, 3, 3, device="cuda")
+        _same(vol.extract(V, field="f", out=out).cpu().numpy(), ref)
+        n = ctypes.c_int64()
+        N.check(N.lib().vol_extract(vol._h, 1, V, 0.0, None, 0, ctypes.byref(n)))
+        assert n.value == ref.shape[0]
