@@ -158,10 +158,10 @@ __device__ __forceinline__ void walk_axis(float a, float b, float inv_bm, int32_
     if (n > 0) {
         const float dir = __fsub_rn(sb, sa);
         if (dir > 0.0f) {
-            tdel = __fdiv_rn(1.0f, dir);
+            tdel = __frcp_rn(dir);
             tmax = __fmul_rn(__fsub_rn(__fadd_rn(fa, 1.0f), sa), tdel);
         } else {
-            tdel = __fdiv_rn(1.0f, -dir);
+            tdel = __frcp_rn(-dir);
             tmax = __fmul_rn(__fsub_rn(sa, fa), tdel);
         }
     }
@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(128) k_fuse_integrate(FuseArgs A, const unsign
                     const float zc = __fadd_rn(__fadd_rn(__fmul_rn(r0.z, d0), e1z), e2z);
                     if (!(zc > 0.0f)) continue;
                     // step 2: nearest pixel (reading F-1)
-                    const float rz = __fdiv_rn(1.0f, zc);   // reading F-12: one reciprocal of z_c
+                    const float rz = __frcp_rn(zc);   // reading F-12: one correctly rounded reciprocal of z_c
                     const float ix = __fadd_rn(__fmul_rn(A.fx, __fmul_rn(xc, rz)), A.cx);
                     const float iy = __fadd_rn(__fmul_rn(A.fy, __fmul_rn(yc, rz)), A.cy);
                     const float fi = floorf(__fadd_rn(ix, 0.5f));
