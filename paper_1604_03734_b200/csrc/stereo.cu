@@ -124,8 +124,12 @@ struct Steps {
 };
 
 // Projections onto the α-balls: p·fl(α/‖p‖) when ‖p‖ > α (reading S-13), sums in the written order.
+// ‖p‖² <= α²·(1 − 2·10⁻⁶) (fp32, every rounding far inside that margin) proves fl(√‖p‖²) < α: no square root
+// is needed to know that the projection is the identity (same bits as the written order).
 __device__ __forceinline__ void project2(float &p1, float &p2, float alpha) {
-    const float nrm = __fsqrt_rn(__fadd_rn(__fmul_rn(p1, p1), __fmul_rn(p2, p2)));
+    const float n2 = __fadd_rn(__fmul_rn(p1, p1), __fmul_rn(p2, p2));
+    if (n2 <= alpha * alpha * 0.999998f) return;
+    const float nrm = __fsqrt_rn(n2);
     if (nrm > alpha) {
         const float r = __fdiv_rn(alpha, nrm);
         p1 = __fmul_rn(p1, r);
@@ -135,6 +139,7 @@ __device__ __forceinline__ void project2(float &p1, float &p2, float alpha) {
 __device__ __forceinline__ void project4(float &q1, float &q2, float &q3, float &q4, float alpha) {
     const float n2 = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(q1, q1), __fmul_rn(q2, q2)), __fmul_rn(q3, q3)),
                                __fmul_rn(q4, q4));
+    if (n2 <= alpha * alpha * 0.999998f) return;
     const float nrm = __fsqrt_rn(n2);
     if (nrm > alpha) {
         const float r = __fdiv_rn(alpha, nrm);
