@@ -677,11 +677,12 @@ namespace {
 // state (~116 B per pixel) is sized to stay resident in the 126 MB L2 across its iterations.
 // mode: 0 fused k_tgv_iter, 1 k_dual + k_primal, 2 k_dual4 + k_primal4 where the width allows (product)
 void enqueue_solve(const StereoLayout &L, const vol_stereo_params *prm, int32_t F, int chunk, int mode,
-                   cudaStream_t s, long long &launches) {
+                   const cudaStream_t *streams, int n_streams, long long &launches) {
     const long long HW = (long long)prm->width * prm->height;
     const int maxc = prm->window * prm->window - 1;
     const int TPB = 256;
-    for (int c0 = 0; c0 < F; c0 += chunk) {
+    for (int c0 = 0, ci = 0; c0 < F; c0 += chunk, ci++) {
+        cudaStream_t s = streams[ci % n_streams];   // chunks are independent: round-robin over the streams
         const int C = F - c0 < chunk ? F - c0 : chunk;
         const long long o = (long long)c0 * HW, n = (long long)C * HW;
         const unsigned nb = blocks_for(n, TPB);
@@ -808,19 +809,26 @@ extern "C" vol_status vol_stereo(const float *left, const float *right, int32_t 
     // selectable (experiments only).
     // HVG_STEREO_FUSED / HVG_STEREO_SCALAR select the other kernel forms (bit-identical; tests, experiments)
     const int mode = getenv("HVG_STEREO_FUSED") ? 0 : (getenv("HVG_STEREO_SCALAR") ? 1 : 2);
+    // Two chunks in flight on two streams (forked inside the graph), each half of the L2 budget: the
+    // iteration kernels of one chunk are ~1 wave, so two independent chunks fill the GPU and hide each
+    // other's launch gaps and tails (8 pairs 1240x376: 2 streams x 1 frame 11.1 ms, 1 stream x 2 frames
+    // 13.5 ms, 3 x 1 12.4 ms, 2 x 2 15.5 ms — DESIGN.md §13)
     const long long per_frame = (long long)prm->width * prm->height * 64;
-    int chunk = (int)((80ll << 20) / (per_frame > 0 ? per_frame : 1));
+    int n_streams = 2;
+    if (const char *e = getenv("HVG_STEREO_STREAMS")) n_streams = std::max(1, std::min(4, atoi(e)));   // experiments
+    int chunk = (int)((80ll << 20) / (per_frame > 0 ? per_frame : 1)) / n_streams;
     if (const char *e = getenv("HVG_STEREO_CHUNK")) chunk = atoi(e);      // experiments only
     if (chunk < 1) chunk = 1;
     if (chunk > n_frames) chunk = n_frames;
+    if (n_streams > (n_frames + chunk - 1) / chunk) n_streams = (n_frames + chunk - 1) / chunk;
     long long launches = 0;
     if (owns || getenv("HVG_STEREO_NO_GRAPH")) {
-        enqueue_solve(L, prm, n_frames, chunk, mode, s, launches);
+        enqueue_solve(L, prm, n_frames, chunk, mode, &s, 1, launches);
         CK(cudaPeekAtLastError());
     } else {
         int dev = 0;
         cudaGetDevice(&dev);
-        StereoGraphKey key{ws, n_frames, chunk, mode, dev, *prm};
+        StereoGraphKey key{ws, n_frames, chunk, mode * 8 + n_streams, dev, *prm};
         ExecRef exec;
         {
             std::lock_guard<std::mutex> lk(g_graph_mu);
@@ -837,8 +845,27 @@ extern "C" vol_status vol_stereo(const float *left, const float *right, int32_t 
             cudaGraphExec_t ge = nullptr;
             cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
             if (e == cudaSuccess) {
-                enqueue_solve(L, prm, n_frames, chunk, mode, cs, launches);
+                // extra streams fork from the capture stream and join back (graph edges)
+                cudaStream_t ss[4] = {cs, nullptr, nullptr, nullptr};
+                cudaEvent_t fork = nullptr, join[4] = {};
+                cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+                cudaEventRecord(fork, cs);
+                for (int k = 1; k < n_streams; k++) {
+                    cudaStreamCreateWithFlags(&ss[k], cudaStreamNonBlocking);
+                    cudaStreamWaitEvent(ss[k], fork, 0);
+                }
+                enqueue_solve(L, prm, n_frames, chunk, mode, ss, n_streams, launches);
+                for (int k = 1; k < n_streams; k++) {
+                    cudaEventCreateWithFlags(&join[k], cudaEventDisableTiming);
+                    cudaEventRecord(join[k], ss[k]);
+                    cudaStreamWaitEvent(cs, join[k], 0);
+                }
                 e = cudaStreamEndCapture(cs, &graph);
+                for (int k = 1; k < n_streams; k++) {
+                    cudaEventDestroy(join[k]);
+                    cudaStreamDestroy(ss[k]);
+                }
+                cudaEventDestroy(fork);
             }
             if (e == cudaSuccess) {
                 e = cudaGraphInstantiate(&ge, graph, 0);
