@@ -814,15 +814,16 @@ extern "C" vol_status vol_stereo(const float *left, const float *right, int32_t 
     // other's launch gaps and tails (8 pairs 1240x376: 2 streams x 1 frame 11.1 ms, 1 stream x 2 frames
     // 13.5 ms, 3 x 1 12.4 ms, 2 x 2 15.5 ms — DESIGN.md §13)
     const long long per_frame = (long long)prm->width * prm->height * 64;
-    int n_streams = 2;
-    if (const char *e = getenv("HVG_STEREO_STREAMS")) n_streams = std::max(1, std::min(4, atoi(e)));   // experiments
+    const bool graph = !(owns || getenv("HVG_STEREO_NO_GRAPH"));   // the extra streams live inside the graph
+    int n_streams = graph ? 2 : 1;
+    if (const char *e = getenv("HVG_STEREO_STREAMS"); e && graph) n_streams = std::max(1, std::min(4, atoi(e)));
     int chunk = (int)((80ll << 20) / (per_frame > 0 ? per_frame : 1)) / n_streams;
     if (const char *e = getenv("HVG_STEREO_CHUNK")) chunk = atoi(e);      // experiments only
     if (chunk < 1) chunk = 1;
     if (chunk > n_frames) chunk = n_frames;
     if (n_streams > (n_frames + chunk - 1) / chunk) n_streams = (n_frames + chunk - 1) / chunk;
     long long launches = 0;
-    if (owns || getenv("HVG_STEREO_NO_GRAPH")) {
+    if (!graph) {
         enqueue_solve(L, prm, n_frames, chunk, mode, &s, 1, launches);
         CK(cudaPeekAtLastError());
     } else {
