@@ -11,6 +11,8 @@
 
 #include <cub/device/device_radix_sort.cuh>
 
+#include <mutex>
+
 #include "internal.h"
 
 namespace hvg {
@@ -108,6 +110,61 @@ int launch_row_maps(const int32_t *perm, int64_t n, int32_t *sog, int64_t *rows,
     if (n == 0) return 0;
     k_row_maps<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(perm, n, sog, rows);
     return cudaPeekAtLastError() == cudaSuccess ? counted(1) : -1;
+}
+
+// Order-independent 64-bit digest of block coordinates: Σ_i mix(i, x_i, y_i, z_i) mod 2^64 (splitmix64 rounds),
+// the same function on the host (coord_digest_host) and the device (one reduction, no host copy of the
+// coordinates).
+__host__ __device__ inline unsigned long long dig_mix(unsigned long long z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__host__ __device__ inline unsigned long long dig_term(int64_t i, int32_t x, int32_t y, int32_t z) {
+    const unsigned long long a = dig_mix((unsigned long long)i);
+    const unsigned long long b = dig_mix(a ^ (unsigned long long)(uint32_t)x);
+    return dig_mix(b ^ (((unsigned long long)(uint32_t)y << 32) | (uint32_t)z));
+}
+
+namespace {
+__global__ void k_coord_digest(const int32_t *__restrict__ xyz, int64_t n, unsigned long long *out) {
+    unsigned long long acc = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        acc += dig_term(i, xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
+}
+}  // namespace
+
+unsigned long long coord_digest_host(const int32_t *xyz, int64_t n) {
+    unsigned long long acc = 0;
+    for (int64_t i = 0; i < n; i++) acc += dig_term(i, xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2]);
+    return acc ^ dig_mix((unsigned long long)n);
+}
+
+bool coord_digest_device(const int32_t *xyz, int64_t n, unsigned long long *out) {
+    // one scratch word per device, kept for the process; the per-thread default stream; serialised by a
+    // mutex (the call is synchronous: it gates the shard plan)
+    static std::mutex mu;
+    static unsigned long long *words[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!words[dev] && cudaMalloc(&words[dev], 8) != cudaSuccess) return false;
+    unsigned long long *d = words[dev], h = 0;
+    const cudaStream_t s = cudaStreamPerThread;
+    bool ok = cudaMemsetAsync(d, 0, 8, s) == cudaSuccess;
+    if (ok && n > 0) {
+        const unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8);
+        k_coord_digest<<<g, 256, 0, s>>>(xyz, n, d);
+        ok = cudaPeekAtLastError() == cudaSuccess;
+        if (ok) counted(1);
+    }
+    ok = ok && cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, s) == cudaSuccess && cudaStreamSynchronize(s) == cudaSuccess;
+    *out = h ^ dig_mix((unsigned long long)n);
+    return ok;
 }
 
 }  // namespace hvg

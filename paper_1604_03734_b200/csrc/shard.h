@@ -28,6 +28,10 @@ struct ShardPlan {
     std::vector<int64_t> send_off, send_cnt;  // [world] slice of send_rows per peer
     std::string error;
     uint64_t digest = 0;               // digest of the plan's inputs (coordinates, owner map) when known, else 0
+    // row maps of the store (filled with the cached plan): global index of store row r (local, then ghost
+    // rows) and the store row of every global block (−1: not held)
+    std::vector<int64_t> rows;
+    std::vector<int32_t> store_of_global;
     int64_t n_local() const { return (int64_t)local.size(); }
     int64_t n_ghost() const { return (int64_t)ghost.size(); }
 };

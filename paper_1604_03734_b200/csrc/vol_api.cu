@@ -126,46 +126,68 @@ static size_t layout_bytes(const Layout &L) {
     return c.off + 512;
 }
 
-// The shard plan is needed twice per volume (workspace size, then creation); the last plan is cached
-// per thread, keyed by a digest of the coordinates and the owner map.
+// The shard plan is needed twice per volume (workspace size, then creation) and, in a loop that creates one
+// volume per step, again and again for the same blocks; the last plan is cached per thread, keyed by an
+// order-independent digest of the coordinates computed where they live (device coordinates are not copied
+// to the host on a hit) and a digest of the owner map.  The store's row maps come with it.
 namespace {
 struct PlanCache {
     bool valid = false;
     int64_t n = 0;
     int world = 0, rank = 0;
-    uint64_t digest = 0;
+    uint64_t cdig = 0, pdig = 0;
     ShardPlan plan;
 };
 thread_local PlanCache g_plan_cache;
 }  // namespace
 
-static uint64_t plan_digest(const int32_t *xyz, int64_t n, const int32_t *part) {
+static uint64_t part_digest(const int32_t *part, int64_t n) {
     uint64_t h = 1469598103934665603ull;
-    for (int64_t i = 0; i < n; i++) {
-        const uint64_t a = ((uint64_t)(uint32_t)xyz[3 * i] << 32) ^ (uint32_t)xyz[3 * i + 1];
-        const uint64_t b = ((uint64_t)(uint32_t)xyz[3 * i + 2] << 32) ^ (uint32_t)part[i];
-        h = (h ^ a) * 1099511628211ull;
-        h = (h ^ b) * 1099511628211ull;
-    }
+    for (int64_t i = 0; i < n; i++) h = (h ^ (uint32_t)part[i]) * 1099511628211ull;
     return h;
 }
 
-static bool get_shard_plan(const int32_t *xyz, int64_t n, const vol_dist *d, ShardPlan &out) {
-    const uint64_t dg = plan_digest(xyz, n, d->part);
-    PlanCache &c = g_plan_cache;
-    if (c.valid && c.n == n && c.world == d->world && c.rank == d->rank && c.digest == dg) {
-        out = c.plan;
-        return true;
+static vol_status get_shard_plan(const int32_t *block_xyz, int64_t n, const vol_dist *d, ShardPlan &out) {
+    const bool dev = is_device_ptr(block_xyz);
+    unsigned long long cd = 0;
+    if (dev) {
+        if (!coord_digest_device(block_xyz, n, &cd)) return fail(VOL_ECUDA, "coordinate digest failed");
+    } else {
+        cd = coord_digest_host(block_xyz, n);
     }
-    if (!make_shard_plan(xyz, n, d->part, d->world, d->rank, out)) return false;
-    out.digest = dg ? dg : 1;
+    const uint64_t pd = part_digest(d->part, n);
+    PlanCache &c = g_plan_cache;
+    if (c.valid && c.n == n && c.world == d->world && c.rank == d->rank && c.cdig == cd && c.pdig == pd) {
+        out = c.plan;
+        return VOL_OK;
+    }
+    std::vector<int32_t> h;
+    const int32_t *xyz = block_xyz;
+    if (dev) {
+        h.resize(3 * (size_t)n);
+        if (cudaMemcpy(h.data(), block_xyz, h.size() * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
+            return fail(VOL_ECUDA, "copy of block_xyz failed");
+        xyz = h.data();
+    }
+    // block coordinates must leave room for the ±1 neighbour offsets in int32 arithmetic
+    for (int64_t k = 0; k < 3 * n; k++)
+        if (xyz[k] <= -(1 << 30) || xyz[k] >= (1 << 30))
+            return fail(VOL_EDATA, "block %lld: coordinate %d outside (-2^30, 2^30)", (long long)(k / 3), xyz[k]);
+    if (!make_shard_plan(xyz, n, d->part, d->world, d->rank, out))
+        return fail(VOL_EDATA, "vol_create: shard plan failed: %s", out.error.c_str());
+    out.digest = (cd ^ (pd * 0x9E3779B97F4A7C15ull)) | 1ull;
+    out.rows = out.local;
+    out.rows.insert(out.rows.end(), out.ghost.begin(), out.ghost.end());
+    out.store_of_global.assign(n, -1);
+    for (size_t r = 0; r < out.rows.size(); r++) out.store_of_global[out.rows[r]] = (int32_t)r;
     c.valid = true;
     c.n = n;
     c.world = d->world;
     c.rank = d->rank;
-    c.digest = dg;
+    c.cdig = cd;
+    c.pdig = pd;
     c.plan = out;
-    return true;
+    return VOL_OK;
 }
 
 extern "C" size_t vol_workspace_bytes(const int32_t *block_xyz, int64_t n_global, const vol_dist *dist) {
@@ -179,15 +201,8 @@ extern "C" size_t vol_workspace_bytes(const int32_t *block_xyz, int64_t n_global
         return layout_bytes(L);
     }
     if (!block_xyz || !dist->part) return 0;
-    std::vector<int32_t> hxyz;
-    const int32_t *xyz = block_xyz;
-    if (is_device_ptr(block_xyz)) {   // the plan is a host-side schedule
-        hxyz.resize(3 * (size_t)n_global);
-        if (cudaMemcpy(hxyz.data(), block_xyz, hxyz.size() * 4, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
-        xyz = hxyz.data();
-    }
     ShardPlan plan;
-    if (!get_shard_plan(xyz, n_global, dist, plan)) return 0;
+    if (get_shard_plan(block_xyz, n_global, dist, plan) != VOL_OK) return 0;
     L.n_local = plan.n_local();
     L.S = plan.n_local() + plan.n_ghost();
     return layout_bytes(L) + shard_extra_bytes(plan);
@@ -257,32 +272,20 @@ static vol_status create_impl(const int32_t *block_xyz, int64_t n_global, const 
     if (cudaStreamCreateWithFlags(&v->cap, cudaStreamNonBlocking) != cudaSuccess)
         return bail(fail(VOL_ECUDA, "cudaStreamCreate failed"));
 
-    // host copy of the coordinates: the shard plan is a host-side schedule (sharded volumes only — one GPU
-    // orders and checks the blocks on the device, order.cu)
-    std::vector<int32_t> hxyz;
+    // the shard plan is a host-side schedule (sharded volumes; cached across volumes of the same blocks — the
+    // coordinates are copied to the host only to build it); one GPU orders and checks the blocks on the
+    // device (order.cu)
+    ShardPlan plan;
     if (sharded) {
-        hxyz.resize(3 * (size_t)n_global);
-        if (is_device_ptr(block_xyz)) {
-            if (cudaMemcpy(hxyz.data(), block_xyz, hxyz.size() * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
-                return bail(fail(VOL_ECUDA, "copy of block_xyz failed"));
-        } else {
-            memcpy(hxyz.data(), block_xyz, hxyz.size() * 4);
-        }
-        // block coordinates must leave room for the ±1 neighbour offsets in int32 arithmetic
-        for (size_t k = 0; k < hxyz.size(); k++)
-            if (hxyz[k] <= -(1 << 30) || hxyz[k] >= (1 << 30))
-                return bail(fail(VOL_EDATA, "block %lld: coordinate %d outside (-2^30, 2^30)", (long long)(k / 3),
-                                 hxyz[k]));
+        vol_status pst = get_shard_plan(block_xyz, n_global, dist, plan);
+        if (pst != VOL_OK) return bail(pst);
     }
     trace("stream (+ coords D2H)");
 
-    ShardPlan plan;
     Layout L{};
     L.n_global = n_global;
     L.T = table_size(n_global);
     if (sharded) {
-        if (!get_shard_plan(hxyz.data(), n_global, dist, plan))
-            return bail(fail(VOL_EDATA, "vol_create: shard plan failed: %s", plan.error.c_str()));
         L.n_local = plan.n_local();
         L.S = plan.n_local() + plan.n_ghost();
     } else {
@@ -323,8 +326,6 @@ static vol_status create_impl(const int32_t *block_xyz, int64_t n_global, const 
     // [launch A | launch B] rows + ghosts; d_perm[r] is the block's index in the caller's f / W / u arrays
     vol_status st;
     if ((st = copy_in(v->d_xyz, block_xyz, 3 * (size_t)n_global * 4, s)) != VOL_OK) return bail(st);
-    std::vector<int64_t> row_global;
-    std::vector<int32_t> row_caller, store_of_global;
     if (!sharded) {
         const size_t ms = morton_order_scratch_bytes(n_global);
         void *scr = v->d_tmp;
@@ -334,12 +335,7 @@ static vol_status create_impl(const int32_t *block_xyz, int64_t n_global, const 
         if (own) cudaFreeAsync(scr, s);
         if (r < 0) return bail(fail(VOL_ECUDA, "store order launch failed: %s", cudaGetErrorString(cudaGetLastError())));
     } else {
-        row_global = plan.local;
-        row_global.insert(row_global.end(), plan.ghost.begin(), plan.ghost.end());
-        row_caller = plan.local_caller;
-        store_of_global.assign(n_global, -1);
-        for (int64_t r = 0; r < L.S; r++) store_of_global[row_global[r]] = (int32_t)r;
-        if (cudaMemcpyAsync(v->d_perm, row_caller.data(), (size_t)L.n_local * 4, cudaMemcpyHostToDevice, s) !=
+        if (cudaMemcpyAsync(v->d_perm, plan.local_caller.data(), (size_t)L.n_local * 4, cudaMemcpyHostToDevice, s) !=
             cudaSuccess)
             return bail(fail(VOL_ECUDA, "permutation upload failed"));
     }
@@ -380,12 +376,9 @@ static vol_status create_impl(const int32_t *block_xyz, int64_t n_global, const 
     // reports the first input error the status words hold (caller block indices and coordinates fetched on
     // demand), else records |Ω|
     auto check_inputs = [&](const unsigned long long *misc) -> vol_status {
-        auto coord = [&](long long i, int32_t *xyz3) {
-            if (!hxyz.empty()) {
-                for (int a = 0; a < 3; a++) xyz3[a] = hxyz[3 * i + a];
-            } else if (cudaMemcpy(xyz3, v->d_xyz + 3 * i, 12, cudaMemcpyDeviceToHost) != cudaSuccess) {
+        auto coord = [&](long long i, int32_t *xyz3) {   // fetched from the device copy, on error only
+            if (cudaMemcpy(xyz3, v->d_xyz + 3 * i, 12, cudaMemcpyDeviceToHost) != cudaSuccess)
                 xyz3[0] = xyz3[1] = xyz3[2] = 0;
-            }
         };
         int32_t q[3];
         if (misc[4] != ~0ULL) {
@@ -434,8 +427,9 @@ static vol_status create_impl(const int32_t *block_xyz, int64_t n_global, const 
         trace("store build + sync");
         if ((st = check_inputs(misc)) != VOL_OK) return bail(st);
         // K2: neighbour table in store rows (faces + edges)
-        if (cudaMemcpyAsync(d_sog, store_of_global.data(), (size_t)n_global * 4, cudaMemcpyHostToDevice, s) != cudaSuccess ||
-            cudaMemcpyAsync(d_rows, row_global.data(), (size_t)L.S * 8, cudaMemcpyHostToDevice, s) != cudaSuccess)
+        if (cudaMemcpyAsync(d_sog, plan.store_of_global.data(), (size_t)n_global * 4, cudaMemcpyHostToDevice, s) !=
+                cudaSuccess ||
+            cudaMemcpyAsync(d_rows, plan.rows.data(), (size_t)L.S * 8, cudaMemcpyHostToDevice, s) != cudaSuccess)
             return bail(fail(VOL_ECUDA, "row map upload failed"));
         // (copies from pageable host memory return once the data is staged: the host row maps may go)
         if (launch_neighbours(v->d_xyz, n_global, v->d_start, v->d_entry, L.T, d_sog, d_rows, L.S, v->d_nbr, s) < 0)
