@@ -658,11 +658,18 @@ vol_status shard_after_create(vol_s *v) {
     if ((st = nccl_exchange(v, s)) != VOL_OK) return st;
     if ((st = unpack(v, W, f, v->F.ub[0], v->F.ub[1], s)) != VOL_OK) return st;
     CKL(launch_init_state(v->F, v->L.S * kBlockVox, 0, s));
+    // the 8-bit weight copy (finalize_w8) in the same synchronisation: every held W, ghosts included, is final
+    unsigned *d_bad = reinterpret_cast<unsigned *>(&v->d_misc[3]);
+    unsigned bad = 0;
+    CK(cudaMemsetAsync(d_bad, 0, sizeof(unsigned), s));
+    CKL(launch_pack_w8(v->F.W, v->d_w8, v->L.S * kBlockVox, d_bad, s));
+    CK(cudaMemcpyAsync(&bad, d_bad, sizeof bad, cudaMemcpyDeviceToHost, s));
     unsigned long long cnt = (unsigned long long)v->n_omega_local, tot = 0;
     CK(cudaMemcpyAsync(R->omega, &cnt, 8, cudaMemcpyHostToDevice, s));
     NCK(ncclAllReduce(R->omega, R->omega + 1, 1, ncclUint64, ncclSum, R->comm, s));
     CK(cudaMemcpyAsync(&tot, R->omega + 1, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    v->F.W8 = bad ? nullptr : v->d_w8;
     v->n_omega_global = (int64_t)tot;
     R->connected = true;
     return VOL_OK;

@@ -444,10 +444,7 @@ static vol_status create_impl(const int32_t *block_xyz, int64_t n_global, const 
         st = shard_after_create(v);
         if (st != VOL_OK) return bail(st);
         trace("shard setup + init");
-        if (v->shard_nccl()) {   // loopback shards finish in vol_group_connect
-            st = finalize_w8(v);
-            if (st != VOL_OK) return bail(st);
-        }
+        // (NCCL shards set up their 8-bit weights in shard_after_create; loopback shards in vol_group_connect)
     }
     v->cur = 0;
     v->initialised = true;
