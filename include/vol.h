@@ -84,7 +84,9 @@ void vol_default_opts(vol_opts *opts);
 
 /* Device bytes vol_create needs for a volume of n_global blocks (exact for dist == NULL; for a
  * sharded volume pass the same dist as to vol_create, the value then covers local + ghost blocks).
- * block_xyz may be NULL when dist == NULL.  Returns 0 on invalid arguments.                        */
+ * block_xyz may be NULL when dist == NULL.  Device coordinates of a sharded volume are read on the
+ * legacy default stream (the call takes no stream): writes to them on another stream must be
+ * complete.  Returns 0 on invalid arguments.                                                      */
 size_t vol_workspace_bytes(const int32_t *block_xyz, int64_t n_global, const vol_dist *dist);
 
 /* Build a volume:

@@ -130,7 +130,8 @@ int launch_row_maps(const int32_t *perm, int64_t n, int32_t *sog, int64_t *rows,
 
 // order-independent 64-bit digest of n block coordinates ([n][3] int32), the same value on host and device
 unsigned long long coord_digest_host(const int32_t *xyz, int64_t n);
-bool coord_digest_device(const int32_t *xyz, int64_t n, unsigned long long *out);
+// (computed on stream s, returns when done)
+bool coord_digest_device(const int32_t *xyz, int64_t n, unsigned long long *out, cudaStream_t s);
 
 uint32_t host_hash(int32_t x, int32_t y, int32_t z, uint32_t T);
 

@@ -144,9 +144,10 @@ unsigned long long coord_digest_host(const int32_t *xyz, int64_t n) {
     return acc ^ dig_mix((unsigned long long)n);
 }
 
-bool coord_digest_device(const int32_t *xyz, int64_t n, unsigned long long *out) {
-    // one scratch word per device, kept for the process; the per-thread default stream; serialised by a
-    // mutex (the call is synchronous: it gates the shard plan)
+bool coord_digest_device(const int32_t *xyz, int64_t n, unsigned long long *out, cudaStream_t s) {
+    // one scratch word per device, kept for the process; runs on `s` — the caller's stream in vol_create, so
+    // coordinates still being written there are read after they are complete — and returns synchronously
+    // (it gates the shard plan); serialised by a mutex
     static std::mutex mu;
     static unsigned long long *words[64] = {};
     int dev = 0;
@@ -154,7 +155,6 @@ bool coord_digest_device(const int32_t *xyz, int64_t n, unsigned long long *out)
     std::lock_guard<std::mutex> lk(mu);
     if (!words[dev] && cudaMalloc(&words[dev], 8) != cudaSuccess) return false;
     unsigned long long *d = words[dev], h = 0;
-    const cudaStream_t s = cudaStreamPerThread;
     bool ok = cudaMemsetAsync(d, 0, 8, s) == cudaSuccess;
     if (ok && n > 0) {
         const unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8);

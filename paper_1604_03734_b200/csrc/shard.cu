@@ -475,10 +475,22 @@ static vol_status comm_acquire(const void *id_bytes, int world, int rank, int de
 // size, layout, shard-plan digest, communicator, rank, device and the loop's parameters — is identical:
 // that volume's buffers sit at the same addresses with the same sizes and counts.  Entries of a
 // communicator are destroyed when it is evicted or released; at most kSharedGraphs are kept.
+// The executable is reference-counted: a call holds its own reference from lookup through its launches, so an
+// eviction by another thread (a 9th key, or the communicator's release) cannot destroy an exec that call is
+// about to launch; the last reference synchronises the device and destroys it.
 namespace {
+using SharedExec = std::shared_ptr<CUgraphExec_st>;
+SharedExec shared_exec(cudaGraphExec_t e) {
+    return SharedExec(e, [](cudaGraphExec_t x) {
+        if (x) {
+            cudaDeviceSynchronize();   // the exec may still run on some volume's stream
+            cudaGraphExecDestroy(x);
+        }
+    });
+}
 struct SharedGraph {
     std::string key;
-    cudaGraphExec_t exec;
+    SharedExec exec;
     int64_t per;
     ncclComm_t comm;
 };
@@ -499,19 +511,19 @@ void shared_graphs_drop(ncclComm_t comm) {   // comm == nullptr: all
             }
         }
     }
-    if (!dead.empty()) cudaDeviceSynchronize();
-    for (auto &e : dead) cudaGraphExecDestroy(e.exec);
+    dead.clear();   // each exec is destroyed with its last reference
 }
 }  // namespace
 
 template <class Body>
-static vol_status cached_graph_shared(vol_s *v, const GraphKey &key, ncclComm_t comm, Body body, cudaGraphExec_t *exec,
-                                      int64_t *per) {
+static vol_status cached_graph_shared(vol_s *v, const GraphKey &key, ncclComm_t comm, Body body, SharedExec *hold,
+                                      cudaGraphExec_t *exec, int64_t *per) {
     {
         std::lock_guard<std::mutex> lk(g_sg_mu);
         for (const SharedGraph &e : g_sg)
             if (e.key == key.bytes) {
-                *exec = e.exec;
+                *hold = e.exec;
+                *exec = e.exec.get();
                 *per = e.per;
                 return VOL_OK;
             }
@@ -532,21 +544,18 @@ static vol_status cached_graph_shared(vol_s *v, const GraphKey &key, ncclComm_t 
     e = cudaGraphInstantiate(&ge, g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return fail(VOL_ECUDA, "graph instantiate failed: %s", cudaGetErrorString(e));
+    SharedExec ref = shared_exec(ge);
     SharedGraph old{};
-    bool evict = false;
     {
         std::lock_guard<std::mutex> lk(g_sg_mu);
         if (g_sg.size() >= kSharedGraphs) {
-            old = g_sg.front();
+            old = std::move(g_sg.front());   // released below, outside the lock
             g_sg.erase(g_sg.begin());
-            evict = true;
         }
-        g_sg.push_back(SharedGraph{key.bytes, ge, n, comm});
+        g_sg.push_back(SharedGraph{key.bytes, ref, n, comm});
     }
-    if (evict) {   // the oldest entry may still run on some volume's stream
-        cudaDeviceSynchronize();
-        cudaGraphExecDestroy(old.exec);
-    }
+    old = SharedGraph{};
+    *hold = std::move(ref);
     *exec = ge;
     *per = n;
     return VOL_OK;
@@ -817,6 +826,7 @@ static vol_status nccl_skew(vol_s *v, const IterParams &P, int32_t iters) {
         GraphKey key;
         key.add('N').add(c).add(m).add(iters & 1).add(v->pending_frozen).add(v->pending_exchange).add(P);
         cudaGraphExec_t ge = nullptr;
+        SharedExec hold;   // keeps a shared exec alive through the launches below
         int64_t per = 0;
         auto capture = [&](cudaStream_t cap, int64_t &n) -> vol_status {
             for (int k = 0; k < 2 * m; k++) {
@@ -828,7 +838,7 @@ static vol_status nccl_skew(vol_s *v, const IterParams &P, int32_t iters) {
         if (SP.digest != 0 && R->comm) {   // reusable by later volumes with the same workspace and plan
             key.add(v->ws).add(v->ws_bytes).add(v->L.n_global).add(v->L.n_local).add(v->L.S).add(v->L.T)
                 .add(SP.digest).add(SP.rank).add(SP.world).add(R->comm).add(v->device);
-            st = cached_graph_shared(v, key, R->comm, capture, &ge, &per);
+            st = cached_graph_shared(v, key, R->comm, capture, &hold, &ge, &per);
         } else {
             st = cached_graph(v, key, capture, &ge, &per);
         }

@@ -147,11 +147,14 @@ static uint64_t part_digest(const int32_t *part, int64_t n) {
     return h;
 }
 
-static vol_status get_shard_plan(const int32_t *block_xyz, int64_t n, const vol_dist *d, ShardPlan &out) {
+// Device coordinates are read on stream s (vol_create: the caller's stream; vol_workspace_bytes, which has no
+// stream: the legacy default stream).
+static vol_status get_shard_plan(const int32_t *block_xyz, int64_t n, const vol_dist *d, ShardPlan &out,
+                                 cudaStream_t s) {
     const bool dev = is_device_ptr(block_xyz);
     unsigned long long cd = 0;
     if (dev) {
-        if (!coord_digest_device(block_xyz, n, &cd)) return fail(VOL_ECUDA, "coordinate digest failed");
+        if (!coord_digest_device(block_xyz, n, &cd, s)) return fail(VOL_ECUDA, "coordinate digest failed");
     } else {
         cd = coord_digest_host(block_xyz, n);
     }
@@ -165,7 +168,8 @@ static vol_status get_shard_plan(const int32_t *block_xyz, int64_t n, const vol_
     const int32_t *xyz = block_xyz;
     if (dev) {
         h.resize(3 * (size_t)n);
-        if (cudaMemcpy(h.data(), block_xyz, h.size() * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
+        if (cudaMemcpyAsync(h.data(), block_xyz, h.size() * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess)
             return fail(VOL_ECUDA, "copy of block_xyz failed");
         xyz = h.data();
     }
@@ -202,7 +206,7 @@ extern "C" size_t vol_workspace_bytes(const int32_t *block_xyz, int64_t n_global
     }
     if (!block_xyz || !dist->part) return 0;
     ShardPlan plan;
-    if (get_shard_plan(block_xyz, n_global, dist, plan) != VOL_OK) return 0;
+    if (get_shard_plan(block_xyz, n_global, dist, plan, cudaStreamLegacy) != VOL_OK) return 0;
     L.n_local = plan.n_local();
     L.S = plan.n_local() + plan.n_ghost();
     return layout_bytes(L) + shard_extra_bytes(plan);
@@ -277,7 +281,7 @@ static vol_status create_impl(const int32_t *block_xyz, int64_t n_global, const 
     // device (order.cu)
     ShardPlan plan;
     if (sharded) {
-        vol_status pst = get_shard_plan(block_xyz, n_global, dist, plan);
+        vol_status pst = get_shard_plan(block_xyz, n_global, dist, plan, v->stream);
         if (pst != VOL_OK) return bail(pst);
     }
     trace("stream (+ coords D2H)");

@@ -159,6 +159,10 @@ class Volume:
             fp, fk = _ptr(f)
             wp, wk = _ptr(W)
             dptr = ctypes.byref(dist) if dist is not None else None
+            if dist is not None and isinstance(coords, torch.Tensor) and coords.is_cuda:
+                # vol_workspace_bytes reads device coordinates on the legacy default stream (it takes no
+                # stream): they must be complete
+                self.stream.synchronize()
             nbytes = self._lib.vol_workspace_bytes(cp, n, dptr)
             if nbytes == 0:
                 raise N.VolError(N.VOL_EINVAL, "vol_workspace_bytes failed (bad coordinates or partition)")
