@@ -29,3 +29,6 @@ for cap in (n, None):
         ts.append(a.elapsed_time(b))
     print("vol_fuse ms", [round(t, 3) for t in ts])
     break
+st2 = {}
+fuse(ds.depth, ds.poses, intr, ds.voxel, ds.mu, ds.max_range, ds.w_max, stats=st2)
+print("warm stats", {k: round(v, 4) for k, v in st2.items() if k.startswith("ms_")})

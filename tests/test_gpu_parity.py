@@ -382,6 +382,16 @@ def test_nccl_runtime_world1(V):
             vol2.regularise_scene(s2)
             assert np.array_equal(vol2.u().cpu().numpy(), u2)
             vol2.close()
+        # more distinct loop graphs than the process-wide cache keeps (8): each insertion past that evicts
+        # an entry whose last launch may still be in flight (reference-counted executables); every call's
+        # result still equals the single-GPU one, and the first count, evicted by then, is captured again
+        vol3 = Volume(s.coords.cuda(), s.f.cuda(), s.W.cuda(), part=part, group=dist.group.WORLD)
+        counts = list(range(6, 26, 2)) + [6]
+        for k in counts:
+            vol3.regularise_scene(s, iters=k)
+            single.regularise_scene(s, iters=k)
+            assert np.array_equal(vol3.u().cpu().numpy(), single.u().cpu().numpy()), k
+        vol3.close()
     finally:
         dist.destroy_process_group()
 
