@@ -579,7 +579,7 @@ def reference_arm(args):
     val = n_alloc * per_step_iters / t
     sample = f"{per_step_iters} oracle iteration(s) over the whole {scene.name} volume ({n_alloc} voxels) per step"
     line = {"impl": "reference", "metric": "voxel-updates/s", "value": val, "unit": "voxel-updates/s",
-            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t,
             "higher_is_better": True, "scaling": "strong" if cfg in ("city", "city-heavy") else "weak",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": scene.name, "n_alloc": n_alloc, "blocks": scene.n_blocks,
