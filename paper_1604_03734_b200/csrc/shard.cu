@@ -495,7 +495,9 @@ struct SharedGraph {
     ncclComm_t comm;
 };
 std::mutex g_sg_mu;
-std::vector<SharedGraph> g_sg;
+// heap-allocated and never destroyed: no graph destruction (device synchronisation, NCCL resources) runs
+// during static destruction at process exit, after the CUDA runtime or a communicator may be gone
+std::vector<SharedGraph> &g_sg = *new std::vector<SharedGraph>();
 constexpr size_t kSharedGraphs = 8;
 
 void shared_graphs_drop(ncclComm_t comm) {   // comm == nullptr: all

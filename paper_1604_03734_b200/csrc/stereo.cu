@@ -760,7 +760,8 @@ struct StereoGraphEntry {
 };
 
 std::mutex g_graph_mu;
-std::vector<StereoGraphEntry> g_graphs;   // most recent last; at most 8
+// most recent last; at most 8 (heap-allocated and never destroyed: no graph destruction at process exit)
+std::vector<StereoGraphEntry> &g_graphs = *new std::vector<StereoGraphEntry>();
 
 bool same_key(const StereoGraphKey &a, const StereoGraphKey &b) {
     return a.ws == b.ws && a.F == b.F && a.chunk == b.chunk && a.mode == b.mode && a.device == b.device &&
