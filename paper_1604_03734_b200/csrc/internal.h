@@ -79,9 +79,9 @@ int launch_primal_only(const View &V, const int32_t *nbr, int64_t n_work, const 
 // [first, first + n_blocks); reads u_in and p[p_in] (p^{k+1}), writes u_out and p[p_in ^ 1] (p^{k+2}).
 int launch_skew(const Fields &F, const float *u_in, float *u_out, int p_in, const uint32_t *frozen,
                 const int32_t *nbr, int64_t first, int64_t n_blocks, const IterParams &P, cudaStream_t s);
-// The same launch of all rows with programmatic dependent launch (the single-GPU loop, HVG_SKEW_PDL): its
-// static prologue overlaps the previous launch's tail.
-int launch_skew_pdl(const Fields &F, const float *u_in, float *u_out, int p_in, const uint32_t *frozen,
+// The single-GPU loop's launch of all rows: launch_skew, or with HVG_SKEW_PDL (off: measured ±0)
+// the programmatic-dependent-launch form whose static prologue overlaps the previous launch's tail.
+int launch_skew_loop(const Fields &F, const float *u_in, float *u_out, int p_in, const uint32_t *frozen,
                     const int32_t *nbr, int64_t n_blocks, const IterParams &P, cudaStream_t s);
 // The same launch for the boundary rows of a peer-connected shard: every output of a row is also stored
 // into its peer destinations (peer.cuh), followed by a system-scope fence.
