@@ -509,8 +509,8 @@ static vol_status run_iterations_skew(vol_s *v, const IterParams &P, int32_t ite
         launches += r;
     }
     auto skew = [&](cudaStream_t st, int j) -> int {
-        return launch_skew_loop(v->F, B[j & 1], B[(j + 1) & 1], cur ^ ((j + 1) & 1), v->pending_frozen, v->d_nbr, n, P,
-                               st);
+        return launch_skew_loop(v->F, B[j & 1], B[(j + 1) & 1], cur ^ ((j + 1) & 1), v->pending_frozen, v->d_nbr, n,
+                                P, st);
     };
     int j = 0;
     const int total = iters - 1;
